@@ -1,0 +1,180 @@
+/*
+ * rk.h — C ABI of librk, the B200-native (sm_100a) exhaustive evaluator of
+ * kernel launch orders under the execution-round model of Li, Narayana &
+ * El-Ghazawi, "Reordering GPU Kernel Launches to Enable Efficient Concurrent
+ * Execution" (arXiv 1511.07983).
+ *
+ * Citations: PAPER:L = reference PAPER.md line L (section/table/algorithm
+ * named); SPEC:L = reference SPEC.md line L.  The model readings (L1..L23)
+ * are listed in DESIGN.md §3.
+ *
+ * Conventions (every entry point):
+ *   - Returns rk_status; no exception or abort crosses the ABI.  On error the
+ *     outputs are left untouched and rk_last_error(ctx) holds a message
+ *     (owned by ctx, valid until the next call on that ctx).
+ *   - The caller owns every host array; the library copies what it keeps.
+ *     Device buffers (*_dev) are allocated by the caller (e.g. torch tensors)
+ *     on the ctx's device; the library never frees them.
+ *   - One ctx per host thread (no global mutable state).  The ctx owns its
+ *     device tables and scratch; rk_destroy frees them.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  *_async
+ *     calls only enqueue work; the synchronous calls return after the
+ *     results are on the host.
+ *   - There is no CPU fallback: every call that evaluates the model runs on
+ *     the GPU and returns RK_ENODEVICE on a host-only ctx.
+ */
+#ifndef RK_H
+#define RK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RK_OK = 0,
+    RK_EINVAL = 1,         /* invalid argument / profile (SPEC:359 ValidationError)           */
+    RK_EINFEASIBLE = 2,    /* a single block exceeds an SM limit      */
+    RK_ETOOMANY = 3,       /* n > 12: index no longer fits u32                */
+    RK_EMISSINGRATIO = 4,  /* mem_per_block == 0: R_i undefined                 */
+    RK_EOVERFLOW = 5,      /* exact key bound sum_i T_i(den*A_i + num*M_i) >= 2^63            */
+    RK_ESTATE = 6,         /* call order (params/kernels not set)                              */
+    RK_ECUDA = 7,          /* CUDA runtime error (message in rk_last_error)                   */
+    RK_ENODEVICE = 8,      /* compute call on a host-only ctx (rk_create(..., -1))            */
+    RK_EUNSUPPORTED = 9    /* input outside the device fast path's packing     */
+} rk_status;
+
+typedef struct rk_ctx rk_ctx;
+
+/* Create a context bound to CUDA device `cuda_device` (>= 0), or a host-only
+ * context (cuda_device = -1) that can validate inputs and run Algorithm 1 but
+ * returns RK_ENODEVICE for every model evaluation. */
+rk_status rk_create(rk_ctx** out, int cuda_device);
+void rk_destroy(rk_ctx* ctx);
+const char* rk_last_error(const rk_ctx* ctx);
+
+/* GPU parameters, Table 1 top half: N_SM, N_reg_SM, N_shm_SM,
+ * N_warp_SM, N_blk_SM, and the balanced inst/mem ratio R_B
+ * as the exact rational rb_num / rb_den (reading L10; GTX580 preset
+ * {16, 32768, 49152, 48, 8, 411, 100}).  All fields > 0
+ * (SPEC:30-32); n_sm <= 32 and max_blocks_per_sm <= 255 on the device path.
+ * Invalidates previously set kernels.  Errors: RK_EINVAL. */
+typedef struct {
+    uint32_t n_sm, regs_per_sm, shm_bytes_per_sm, max_warps_per_sm, max_blocks_per_sm;
+    uint32_t rb_num, rb_den;
+} rk_gpu_params;
+rk_status rk_set_gpu_params(rk_ctx* ctx, const rk_gpu_params* p);
+
+/* Kernel profile, Table 1 bottom half:
+ *   grid_blocks         N_tblk_i >= 1
+ *   threads_per_block   1..1024; warps/block = ceil(tpb/32) (reading L7)
+ *   regs_per_thread     registers/block = regs_per_thread * tpb (reading L6)
+ *   shm_bytes_per_block
+ *   inst_per_block      A_i = N_inst_i / N_tblk_i >= 1
+ *   mem_per_block       M_i = A_i / R_i = 4*mem_events_i / N_tblk_i >= 1,
+ *                       in instruction units
+ * Per-block demand is used by the simulator, the per-SM footprint
+ * (demand * ceil(N_tblk/N_SM)) by Algorithm 1 (reading L2). */
+typedef struct {
+    uint32_t grid_blocks, threads_per_block, regs_per_thread, shm_bytes_per_block;
+    uint32_t inst_per_block, mem_per_block;
+} rk_kernel;
+
+/* Copy and validate n kernels (1 <= n <= 12) and upload the device tables.
+ * Errors: RK_ESTATE (no gpu params), RK_EINVAL, RK_EINFEASIBLE,
+ * RK_ETOOMANY, RK_EMISSINGRATIO, RK_EOVERFLOW, RK_EUNSUPPORTED, RK_ECUDA. */
+rk_status rk_set_kernels(rk_ctx* ctx, const rk_kernel* k, uint32_t n);
+
+/* Reduction record over an index range (Table 3 columns, PAPER:236;
+ * SPEC:281-286).  Keys are exact: K = sum_r max(rb_den*I_r, rb_num*M_r) =
+ * rb_den * T (O4), so T = K / rb_den.  argmin/argmax = smallest lexicographic
+ * index attaining the extreme (reading L12).  n_lt/n_eq/n_gt count keys
+ * below/equal/above the candidate key.  56 bytes, no padding. */
+typedef struct {
+    uint64_t key_min, key_max;
+    uint32_t argmin, argmax;
+    uint64_t n_lt, n_eq, n_gt;
+    uint64_t evaluated;
+} rk_stats;
+
+/* Evaluate every launch order with lexicographic index in [first, first+count)
+ * ("all possible kernel orderings (all permutations)"; order <->
+ * index is the Lehmer code, reading L11): unrank, place all blocks
+ * round-robin into execution rounds, score the rounds
+ * and reduce.  first + count <= n!.
+ *   candidate_key  key the counts compare against (e.g. from rk_heuristic_order)
+ *   out_host       host rk_stats (synchronous call)
+ *   keys_dev       nullable device u64[count]: key of index first+j at [j]
+ * Errors: RK_ESTATE, RK_EINVAL, RK_ENODEVICE, RK_ECUDA. */
+rk_status rk_eval_range(rk_ctx* ctx, uint64_t first, uint64_t count, uint64_t candidate_key,
+                        rk_stats* out_host, uint64_t* keys_dev, void* stream);
+
+/* Stream-ordered variant: the candidate key is read from device memory
+ * (cand_key_dev, nullable = 0) and the record written to stats_dev (device).
+ * Only enqueues. */
+rk_status rk_eval_range_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                              rk_stats* stats_dev, uint64_t* keys_dev, void* stream);
+
+/* Deterministic merge of n_records device records (e.g. all-gathered per-rank
+ * records) into out_dev: min/max with smallest-index ties, counts summed.
+ * The result is independent of record order.  Only enqueues. */
+rk_status rk_merge_stats_async(rk_ctx* ctx, const rk_stats* in_dev, uint32_t n_records, rk_stats* out_dev,
+                               void* stream);
+
+/* Time histogram (Fig. 1): `bins` equal-width bins
+ * over [kmin, kmax]; bin = min(bins-1, floor((K-kmin)*bins/(kmax-kmin))) in
+ * exact integers; all keys in bin 0 when kmax == kmin.  hist_dev (device u64
+ * [bins]) is ACCUMULATED (+=), so shards can be summed in place.  Keys outside
+ * [kmin,kmax] are an error of the caller (counted in the nearest end bin).
+ * Stream-ordered (returns after enqueueing).  1 <= bins <= 65536. */
+rk_status rk_histogram(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
+                       uint32_t bins, uint64_t* hist_dev, void* stream);
+/* Same, with [kmin,kmax] read from a device record (range_dev->key_min/max). */
+rk_status rk_histogram_async(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, const rk_stats* range_dev,
+                             uint32_t bins, uint64_t* hist_dev, void* stream);
+
+/* Algorithm 1 (readings L2, L16-L19), on the
+ * host (sequential by nature).  order_out[n] = launch order Rd_1..Rd_r
+ * (PAPER:134); round_of_out[n] (nullable) = round of each position;
+ * index_out (nullable) = its lexicographic index; key_out (nullable) = its
+ * exact key, evaluated on the device (RK_ENODEVICE on a host-only ctx). */
+rk_status rk_heuristic_order(rk_ctx* ctx, int32_t* order_out, int32_t* round_of_out, uint64_t* index_out,
+                             uint64_t* key_out);
+
+/* Percentile support (Table 3 "Percentile rank"):
+ * key of `order` and the number of indices in [first, first+count) whose key
+ * is >= it (ties count for the candidate, reading L13).  Shard-aware: sum
+ * n_ge over shards and divide by n!.  Synchronous. */
+rk_status rk_percentile(rk_ctx* ctx, const int32_t* order, uint64_t first, uint64_t count, uint64_t* n_ge_out,
+                        uint64_t* key_out);
+
+/* Batch mode (config C5): n_sets independent kernel sets of equal size n,
+ * sets[s*n + i]; per set the full n! space is evaluated against that set's
+ * candidate.  cand_index (nullable host u64[n_sets]): candidate indices; if
+ * NULL, Algorithm 1 is run for each set on the host.  out_host[n_sets] per-set
+ * records; cand_key_out (nullable host u64[n_sets]).  Synchronous.
+ * Uses the ctx's gpu params; does not change the ctx's kernel set. */
+rk_status rk_eval_batch(rk_ctx* ctx, const rk_kernel* sets, uint32_t n, uint32_t n_sets, const uint64_t* cand_index,
+                        rk_stats* out_host, uint64_t* cand_key_out, void* stream);
+
+/* Round partition of one order (SPEC:209-219 PlacedRound), computed by the
+ * device path: rounds_out (host u32[max_rounds*n], row-major p[r][i] = blocks
+ * of kernel i placed in round r), n_rounds_out, key_out.  RK_EINVAL if the
+ * order has more than max_rounds rounds (n_rounds_out still set). */
+rk_status rk_simulate_order(rk_ctx* ctx, const int32_t* order, uint32_t* rounds_out, uint32_t max_rounds,
+                            uint32_t* n_rounds_out, uint64_t* key_out);
+
+/* Lexicographic rank/unrank (factorial number system; reading L11). Pure host
+ * helpers, no ctx.  1 <= n <= 20. RK_EINVAL on a non-permutation / idx >= n!. */
+rk_status rk_rank(const int32_t* order, uint32_t n, uint64_t* idx_out);
+rk_status rk_unrank(uint64_t idx, uint32_t n, int32_t* order_out);
+
+/* Number of kernel launches the last synchronous/async call enqueued on the
+ * device (for the bench's gpu_launches count). */
+uint32_t rk_last_launch_count(const rk_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RK_H */

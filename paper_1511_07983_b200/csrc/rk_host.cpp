@@ -1,0 +1,673 @@
+/*
+ * rk_host.cpp — host side of librk: the C ABI of include/rk.h, input
+ * validation and device-table packing, Algorithm 1 (kept on the CPU because
+ * it is sequential, BASELINE north_star), Lehmer rank/unrank, and the launch
+ * orchestration of rk_kernels.cu.  Product path; shares nothing with oracle/.
+ */
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "rk.h"
+#include "rk_internal.h"
+
+typedef unsigned __int128 u128;
+
+struct rk_ctx {
+    int device = -1;
+    std::string err;
+    bool has_params = false, has_kernels = false;
+    rk_gpu_params gp{};
+    std::vector<rk_kernel> ks;
+    RkTables tab{};
+    RkTables* tab_dev = nullptr;
+    rk_stats* recs_dev = nullptr;     /* per-CTA records of rk_eval_kernel */
+    uint32_t* counter_dev = nullptr;  /* last-CTA counter (self-resetting) */
+    rk_stats* stats_dev = nullptr;    /* one record for the synchronous calls */
+    uint64_t* u64_dev = nullptr;      /* small scratch (indices / keys) */
+    uint32_t max_ctas = 0;
+    uint32_t launches = 0;
+};
+
+namespace {
+
+rk_status fail(rk_ctx* c, rk_status s, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return s;
+}
+
+rk_status cuda_fail(rk_ctx* c, int e, const char* where) {
+    return fail(c, RK_ECUDA, "%s: %s", where, cudaGetErrorString((cudaError_t)e));
+}
+
+struct DeviceGuard { /* keep the caller's current device */
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+uint64_t fact64(uint32_t m) {
+    uint64_t f = 1;
+    for (uint32_t i = 2; i <= m; i++) f *= i;
+    return f;
+}
+
+/* ---------------- validation + device table packing ---------------------- */
+struct Derived {
+    uint64_t regs, shm, warps; /* per-block demand (O1 readings L6, L7) */
+};
+
+Derived derive(const rk_kernel& k) {
+    Derived d;
+    d.regs = (uint64_t)k.regs_per_thread * k.threads_per_block;
+    d.shm = k.shm_bytes_per_block;
+    d.warps = (k.threads_per_block + 31u) / 32u;
+    return d;
+}
+
+rk_status check_params(rk_ctx* c, const rk_gpu_params& p) {
+    if (!p.n_sm || !p.regs_per_sm || !p.shm_bytes_per_sm || !p.max_warps_per_sm || !p.max_blocks_per_sm ||
+        !p.rb_num || !p.rb_den)
+        return fail(c, RK_EINVAL, "gpu params must all be > 0 (SPEC:30-32)");
+    if (p.n_sm > RK_SMAX) return fail(c, RK_EUNSUPPORTED, "n_sm %u > %d (device fast path)", p.n_sm, RK_SMAX);
+    if (p.max_blocks_per_sm > 255) return fail(c, RK_EUNSUPPORTED, "max_blocks_per_sm > 255");
+    if (p.max_warps_per_sm > 32767) return fail(c, RK_EUNSUPPORTED, "max_warps_per_sm > 32767");
+    return RK_OK;
+}
+
+/* Builds the device tables for one kernel set; validates everything. */
+rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, uint32_t n, RkTables& t) {
+    rk_status s = check_params(c, p);
+    if (s) return s;
+    if (n == 0) return fail(c, RK_EINVAL, "need at least one kernel");
+    if (n > RK_MAX_N) return fail(c, RK_ETOOMANY, "n = %u > %d: index space exceeds u32", n, RK_MAX_N);
+    u128 bound = 0;
+    uint64_t gr = p.regs_per_sm, gs = p.shm_bytes_per_sm;
+    std::vector<Derived> d(n);
+    for (uint32_t i = 0; i < n; i++) {
+        const rk_kernel& k = ks[i];
+        if (k.grid_blocks < 1) return fail(c, RK_EINVAL, "kernel %u: grid_blocks must be >= 1 (SPEC:38)", i);
+        if (k.threads_per_block < 1 || k.threads_per_block > 1024)
+            return fail(c, RK_EINVAL, "kernel %u: threads_per_block must be in 1..1024 (SPEC:38)", i);
+        if (k.inst_per_block < 1) return fail(c, RK_EINVAL, "kernel %u: inst_per_block must be >= 1 (SPEC:39)", i);
+        if (k.mem_per_block < 1)
+            return fail(c, RK_EMISSINGRATIO, "kernel %u: mem_per_block = 0, R_i undefined (SPEC:61,71)", i);
+        d[i] = derive(k);
+        if (d[i].regs > p.regs_per_sm || d[i].shm > p.shm_bytes_per_sm || d[i].warps > p.max_warps_per_sm)
+            return fail(c, RK_EINFEASIBLE, "kernel %u: one block exceeds an SM limit (SPEC:46)", i);
+        bound += (u128)k.grid_blocks * ((u128)p.rb_den * k.inst_per_block + (u128)p.rb_num * k.mem_per_block);
+        gr = std::gcd(gr, d[i].regs);
+        gs = std::gcd(gs, d[i].shm);
+    }
+    if (bound >= ((u128)1 << 63)) return fail(c, RK_EOVERFLOW, "exact key bound >= 2^63");
+    const uint64_t R = p.regs_per_sm / gr, Sh = p.shm_bytes_per_sm / gs;
+    if (R > 32767 || Sh > 32767)
+        return fail(c, RK_EUNSUPPORTED, "scaled regs %llu / shm %llu exceed the 15-bit packing", (unsigned long long)R,
+                    (unsigned long long)Sh);
+    std::memset(&t, 0, sizeof t);
+    RkGTab& g = t.g;
+    g.S = p.n_sm;
+    g.num = p.rb_num;
+    g.den = p.rb_den;
+    g.freshA = (uint32_t)(2 * R + 1) | (uint32_t)(2 * Sh + 1) << 16;
+    g.freshB = (uint32_t)(2 * p.max_warps_per_sm + 1) | (uint32_t)(2 * p.max_blocks_per_sm + 1) << 16;
+    g.smagic = (uint32_t)(((1ull << 32) + p.n_sm - 1) / p.n_sm);
+    uint32_t tb = 1;
+    while (tb * 2 <= p.max_blocks_per_sm) tb *= 2;
+    g.tbits = tb;
+    g.n = n;
+    for (uint32_t i = 0; i <= RK_MAX_N; i++) g.fact[i] = (uint32_t)fact64(i);
+    const uint64_t caps[3] = {R, Sh, p.max_warps_per_sm};
+    for (uint32_t i = 0; i < n; i++) {
+        const uint64_t dem[3] = {d[i].regs / gr, d[i].shm / gs, d[i].warps};
+        uint32_t mag[3], add[3];
+        uint64_t C = p.max_blocks_per_sm;
+        for (int r = 0; r < 3; r++) {
+            if (dem[r] == 0) {
+                mag[r] = 0;
+                add[r] = 0xFFFFu;
+                continue;
+            }
+            C = std::min<uint64_t>(C, caps[r] / dem[r]);
+            const uint64_t D = 2 * dem[r];
+            const uint64_t m = ((1ull << 32) + D - 1) / D; /* ceil(2^32 / 2d) <= 2^31 */
+            /* exhaustive exactness check of floor((2x+1)*m / 2^32) == floor(x/d) */
+            for (uint64_t x = 0; x <= caps[r]; x++)
+                if ((((2 * x + 1) * m) >> 32) != x / dem[r])
+                    return fail(c, RK_EUNSUPPORTED, "kernel %u: no exact 32-bit magic for demand %llu", i,
+                                (unsigned long long)dem[r]);
+            mag[r] = (uint32_t)m;
+            add[r] = 0;
+        }
+        RkKTab& k = t.k[i];
+        k.T = ks[i].grid_blocks;
+        k.mr = mag[0];
+        k.ms = mag[1];
+        k.mw = mag[2];
+        k.zr = add[0];
+        k.zs = add[1];
+        k.zw = add[2];
+        k.dA = (uint32_t)(2 * dem[0]) | (uint32_t)(2 * dem[1]) << 16;
+        k.dB = (uint32_t)(2 * dem[2]) | 2u << 16;
+        k.A = ks[i].inst_per_block;
+        k.M = ks[i].mem_per_block;
+        k.C = (uint32_t)C;
+        k.SC = (uint32_t)(C * p.n_sm);
+        const u128 ci = (u128)k.SC * k.A * p.rb_den, cm = (u128)k.SC * k.M * p.rb_num;
+        const u128 fk = ci >= cm ? ci : cm;
+        k.fullkey = fk >> 64 ? ~0ull : (uint64_t)fk; /* only used when T > SC, then bounded */
+    }
+    return RK_OK;
+}
+
+/* ------------------------- Algorithm 1 (host) ---------------------------- */
+/* PAPER:110-198 with the readings of DESIGN.md §3 (L2 footprints, L16 ties /
+ * infeasible / no-pair / odd n, L17 insertion, L18 inclusive straddle, L19).
+ * Double arithmetic in the fixed order: shm, regs, warps slack, then bonus. */
+struct Prof {
+    uint64_t shm, regs, warps, blocks; /* per-SM footprint (reading L2) */
+    double inst, ratio;
+};
+
+struct Alg1 {
+    const rk_gpu_params& p;
+    double RB;
+    explicit Alg1(const rk_gpu_params& gp) : p(gp), RB((double)gp.rb_num / (double)gp.rb_den) {}
+
+    Prof footprint(const rk_kernel& k) const {
+        const uint64_t per_sm = (k.grid_blocks + p.n_sm - 1) / p.n_sm; /* ceil(N_tblk/N_SM) */
+        const Derived d = derive(k);
+        Prof f;
+        f.shm = d.shm * per_sm;
+        f.regs = d.regs * per_sm;
+        f.warps = d.warps * per_sm;
+        f.blocks = per_sm;
+        f.inst = (double)k.grid_blocks * (double)k.inst_per_block;   /* N_inst_i */
+        f.ratio = (double)k.inst_per_block / (double)k.mem_per_block; /* R_i */
+        return f;
+    }
+    static Prof combine(const Prof& a, const Prof& b) { /* ProfileCombine */
+        Prof c;
+        c.shm = a.shm + b.shm;
+        c.regs = a.regs + b.regs;
+        c.warps = a.warps + b.warps;
+        c.blocks = a.blocks + b.blocks;
+        c.inst = a.inst + b.inst;
+        c.ratio = (a.inst + b.inst) / (a.inst / a.ratio + b.inst / b.ratio);
+        return c;
+    }
+    bool fits(const Prof& a, const Prof& b) const { /* PAPER:141 + slots */
+        return a.shm + b.shm <= p.shm_bytes_per_sm && a.regs + b.regs <= p.regs_per_sm &&
+               a.warps + b.warps <= p.max_warps_per_sm && a.blocks + b.blocks <= p.max_blocks_per_sm;
+    }
+    static double slack(uint64_t cap, uint64_t x, uint64_t y) {
+        const double v = (double)((int64_t)cap - (int64_t)x - (int64_t)y) / (double)cap;
+        return v > 0.0 ? v : 0.0;
+    }
+    double score(const Prof& a, const Prof& b) const { /* ScoreGen body */
+        double s = 0.0;
+        s += slack(p.shm_bytes_per_sm, a.shm, b.shm);
+        s += slack(p.regs_per_sm, a.regs, b.regs);
+        s += slack(p.max_warps_per_sm, a.warps, b.warps);
+        const bool straddle = (a.ratio <= RB && RB <= b.ratio) || (b.ratio <= RB && RB <= a.ratio);
+        if (straddle) {
+            const double rc = (a.inst + b.inst) / (a.inst / a.ratio + b.inst / b.ratio);
+            const double bonus = 1.0 - std::fabs(rc - RB) / RB;
+            s += bonus > 0.0 ? bonus : 0.0;
+        }
+        return s;
+    }
+
+    void run(const rk_kernel* ks, uint32_t n, int32_t* order, int32_t* round_of) const {
+        std::vector<Prof> f(n);
+        for (uint32_t i = 0; i < n; i++) f[i] = footprint(ks[i]);
+        std::vector<char> used(n, 0);
+        uint32_t left = n, pos = 0;
+        int32_t r = 0;
+        auto emit = [&](const std::vector<uint32_t>& rd) {
+            for (uint32_t x : rd) {
+                order[pos] = (int32_t)x;
+                if (round_of) round_of[pos] = r;
+                pos++;
+                used[x] = 1;
+                left--;
+            }
+            r++;
+        };
+        while (left > 0) {
+            if (left == 1) { /* lone kernel: singleton round */
+                for (uint32_t i = 0; i < n; i++)
+                    if (!used[i]) emit({i});
+                break;
+            }
+            int ba = -1, bb = -1;
+            double bs = 0.0;
+            for (uint32_t a = 0; a < n; a++) {
+                if (used[a]) continue;
+                for (uint32_t b = a + 1; b < n; b++) {
+                    if (used[b] || !fits(f[a], f[b])) continue;
+                    const double sc = score(f[a], f[b]);
+                    if (ba < 0 || sc > bs) {
+                        ba = (int)a;
+                        bb = (int)b;
+                        bs = sc;
+                    }
+                }
+            }
+            if (ba < 0) { /* no feasible pair: singletons by decreasing shm, index order on ties */
+                std::vector<uint32_t> rest;
+                for (uint32_t i = 0; i < n; i++)
+                    if (!used[i]) rest.push_back(i);
+                std::stable_sort(rest.begin(), rest.end(),
+                                 [&](uint32_t x, uint32_t y) { return f[x].shm > f[y].shm; });
+                for (uint32_t x : rest) emit({x});
+                break;
+            }
+            std::vector<uint32_t> rd;
+            if (f[bb].shm > f[ba].shm) rd = {(uint32_t)bb, (uint32_t)ba};
+            else rd = {(uint32_t)ba, (uint32_t)bb};
+            used[ba] = used[bb] = 1; /* removed from K */
+            Prof comb = combine(f[ba], f[bb]);
+            for (;;) {
+                int bc = -1;
+                double cs = 0.0;
+                for (uint32_t x = 0; x < n; x++) {
+                    if (used[x] || !fits(comb, f[x])) continue;
+                    const double sc = score(comb, f[x]);
+                    if (bc < 0 || sc > cs) {
+                        bc = (int)x;
+                        cs = sc;
+                    }
+                }
+                if (bc < 0) break;
+                auto it = rd.begin();
+                while (it != rd.end() && f[*it].shm >= f[bc].shm) ++it; /* stable decreasing shm */
+                rd.insert(it, (uint32_t)bc);
+                comb = combine(comb, f[bc]);
+                used[bc] = 1;
+            }
+            for (uint32_t x : rd) used[x] = 0; /* emit() re-marks and counts them */
+            emit(rd);
+        }
+    }
+};
+
+/* ----------------------- rank / unrank (Lehmer) --------------------------- */
+rk_status do_rank(const int32_t* order, uint32_t n, uint64_t* idx) {
+    if (n < 1 || n > 20) return RK_EINVAL;
+    uint32_t seen = 0;
+    uint64_t v = 0;
+    for (uint32_t j = 0; j < n; j++) {
+        const int32_t x = order[j];
+        if (x < 0 || (uint32_t)x >= n || (seen >> x & 1u)) return RK_EINVAL;
+        /* digit = number of unused values smaller than x */
+        const uint32_t smaller_unused = (uint32_t)__builtin_popcount(~seen & ((1u << x) - 1u));
+        v = v * (n - j) + smaller_unused;
+        seen |= 1u << x;
+    }
+    *idx = v;
+    return RK_OK;
+}
+
+rk_status do_unrank(uint64_t idx, uint32_t n, int32_t* out) {
+    if (n < 1 || n > 20 || idx >= fact64(n)) return RK_EINVAL;
+    uint32_t digits[20];
+    for (uint32_t j = n; j-- > 0;) { /* factorial base, least significant first */
+        const uint32_t base = n - j;
+        digits[j] = (uint32_t)(idx % base);
+        idx /= base;
+    }
+    uint32_t unused = (n == 32) ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    for (uint32_t j = 0; j < n; j++) {
+        uint32_t m = unused;
+        for (uint32_t q = 0; q < digits[j]; q++) m &= m - 1; /* drop the lowest set bits */
+        const uint32_t x = (uint32_t)__builtin_ctz(m);
+        out[j] = (int32_t)x;
+        unused &= ~(1u << x);
+    }
+    return RK_OK;
+}
+
+rk_status need_device(rk_ctx* c) {
+    if (!c) return RK_EINVAL;
+    if (c->device < 0) return fail(c, RK_ENODEVICE, "host-only context: no device evaluation (no CPU fallback)");
+    return RK_OK;
+}
+
+rk_status need_kernels(rk_ctx* c) {
+    if (!c->has_params || !c->has_kernels) return fail(c, RK_ESTATE, "call rk_set_gpu_params and rk_set_kernels first");
+    return RK_OK;
+}
+
+uint64_t space(const rk_ctx* c) { return fact64((uint32_t)c->ks.size()); }
+
+}  // namespace
+
+/* ================================ C ABI ================================== */
+extern "C" {
+
+rk_status rk_create(rk_ctx** out, int cuda_device) {
+    if (!out) return RK_EINVAL;
+    rk_ctx* c = new rk_ctx();
+    c->device = cuda_device;
+    if (cuda_device >= 0) {
+        int ndev = 0;
+        cudaError_t e = cudaGetDeviceCount(&ndev);
+        if (e != cudaSuccess || cuda_device >= ndev) {
+            delete c;
+            return RK_ENODEVICE;
+        }
+        DeviceGuard dg(cuda_device);
+        c->max_ctas = (uint32_t)rk_eval_max_ctas(RK_SMAX, cuda_device);
+        if (c->max_ctas < 256) c->max_ctas = 256;
+        bool ok = cudaMalloc(&c->tab_dev, sizeof(RkTables)) == cudaSuccess &&
+                  cudaMalloc(&c->recs_dev, sizeof(rk_stats) * c->max_ctas * 2) == cudaSuccess &&
+                  cudaMalloc(&c->counter_dev, sizeof(uint32_t)) == cudaSuccess &&
+                  cudaMalloc(&c->stats_dev, sizeof(rk_stats)) == cudaSuccess &&
+                  cudaMalloc(&c->u64_dev, sizeof(uint64_t) * 64) == cudaSuccess &&
+                  cudaMemset(c->counter_dev, 0, sizeof(uint32_t)) == cudaSuccess &&
+                  cudaDeviceSynchronize() == cudaSuccess;
+        if (!ok) {
+            rk_destroy(c);
+            return RK_ECUDA;
+        }
+    }
+    *out = c;
+    return RK_OK;
+}
+
+void rk_destroy(rk_ctx* c) {
+    if (!c) return;
+    if (c->device >= 0) {
+        DeviceGuard dg(c->device);
+        cudaFree(c->tab_dev);
+        cudaFree(c->recs_dev);
+        cudaFree(c->counter_dev);
+        cudaFree(c->stats_dev);
+        cudaFree(c->u64_dev);
+    }
+    delete c;
+}
+
+const char* rk_last_error(const rk_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+uint32_t rk_last_launch_count(const rk_ctx* c) { return c ? c->launches : 0; }
+
+rk_status rk_set_gpu_params(rk_ctx* c, const rk_gpu_params* p) {
+    if (!c || !p) return RK_EINVAL;
+    rk_status s = check_params(c, *p);
+    if (s) return s;
+    c->gp = *p;
+    c->has_params = true;
+    c->has_kernels = false;
+    return RK_OK;
+}
+
+rk_status rk_set_kernels(rk_ctx* c, const rk_kernel* k, uint32_t n) {
+    if (!c || (!k && n)) return RK_EINVAL;
+    if (!c->has_params) return fail(c, RK_ESTATE, "rk_set_gpu_params first");
+    RkTables t;
+    rk_status s = build_tables(c, c->gp, k, n, t);
+    if (s) return s;
+    if (c->device >= 0) {
+        DeviceGuard dg(c->device);
+        cudaError_t e = cudaMemcpy(c->tab_dev, &t, sizeof t, cudaMemcpyHostToDevice);
+        if (e) return cuda_fail(c, e, "upload tables");
+    }
+    c->tab = t;
+    c->ks.assign(k, k + n);
+    c->has_kernels = true;
+    return RK_OK;
+}
+
+rk_status rk_eval_range_async(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                              rk_stats* stats_dev, uint64_t* keys_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!stats_dev) return fail(c, RK_EINVAL, "stats_dev is required");
+    if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, cand_key_dev, 0, stats_dev, keys_dev,
+                           c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
+    return e ? cuda_fail(c, e, "rk_eval_kernel launch") : RK_OK;
+}
+
+rk_status rk_eval_range(rk_ctx* c, uint64_t first, uint64_t count, uint64_t candidate_key, rk_stats* out_host,
+                        uint64_t* keys_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!out_host) return fail(c, RK_EINVAL, "out_host is required");
+    if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (count == 0) {
+        std::memset(out_host, 0, sizeof *out_host);
+        return RK_OK;
+    }
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, nullptr, candidate_key, c->stats_dev,
+                           keys_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
+    if (e) return cuda_fail(c, e, "rk_eval_kernel launch");
+    rk_stats h;
+    e = cudaMemcpyAsync(&h, c->stats_dev, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    if (e) return cuda_fail(c, e, "rk_eval_range");
+    *out_host = h;
+    return RK_OK;
+}
+
+rk_status rk_merge_stats_async(rk_ctx* c, const rk_stats* in_dev, uint32_t n_records, rk_stats* out_dev,
+                               void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (!in_dev || !out_dev || n_records == 0) return fail(c, RK_EINVAL, "bad merge arguments");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    int e = rk_launch_merge(in_dev, n_records, out_dev, stream, &c->launches);
+    return e ? cuda_fail(c, e, "merge launch") : RK_OK;
+}
+
+static rk_status hist_common(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
+                             const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (bins < 1 || bins > 65536 || !hist_dev || (count && !keys_dev)) return fail(c, RK_EINVAL, "bad histogram args");
+    if (!range_dev && kmax < kmin) return fail(c, RK_EINVAL, "kmax < kmin");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    if (count == 0) return RK_OK;
+    int e = rk_launch_histogram(keys_dev, count, kmin, kmax, range_dev, bins, hist_dev, stream, &c->launches);
+    return e ? cuda_fail(c, e, "histogram launch") : RK_OK;
+}
+
+rk_status rk_histogram(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
+                       uint32_t bins, uint64_t* hist_dev, void* stream) {
+    return hist_common(c, keys_dev, count, kmin, kmax, nullptr, bins, hist_dev, stream);
+}
+
+rk_status rk_histogram_async(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, const rk_stats* range_dev,
+                             uint32_t bins, uint64_t* hist_dev, void* stream) {
+    if (!range_dev) return fail(c, RK_EINVAL, "range_dev is required");
+    return hist_common(c, keys_dev, count, 0, 0, range_dev, bins, hist_dev, stream);
+}
+
+/* key of one index on the device (synchronous) */
+static rk_status key_of_index(rk_ctx* c, uint64_t idx, uint64_t* key, void* stream) {
+    DeviceGuard dg(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    int e = cudaMemcpyAsync(c->u64_dev, &idx, sizeof idx, cudaMemcpyHostToDevice, st);
+    if (!e) e = rk_launch_keys_of_same(c->tab_dev, c->tab.g.S, c->u64_dev, 1, c->u64_dev + 1, stream, &c->launches);
+    uint64_t h = 0;
+    if (!e) e = cudaMemcpyAsync(&h, c->u64_dev + 1, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    if (e) return cuda_fail(c, e, "key_of_index");
+    *key = h;
+    return RK_OK;
+}
+
+rk_status rk_heuristic_order(rk_ctx* c, int32_t* order_out, int32_t* round_of_out, uint64_t* index_out,
+                             uint64_t* key_out) {
+    if (!c || !order_out) return RK_EINVAL;
+    rk_status s = need_kernels(c);
+    if (s) return s;
+    if (key_out && (s = need_device(c))) return s;
+    const uint32_t n = (uint32_t)c->ks.size();
+    std::vector<int32_t> order(n), rounds(n);
+    Alg1(c->gp).run(c->ks.data(), n, order.data(), rounds.data());
+    uint64_t idx = 0;
+    do_rank(order.data(), n, &idx);
+    c->launches = 0;
+    if (key_out) {
+        uint64_t k = 0;
+        if ((s = key_of_index(c, idx, &k, nullptr))) return s;
+        *key_out = k;
+    }
+    std::memcpy(order_out, order.data(), n * sizeof(int32_t));
+    if (round_of_out) std::memcpy(round_of_out, rounds.data(), n * sizeof(int32_t));
+    if (index_out) *index_out = idx;
+    return RK_OK;
+}
+
+rk_status rk_percentile(rk_ctx* c, const int32_t* order, uint64_t first, uint64_t count, uint64_t* n_ge_out,
+                        uint64_t* key_out) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!order || !n_ge_out) return fail(c, RK_EINVAL, "null argument");
+    uint64_t idx;
+    if (do_rank(order, (uint32_t)c->ks.size(), &idx)) return fail(c, RK_EINVAL, "order is not a permutation");
+    uint64_t key;
+    if ((s = key_of_index(c, idx, &key, nullptr))) return s;
+    uint32_t l0 = c->launches;
+    rk_stats st;
+    if ((s = rk_eval_range(c, first, count, key, &st, nullptr, nullptr))) return s;
+    c->launches += l0;
+    *n_ge_out = st.n_eq + st.n_gt;
+    if (key_out) *key_out = key;
+    return RK_OK;
+}
+
+rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n_sets, const uint64_t* cand_index,
+                        rk_stats* out_host, uint64_t* cand_key_out, void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (!c->has_params) return fail(c, RK_ESTATE, "rk_set_gpu_params first");
+    if (!sets || !out_host || n_sets == 0) return fail(c, RK_EINVAL, "bad batch arguments");
+    std::vector<RkTables> tabs(n_sets);
+    std::vector<uint64_t> idx(n_sets);
+    std::vector<int32_t> order(n);
+    for (uint32_t q = 0; q < n_sets; q++) {
+        if ((s = build_tables(c, c->gp, sets + (size_t)q * n, n, tabs[q]))) {
+            c->err = "set " + std::to_string(q) + ": " + c->err;
+            return s;
+        }
+        if (cand_index) {
+            if (cand_index[q] >= fact64(n)) return fail(c, RK_EINVAL, "set %u: candidate index >= n!", q);
+            idx[q] = cand_index[q];
+        } else {
+            Alg1(c->gp).run(sets + (size_t)q * n, n, order.data(), nullptr);
+            do_rank(order.data(), n, &idx[q]);
+        }
+    }
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t chunks = (uint32_t)rk_batch_chunks_per_set(n);
+    RkTables* tabs_dev = nullptr;
+    uint64_t *idx_dev = nullptr, *keys_dev = nullptr;
+    rk_stats *recs = nullptr, *out_dev = nullptr;
+    int e = cudaMalloc(&tabs_dev, sizeof(RkTables) * n_sets);
+    if (!e) e = cudaMalloc(&idx_dev, sizeof(uint64_t) * n_sets);
+    if (!e) e = cudaMalloc(&keys_dev, sizeof(uint64_t) * n_sets);
+    if (!e) e = cudaMalloc(&recs, sizeof(rk_stats) * (size_t)n_sets * chunks);
+    if (!e) e = cudaMalloc(&out_dev, sizeof(rk_stats) * n_sets);
+    if (!e) e = cudaMemcpyAsync(tabs_dev, tabs.data(), sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemcpyAsync(idx_dev, idx.data(), sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = rk_launch_keys_of(tabs_dev, n, c->gp.n_sm, idx_dev, n_sets, keys_dev, stream, &c->launches);
+    if (!e) e = rk_launch_batch(tabs_dev, n, c->gp.n_sm, n_sets, keys_dev, out_dev, recs, chunks, stream, &c->launches);
+    std::vector<uint64_t> keys(n_sets);
+    if (!e) e = cudaMemcpyAsync(out_host, out_dev, sizeof(rk_stats) * n_sets, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaMemcpyAsync(keys.data(), keys_dev, sizeof(uint64_t) * n_sets, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    cudaFree(tabs_dev);
+    cudaFree(idx_dev);
+    cudaFree(keys_dev);
+    cudaFree(recs);
+    cudaFree(out_dev);
+    if (e) return cuda_fail(c, e, "rk_eval_batch");
+    if (cand_key_out) std::memcpy(cand_key_out, keys.data(), sizeof(uint64_t) * n_sets);
+    return RK_OK;
+}
+
+rk_status rk_simulate_order(rk_ctx* c, const int32_t* order, uint32_t* rounds_out, uint32_t max_rounds,
+                            uint32_t* n_rounds_out, uint64_t* key_out) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    const uint32_t n = (uint32_t)c->ks.size();
+    uint64_t idx;
+    if (!order || do_rank(order, n, &idx)) return fail(c, RK_EINVAL, "order is not a permutation");
+    if (max_rounds == 0 || !rounds_out) return fail(c, RK_EINVAL, "rounds_out / max_rounds");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    int32_t* order_dev = nullptr;
+    uint32_t* rounds_dev = nullptr;
+    uint32_t* nr_dev = nullptr;
+    uint64_t* key_dev = nullptr;
+    int e = cudaMalloc(&order_dev, n * sizeof(int32_t));
+    if (!e) e = cudaMalloc(&rounds_dev, (size_t)max_rounds * n * sizeof(uint32_t));
+    if (!e) e = cudaMalloc(&nr_dev, sizeof(uint32_t));
+    if (!e) e = cudaMalloc(&key_dev, sizeof(uint64_t));
+    if (!e) e = cudaMemcpy(order_dev, order, n * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (!e) e = rk_launch_simulate(c->tab_dev, n, c->tab.g.S, order_dev, rounds_dev, max_rounds, nr_dev, key_dev,
+                                   nullptr, &c->launches);
+    uint32_t nr = 0;
+    uint64_t key = 0;
+    std::vector<uint32_t> rounds((size_t)max_rounds * n);
+    if (!e) e = cudaMemcpy(rounds.data(), rounds_dev, rounds.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    if (!e) e = cudaMemcpy(&nr, nr_dev, sizeof nr, cudaMemcpyDeviceToHost);
+    if (!e) e = cudaMemcpy(&key, key_dev, sizeof key, cudaMemcpyDeviceToHost);
+    cudaFree(order_dev);
+    cudaFree(rounds_dev);
+    cudaFree(nr_dev);
+    cudaFree(key_dev);
+    if (e) return cuda_fail(c, e, "rk_simulate_order");
+    std::memcpy(rounds_out, rounds.data(), rounds.size() * sizeof(uint32_t));
+    if (n_rounds_out) *n_rounds_out = nr;
+    if (key_out) *key_out = key;
+    if (nr > max_rounds) return fail(c, RK_EINVAL, "order has %u rounds > max_rounds %u", nr, max_rounds);
+    return RK_OK;
+}
+
+rk_status rk_rank(const int32_t* order, uint32_t n, uint64_t* idx_out) {
+    if (!order || !idx_out) return RK_EINVAL;
+    return do_rank(order, n, idx_out);
+}
+
+rk_status rk_unrank(uint64_t idx, uint32_t n, int32_t* order_out) {
+    if (!order_out) return RK_EINVAL;
+    return do_unrank(idx, n, order_out);
+}
+
+} /* extern "C" */

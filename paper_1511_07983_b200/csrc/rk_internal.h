@@ -1,0 +1,74 @@
+/* rk_internal.h — tables and launchers shared by rk_host.cpp and rk_kernels.cu
+ * (product path only; the oracle never includes this).
+ *
+ * Device state layout: each SM's free resources are packed in
+ * two u32 words, every field stored as 2*x+1 (odd encoding) so that
+ * floor(x/d) = floor((2x+1)/(2d)) is one IMAD.HI with a host-verified magic:
+ *   fa = (2*regs+1)  | (2*shm+1)   << 16
+ *   fb = (2*warps+1) | (2*slots+1) << 16
+ * A block of kernel k subtracts dA = 2*dr | 2*ds << 16 and dB = 2*dw | 2 << 16.
+ * Register and shared-memory quantities are divided by their gcd over the GPU
+ * capacity and all kernel demands first (exact: fit tests are scale-free).
+ */
+#ifndef RK_INTERNAL_H
+#define RK_INTERNAL_H
+
+#include <stdint.h>
+#include "rk.h"
+
+#define RK_MAX_N 12
+#define RK_SMAX 32
+
+struct RkKTab {        /* one kernel; 64 B */
+    uint32_t T;        /* N_tblk */
+    uint32_t mr, ms, mw;   /* magic multipliers for floor((2x+1)/(2d)); 0 if d == 0 */
+    uint32_t zr, zs, zw;   /* addends: 0, or 0xFF (>= any cap) if d == 0 */
+    uint32_t dA, dB;       /* per-block decrement of fa / fb */
+    uint32_t A, M;         /* inst / mem units per block */
+    uint32_t C;            /* blocks per fresh SM */
+    uint32_t SC;           /* S * C: blocks per full single-kernel round */
+    uint32_t pad;
+    uint64_t fullkey;      /* max(den*SC*A, num*SC*M): key of one full round */
+};
+
+struct RkGTab {
+    uint32_t S;            /* N_SM */
+    uint32_t num, den;     /* R_B = num / den */
+    uint32_t freshA, freshB;   /* packed words of a fresh SM */
+    uint32_t smagic;       /* ceil(2^32 / S) */
+    uint32_t tbits;        /* highest power of two <= max_blocks_per_sm (binary search) */
+    uint32_t n;            /* number of kernels */
+    uint32_t fact[RK_MAX_N + 1];
+};
+
+struct RkTables {
+    RkGTab g;
+    RkKTab k[RK_MAX_N];
+};
+
+/* ---- launchers (rk_kernels.cu); return cudaError_t as int -------------- */
+int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t first, uint64_t count,
+                   const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
+                   rk_stats* scratch_recs, uint32_t* scratch_counter, uint32_t max_ctas, void* stream,
+                   uint32_t* launches);
+int rk_launch_merge(const rk_stats* in_dev, uint32_t n_records, rk_stats* out_dev, void* stream, uint32_t* launches);
+int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
+                        const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream,
+                        uint32_t* launches);
+/* keys of explicit indices (1 thread each): out_dev[i] = key(idx_dev[i]) of set (set_dev ? set_dev[i] : 0) */
+int rk_launch_keys_of(const RkTables* tabs_dev, uint32_t n, uint32_t S, const uint64_t* idx_dev,
+                      uint32_t m, uint64_t* out_dev, void* stream, uint32_t* launches);
+int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* idx_dev, uint32_t m,
+                           uint64_t* out_dev, void* stream, uint32_t* launches);
+/* one order -> rounds partition (1 thread) */
+int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const int32_t* order_dev,
+                       uint32_t* rounds_dev, uint32_t max_rounds, uint32_t* n_rounds_dev, uint64_t* key_dev,
+                       void* stream, uint32_t* launches);
+/* batch: tabs_dev[n_sets]; per-set candidate keys (device); per-set records out */
+int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n_sets, const uint64_t* cand_keys_dev,
+                    rk_stats* out_dev, rk_stats* scratch_recs, uint32_t chunks_per_set, void* stream,
+                    uint32_t* launches);
+int rk_batch_chunks_per_set(uint32_t n);
+int rk_eval_max_ctas(uint32_t S, int device);
+
+#endif

@@ -1,0 +1,51 @@
+"""Multi-GPU partitioning of the permutation index space.
+
+One process per GPU (torchrun), ``torch.distributed`` with NCCL over NVLink 5 /
+NVSwitch for the two real exchange steps of the path:
+
+1. ``all_gather_into_tensor`` of one 56-byte ``rk_stats`` record per rank, then
+   the deterministic device merge (``rk_merge_stats_async``) — every rank gets
+   the global min/argmin, max/argmax and candidate counts.  Equal-width bins
+   over [best, worst] need these extremes before any key is binned.
+2. ``all_reduce(SUM)`` of the per-rank u64 histograms (integer adds: order-free,
+   so bit-exact).
+
+Everything else is local: rank g evaluates the contiguous index shard
+[g*N/G, (g+1)*N/G) with its own kernels and keeps its keys in its own HBM.
+The collective helpers are device-agnostic so the same code runs over gloo on
+CPU tensors in tests.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+REC_WORDS = 7  # rk_stats = 56 bytes = 7 x int64
+
+
+def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced shard of [0, total): (first, count)."""
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return lo, hi - lo
+
+
+def all_gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
+    """rec: int64[7] (one rk_stats) -> int64[world, 7] on every rank."""
+    world = dist.get_world_size(group)
+    out = torch.empty((world, REC_WORDS), dtype=torch.int64, device=rec.device)
+    dist.all_gather_into_tensor(out, rec.view(1, REC_WORDS), group=group)
+    return out
+
+
+def all_reduce_hist(hist: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum u64 (stored as int64) histograms over ranks, in place."""
+    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
+    return hist
+
+
+def max_over_ranks(x: float, device, group=None) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

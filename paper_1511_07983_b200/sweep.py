@@ -1,0 +1,130 @@
+"""Public API: evaluate the whole launch-order space of a kernel set.
+
+``Sweeper(gpu).run(kernels)`` is the call a user makes: host kernel profiles
+in, a Table-3-style report out (PAPER:236 columns; Fig. 1 histogram).  Every
+step runs in librk's sm_100a kernels; across ranks the index space is sharded
+(dist.py).  ``Sweeper.step_device`` is the same path with inputs resident and
+no host synchronisation, as timed by bench.py.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import rk
+from .dist import REC_WORDS, all_gather_records, all_reduce_hist, shard_bounds
+
+
+@dataclass
+class Report:
+    """SweepReport in exact keys (T = key / rb_den)."""
+    n_orders: int
+    best_key: int
+    best_index: int
+    worst_key: int
+    worst_index: int
+    cand_order: list
+    cand_index: int
+    cand_key: int
+    n_lt: int
+    n_eq: int
+    n_gt: int
+    hist: list
+    rb_den: int
+
+    @property
+    def percentile(self) -> float:  # ties count for the candidate
+        return 100.0 * (self.n_eq + self.n_gt) / self.n_orders
+
+    @property
+    def speedup_over_worst(self) -> float:  # Table 3: worst / algorithm
+        return self.worst_key / self.cand_key
+
+    @property
+    def deviation_pct(self) -> float:  # Table 3: (algorithm - optimal) / optimal
+        return 100.0 * (self.cand_key - self.best_key) / self.best_key
+
+    def time(self, key: int) -> float:
+        return key / self.rb_den
+
+
+class Sweeper:
+    def __init__(self, gpu, device: int | None = None, bins: int = 256, group=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("Sweeper needs a CUDA device (no CPU fallback)")
+        self.group = group
+        self.distributed = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if self.distributed else 1
+        self.rank = dist.get_rank(group) if self.distributed else 0
+        self.device = torch.cuda.current_device() if device is None else device
+        self.dev = torch.device("cuda", self.device)
+        self.ctx = rk.Context(self.device)
+        self.gpu = tuple(int(x) for x in gpu)
+        self.ctx.rk_set_gpu_params(self.gpu)
+        self.bins = bins
+        self.n = 0
+        self.keys = None
+        self.rec = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
+        self.glob = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
+        self.cand = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.hist = torch.zeros(bins, dtype=torch.int64, device=self.dev)
+        self.launches = 0
+
+    def set_kernels(self, kernels):
+        self.ctx.rk_set_kernels(kernels)
+        self.n = len(kernels)
+        self.total = math.factorial(self.n)
+        self.first, self.count = shard_bounds(self.total, self.world, self.rank)
+        if self.keys is None or self.keys.numel() < self.count:
+            self.keys = torch.empty(max(1, self.count), dtype=torch.int64, device=self.dev)
+
+    def step_device(self, cand_index: int, stream=None):
+        """Enqueue one pass of the hot path; no host sync.  Returns #our launches."""
+        c = self.ctx
+        L = 0
+        c.rk_eval_index_async(cand_index, self.cand, stream)                                  # a5 candidate key
+        L += c.launches
+        c.rk_eval_range_async(self.first, self.count, self.cand, self.rec, self.keys, stream)  # a1-a4
+        L += c.launches
+        if self.world > 1:                                                                      # a6 combine
+            recs = all_gather_records(self.rec, self.group)
+            c.rk_merge_stats_async(recs, self.world, self.glob, stream)
+            L += c.launches
+            rng = self.glob
+        else:
+            rng = self.rec
+        self.hist.zero_()
+        c.rk_histogram_async(self.keys, self.count, rng, self.bins, self.hist, stream)          # a4 histogram
+        L += c.launches
+        if self.world > 1:
+            all_reduce_hist(self.hist, self.group)
+        self.launches = L
+        return L
+
+    def heuristic(self):
+        order, _, idx, _ = self.ctx.rk_heuristic_order(with_key=False)  # Algorithm 1 on the host
+        return order, idx
+
+    def run(self, kernels) -> Report:
+        """End to end: host profiles in (H2D), report out (D2H)."""
+        self.set_kernels(kernels)
+        order, idx = self.heuristic()
+        self.step_device(idx)
+        out = torch.cat([(self.glob if self.world > 1 else self.rec), self.cand, self.hist]).cpu()
+        st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(out[:REC_WORDS].numpy().tobytes()))
+        return Report(n_orders=self.total, best_key=st.key_min, best_index=st.argmin, worst_key=st.key_max,
+                      worst_index=st.argmax, cand_order=order, cand_index=idx,
+                      cand_key=int(out[REC_WORDS].item()) & ((1 << 64) - 1), n_lt=st.n_lt, n_eq=st.n_eq,
+                      n_gt=st.n_gt, hist=[int(x) for x in out[REC_WORDS + 1:].tolist()], rb_den=self.gpu[6])
+
+    @property
+    def h2d_bytes(self) -> int:
+        """Bytes the host sends per run(): the packed kernel tables + params."""
+        return rk.TABLE_BYTES
+
+    @property
+    def d2h_bytes(self) -> int:
+        return 8 * (REC_WORDS + 1 + self.bins)

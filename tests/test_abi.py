@@ -1,0 +1,159 @@
+"""C-ABI library: loads, exports every symbol include/rk.h declares, and its
+host-side logic (validation, Lehmer rank/unrank, Algorithm 1) agrees with the
+independent oracle.  No device compute here (runs on CPU)."""
+import ctypes
+import itertools
+import os
+import re
+
+import pytest
+
+import oracle as O
+from paper_1511_07983_b200 import build as B
+from paper_1511_07983_b200 import rk
+from paper_1511_07983_b200 import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    B.build()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "rk.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rk_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declarations_match_binding_exports():
+    assert declared_symbols() == sorted(rk.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = ctypes.CDLL(rk.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+
+
+def test_sm100a_cubin_embedded():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", rk.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_rank_unrank_match_library_enumeration():
+    for n in range(1, 8):
+        for idx, p in enumerate(itertools.permutations(range(n))):
+            assert rk.rk_unrank(idx, n) == list(p)
+            assert rk.rk_rank(list(p)) == idx
+    for idx in (0, 1, 12345678, 479001599):
+        assert rk.rk_unrank(idx, 12) == O.unrank(idx, 12)
+    with pytest.raises(rk.RkError):
+        rk.rk_rank([0, 0, 1])
+    with pytest.raises(rk.RkError):
+        rk.rk_unrank(24, 4)
+
+
+def test_host_only_ctx_refuses_compute():
+    c = rk.Context(-1)
+    c.rk_set_gpu_params(W.GTX580)
+    c.rk_set_kernels(W.W4)
+    with pytest.raises(rk.RkError) as e:
+        c.rk_eval_range(0, 24)
+    assert e.value.status == rk.RK_ENODEVICE
+    with pytest.raises(rk.RkError) as e:
+        c.rk_heuristic_order(with_key=True)
+    assert e.value.status == rk.RK_ENODEVICE
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(rk.RkError) as e:
+        rk.Context(0)
+    assert e.value.status == rk.RK_ENODEVICE
+
+
+CASES = [
+    ([(16, 0, 1, 0, 1, 1)], O.OR_EINVAL),
+    ([(16, 1025, 1, 0, 1, 1)], O.OR_EINVAL),
+    ([(0, 32, 1, 0, 1, 1)], O.OR_EINVAL),
+    ([(16, 32, 1, 0, 0, 1)], O.OR_EINVAL),
+    ([(16, 32, 1, 0, 1, 0)], O.OR_EMISSINGRATIO),
+    ([(16, 1024, 33, 0, 1, 1)], O.OR_EINFEASIBLE),
+    ([(16, 128, 20, 65536, 311, 100)], O.OR_EINFEASIBLE),
+    ([(16, 128, 20, 0, 311, 100)] * 13, O.OR_ETOOMANY),
+    ([(1 << 31, 32, 1, 0, 1 << 31, 1)], O.OR_EOVERFLOW),
+]
+
+
+@pytest.mark.parametrize("kernels,code", CASES)
+def test_validation_codes_agree_with_oracle(kernels, code):
+    c = rk.Context(-1)
+    c.rk_set_gpu_params(W.GTX580)
+    if code != O.OR_EOVERFLOW and code != O.OR_ETOOMANY:
+        assert O.check_inputs(W.GTX580, kernels) == code
+    with pytest.raises(rk.RkError) as e:
+        c.rk_set_kernels(kernels)
+    want = {O.OR_EINVAL: rk.RK_EINVAL, O.OR_EINFEASIBLE: rk.RK_EINFEASIBLE, O.OR_ETOOMANY: rk.RK_ETOOMANY,
+            O.OR_EMISSINGRATIO: rk.RK_EMISSINGRATIO, O.OR_EOVERFLOW: rk.RK_EOVERFLOW}[code]
+    assert e.value.status == want
+
+
+def test_bad_gpu_params():
+    c = rk.Context(-1)
+    with pytest.raises(rk.RkError) as e:
+        c.rk_set_gpu_params((0, 32768, 49152, 48, 8, 411, 100))
+    assert e.value.status == rk.RK_EINVAL
+    with pytest.raises(rk.RkError) as e:
+        c.rk_set_gpu_params((33, 32768, 49152, 48, 8, 411, 100))
+    assert e.value.status == rk.RK_EUNSUPPORTED
+    c2 = rk.Context(-1)
+    with pytest.raises(rk.RkError) as e:
+        c2.rk_set_kernels(W.W4)
+    assert e.value.status == rk.RK_ESTATE
+
+
+def test_w4_heuristic_host():
+    c = rk.Context(-1)
+    c.rk_set_gpu_params(W.GTX580)
+    c.rk_set_kernels(W.W4)
+    order, round_of, idx, _ = c.rk_heuristic_order(with_key=False)
+    assert order == [2, 1, 0, 3] and round_of == [0, 0, 1, 1] and idx == 14
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_heuristic_matches_oracle_algorithm1(seed):
+    # product Algorithm 1 (rk_host.cpp) vs the oracle's independent implementation
+    gpus = [W.GTX580, (8, 65536, 102400, 64, 16, 7, 2), (24, 32768, 49152, 48, 8, 311, 100)]
+    sets = W.random_small_sets(0xA160 + seed, 25, 1, 12)
+    c = rk.Context(-1)
+    for i, ks in enumerate(sets):
+        gpu = gpus[i % len(gpus)]
+        if not all(W.feasible(gpu, k) for k in ks):
+            continue
+        c.rk_set_gpu_params(gpu)
+        c.rk_set_kernels(ks)
+        order, round_of, idx, _ = c.rk_heuristic_order(with_key=False)
+        o2, r2 = O.heuristic(gpu, ks)
+        assert (order, round_of) == (o2, r2)
+        assert idx == O.rank(o2)
+
+
+def test_heuristic_matches_oracle_on_configs():
+    c = rk.Context(-1)
+    for name in ("C1", "C2", "C3", "C4"):
+        gpu, ks = W.config(name)
+        c.rk_set_gpu_params(gpu)
+        c.rk_set_kernels(ks)
+        order, round_of, _, _ = c.rk_heuristic_order(with_key=False)
+        assert (order, round_of) == O.heuristic(gpu, ks)
+    sets = W.c5_sets(64)
+    c.rk_set_gpu_params(W.GTX580)
+    for ks in sets:
+        c.rk_set_kernels(ks)
+        assert c.rk_heuristic_order(with_key=False)[:2] == O.heuristic(W.GTX580, ks)

@@ -1,0 +1,264 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the oracle, element by
+element on the same seeded inputs.  Bit-exact keys, round partitions,
+argmin/argmax, counts, histograms; doubles K/den within 1e-12 of the oracle's
+naive SPEC:210 double (O5).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle as O  # noqa: E402
+from paper_1511_07983_b200 import rk  # noqa: E402
+from paper_1511_07983_b200 import workloads as W  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+NCPU = os.cpu_count() or 1
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.fail("no CUDA device: the -m gpu suite needs a B200 (no CPU fallback)")
+    c = rk.Context(0)
+    yield c
+    c.close()
+
+
+def gpu_keys(ctx, gpu, ks, first=0, count=None, cand=0):
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    n = len(ks)
+    if count is None:
+        count = math.factorial(n) - first
+    keys = torch.zeros(max(count, 1), dtype=torch.int64, device="cuda")
+    st = ctx.rk_eval_range(first, count, cand, keys_dev=keys)
+    return st, keys[:count].cpu().numpy().view(np.uint64)
+
+
+def check_full_space(ctx, gpu, ks, cand=None, bins=(1, 4, 256)):
+    n = len(ks)
+    if cand is None:
+        cand = O.simulate(gpu, ks, O.heuristic(gpu, ks)[0]).key
+    st, keys = gpu_keys(ctx, gpu, ks, cand=cand)
+    ost, okeys = O.sweep(gpu, ks, cand_key=cand, threads=NCPU, keys=True)
+    assert np.array_equal(keys, okeys), "per-order keys differ"
+    assert st.as_tuple() == ost.as_tuple()
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    for B in bins:
+        h = torch.zeros(B, dtype=torch.int64, device="cuda")
+        ctx.rk_histogram(kd, len(keys), st.key_min, st.key_max, B, h)
+        torch.cuda.synchronize()
+        assert h.cpu().tolist() == O.histogram(okeys, ost.key_min, ost.key_max, B)
+    return st
+
+
+def test_w4_golden(ctx):
+    g = _gold("w4.json")
+    st, keys = gpu_keys(ctx, g["gpu"], g["kernels"], cand=100 * g["heuristic"]["T"])
+    assert [int(k) for k in keys] == [100 * row[3] for row in g["orders"]]
+    assert st.key_min == 100 * g["stats"]["best"] and st.argmin == g["stats"]["argmin"]
+    assert st.key_max == 100 * g["stats"]["worst"] and st.argmax == g["stats"]["argmax"]
+    assert st.n_eq + st.n_gt == 24 and st.n_lt == 0
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    for B, want in ((4, g["hist4"]), (8, g["hist8"])):
+        h = torch.zeros(B, dtype=torch.int64, device="cuda")
+        ctx.rk_histogram(kd, 24, st.key_min, st.key_max, B, h)
+        assert h.cpu().tolist() == want
+    order, round_of, idx, key = ctx.rk_heuristic_order()
+    assert order == g["heuristic"]["order"] and idx == g["heuristic"]["index"] and key == 100 * g["heuristic"]["T"]
+    nge, k2 = ctx.rk_percentile(order, 0, 24)
+    assert k2 == key and 100.0 * nge / 24 == g["heuristic"]["percentile"]
+    for row in g["orders"]:
+        rounds, key = ctx.rk_simulate_order([int(c) for c in row[1]])
+        assert key == 100 * row[3]
+        assert rounds == O.simulate(g["gpu"], g["kernels"], [int(c) for c in row[1]]).rounds
+
+
+def test_w2_cursor_and_counterexamples(ctx):
+    w = _gold("w2_cursor.json")
+    ctx.rk_set_gpu_params(w["gpu"])
+    ctx.rk_set_kernels(w["kernels"])
+    rounds, key = ctx.rk_simulate_order(w["order"])
+    assert rounds == w["rounds"] and key == w["T"]
+    c = _gold("counterexamples.json")
+    ctx.rk_set_gpu_params(c["C1"]["gpu"])
+    ctx.rk_set_kernels(c["C1"]["kernels"])
+    for order, T, rr in c["C1"]["cases"]:
+        assert ctx.rk_simulate_order(order) == (rr, T)
+    c2 = c["C2"]
+    ctx.rk_set_gpu_params(c2["gpu"])
+    ctx.rk_set_kernels(c2["kernels"])
+    assert ctx.rk_simulate_order(c2["with_X_first"]["order"])[1] == c2["with_X_first"]["T"]
+    ctx.rk_set_kernels([c2["kernels"][i] for i in c2["without_X"]["kernels_idx"]])
+    assert ctx.rk_simulate_order(c2["without_X"]["order"])[1] == c2["without_X"]["T"]
+
+
+def test_c1_random_sets(ctx):
+    for ks in W.c1_random_sets():
+        check_full_space(ctx, W.GTX580, ks, bins=(3,))
+
+
+def test_c2_full_space_vs_oracle_and_golden(ctx):
+    gpu, ks = W.config("C2")
+    g = _gold("c2_oracle.json")
+    st = check_full_space(ctx, gpu, ks, cand=g["cand_key"])
+    assert list(st.as_tuple()) == [g["stats"][f] for f in
+                                   ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt", "evaluated")]
+
+
+def test_c3_full_space_vs_oracle(ctx):
+    gpu, ks = W.config("C3")
+    g = _gold("c3_oracle.json")
+    st = check_full_space(ctx, gpu, ks, cand=g["cand_key"], bins=(256,))
+    assert st.evaluated == 3628800 and st.key_min == g["stats"]["key_min"] and st.argmin == g["stats"]["argmin"]
+
+
+GPUS = [W.GTX580, (8, 65536, 102400, 64, 16, 7, 2), (3, 16384, 16384, 32, 4, 5, 1), (32, 65536, 98304, 64, 32, 1, 1),
+        (13, 32768, 49152, 48, 8, 411, 100), (1, 65536, 49152, 48, 2, 1, 1), (5, 65536, 65536, 64, 3, 9, 4)]
+
+
+@pytest.mark.parametrize("gi", range(len(GPUS)))
+def test_random_sets_many_gpu_shapes(ctx, gi):
+    gpu = GPUS[gi]
+    sets = W.random_small_sets(0xD00D + gi, 30, 1, 7, gpu=gpu)
+    done = 0
+    for ks in sets:
+        if not all(W.feasible(gpu, k) for k in ks):
+            continue
+        try:
+            ctx.rk_set_gpu_params(gpu)
+            ctx.rk_set_kernels(ks)
+        except rk.RkError as e:
+            assert e.status == rk.RK_EUNSUPPORTED
+            continue
+        check_full_space(ctx, gpu, ks, bins=(7,))
+        done += 1
+    assert done >= 5
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_round_partitions_random_orders(ctx, seed):
+    rng = W.SplitMix64(0x9A27 + seed)
+    for gi, gpu in enumerate(GPUS):
+        for ks in W.random_small_sets(0x51 + seed * 31 + gi, 4, 1, 12, gpu=gpu):
+            if not all(W.feasible(gpu, k) for k in ks):
+                continue
+            try:
+                ctx.rk_set_gpu_params(gpu)
+                ctx.rk_set_kernels(ks)
+            except rk.RkError as e:
+                assert e.status == rk.RK_EUNSUPPORTED
+                continue
+            for _ in range(5):
+                order = list(range(len(ks)))
+                for i in range(len(order) - 1, 0, -1):
+                    j = rng.below(i + 1)
+                    order[i], order[j] = order[j], order[i]
+                rounds, key = ctx.rk_simulate_order(order)
+                o = O.simulate(gpu, ks, order)
+                assert rounds == o.rounds and key == o.key
+                T = key / gpu[6]
+                assert abs(T - o.t_naive) <= 1e-12 * T  # north_star 1e-12 on the float time
+
+
+def test_ranges_edges_and_sharding(ctx):
+    gpu, ks = W.config("C2")
+    full, fkeys = gpu_keys(ctx, gpu, ks, cand=12130259200)
+    N = 40320
+    for first, count in ((0, 1), (1, 1), (5, 7), (7, 13), (40319, 1), (12345, 6789), (0, 0), (40314, 6)):
+        st, keys = gpu_keys(ctx, gpu, ks, first, count, cand=12130259200)
+        assert np.array_equal(keys, fkeys[first:first + count])
+        if count:
+            ost, _ = O.sweep(gpu, ks, first, count, cand_key=12130259200)
+            assert st.as_tuple() == ost.as_tuple()
+        else:
+            assert st.evaluated == 0
+    # G shards merged on the device == unsharded (deterministic merge)
+    for G in (2, 3, 8):
+        recs = torch.zeros((G, 7), dtype=torch.int64, device="cuda")  # 56 B per record
+        bounds = [N * g // G for g in range(G + 1)]
+        cand = torch.tensor([12130259200], dtype=torch.int64, device="cuda")
+        for g in range(G):
+            ctx.rk_eval_range_async(bounds[g], bounds[g + 1] - bounds[g], cand, recs[g])
+        out = torch.zeros(7, dtype=torch.int64, device="cuda")
+        ctx.rk_merge_stats_async(recs, G, out)
+        torch.cuda.synchronize()
+        assert rk.Stats.from_c(rk.rk_stats.from_buffer_copy(out.cpu().numpy().tobytes())).as_tuple() == full.as_tuple()
+
+
+def test_small_n(ctx):
+    for n in (1, 2, 3):
+        for ks in W.random_small_sets(0x5A + n, 5, n, n):
+            check_full_space(ctx, W.GTX580, ks, bins=(2,))
+
+
+def test_errors_through_abi(ctx):
+    ctx.rk_set_gpu_params(W.GTX580)
+    with pytest.raises(rk.RkError) as e:
+        ctx.rk_set_kernels([(16, 128, 20, 65536, 311, 100)])
+    assert e.value.status == rk.RK_EINFEASIBLE
+    ctx.rk_set_kernels(W.W4)
+    with pytest.raises(rk.RkError) as e:
+        ctx.rk_eval_range(20, 5)
+    assert e.value.status == rk.RK_EINVAL
+
+
+def test_c4_full_space_bench_config_vs_oracle_golden(ctx):
+    """12! in the launch configuration bench.py times: aggregates + histogram vs
+    the full multi-core oracle run (tests/golden/c4_oracle.json), per-order keys
+    on samples the oracle computes one by one."""
+    g = _gold("c4_oracle.json")
+    gpu, ks = W.config("C4")
+    assert g["kernels"] == [list(k) for k in ks]
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    order, _, idx, key = ctx.rk_heuristic_order()
+    assert order == g["cand_order"] and idx == g["cand_index"] and key == g["cand_key"]
+    N = math.factorial(12)
+    keys = torch.empty(N, dtype=torch.int64, device="cuda")
+    st = ctx.rk_eval_range(0, N, key, keys_dev=keys)
+    assert list(st.as_tuple()) == [g["stats"][f] for f in
+                                   ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt", "evaluated")]
+    h = torch.zeros(g["bins"], dtype=torch.int64, device="cuda")
+    ctx.rk_histogram(keys, N, st.key_min, st.key_max, g["bins"], h)
+    assert h.cpu().tolist() == g["hist"]
+    rng = np.random.default_rng(12)
+    sample = np.concatenate([rng.integers(0, N, 20000), np.arange(0, 2000), np.arange(N - 2000, N)] +
+                            [np.arange(s * N // 8, s * N // 8 + 500) for s in range(1, 8)])
+    kh = keys[torch.from_numpy(sample).cuda()].cpu().numpy().view(np.uint64)
+    for i, k in zip(sample.tolist(), kh.tolist()):
+        assert O.simulate(gpu, ks, O.unrank(i, 12)).key == k, i
+
+
+def test_c5_batch_vs_oracle_golden(ctx):
+    g = _gold("c5_oracle.json")
+    sets = W.c5_sets(g["n_sets"])
+    ctx.rk_set_gpu_params(W.GTX580)
+    res = ctx.rk_eval_batch(sets)
+    for (st, ck), want in zip(res, g["sets"]):
+        assert list(st.as_tuple()) == want["stats"]
+        assert ck == want["cand_key"]
+    idx = [w["cand_index"] for w in g["sets"]]
+    res2 = ctx.rk_eval_batch(sets, cand_index=idx)
+    assert [r[0].as_tuple() for r in res2] == [r[0].as_tuple() for r in res]
+
+
+def test_c5_full_batch_properties(ctx):
+    sets = W.c5_sets(4096)
+    ctx.rk_set_gpu_params(W.GTX580)
+    res = ctx.rk_eval_batch(sets)
+    F = math.factorial(9)
+    for st, ck in res:
+        assert st.evaluated == F and st.n_lt + st.n_eq + st.n_gt == F
+        assert st.key_min <= ck <= st.key_max and st.n_eq >= 1
