@@ -1,0 +1,328 @@
+#!/usr/bin/env python3
+"""Benchmark: launch-order permutations evaluated per second (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3]): config C4 — 12 kernels from
+Generator G (seed 0x0151107983000004) on the GTX580 model parameters, the full
+12! = 479,001,600 launch-order space.  One step = one pass of the whole hot
+path: Algorithm 1 candidate (host) + its key
+(device), unrank/pack/score/reduce over the rank's index shard with keys kept
+in HBM, [N>1: NCCL all_gather of the 56-B records + device merge], the exact
+256-bin histogram over the global [min,max], [N>1: NCCL all_reduce].  Total
+work per step is fixed (12!), shards are contiguous index ranges: strong
+scaling.  For N>1 launch with torchrun (one rank per GPU).
+
+--impl reference times the oracle (oracle/, plain C++ on the host cores) on
+bounded samples of the same workload — rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "launch-order permutations evaluated/sec at 1/2/4/8 B200; % INT32 issue peak"
+UNIT = "perms/s"
+CONFIG_NAME = "C4"
+WORKLOAD = ("C4: 12 kernels (Generator G, seed 0x0151107983000004), full 12! = 479,001,600 launch orders, "
+            "GTX580 model parameters (PAPER:254), exact integer keys, 256-bin histogram, Algorithm 1 candidate")
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def algorithmic_ops_per_order(kernels) -> int:
+    """SURVEY §8(d) work of the plain block-level method per order (lower-bound
+    form): 9 ops per block placement (4 compares, 4 subtracts, 1
+    cursor), >= 4 per kernel (unrank digit) + 4 per (round, kernel) pair, >= 6
+    per round, 8 for the reductions: W = 9*sum(T) + 8n + 14."""
+    return 9 * sum(k[0] for k in kernels) + 8 * len(kernels) + 14
+
+
+def int_issue_peak_ops(sm_mhz: float, n_sms: int = 148) -> float:
+    """Integer issue peak: 148 SMs x 4 SMSPs x 1 warp-instr/clk x 32 lanes
+    (alu and fma pipes each 16 lanes/clk/SMSP, B300_MICROARCH 'Pipe rates')."""
+    return n_sms * 4 * 32 * sm_mhz * 1e6
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int, period_ms: int = 50):
+        self.device, self.period_ms = device, period_ms
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", f"-lms={self.period_ms}"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 3:
+                continue
+            try:
+                s, m = float(p[0]), float(p[1])
+                bits = int(p[2], 16)
+            except ValueError:
+                continue
+            sm.append(s)
+            mx.append(m)
+            for b, name in REASON_BITS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_rate(gpu, kernels, seconds: float, threads: int, first: int):
+    """Time the oracle as it stands on a bounded contiguous sample of the workload."""
+    import oracle as O
+
+    calib = 20000
+    t0 = time.perf_counter()
+    O.sweep(gpu, kernels, first, calib, threads=1)
+    per = (time.perf_counter() - t0) / calib
+    count = max(threads * 1000, int(seconds * threads / per))
+    count = min(count, math.factorial(len(kernels)) - first)
+    t0 = time.perf_counter()
+    O.sweep(gpu, kernels, first, count, threads=threads)
+    dt = time.perf_counter() - t0
+    return count / dt, count, dt
+
+
+def read_profile_traffic():
+    """Per-launch DRAM bytes of rk_eval_kernel from the committed ncu capture, if any."""
+    fn = os.path.join(ROOT, "profiles", "eval_kernel_ncu.json")
+    try:
+        with open(fn) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d.get("issue_active_pct")
+    except (OSError, ValueError):
+        return None, None
+
+
+def run_reference(args):
+    from paper_1511_07983_b200 import workloads as W
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    gpu, ks = W.config(CONFIG_NAME)
+    threads = os.cpu_count() or 1
+    N = math.factorial(len(ks))
+    per_step_s = float(os.environ.get("RK_REF_STEP_SECONDS", "2.0"))
+    import oracle as O
+
+    # size each step (a bounded contiguous sample) from a short calibration
+    t0 = time.perf_counter()
+    O.sweep(gpu, ks, N // 2, 20000, threads=1)
+    per = (time.perf_counter() - t0) / 20000
+    count = max(threads * 1000, int(per_step_s * threads / per))
+    first = N // 2 - count * (args.warmup + args.steps) // 2
+    for w in range(args.warmup):
+        O.sweep(gpu, ks, first + w * count, count, threads=threads)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        O.sweep(gpu, ks, first + (args.warmup + s) * count, count, threads=threads)
+    dt = time.perf_counter() - t0
+    value = count * args.steps / dt
+    sample = (f"{count} consecutive C4 orders per step starting at index {first} "
+              f"({args.steps} timed steps, {threads} threads)")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "n": len(ks), "orders": N, "sample_per_step": count},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bins", type=int, default=256)
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1511_07983_b200 import workloads as W
+    from paper_1511_07983_b200.dist import max_over_ranks
+    from paper_1511_07983_b200.sweep import Sweeper
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert world == args.gpus or world == 1, "launch N>1 with torchrun --nproc-per-node N"
+
+    gpu, ks = W.config(CONFIG_NAME)
+    sw = Sweeper(gpu, device=local, bins=args.bins)
+    sw.set_kernels(ks)
+    stream = torch.cuda.current_stream()
+    N = math.factorial(len(ks))
+
+    ev_eval = []
+
+    def step():
+        _, idx = sw.heuristic()  # a5: Algorithm 1 on the host (microseconds)
+        c = sw.ctx
+        c.rk_eval_index_async(idx, sw.cand, stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        c.rk_eval_range_async(sw.first, sw.count, sw.cand, sw.rec, sw.keys, stream)
+        e1.record(stream)
+        ev_eval.append((e0, e1))
+        launches = 2
+        rngrec = sw.rec
+        if world > 1:
+            from paper_1511_07983_b200.dist import all_gather_records, all_reduce_hist
+            recs = all_gather_records(sw.rec)
+            c.rk_merge_stats_async(recs, world, sw.glob, stream)
+            launches += 1
+            rngrec = sw.glob
+        sw.hist.zero_()
+        c.rk_histogram_async(sw.keys, sw.count, rngrec, sw.bins, sw.hist, stream)
+        launches += 1
+        if world > 1:
+            all_reduce_hist(sw.hist)
+        return launches
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    ev_eval.clear()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for _ in range(args.steps):
+            launches += step()
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = t_start.elapsed_time(t_end)
+    ms_max = max_over_ranks(ms, sw.dev)
+    value = N * args.steps / (ms_max / 1e3)
+    eval_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_eval)
+    eval_ms_max = max_over_ranks(eval_ms, sw.dev)
+
+    # correctness of the timed pipeline's result (global record, histogram mass)
+    out = torch.cat([sw.glob if world > 1 else sw.rec, sw.hist]).cpu()
+    evaluated = int(out[6].item())
+    hist_mass = int(out[7:].sum().item())
+    assert hist_mass == N and (world > 1 or evaluated == N), (hist_mass, evaluated)
+
+    # e2e: the public API with host buffers (Sweeper.run: H2D tables, D2H report)
+    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    for _ in range(2):
+        sw.run(ks)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(e2e_steps):
+        rep = sw.run(ks)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(a.elapsed_time(b), sw.dev)
+    e2e_value = N * e2e_steps / (e2e_ms / 1e3)
+
+    clocks = clk.summary()
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        ops = algorithmic_ops_per_order(ks)
+        per_launch_orders = sw.count
+        achieved = ops * per_launch_orders / (eval_ms_max / 1e3)
+        peak = int_issue_peak_ops(1965.0)
+        traffic, issue_pct = read_profile_traffic()
+        roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "kernel": "rk_eval_kernel<16>", "kernel_ms": eval_ms_max,
+                    "ops_per_order": ops, "orders_per_launch": per_launch_orders,
+                    "peak_basis": "148 SM x 4 SMSP x 32 lanes x 1965 MHz (integer issue, DESIGN.md §6)",
+                    "ncu_issue_active_pct": issue_pct}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "n": len(ks), "orders": N, "bins": args.bins,
+                           "shards": world, "parallelism": f"index-space shards x{world}",
+                           "l2": "keys array 8 B/order (3.83 GB at N=1) > 126 MB L2; eval phase reads no HBM input"},
+                "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sw.h2d_bytes,
+                        "d2h_bytes_per_step": sw.d2h_bytes, "steps": e2e_steps},
+                "result": {"best_T": rep.best_key / gpu[6], "best_index": rep.best_index,
+                           "worst_T": rep.worst_key / gpu[6], "cand_index": rep.cand_index,
+                           "percentile": rep.percentile, "speedup_over_worst": rep.speedup_over_worst,
+                           "deviation_pct": rep.deviation_pct}}
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            v, cnt, dt = oracle_rate(gpu, ks, args.cpu_seconds, threads, N // 3)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                    "sample": f"{cnt} consecutive C4 orders from index {N // 3} "
+                                              f"({dt:.1f} s on {threads} threads)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -116,6 +116,11 @@ rk_status rk_eval_range(rk_ctx* ctx, uint64_t first, uint64_t count, uint64_t ca
 rk_status rk_eval_range_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
                               rk_stats* stats_dev, uint64_t* keys_dev, void* stream);
 
+/* Exact key of the single launch order with lexicographic index `index`,
+ * written to key_dev (device u64).  Stream-ordered, no host sync (used for the
+ * candidate order inside a device pipeline).  index < n!. */
+rk_status rk_eval_index_async(rk_ctx* ctx, uint64_t index, uint64_t* key_dev, void* stream);
+
 /* Deterministic merge of n_records device records (e.g. all-gathered per-rank
  * records) into out_dev: min/max with smallest-index ties, counts summed.
  * The result is independent of record order.  Only enqueues. */
@@ -169,6 +174,9 @@ rk_status rk_simulate_order(rk_ctx* ctx, const int32_t* order, uint32_t* rounds_
  * helpers, no ctx.  1 <= n <= 20. RK_EINVAL on a non-permutation / idx >= n!. */
 rk_status rk_rank(const int32_t* order, uint32_t n, uint64_t* idx_out);
 rk_status rk_unrank(uint64_t idx, uint32_t n, int32_t* order_out);
+
+/* Bytes of the packed device tables rk_set_kernels uploads (host -> device). */
+uint32_t rk_table_bytes(void);
 
 /* Number of kernel launches the last synchronous/async call enqueued on the
  * device (for the bench's gpu_launches count). */

@@ -479,6 +479,19 @@ rk_status rk_eval_range(rk_ctx* c, uint64_t first, uint64_t count, uint64_t cand
     return RK_OK;
 }
 
+rk_status rk_eval_index_async(rk_ctx* c, uint64_t index, uint64_t* key_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!key_dev) return fail(c, RK_EINVAL, "key_dev is required");
+    if (index >= space(c)) return fail(c, RK_EINVAL, "index >= n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    int e = rk_launch_key_of_index(c->tab_dev, c->tab.g.S, index, key_dev, stream, &c->launches);
+    return e ? cuda_fail(c, e, "rk_eval_index_async") : RK_OK;
+}
+
+uint32_t rk_table_bytes(void) { return (uint32_t)sizeof(RkTables); }
+
 rk_status rk_merge_stats_async(rk_ctx* c, const rk_stats* in_dev, uint32_t n_records, rk_stats* out_dev,
                                void* stream) {
     rk_status s = need_device(c);

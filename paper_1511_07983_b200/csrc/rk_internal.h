@@ -60,6 +60,8 @@ int rk_launch_keys_of(const RkTables* tabs_dev, uint32_t n, uint32_t S, const ui
                       uint32_t m, uint64_t* out_dev, void* stream, uint32_t* launches);
 int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* idx_dev, uint32_t m,
                            uint64_t* out_dev, void* stream, uint32_t* launches);
+int rk_launch_key_of_index(const RkTables* tab_dev, uint32_t S, uint64_t index, uint64_t* out_dev, void* stream,
+                           uint32_t* launches);
 /* one order -> rounds partition (1 thread) */
 int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const int32_t* order_dev,
                        uint32_t* rounds_dev, uint32_t max_rounds, uint32_t* n_rounds_dev, uint64_t* key_dev,

@@ -501,6 +501,16 @@ __global__ void rk_keys_of_same_kernel(const RkTables* __restrict__ tab, const u
 }
 
 template <int SMAX>
+__global__ void rk_key_of_index_kernel(const RkTables* __restrict__ tab, uint32_t index, uint64_t* __restrict__ out) {
+    __shared__ RkTables t;
+    load_tables(t, tab);
+    if (threadIdx.x == 0) {
+        NoRec nr;
+        *out = eval_index<SMAX>(t, index, nr);
+    }
+}
+
+template <int SMAX>
 __global__ void rk_simulate_kernel(const RkTables* __restrict__ tab, const int32_t* __restrict__ order,
                                    uint32_t* rounds, uint32_t max_rounds, uint32_t* n_rounds, uint64_t* key) {
     const RkTables& t = *tab;
@@ -641,6 +651,14 @@ int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* 
     unsigned blocks = (m + 127) / 128;
     if (S <= 16) rk_keys_of_same_kernel<16><<<blocks, 128, 0, (cudaStream_t)stream>>>(tab_dev, idx_dev, m, out_dev);
     else rk_keys_of_same_kernel<32><<<blocks, 128, 0, (cudaStream_t)stream>>>(tab_dev, idx_dev, m, out_dev);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_launch_key_of_index(const RkTables* tab_dev, uint32_t S, uint64_t index, uint64_t* out_dev, void* stream,
+                           uint32_t* launches) {
+    if (S <= 16) rk_key_of_index_kernel<16><<<1, 32, 0, (cudaStream_t)stream>>>(tab_dev, (uint32_t)index, out_dev);
+    else rk_key_of_index_kernel<32><<<1, 32, 0, (cudaStream_t)stream>>>(tab_dev, (uint32_t)index, out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

@@ -22,9 +22,9 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 
 #: every symbol include/rk.h declares (checked by tests/test_abi.py)
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
-           "rk_eval_range_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
+           "rk_eval_range_async", "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
            "rk_heuristic_order", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
-           "rk_last_launch_count"]
+           "rk_last_launch_count", "rk_table_bytes"]
 
 
 class rk_gpu_params(ctypes.Structure):
@@ -73,6 +73,8 @@ def lib():
             "rk_set_kernels": ([vp, P(rk_kernel), u32], ctypes.c_int),
             "rk_eval_range": ([vp, u64, u64, u64, P(rk_stats), vp, vp], ctypes.c_int),
             "rk_eval_range_async": ([vp, u64, u64, vp, vp, vp, vp], ctypes.c_int),
+            "rk_eval_index_async": ([vp, u64, vp, vp], ctypes.c_int),
+            "rk_table_bytes": ([], u32),
             "rk_merge_stats_async": ([vp, vp, u32, vp, vp], ctypes.c_int),
             "rk_histogram": ([vp, vp, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_histogram_async": ([vp, vp, u64, vp, u32, vp, vp], ctypes.c_int),
@@ -118,6 +120,10 @@ def kernels_array(kernels):
     for i, k in enumerate(kernels):
         arr[i] = rk_kernel(*[int(x) for x in k])
     return arr
+
+
+def rk_table_bytes() -> int:
+    return int(lib().rk_table_bytes())
 
 
 def rk_rank(order) -> int:
@@ -210,6 +216,9 @@ class Context:
     def rk_eval_range_async(self, first: int, count: int, cand_key_dev, stats_dev, keys_dev=None, stream=None):
         self._chk(self._L.rk_eval_range_async(self.h, first, count, _ptr(cand_key_dev), _ptr(stats_dev),
                                               _ptr(keys_dev), _stream(stream)), "rk_eval_range_async")
+
+    def rk_eval_index_async(self, index: int, key_dev, stream=None):
+        self._chk(self._L.rk_eval_index_async(self.h, index, _ptr(key_dev), _stream(stream)), "rk_eval_index_async")
 
     def rk_merge_stats_async(self, in_dev, n_records: int, out_dev, stream=None):
         self._chk(self._L.rk_merge_stats_async(self.h, _ptr(in_dev), n_records, _ptr(out_dev), _stream(stream)),

@@ -123,7 +123,7 @@ class Sweeper:
     @property
     def h2d_bytes(self) -> int:
         """Bytes the host sends per run(): the packed kernel tables + params."""
-        return rk.TABLE_BYTES
+        return rk.rk_table_bytes()
 
     @property
     def d2h_bytes(self) -> int:
