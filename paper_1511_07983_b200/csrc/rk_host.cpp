@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -34,6 +35,7 @@ struct rk_ctx {
     uint64_t* u64_dev = nullptr;      /* small scratch (indices / keys) */
     uint32_t max_ctas = 0;
     uint32_t launches = 0;
+    bool no_reduce = false; /* RK_NO_REDUCE=1: disable the symmetry reduction (testing) */
 };
 
 namespace {
@@ -91,7 +93,6 @@ rk_status check_params(rk_ctx* c, const rk_gpu_params& p) {
     if (!p.n_sm || !p.regs_per_sm || !p.shm_bytes_per_sm || !p.max_warps_per_sm || !p.max_blocks_per_sm ||
         !p.rb_num || !p.rb_den)
         return fail(c, RK_EINVAL, "gpu params must all be > 0 (SPEC:30-32)");
-    if (p.n_sm > RK_SMAX) return fail(c, RK_EUNSUPPORTED, "n_sm %u > %d (device fast path)", p.n_sm, RK_SMAX);
     if (p.max_blocks_per_sm > 255) return fail(c, RK_EUNSUPPORTED, "max_blocks_per_sm > 255");
     if (p.max_warps_per_sm > 32767) return fail(c, RK_EUNSUPPORTED, "max_warps_per_sm > 32767");
     return RK_OK;
@@ -122,18 +123,35 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
         gs = std::gcd(gs, d[i].shm);
     }
     if (bound >= ((u128)1 << 63)) return fail(c, RK_EOVERFLOW, "exact key bound >= 2^63");
+    /* symmetry reduction: g SMs behave as one super-SM */
+    uint64_t gb = p.n_sm;
+    uint64_t amax = 0;
+    for (uint32_t i = 0; i < n; i++) {
+        gb = std::gcd(gb, (uint64_t)ks[i].grid_blocks);
+        amax = std::max<uint64_t>(amax, std::max(ks[i].inst_per_block, ks[i].mem_per_block));
+    }
+    while (gb > 1 && amax * gb > 0xFFFFFFFFull) { /* scaled A, M must stay u32: use a divisor of g */
+        uint64_t d = 2;
+        while (gb % d) d++;
+        gb /= d;
+    }
+    if (c && c->no_reduce) gb = 1;
+    const uint32_t Sred = (uint32_t)(p.n_sm / gb);
+    if (Sred > RK_SMAX)
+        return fail(c, RK_EUNSUPPORTED, "N_SM/gcd(N_SM, grids) = %u > %d (device fast path)", Sred, RK_SMAX);
     const uint64_t R = p.regs_per_sm / gr, Sh = p.shm_bytes_per_sm / gs;
     if (R > 32767 || Sh > 32767)
         return fail(c, RK_EUNSUPPORTED, "scaled regs %llu / shm %llu exceed the 15-bit packing", (unsigned long long)R,
                     (unsigned long long)Sh);
     std::memset(&t, 0, sizeof t);
     RkGTab& g = t.g;
-    g.S = p.n_sm;
+    g.S = Sred;
+    g.blkscale = (uint32_t)gb;
     g.num = p.rb_num;
     g.den = p.rb_den;
     g.freshA = (uint32_t)(2 * R + 1) | (uint32_t)(2 * Sh + 1) << 16;
     g.freshB = (uint32_t)(2 * p.max_warps_per_sm + 1) | (uint32_t)(2 * p.max_blocks_per_sm + 1) << 16;
-    g.smagic = (uint32_t)(((1ull << 32) + p.n_sm - 1) / p.n_sm);
+    g.smagic = Sred > 1 ? (uint32_t)(((1ull << 32) + Sred - 1) / Sred) : 0u;
     uint32_t tb = 1;
     while (tb * 2 <= p.max_blocks_per_sm) tb *= 2;
     g.tbits = tb;
@@ -162,7 +180,7 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
             add[r] = 0;
         }
         RkKTab& k = t.k[i];
-        k.T = ks[i].grid_blocks;
+        k.T = (uint32_t)(ks[i].grid_blocks / gb);
         k.mr = mag[0];
         k.ms = mag[1];
         k.mw = mag[2];
@@ -171,10 +189,10 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
         k.zw = add[2];
         k.dA = (uint32_t)(2 * dem[0]) | (uint32_t)(2 * dem[1]) << 16;
         k.dB = (uint32_t)(2 * dem[2]) | 2u << 16;
-        k.A = ks[i].inst_per_block;
-        k.M = ks[i].mem_per_block;
+        k.A = (uint32_t)(ks[i].inst_per_block * gb);
+        k.M = (uint32_t)(ks[i].mem_per_block * gb);
         k.C = (uint32_t)C;
-        k.SC = (uint32_t)(C * p.n_sm);
+        k.SC = (uint32_t)(C * Sred);
         const u128 ci = (u128)k.SC * k.A * p.rb_den, cm = (u128)k.SC * k.M * p.rb_num;
         const u128 fk = ci >= cm ? ci : cm;
         k.fullkey = fk >> 64 ? ~0ull : (uint64_t)fk; /* only used when T > SC, then bounded */
@@ -372,6 +390,8 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
     if (!out) return RK_EINVAL;
     rk_ctx* c = new rk_ctx();
     c->device = cuda_device;
+    const char* nr = getenv("RK_NO_REDUCE");
+    c->no_reduce = nr && nr[0] == '1';
     if (cuda_device >= 0) {
         int ndev = 0;
         cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -380,7 +400,9 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
             return RK_ENODEVICE;
         }
         DeviceGuard dg(cuda_device);
-        c->max_ctas = (uint32_t)rk_eval_max_ctas(RK_SMAX, cuda_device);
+        c->max_ctas = 0;
+        for (uint32_t S : {1u, 2u, 3u, 4u, 5u, 8u, 9u, 16u, 17u, 32u})
+            c->max_ctas = std::max(c->max_ctas, (uint32_t)rk_eval_max_ctas(S, cuda_device));
         if (c->max_ctas < 256) c->max_ctas = 256;
         bool ok = cudaMalloc(&c->tab_dev, sizeof(RkTables)) == cudaSuccess &&
                   cudaMalloc(&c->recs_dev, sizeof(rk_stats) * c->max_ctas * 2) == cudaSuccess &&
@@ -618,8 +640,17 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     if (!e) e = cudaMalloc(&out_dev, sizeof(rk_stats) * n_sets);
     if (!e) e = cudaMemcpyAsync(tabs_dev, tabs.data(), sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
     if (!e) e = cudaMemcpyAsync(idx_dev, idx.data(), sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
-    if (!e) e = rk_launch_keys_of(tabs_dev, n, c->gp.n_sm, idx_dev, n_sets, keys_dev, stream, &c->launches);
-    if (!e) e = rk_launch_batch(tabs_dev, n, c->gp.n_sm, n_sets, keys_dev, out_dev, recs, chunks, stream, &c->launches);
+    uint32_t smax_k = 0;
+    for (uint32_t q = 0; q < n_sets; q++) smax_k = std::max(smax_k, tabs[q].g.S);
+    if (!e) e = rk_launch_keys_of(tabs_dev, n, smax_k, idx_dev, n_sets, keys_dev, stream, &c->launches);
+    uint32_t smax = 0;
+    bool uniform = true;
+    for (uint32_t q = 0; q < n_sets; q++) {
+        if (q && tabs[q].g.S != tabs[0].g.S) uniform = false;
+        smax = std::max(smax, tabs[q].g.S);
+    }
+    if (!e) e = rk_launch_batch(tabs_dev, n, smax | (uniform ? 0x80000000u : 0u), n_sets, keys_dev, out_dev, recs,
+                                chunks, stream, &c->launches);
     std::vector<uint64_t> keys(n_sets);
     if (!e) e = cudaMemcpyAsync(out_host, out_dev, sizeof(rk_stats) * n_sets, cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaMemcpyAsync(keys.data(), keys_dev, sizeof(uint64_t) * n_sets, cudaMemcpyDeviceToHost, st);

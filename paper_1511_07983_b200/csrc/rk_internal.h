@@ -9,6 +9,11 @@
  * A block of kernel k subtracts dA = 2*dr | 2*ds << 16 and dB = 2*dw | 2 << 16.
  * Register and shared-memory quantities are divided by their gcd over the GPU
  * capacity and all kernel demands first (exact: fit tests are scale-free).
+ *
+ * Symmetry reduction: with g = gcd(N_SM, N_tblk_1..n), every run of equal SMs
+ * in ring order from the cursor has a length that is a multiple of g, so the
+ * model on (N_SM, N_tblk_i, A_i, M_i) is the model on (N_SM/g, N_tblk_i/g,
+ * g*A_i, g*M_i) with identical exact keys.
  */
 #ifndef RK_INTERNAL_H
 #define RK_INTERNAL_H
@@ -32,7 +37,8 @@ struct RkKTab {        /* one kernel; 64 B */
 };
 
 struct RkGTab {
-    uint32_t S;            /* N_SM */
+    uint32_t S;            /* super-SMs: N_SM / blkscale (DESIGN.md §5 symmetry reduction) */
+    uint32_t blkscale;     /* g = gcd(N_SM, all N_tblk): SMs per super-SM, blocks per super-block */
     uint32_t num, den;     /* R_B = num / den */
     uint32_t freshA, freshB;   /* packed words of a fresh SM */
     uint32_t smagic;       /* ceil(2^32 / S) */

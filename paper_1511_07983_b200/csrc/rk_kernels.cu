@@ -2,23 +2,27 @@
  * rk_kernels.cu — sm_100a kernels of the exhaustive launch-order evaluation
  * (arXiv 1511.07983).  Product path; shares nothing with oracle/.
  *
- * One thread evaluates a "run": the m! = 6 consecutive lexicographic indices
- * that share an (n-3)-prefix (SURVEY §7 "prefix sharing").  It unranks the
+ * One thread evaluates a "run": the 3! = 6 consecutive lexicographic indices
+ * that share an (n-3)-prefix (prefix sharing).  It unranks the
  * prefix (Lehmer code, PAPER:254 / SPEC:292), places the prefix kernels once,
- * then walks the 3-level suffix tree.  Placement of one kernel is the
- * closed-form "water-fill" equivalent of the paper's block-by-block
- * round-robin dispatch (derivation in DESIGN.md
- * §5): per SM the capacity c_s = min over the four limits of
- * floor(free/demand); blocks go round-robin over SMs with remaining capacity,
- * starting at the cursor, so after t full passes SM s holds min(c_s, t); the
- * pass holding the last block and the last block's SM follow from a binary
- * search on t and a select on the ring-rotated eligibility mask.  A block
- * that fits nowhere closes the execution round; rounds are
- * scored exactly as K += max(den*I_r, num*M_r) (reading L1).
+ * places each of the 3 level-(n-2) kernels, and for each of the 6 leaves places
+ * the level-(n-1) kernel fused with the evaluation of the last kernel (the
+ * leaf's SM state is never materialised).
+ *
+ * Placement of one kernel is the closed-form "water-fill" equivalent of the
+ * paper's block-by-block round-robin dispatch:
+ * per SM the capacity c_s = min over the four limits of
+ * floor(free/demand); blocks go round-robin over the SMs with remaining
+ * capacity starting at the cursor, so after t passes SM s holds min(c_s, t);
+ * the pass holding the last block comes from a binary search on t (16x2 SIMD
+ * mins over SM pairs), the last block's SM from a select on the ring-rotated
+ * eligibility mask.  A block that fits nowhere closes the execution round
+ * (PAPER:79-81); rounds are scored exactly as K += max(den*I_r, num*M_r)
+ * (reading L1).
  *
  * SM state lives in registers (2 packed u32 per SM, fully unrolled over
- * SMAX), kernel tables in shared memory, reductions via warp shuffles then
- * shared memory then a last-CTA merge (no extra launch).
+ * SMAX; FULL = compile-time S == SMAX), kernel tables in shared memory,
+ * reductions via warp shuffles then shared memory then a last-CTA merge.
  */
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -47,6 +51,18 @@ struct St {
     uint64_t I, M, K; /* open round's inst/mem units; closed rounds' key */
 };
 
+/* number of SMs: compile-time when FULL */
+template <int SMAX, bool FULL>
+__device__ __forceinline__ uint32_t nsm(const RkGTab& g) {
+    if constexpr (FULL) return (uint32_t)SMAX;
+    else return g.S;
+}
+template <int SMAX, bool FULL>
+__device__ __forceinline__ bool live_sm(int i, const RkGTab& g) {
+    if constexpr (FULL) return true;
+    else return (uint32_t)i < g.S;
+}
+
 struct NoRec {
     __device__ __forceinline__ void add(uint32_t, uint32_t) {}
     __device__ __forceinline__ void close() {}
@@ -56,9 +72,9 @@ struct NoRec {
 /* Records the round partition p[r][i] for rk_simulate_order. */
 struct Rec {
     uint32_t* rounds;
-    uint32_t max_rounds, n, r;
+    uint32_t max_rounds, n, r, scale; /* scale: SMs per super-SM */
     __device__ void add(uint32_t k, uint32_t cnt) {
-        if (r < max_rounds) rounds[r * n + k] += cnt;
+        if (r < max_rounds) rounds[r * n + k] += cnt * scale;
     }
     __device__ void close() { r++; }
     __device__ void full(uint32_t k, uint32_t nfull, uint32_t sc) {
@@ -69,39 +85,44 @@ struct Rec {
     }
 };
 
-template <int SMAX>
+template <int SMAX, bool FULL>
 __device__ __forceinline__ void st_fresh(St<SMAX>& s, const RkGTab& g) {
 #pragma unroll
     for (int i = 0; i < SMAX; i++) {
-        s.fa[i] = (uint32_t)i < g.S ? g.freshA : 0u;
-        s.fb[i] = (uint32_t)i < g.S ? g.freshB : 0u;
+        s.fa[i] = live_sm<SMAX, FULL>(i, g) ? g.freshA : 0u;
+        s.fb[i] = live_sm<SMAX, FULL>(i, g) ? g.freshB : 0u;
     }
     s.cur = 0;
     s.I = s.M = s.K = 0;
 }
 
-/* c_s = min(floor(regs/dr), floor(shm/ds), floor(warps/dw), slots) per SM
- * (the four limits of PAPER:76-78, inclusive <=, reading L8). Returns sum. */
-template <int SMAX>
-__device__ __forceinline__ uint32_t sm_caps(const St<SMAX>& s, const RkKTab& k, uint32_t (&c)[SMAX]) {
-    uint32_t F = 0;
-#pragma unroll
-    for (int i = 0; i < SMAX; i++) {
-        uint32_t qr = mad_hi(s.fa[i] & 0xFFFFu, k.mr, k.zr);
-        uint32_t qs = mad_hi(s.fa[i] >> 16, k.ms, k.zs);
-        uint32_t qw = mad_hi(s.fb[i] & 0xFFFFu, k.mw, k.zw);
-        uint32_t qb = s.fb[i] >> 17;
-        c[i] = min(__vimin3_u32(qr, qs, qw), qb);
-        F += c[i];
-    }
-    return F;
+/* Capacity of one SM for kernel k: min(floor(regs/dr), floor(shm/ds),
+ * floor(warps/dw), slots) — the four limits of PAPER:76-78, inclusive <=
+ * (reading L8).  Fields are stored as 2x+1, so floor(x/d) = floor((2x+1)/(2d))
+ * = IMAD.HI with a host-verified magic; a zero demand adds 0xFFFF instead. */
+struct CapK {
+    uint32_t mr, ms, mw, zr, zs, zw;
+};
+__device__ __forceinline__ CapK capk(const RkKTab& k) { return CapK{k.mr, k.ms, k.mw, k.zr, k.zs, k.zw}; }
+__device__ __forceinline__ uint32_t cap1(uint32_t fa, uint32_t fb, const CapK& k) {
+    const uint32_t qr = mad_hi(fa & 0xFFFFu, k.mr, k.zr);
+    const uint32_t qs = mad_hi(fa >> 16, k.ms, k.zs);
+    const uint32_t qw = mad_hi(fb & 0xFFFFu, k.mw, k.zw);
+    return min(__vimin3_u32(qr, qs, qw), fb >> 17);
 }
 
-template <int SMAX>
+/* Ring rotation of an S-bit mask (S <= 32). */
+template <int SMAX, bool FULL>
 __device__ __forceinline__ uint32_t rotr_s(uint32_t m, uint32_t r, uint32_t S) {
-    uint64_t mm = (uint64_t)m | ((uint64_t)m << S);
-    uint32_t full = (S >= 32) ? 0xFFFFFFFFu : ((1u << S) - 1u);
-    return (uint32_t)(mm >> r) & full;
+    if constexpr (FULL && SMAX == 1) {
+        return m;
+    } else if constexpr (FULL && SMAX <= 16) {
+        return ((m | (m << SMAX)) >> r) & ((1u << SMAX) - 1u);
+    } else {
+        const uint64_t mm = (uint64_t)m | ((uint64_t)m << S);
+        const uint32_t full = (S >= 32) ? 0xFFFFFFFFu : ((1u << S) - 1u);
+        return (uint32_t)(mm >> r) & full;
+    }
 }
 
 /* 0-based position of the r-th (1-based) set bit of m (r <= popc(m)). */
@@ -109,8 +130,8 @@ template <int SMAX>
 __device__ __forceinline__ uint32_t select_bit(uint32_t m, uint32_t r) {
     uint32_t p = 0;
 #pragma unroll
-    for (int w = (SMAX > 16 ? 16 : 8); w >= 1; w >>= 1) {
-        uint32_t lowc = __popc(m & ((1u << w) - 1u));
+    for (int w = SMAX / 2; w >= 1; w >>= 1) {
+        const uint32_t lowc = __popc(m & ((1u << w) - 1u));
         if (lowc < r) {
             r -= lowc;
             m >>= w;
@@ -120,75 +141,147 @@ __device__ __forceinline__ uint32_t select_bit(uint32_t m, uint32_t r) {
     return p;
 }
 
-/* Dispatch all T_k blocks of kernel k into the open round. */
-template <int SMAX, class R>
-__device__ __forceinline__ void place(St<SMAX>& s, const RkKTab& k, uint32_t kid, const RkGTab& g, R& rec) {
+/* Outcome of placing kernel k into an SM state (everything but the per-SM words). */
+struct Placed {
+    uint32_t cur;
+    uint64_t I, M, K;
+};
+
+/* Dispatch all T_k blocks of kernel k on state `in`; the new
+ * per-SM words are handed to upd(i, fa, fb) so callers either store them
+ * (a new state) or consume them on the fly (the fused last level). */
+template <int SMAX, bool FULL, class R, class U>
+__device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k, uint32_t kid, const RkGTab& g,
+                                             R& rec, U& upd) {
+    const CapK ck = capk(k);
     uint32_t c[SMAX];
-    uint32_t F = sm_caps<SMAX>(s, k, c);
-    uint32_t n = k.T;
-    if (n > F) {
-        /* every SM takes its c_s, the next block fits nowhere: the round closes
-         * (PAPER:79-80); the rest starts fresh rounds at cursor 0 (reading L4). */
-        s.I += (uint64_t)F * k.A;
-        s.M += (uint64_t)F * k.M;
-        rec.add(kid, F);
-        s.K += round_key(s.I, s.M, g.num, g.den);
-        rec.close();
-        n -= F;
-        uint32_t nfull = (n - 1u) / k.SC; /* complete single-kernel rounds */
-        s.K += (uint64_t)nfull * k.fullkey;
-        rec.full(kid, nfull, k.SC);
-        n -= nfull * k.SC;
-#pragma unroll
-        for (int i = 0; i < SMAX; i++) {
-            s.fa[i] = (uint32_t)i < g.S ? g.freshA : 0u;
-            s.fb[i] = (uint32_t)i < g.S ? g.freshB : 0u;
-            c[i] = (uint32_t)i < g.S ? k.C : 0u;
-        }
-        s.cur = 0;
-        s.I = s.M = 0;
-    }
-    /* n in [1, sum c]: find the pass t1 = tlo+1 that holds the last block,
-     * tlo = max{t : f(t) < n}, f(t) = sum_s min(c_s, t). */
-    uint32_t tlo = 0, flo = 0;
-    for (uint32_t b = g.tbits; b; b >>= 1) {
-        uint32_t tt = tlo + b, f = 0;
-#pragma unroll
-        for (int i = 0; i < SMAX; i++) f += min(c[i], tt);
-        if (f < n) {
-            tlo = tt;
-            flo = f;
-        }
-    }
-    uint32_t r = n - flo; /* >= 1 blocks in pass t1, to SMs with c_s > tlo in ring order */
-    uint32_t E = 0;
-#pragma unroll
-    for (int i = 0; i < SMAX; i++) E |= (c[i] > tlo ? 1u : 0u) << i;
-    uint32_t Er = rotr_s<SMAX>(E, s.cur, g.S);
-    uint32_t p = select_bit<SMAX>(Er, r);
-    uint32_t Xr = Er & ((2u << p) - 1u);      /* first r eligible SMs from the cursor */
-    uint32_t X = rotr_s<SMAX>(Xr, g.S - s.cur, g.S);
-    uint32_t nc = s.cur + p + 1u;
-    s.cur = nc >= g.S ? nc - g.S : nc;       /* cursor = SM of the last block + 1 */
+    uint32_t F = 0;
 #pragma unroll
     for (int i = 0; i < SMAX; i++) {
-        uint32_t x = min(c[i], tlo) + ((X >> i) & 1u);
-        s.fa[i] -= x * k.dA;
-        s.fb[i] -= x * k.dB;
+        c[i] = cap1(in.fa[i], in.fb[i], ck);
+        F += c[i];
     }
-    s.I += (uint64_t)n * k.A;
-    s.M += (uint64_t)n * k.M;
+    uint32_t n = k.T;
+    Placed o;
+    const uint32_t S = nsm<SMAX, FULL>(g);
+    if (n > F) {
+        /* every SM takes its c_s and the next block fits nowhere: the round
+         * closes; complete single-kernel rounds follow, the rest
+         * opens a fresh round whose blocks go to SMs 0,1,.. in turn (cursor 0). */
+        rec.add(kid, F);
+        rec.close();
+        o.K = in.K + round_key(in.I + (uint64_t)F * k.A, in.M + (uint64_t)F * k.M, g.num, g.den);
+        n -= F;
+        const uint32_t nfull = (n - 1u) / k.SC;
+        o.K += (uint64_t)nfull * k.fullkey;
+        rec.full(kid, nfull, k.SC);
+        n -= nfull * k.SC;
+        uint32_t q, r;
+        if constexpr (FULL) {
+            q = n / (uint32_t)SMAX; /* power of two: a shift */
+            r = n % (uint32_t)SMAX;
+        } else {
+            q = n / S;
+            r = n - q * S;
+        }
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            const uint32_t x = q + ((uint32_t)i < r ? 1u : 0u);
+            if (live_sm<SMAX, FULL>(i, g)) upd(i, g.freshA - x * k.dA, g.freshB - x * k.dB);
+            else upd(i, 0u, 0u);
+        }
+        o.cur = r;
+        o.I = (uint64_t)n * k.A;
+        o.M = (uint64_t)n * k.M;
+    } else {
+        /* tlo = max{t : f(t) < n}, f(t) = sum_s min(c_s, t); SM pairs in 16x2 SIMD */
+        constexpr int NP = SMAX / 2;
+        uint32_t cp[NP > 0 ? NP : 1];
+#pragma unroll
+        for (int j = 0; j < NP; j++) cp[j] = __byte_perm(c[2 * j], c[2 * j + 1], 0x5410);
+        uint32_t tlo = 0, flo = 0;
+        for (uint32_t b = g.tbits; b; b >>= 1) {
+            const uint32_t tt = tlo + b;
+            uint32_t f;
+            if constexpr (NP > 0) {
+                const uint32_t t2 = tt * 0x10001u;
+                uint32_t s2 = 0;
+#pragma unroll
+                for (int j = 0; j < NP; j++) s2 += __vminu2(cp[j], t2);
+                f = (s2 & 0xFFFFu) + (s2 >> 16);
+            } else {
+                f = min(c[0], tt);
+            }
+            if (f < n) {
+                tlo = tt;
+                flo = f;
+            }
+        }
+        const uint32_t r = n - flo; /* >= 1 blocks of pass tlo+1, to SMs with c_s > tlo in ring order */
+        uint32_t E;
+        if constexpr (NP > 0 && SMAX <= 16) {
+            /* E = {s : c_s > tlo}: per pair min(c, tlo+1) - min(c, tlo) is 0/1 in each half */
+            const uint32_t lo2 = tlo * 0x10001u, hi2 = lo2 + 0x10001u;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int j = 0; j < NP; j++) acc += (__vminu2(cp[j], hi2) - __vminu2(cp[j], lo2)) << (2 * j);
+            E = (acc & 0x5555u) | ((acc >> 15) & 0xAAAAu);
+        } else {
+            E = 0;
+#pragma unroll
+            for (int i = 0; i < SMAX; i++) E |= (c[i] > tlo ? 1u : 0u) << i;
+        }
+        const uint32_t Er = rotr_s<SMAX, FULL>(E, in.cur, S);
+        const uint32_t p = select_bit<SMAX>(Er, r);
+        const uint32_t Xr = Er & ((2u << p) - 1u); /* first r eligible SMs from the cursor */
+        const uint32_t X = rotr_s<SMAX, FULL>(Xr, S - in.cur, S);
+        const uint32_t nc = in.cur + p + 1u;
+        o.cur = nc >= S ? nc - S : nc; /* cursor = SM of the last block + 1 */
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            const uint32_t x = min(c[i], tlo) + ((X >> i) & 1u);
+            upd(i, in.fa[i] - x * k.dA, in.fb[i] - x * k.dB);
+        }
+        o.I = in.I + (uint64_t)n * k.A;
+        o.M = in.M + (uint64_t)n * k.M;
+        o.K = in.K;
+    }
     rec.add(kid, n);
+    return o;
 }
 
-/* Last kernel of an order: only its round split matters, not the SM state. */
-template <int SMAX, class R>
-__device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, uint32_t kid, const RkGTab& g,
-                                           R& rec) {
-    uint32_t c[SMAX];
-    uint32_t F = sm_caps<SMAX>(s, k, c);
+template <int SMAX>
+struct StoreUpd {
+    St<SMAX>& out;
+    __device__ __forceinline__ void operator()(int i, uint32_t a, uint32_t b) {
+        out.fa[i] = a;
+        out.fb[i] = b;
+    }
+};
+
+struct CapSumUpd { /* consume the new words: capacity sum for the next kernel */
+    CapK k;
+    uint32_t F;
+    __device__ __forceinline__ void operator()(int, uint32_t a, uint32_t b) { F += cap1(a, b, k); }
+};
+
+template <int SMAX, bool FULL, class R>
+__device__ __forceinline__ void place(const St<SMAX>& in, St<SMAX>& out, const RkKTab& k, uint32_t kid,
+                                      const RkGTab& g, R& rec) {
+    StoreUpd<SMAX> u{out};
+    const Placed o = place_core<SMAX, FULL>(in, k, kid, g, rec, u);
+    out.cur = o.cur;
+    out.I = o.I;
+    out.M = o.M;
+    out.K = o.K;
+}
+
+/* The last kernel of an order: only its split into the open round and fresh
+ * rounds matters (F = its total capacity on the final state). */
+template <class R>
+__device__ __forceinline__ uint64_t finish_key(uint32_t F, uint64_t I, uint64_t M, uint64_t K, const RkKTab& k,
+                                               uint32_t kid, const RkGTab& g, R& rec) {
     uint32_t n = k.T;
-    uint64_t I = s.I, M = s.M, K = s.K;
     if (n <= F) {
         rec.add(kid, n);
         rec.close();
@@ -198,7 +291,7 @@ __device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, u
     rec.close();
     K += round_key(I + (uint64_t)F * k.A, M + (uint64_t)F * k.M, g.num, g.den);
     n -= F;
-    uint32_t nfull = (n - 1u) / k.SC;
+    const uint32_t nfull = (n - 1u) / k.SC;
     K += (uint64_t)nfull * k.fullkey;
     rec.full(kid, nfull, k.SC);
     n -= nfull * k.SC;
@@ -207,11 +300,31 @@ __device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, u
     return K + round_key((uint64_t)n * k.A, (uint64_t)n * k.M, g.num, g.den);
 }
 
+template <int SMAX, class R>
+__device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, uint32_t kid, const RkGTab& g,
+                                           R& rec) {
+    const CapK ck = capk(k);
+    uint32_t F = 0;
+#pragma unroll
+    for (int i = 0; i < SMAX; i++) F += cap1(s.fa[i], s.fb[i], ck);
+    return finish_key(F, s.I, s.M, s.K, k, kid, g, rec);
+}
+
+/* place kb on `in`, then evaluate the last kernel kc — leaf of the suffix tree */
+template <int SMAX, bool FULL>
+__device__ __forceinline__ uint64_t place_finish(const St<SMAX>& in, const RkKTab& kb, uint32_t kbid,
+                                                 const RkKTab& kc, uint32_t kcid, const RkGTab& g) {
+    NoRec nr;
+    CapSumUpd u{capk(kc), 0u};
+    const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
+    return finish_key(u.F, o.I, o.M, o.K, kc, kcid, g, nr);
+}
+
 /* Nibble list of unused kernels, ascending: remove and return entry d. */
 __device__ __forceinline__ uint32_t take_nibble(uint64_t& L, uint32_t d) {
-    uint32_t sh = 4u * d;
-    uint32_t v = (uint32_t)(L >> sh) & 15u;
-    uint64_t low = L & ((1ull << sh) - 1ull);
+    const uint32_t sh = 4u * d;
+    const uint32_t v = (uint32_t)(L >> sh) & 15u;
+    const uint64_t low = L & ((1ull << sh) - 1ull);
     L = low | ((L >> (sh + 4u)) << sh);
     return v;
 }
@@ -222,22 +335,24 @@ __device__ __forceinline__ uint64_t identity_list(uint32_t n) {
 }
 
 /* Key of one lexicographic index, from scratch (candidate, samples, n < 3). */
-template <int SMAX, class R>
+template <int SMAX, bool FULL, class R>
 __device__ uint64_t eval_index(const RkTables& t, uint32_t idx, R& rec) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
     St<SMAX> s;
-    st_fresh<SMAX>(s, g);
+    st_fresh<SMAX, FULL>(s, g);
     uint64_t L = identity_list(n);
     uint32_t rem = idx;
     for (uint32_t j = 0; j + 1 < n; j++) {
-        uint32_t f = g.fact[n - 1 - j];
-        uint32_t d = rem / f;
+        const uint32_t f = g.fact[n - 1 - j];
+        const uint32_t d = rem / f;
         rem -= d * f;
-        uint32_t k = take_nibble(L, d);
-        place<SMAX>(s, t.k[k], k, g, rec);
+        const uint32_t k = take_nibble(L, d);
+        St<SMAX> s2;
+        place<SMAX, FULL>(s, s2, t.k[k], k, g, rec);
+        s = s2;
     }
-    uint32_t k = (uint32_t)L & 15u;
+    const uint32_t k = (uint32_t)L & 15u;
     return finish<SMAX>(s, t.k[k], k, g, rec);
 }
 
@@ -365,38 +480,37 @@ __device__ void commit(const rk_stats& cta, rk_stats* recs, uint32_t* counter, r
     }
 }
 
-template <int SMAX>
+
+template <int SMAX, bool FULL>
 __device__ __forceinline__ void eval_run(const RkTables& t, uint32_t run, uint32_t lo, uint32_t hi, uint64_t cand,
                                          uint64_t* keys, uint32_t first, TStats& ts) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
     NoRec nr;
-    uint32_t idx0 = run * 6u;
+    const uint32_t idx0 = run * 6u;
     St<SMAX> s0;
-    st_fresh<SMAX>(s0, g);
+    st_fresh<SMAX, FULL>(s0, g);
     uint64_t L = identity_list(n);
     uint32_t rem = idx0;
-    for (uint32_t j = 0; j + 3 < n; j++) {
-        uint32_t f = g.fact[n - 1 - j];
-        uint32_t d = rem / f;
+    for (uint32_t j = 0; j + 3 < n; j++) { /* shared (n-3)-prefix */
+        const uint32_t f = g.fact[n - 1 - j];
+        const uint32_t d = rem / f;
         rem -= d * f;
-        uint32_t k = take_nibble(L, d);
-        place<SMAX>(s0, t.k[k], k, g, nr);
+        const uint32_t k = take_nibble(L, d);
+        place<SMAX, FULL>(s0, s0, t.k[k], k, g, nr);
     }
     const uint32_t r0 = (uint32_t)L & 15u, r1 = (uint32_t)(L >> 4) & 15u, r2 = (uint32_t)(L >> 8) & 15u;
 #pragma unroll 1
     for (uint32_t a = 0; a < 3; a++) {
         const uint32_t ka = a == 0 ? r0 : (a == 1 ? r1 : r2);
         const uint32_t kb0 = a == 0 ? r1 : r0, kb1 = a == 2 ? r1 : r2;
-        St<SMAX> s1 = s0;
-        place<SMAX>(s1, t.k[ka], ka, g, nr);
+        St<SMAX> s1;
+        place<SMAX, FULL>(s0, s1, t.k[ka], ka, g, nr);
 #pragma unroll 1
         for (uint32_t b = 0; b < 2; b++) {
             const uint32_t kb = b == 0 ? kb0 : kb1, kc = b == 0 ? kb1 : kb0;
-            St<SMAX> s2 = s1;
-            place<SMAX>(s2, t.k[kb], kb, g, nr);
-            uint64_t K = finish<SMAX>(s2, t.k[kc], kc, g, nr);
-            uint32_t idx = idx0 + a * 2u + b;
+            const uint64_t K = place_finish<SMAX, FULL>(s1, t.k[kb], kb, t.k[kc], kc, g);
+            const uint32_t idx = idx0 + a * 2u + b;
             if (idx >= lo && idx < hi) {
                 ts.add(K, idx, cand);
                 if (keys) keys[idx - first] = K;
@@ -412,11 +526,14 @@ __device__ __forceinline__ void load_tables(RkTables& sm, const RkTables* src) {
     __syncthreads();
 }
 
-template <int SMAX>
-__global__ void __launch_bounds__(kThreads) rk_eval_kernel(const RkTables* __restrict__ tab, uint32_t first,
-                                                          uint32_t count, const uint64_t* cand_dev,
-                                                          uint64_t cand_imm, rk_stats* out, uint64_t* keys,
-                                                          rk_stats* recs, uint32_t* counter) {
+#ifndef RK_EVAL_MIN_BLOCKS
+#define RK_EVAL_MIN_BLOCKS 1
+#endif
+
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kThreads, RK_EVAL_MIN_BLOCKS)
+    rk_eval_kernel(const RkTables* __restrict__ tab, uint32_t first, uint32_t count, const uint64_t* cand_dev,
+                   uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter) {
     __shared__ RkTables t;
     load_tables(t, tab);
     const uint64_t cand = cand_dev ? *cand_dev : cand_imm;
@@ -426,24 +543,25 @@ __global__ void __launch_bounds__(kThreads) rk_eval_kernel(const RkTables* __res
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
     if (t.g.n >= 3) {
         const uint32_t rb = lo / 6u, re = (hi + 5u) / 6u;
-        for (uint32_t run = rb + gtid; run < re; run += nth) eval_run<SMAX>(t, run, lo, hi, cand, keys, first, ts);
+        for (uint32_t run = rb + gtid; run < re; run += nth)
+            eval_run<SMAX, FULL>(t, run, lo, hi, cand, keys, first, ts);
     } else {
         NoRec nr;
         for (uint32_t idx = lo + gtid; idx < hi; idx += nth) {
-            uint64_t K = eval_index<SMAX>(t, idx, nr);
+            const uint64_t K = eval_index<SMAX, FULL>(t, idx, nr);
             ts.add(K, idx, cand);
             if (keys) keys[idx - first] = K;
         }
     }
-    rk_stats r = block_reduce(to_rec(ts));
+    const rk_stats r = block_reduce(to_rec(ts));
     commit(r, recs, counter, out);
 }
 
-/* C5 batch: blockIdx.y = set, blockIdx.x = chunk of that set's runs. */
-template <int SMAX>
-__global__ void __launch_bounds__(kThreads) rk_batch_kernel(const RkTables* __restrict__ tabs,
-                                                           const uint64_t* __restrict__ cand_keys,
-                                                           rk_stats* recs) {
+/* C5 batch: blockIdx.y = set, blockIdx.x = chunk of that set's runs.  All sets
+ * of one launch share the variant (max super-SM count over the batch). */
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kThreads, RK_EVAL_MIN_BLOCKS)
+    rk_batch_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ cand_keys, rk_stats* recs) {
     __shared__ RkTables t;
     const uint32_t set = blockIdx.y;
     load_tables(t, tabs + set);
@@ -457,12 +575,13 @@ __global__ void __launch_bounds__(kThreads) rk_batch_kernel(const RkTables* __re
         const uint32_t per = (runs + gridDim.x - 1) / gridDim.x;
         const uint32_t rb = blockIdx.x * per, re = min(runs, rb + per);
         for (uint32_t run = rb + threadIdx.x; run < re; run += blockDim.x)
-            eval_run<SMAX>(t, run, 0u, total, cand, nullptr, 0u, ts);
+            eval_run<SMAX, FULL>(t, run, 0u, total, cand, nullptr, 0u, ts);
     } else if (blockIdx.x == 0) {
         NoRec nr;
-        for (uint32_t idx = threadIdx.x; idx < total; idx += blockDim.x) ts.add(eval_index<SMAX>(t, idx, nr), idx, cand);
+        for (uint32_t idx = threadIdx.x; idx < total; idx += blockDim.x)
+            ts.add(eval_index<SMAX, FULL>(t, idx, nr), idx, cand);
     }
-    rk_stats r = block_reduce(to_rec(ts));
+    const rk_stats r = block_reduce(to_rec(ts));
     if (threadIdx.x == 0) recs[set * gridDim.x + blockIdx.x] = r;
 }
 
@@ -482,44 +601,36 @@ __global__ void rk_merge_groups_kernel(const rk_stats* __restrict__ in, uint32_t
     if (lane == 0) out[w] = v;
 }
 
-template <int SMAX>
+/* keys of explicit indices; per_set: item i uses tabs[i], else tabs[0] */
+template <int SMAX, bool FULL>
 __global__ void rk_keys_of_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ idx, uint32_t m,
-                                  uint64_t* __restrict__ out) {
+                                  int per_set, uint64_t* __restrict__ out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     NoRec nr;
-    out[i] = eval_index<SMAX>(tabs[i], (uint32_t)idx[i], nr);
+    out[i] = eval_index<SMAX, FULL>(tabs[per_set ? i : 0], (uint32_t)idx[i], nr);
 }
 
-template <int SMAX>
-__global__ void rk_keys_of_same_kernel(const RkTables* __restrict__ tab, const uint64_t* __restrict__ idx,
-                                       uint32_t m, uint64_t* __restrict__ out) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    NoRec nr;
-    out[i] = eval_index<SMAX>(*tab, (uint32_t)idx[i], nr);
-}
-
-template <int SMAX>
+template <int SMAX, bool FULL>
 __global__ void rk_key_of_index_kernel(const RkTables* __restrict__ tab, uint32_t index, uint64_t* __restrict__ out) {
     __shared__ RkTables t;
     load_tables(t, tab);
     if (threadIdx.x == 0) {
         NoRec nr;
-        *out = eval_index<SMAX>(t, index, nr);
+        *out = eval_index<SMAX, FULL>(t, index, nr);
     }
 }
 
-template <int SMAX>
+template <int SMAX, bool FULL>
 __global__ void rk_simulate_kernel(const RkTables* __restrict__ tab, const int32_t* __restrict__ order,
                                    uint32_t* rounds, uint32_t max_rounds, uint32_t* n_rounds, uint64_t* key) {
     const RkTables& t = *tab;
     const uint32_t n = t.g.n;
     for (uint32_t i = 0; i < max_rounds * n; i++) rounds[i] = 0;
-    Rec rec{rounds, max_rounds, n, 0};
+    Rec rec{rounds, max_rounds, n, 0, t.g.blkscale};
     St<SMAX> s;
-    st_fresh<SMAX>(s, t.g);
-    for (uint32_t j = 0; j + 1 < n; j++) place<SMAX>(s, t.k[order[j]], (uint32_t)order[j], t.g, rec);
+    st_fresh<SMAX, FULL>(s, t.g);
+    for (uint32_t j = 0; j + 1 < n; j++) place<SMAX, FULL>(s, s, t.k[order[j]], (uint32_t)order[j], t.g, rec);
     *key = finish<SMAX>(s, t.k[order[n - 1]], (uint32_t)order[n - 1], t.g, rec);
     *n_rounds = rec.r;
 }
@@ -580,17 +691,72 @@ int num_sms() {
     return g_num_sms;
 }
 
-template <int SMAX>
+template <int SMAX, bool FULL>
 int eval_ctas_per_sm() {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_eval_kernel<SMAX>, kThreads, 0);
-    return b > 0 ? b : 1;
+    static int cached = 0;
+    if (!cached) {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_eval_kernel<SMAX, FULL>, kThreads, 0);
+        cached = b > 0 ? b : 1;
+    }
+    return cached;
+}
+
+/* variant index for a (reduced) SM count S: the smallest power of two >= S,
+ * FULL when equal */
+int variant(uint32_t S) {
+    if (S <= 1) return 0;
+    if (S == 2) return 1;
+    if (S < 4) return 2;
+    if (S == 4) return 3;
+    if (S < 8) return 4;
+    if (S == 8) return 5;
+    if (S < 16) return 6;
+    if (S == 16) return 7;
+    if (S < 32) return 8;
+    return 9;
 }
 
 } /* namespace */
 
+/* Instantiate KERNEL<SMAX, FULL> for the (reduced) SM count. */
+#define RK_DISPATCH(S, KERNEL, CFG, ...)                                     \
+    do {                                                                      \
+        switch (variant(S)) {                                                 \
+            case 0: KERNEL<1, true><<<CFG>>>(__VA_ARGS__); break;             \
+            case 1: KERNEL<2, true><<<CFG>>>(__VA_ARGS__); break;             \
+            case 2: KERNEL<4, false><<<CFG>>>(__VA_ARGS__); break;            \
+            case 3: KERNEL<4, true><<<CFG>>>(__VA_ARGS__); break;             \
+            case 4: KERNEL<8, false><<<CFG>>>(__VA_ARGS__); break;            \
+            case 5: KERNEL<8, true><<<CFG>>>(__VA_ARGS__); break;             \
+            case 6: KERNEL<16, false><<<CFG>>>(__VA_ARGS__); break;           \
+            case 7: KERNEL<16, true><<<CFG>>>(__VA_ARGS__); break;            \
+            case 8: KERNEL<32, false><<<CFG>>>(__VA_ARGS__); break;           \
+            default: KERNEL<32, true><<<CFG>>>(__VA_ARGS__); break;           \
+        }                                                                     \
+    } while (0)
+/* generic (runtime-S) variant for the single-thread helpers */
+#define RK_DISPATCH_GENERIC(S, KERNEL, CFG, ...)                              \
+    do {                                                                      \
+        if ((S) <= 16) KERNEL<16, false><<<CFG>>>(__VA_ARGS__);               \
+        else KERNEL<32, false><<<CFG>>>(__VA_ARGS__);                         \
+    } while (0)
+#define RK_CFG(...) __VA_ARGS__
+
 int rk_eval_max_ctas(uint32_t S, int) {
-    int per = S <= 16 ? eval_ctas_per_sm<16>() : eval_ctas_per_sm<32>();
+    int per;
+    switch (variant(S)) {
+        case 0: per = eval_ctas_per_sm<1, true>(); break;
+        case 1: per = eval_ctas_per_sm<2, true>(); break;
+        case 2: per = eval_ctas_per_sm<4, false>(); break;
+        case 3: per = eval_ctas_per_sm<4, true>(); break;
+        case 4: per = eval_ctas_per_sm<8, false>(); break;
+        case 5: per = eval_ctas_per_sm<8, true>(); break;
+        case 6: per = eval_ctas_per_sm<16, false>(); break;
+        case 7: per = eval_ctas_per_sm<16, true>(); break;
+        case 8: per = eval_ctas_per_sm<32, false>(); break;
+        default: per = eval_ctas_per_sm<32, true>(); break;
+    }
     return per * num_sms();
 }
 
@@ -598,18 +764,14 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
                    rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
     cudaStream_t st = (cudaStream_t)stream;
-    uint64_t units = n >= 3 ? ((first + count + 5) / 6 - first / 6) : count;
+    const uint64_t units = n >= 3 ? ((first + count + 5) / 6 - first / 6) : count;
     uint64_t ctas = (units + kThreads - 1) / kThreads;
+    const uint64_t cap = (uint64_t)rk_eval_max_ctas(S, 0);
+    if (ctas > cap) ctas = cap;
     if (ctas > max_ctas) ctas = max_ctas;
     if (ctas < 1) ctas = 1;
-    if (S <= 16)
-        rk_eval_kernel<16><<<(unsigned)ctas, kThreads, 0, st>>>(tab_dev, (uint32_t)first, (uint32_t)count,
-                                                                  cand_key_dev, cand_key_imm, stats_dev, keys_dev,
-                                                                  recs, counter);
-    else
-        rk_eval_kernel<32><<<(unsigned)ctas, kThreads, 0, st>>>(tab_dev, (uint32_t)first, (uint32_t)count,
-                                                                  cand_key_dev, cand_key_imm, stats_dev, keys_dev,
-                                                                  recs, counter);
+    RK_DISPATCH(S, rk_eval_kernel, RK_CFG((unsigned)ctas, kThreads, 0, st), tab_dev, (uint32_t)first,
+                (uint32_t)count, cand_key_dev, cand_key_imm, stats_dev, keys_dev, recs, counter);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -624,10 +786,10 @@ int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin,
                         const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream,
                         uint32_t* launches) {
     uint64_t ctas = (count + 1023) / 1024;
-    uint64_t cap = (uint64_t)num_sms() * 8;
+    const uint64_t cap = (uint64_t)num_sms() * 8;
     if (ctas > cap) ctas = cap;
     if (ctas < 1) ctas = 1;
-    size_t smem = (size_t)bins * 4;
+    const size_t smem = (size_t)bins * 4;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(rk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     rk_hist_kernel<<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, kmin, kmax, range_dev, bins,
@@ -639,26 +801,24 @@ int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin,
 int rk_launch_keys_of(const RkTables* tabs_dev, uint32_t n, uint32_t S, const uint64_t* idx_dev, uint32_t m,
                       uint64_t* out_dev, void* stream, uint32_t* launches) {
     (void)n;
-    unsigned blocks = (m + 127) / 128;
-    if (S <= 16) rk_keys_of_kernel<16><<<blocks, 128, 0, (cudaStream_t)stream>>>(tabs_dev, idx_dev, m, out_dev);
-    else rk_keys_of_kernel<32><<<blocks, 128, 0, (cudaStream_t)stream>>>(tabs_dev, idx_dev, m, out_dev);
+    const unsigned blocks = (m + 127) / 128;
+    RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tabs_dev, idx_dev, m, 1, out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
 
 int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* idx_dev, uint32_t m,
                            uint64_t* out_dev, void* stream, uint32_t* launches) {
-    unsigned blocks = (m + 127) / 128;
-    if (S <= 16) rk_keys_of_same_kernel<16><<<blocks, 128, 0, (cudaStream_t)stream>>>(tab_dev, idx_dev, m, out_dev);
-    else rk_keys_of_same_kernel<32><<<blocks, 128, 0, (cudaStream_t)stream>>>(tab_dev, idx_dev, m, out_dev);
+    const unsigned blocks = (m + 127) / 128;
+    RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tab_dev, idx_dev, m, 0, out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
 
 int rk_launch_key_of_index(const RkTables* tab_dev, uint32_t S, uint64_t index, uint64_t* out_dev, void* stream,
                            uint32_t* launches) {
-    if (S <= 16) rk_key_of_index_kernel<16><<<1, 32, 0, (cudaStream_t)stream>>>(tab_dev, (uint32_t)index, out_dev);
-    else rk_key_of_index_kernel<32><<<1, 32, 0, (cudaStream_t)stream>>>(tab_dev, (uint32_t)index, out_dev);
+    RK_DISPATCH_GENERIC(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, (uint32_t)index,
+                out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -667,12 +827,8 @@ int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const in
                        uint32_t max_rounds, uint32_t* n_rounds_dev, uint64_t* key_dev, void* stream,
                        uint32_t* launches) {
     (void)n;
-    if (S <= 16)
-        rk_simulate_kernel<16><<<1, 1, 0, (cudaStream_t)stream>>>(tab_dev, order_dev, rounds_dev, max_rounds,
-                                                                   n_rounds_dev, key_dev);
-    else
-        rk_simulate_kernel<32><<<1, 1, 0, (cudaStream_t)stream>>>(tab_dev, order_dev, rounds_dev, max_rounds,
-                                                                   n_rounds_dev, key_dev);
+    RK_DISPATCH_GENERIC(S, rk_simulate_kernel, RK_CFG(1, 1, 0, (cudaStream_t)stream), tab_dev, order_dev, rounds_dev,
+                max_rounds, n_rounds_dev, key_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -681,7 +837,7 @@ int rk_batch_chunks_per_set(uint32_t n) {
     if (n < 3) return 1;
     uint64_t f = 1;
     for (uint32_t i = 2; i <= n; i++) f *= i;
-    uint64_t runs = f / 6;
+    const uint64_t runs = f / 6;
     uint64_t chunks = (runs + kThreads * 4 - 1) / (kThreads * 4); /* ~4 runs per thread */
     if (chunks < 1) chunks = 1;
     if (chunks > 65535) chunks = 65535;
@@ -692,13 +848,21 @@ int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n
                     rk_stats* out_dev, rk_stats* recs, uint32_t chunks, void* stream, uint32_t* launches) {
     (void)n;
     cudaStream_t st = (cudaStream_t)stream;
-    dim3 grid(chunks, n_sets);
-    if (S <= 16) rk_batch_kernel<16><<<grid, kThreads, 0, st>>>(tabs_dev, cand_keys_dev, recs);
-    else rk_batch_kernel<32><<<grid, kThreads, 0, st>>>(tabs_dev, cand_keys_dev, recs);
+    const dim3 grid(chunks, n_sets);
+    /* S = max reduced SM count over the batch, | 0x80000000 when every set has
+     * the same reduced count (then the compile-time variant is exact); otherwise
+     * the runtime-S variant runs every set with its own count. */
+    const bool uniform = (S & 0x80000000u) != 0;
+    const uint32_t Sm = S & 0x7FFFFFFFu;
+    if (uniform) {
+        RK_DISPATCH(Sm, rk_batch_kernel, RK_CFG(grid, kThreads, 0, st), tabs_dev, cand_keys_dev, recs);
+    } else {
+        RK_DISPATCH_GENERIC(Sm, rk_batch_kernel, RK_CFG(grid, kThreads, 0, st), tabs_dev, cand_keys_dev, recs);
+    }
     if (launches) (*launches)++;
-    int e = (int)cudaGetLastError();
+    const int e = (int)cudaGetLastError();
     if (e) return e;
-    unsigned blocks = (n_sets * 32 + 255) / 256;
+    const unsigned blocks = (n_sets * 32 + 255) / 256;
     rk_merge_groups_kernel<<<blocks, 256, 0, st>>>(recs, n_sets, chunks, out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();

@@ -13,7 +13,7 @@ import os
 from dataclasses import dataclass
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librk.so")
+LIB_PATH = os.environ.get("RK_LIB", os.path.join(HERE, "librk.so"))
 
 RK_OK, RK_EINVAL, RK_EINFEASIBLE, RK_ETOOMANY, RK_EMISSINGRATIO, RK_EOVERFLOW, RK_ESTATE, RK_ECUDA, \
     RK_ENODEVICE, RK_EUNSUPPORTED = range(10)

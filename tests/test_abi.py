@@ -109,9 +109,14 @@ def test_bad_gpu_params():
     with pytest.raises(rk.RkError) as e:
         c.rk_set_gpu_params((0, 32768, 49152, 48, 8, 411, 100))
     assert e.value.status == rk.RK_EINVAL
+    # 33 SMs: gcd(33, grids 32/16) = 1 -> 33 super-SMs > 32 on the device fast path
+    c.rk_set_gpu_params((33, 32768, 49152, 48, 8, 411, 100))
     with pytest.raises(rk.RkError) as e:
-        c.rk_set_gpu_params((33, 32768, 49152, 48, 8, 411, 100))
+        c.rk_set_kernels(W.W4)
     assert e.value.status == rk.RK_EUNSUPPORTED
+    # 48 SMs with grids that are multiples of 16: reduced to 3 super-SMs, accepted
+    c.rk_set_gpu_params((48, 32768, 49152, 48, 8, 411, 100))
+    c.rk_set_kernels([(48, 128, 20, 0, 311, 100), (96, 256, 24, 0, 1110, 100)])
     c2 = rk.Context(-1)
     with pytest.raises(rk.RkError) as e:
         c2.rk_set_kernels(W.W4)

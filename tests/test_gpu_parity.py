@@ -262,3 +262,27 @@ def test_c5_full_batch_properties(ctx):
     for st, ck in res:
         assert st.evaluated == F and st.n_lt + st.n_eq + st.n_gt == F
         assert st.key_min <= ck <= st.key_max and st.n_eq >= 1
+
+
+def test_symmetry_reduction_equivalence(ctx):
+    """gcd(N_SM, grids) SMs act as one super-SM.  The reduced and
+    unreduced device paths give bit-identical keys; odd grids (g = 1) still match
+    the oracle."""
+    gpu, ks = W.config("C2")  # g = 16 -> 1 super-SM
+    _, k_red = gpu_keys(ctx, gpu, ks)
+    os.environ["RK_NO_REDUCE"] = "1"
+    try:
+        c2 = rk.Context(0)
+        c2.rk_set_gpu_params(gpu)
+        c2.rk_set_kernels(ks)
+        keys = torch.zeros(40320, dtype=torch.int64, device="cuda")
+        c2.rk_eval_range(0, 40320, 0, keys_dev=keys)
+        assert np.array_equal(keys.cpu().numpy().view(np.uint64), k_red)
+        c2.close()
+    finally:
+        del os.environ["RK_NO_REDUCE"]
+    rng = W.SplitMix64(0x0DD)
+    for _ in range(6):
+        sets = W.random_small_sets(rng.next(), 1, 5, 7)
+        ks = [(k[0] + (rng.below(7) if rng.below(2) else 0),) + tuple(k[1:]) for k in sets[0]]
+        check_full_space(ctx, W.GTX580, ks, bins=(5,))
