@@ -187,6 +187,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-reduce-check", action=argparse.BooleanOptionalAction, default=True)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -212,7 +213,7 @@ def main():
     stream = torch.cuda.current_stream()
     N = math.factorial(len(ks))
 
-    ev_eval = []
+    ev_eval, ev_hist = [], []
 
     def step():
         _, idx = sw.heuristic()  # a5: Algorithm 1 on the host (microseconds)
@@ -232,7 +233,11 @@ def main():
             launches += 1
             rngrec = sw.glob
         sw.hist.zero_()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
         c.rk_histogram_async(sw.keys, sw.count, rngrec, sw.bins, sw.hist, stream)
+        h1.record(stream)
+        ev_hist.append((h0, h1))
         launches += 1
         if world > 1:
             all_reduce_hist(sw.hist)
@@ -242,6 +247,7 @@ def main():
         step()
     torch.cuda.synchronize()
     ev_eval.clear()
+    ev_hist.clear()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -261,6 +267,7 @@ def main():
     value = N * args.steps / (ms_max / 1e3)
     eval_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_eval)
     eval_ms_max = max_over_ranks(eval_ms, sw.dev)
+    hist_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_hist)
 
     # correctness of the timed pipeline's result (global record, histogram mass)
     out = torch.cat([sw.glob if world > 1 else sw.rec, sw.hist]).cpu()
@@ -284,10 +291,35 @@ def main():
     e2e_ms = max_over_ranks(a.elapsed_time(b), sw.dev)
     e2e_value = N * e2e_steps / (e2e_ms / 1e3)
 
+    # the same eval kernel without the SM-symmetry reduction, for reference
+    noreduce_ms = None
+    if args.no_reduce_check:
+        os.environ["RK_NO_REDUCE"] = "1"
+        from paper_1511_07983_b200 import rk as _rk
+        c2 = _rk.Context(local)
+        del os.environ["RK_NO_REDUCE"]
+        c2.rk_set_gpu_params(gpu)
+        c2.rk_set_kernels(ks)
+        rec2 = torch.zeros(7, dtype=torch.int64, device=sw.dev)
+        for _ in range(2):
+            c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, sw.keys, stream)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(3):
+            c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, sw.keys, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        noreduce_ms = max_over_ranks(a.elapsed_time(b) / 3, sw.dev)
+        assert torch.equal(rec2, sw.glob if world > 1 else sw.rec) or world > 1
+        c2.close()
+
     clocks = clk.summary()
     if world > 1:
         dist.barrier()
     if rank == 0:
+        from functools import reduce
+        sym_g = reduce(math.gcd, [gpu[0]] + [k[0] for k in ks])
         ops = algorithmic_ops_per_order(ks)
         per_launch_orders = sw.count
         achieved = ops * per_launch_orders / (eval_ms_max / 1e3)
@@ -306,6 +338,11 @@ def main():
                            "shards": world, "parallelism": f"index-space shards x{world}",
                            "l2": "keys array 8 B/order (3.83 GB at N=1) > 126 MB L2; eval phase reads no HBM input"},
                 "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
+                "kernels_ms": {"rk_eval_kernel": eval_ms_max, "rk_hist_kernel": hist_ms,
+                               "step": ms_max / args.steps},
+                "symmetry": {"g": sym_g, "super_sms": gpu[0] // sym_g,
+                             "eval_ms_without_reduction": noreduce_ms,
+                             "note": "gcd(N_SM, grids) SMs act as one super-SM; exact (DESIGN.md §5)"},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sw.h2d_bytes,
                         "d2h_bytes_per_step": sw.d2h_bytes, "steps": e2e_steps},
                 "result": {"best_T": rep.best_key / gpu[6], "best_index": rep.best_index,

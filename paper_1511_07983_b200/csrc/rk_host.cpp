@@ -152,8 +152,13 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
     g.freshA = (uint32_t)(2 * R + 1) | (uint32_t)(2 * Sh + 1) << 16;
     g.freshB = (uint32_t)(2 * p.max_warps_per_sm + 1) | (uint32_t)(2 * p.max_blocks_per_sm + 1) << 16;
     g.smagic = Sred > 1 ? (uint32_t)(((1ull << 32) + Sred - 1) / Sred) : 0u;
-    uint32_t tb = 1;
-    while (tb * 2 <= p.max_blocks_per_sm) tb *= 2;
+    /* binary search over t in [0, N_blk_SM - 1]: top bit = smallest power of two
+     * with 2*tb >= N_blk_SM (0 when N_blk_SM == 1: t is always 0) */
+    uint32_t tb = 0;
+    if (p.max_blocks_per_sm > 1) {
+        tb = 1;
+        while (2 * tb < p.max_blocks_per_sm) tb *= 2;
+    }
     g.tbits = tb;
     g.n = n;
     for (uint32_t i = 0; i <= RK_MAX_N; i++) g.fact[i] = (uint32_t)fact64(i);

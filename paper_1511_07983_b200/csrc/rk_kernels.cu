@@ -481,41 +481,92 @@ __device__ void commit(const rk_stats& cta, rk_stats* recs, uint32_t* counter, r
 }
 
 
-template <int SMAX, bool FULL>
-__device__ __forceinline__ void eval_run(const RkTables& t, uint32_t run, uint32_t lo, uint32_t hi, uint64_t cand,
-                                         uint64_t* keys, uint32_t first, TStats& ts) {
+/* Suffix-tree depth per SM-count variant: placements are cheap for few
+ * (super-)SMs, so share longer prefixes (DESIGN.md §5 "prefix sharing"). */
+template <int SMAX>
+struct Depth {
+    static constexpr int value = SMAX <= 2 ? 5 : (SMAX <= 8 ? 4 : 3);
+};
+__host__ __device__ constexpr uint32_t cfact(int m) { return m <= 1 ? 1u : (uint32_t)m * cfact(m - 1); }
+
+struct Leaf { /* one evaluated order: statistics + optional key store */
+    TStats& ts;
+    uint64_t* keys;
+    uint32_t lo, hi, first;
+    uint64_t cand;
+    __device__ __forceinline__ void operator()(uint32_t idx, uint64_t K) {
+        if (idx >= lo && idx < hi) {
+            ts.add(K, idx, cand);
+            if (keys) keys[idx - first] = K;
+        }
+    }
+};
+
+/* The D kernels left after a prefix are the low D nibbles of `rem` (ascending);
+ * visit their D! orders in lexicographic order, leaf index idx.. idx+D!-1. */
+template <int SMAX, bool FULL, int D>
+__device__ __forceinline__ void dfs(const RkTables& t, const St<SMAX>& s, uint32_t rem, uint32_t idx, Leaf& leaf) {
+    if constexpr (D == 2) {
+        const uint32_t x = rem & 15u, y = (rem >> 4) & 15u;
+        leaf(idx, place_finish<SMAX, FULL>(s, t.k[x], x, t.k[y], y, t.g));
+        leaf(idx + 1u, place_finish<SMAX, FULL>(s, t.k[y], y, t.k[x], x, t.g));
+    } else {
+        NoRec nr;
+#pragma unroll 1
+        for (uint32_t a = 0; a < (uint32_t)D; a++) {
+            const uint32_t sh = 4u * a;
+            const uint32_t ka = (rem >> sh) & 15u;
+            const uint32_t rest = (rem & ((1u << sh) - 1u)) | ((rem >> (sh + 4u)) << sh);
+            St<SMAX> s1;
+            place<SMAX, FULL>(s, s1, t.k[ka], ka, t.g, nr);
+            dfs<SMAX, FULL, D - 1>(t, s1, rest, idx + a * cfact(D - 1), leaf);
+        }
+    }
+}
+
+/* A run = the D! consecutive indices sharing an (n-D)-prefix. */
+template <int SMAX, bool FULL, int D>
+__device__ __forceinline__ void eval_run(const RkTables& t, uint32_t run, Leaf& leaf) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
     NoRec nr;
-    const uint32_t idx0 = run * 6u;
+    const uint32_t idx0 = run * cfact(D);
     St<SMAX> s0;
     st_fresh<SMAX, FULL>(s0, g);
     uint64_t L = identity_list(n);
     uint32_t rem = idx0;
-    for (uint32_t j = 0; j + 3 < n; j++) { /* shared (n-3)-prefix */
+    for (uint32_t j = 0; j + D < n; j++) { /* shared (n-D)-prefix */
         const uint32_t f = g.fact[n - 1 - j];
         const uint32_t d = rem / f;
         rem -= d * f;
         const uint32_t k = take_nibble(L, d);
         place<SMAX, FULL>(s0, s0, t.k[k], k, g, nr);
     }
-    const uint32_t r0 = (uint32_t)L & 15u, r1 = (uint32_t)(L >> 4) & 15u, r2 = (uint32_t)(L >> 8) & 15u;
-#pragma unroll 1
-    for (uint32_t a = 0; a < 3; a++) {
-        const uint32_t ka = a == 0 ? r0 : (a == 1 ? r1 : r2);
-        const uint32_t kb0 = a == 0 ? r1 : r0, kb1 = a == 2 ? r1 : r2;
-        St<SMAX> s1;
-        place<SMAX, FULL>(s0, s1, t.k[ka], ka, g, nr);
-#pragma unroll 1
-        for (uint32_t b = 0; b < 2; b++) {
-            const uint32_t kb = b == 0 ? kb0 : kb1, kc = b == 0 ? kb1 : kb0;
-            const uint64_t K = place_finish<SMAX, FULL>(s1, t.k[kb], kb, t.k[kc], kc, g);
-            const uint32_t idx = idx0 + a * 2u + b;
-            if (idx >= lo && idx < hi) {
-                ts.add(K, idx, cand);
-                if (keys) keys[idx - first] = K;
-            }
-        }
+    dfs<SMAX, FULL, D>(t, s0, (uint32_t)L, idx0, leaf);
+}
+
+/* All runs of [lo, hi) handled by this thread (stride over the grid). */
+template <int SMAX, bool FULL, int D>
+__device__ __forceinline__ void eval_runs(const RkTables& t, uint32_t lo, uint32_t hi, uint32_t tid, uint32_t nth,
+                                          Leaf& leaf) {
+    constexpr uint32_t R = cfact(D);
+    const uint32_t rb = lo / R, re = (hi + R - 1u) / R;
+    for (uint32_t run = rb + tid; run < re; run += nth) eval_run<SMAX, FULL, D>(t, run, leaf);
+}
+
+/* n-dependent depth: D = min(n, Depth<SMAX>); n == 1 evaluates the single order. */
+template <int SMAX, bool FULL>
+__device__ __forceinline__ void eval_space(const RkTables& t, uint32_t lo, uint32_t hi, uint32_t tid, uint32_t nth,
+                                           Leaf& leaf) {
+    constexpr int DM = Depth<SMAX>::value;
+    const uint32_t n = t.g.n;
+    if (n >= (uint32_t)DM) eval_runs<SMAX, FULL, DM>(t, lo, hi, tid, nth, leaf);
+    else if (DM > 4 && n == 4) eval_runs<SMAX, FULL, (DM > 4 ? 4 : 2)>(t, lo, hi, tid, nth, leaf);
+    else if (DM > 3 && n == 3) eval_runs<SMAX, FULL, (DM > 3 ? 3 : 2)>(t, lo, hi, tid, nth, leaf);
+    else if (n == 2) eval_runs<SMAX, FULL, 2>(t, lo, hi, tid, nth, leaf);
+    else if (tid == 0 && lo < hi) {
+        NoRec nr;
+        leaf(0, eval_index<SMAX, FULL>(t, 0, nr));
     }
 }
 
@@ -526,12 +577,19 @@ __device__ __forceinline__ void load_tables(RkTables& sm, const RkTables* src) {
     __syncthreads();
 }
 
-#ifndef RK_EVAL_MIN_BLOCKS
-#define RK_EVAL_MIN_BLOCKS 1
+/* CTAs per SM the register allocator must allow: few (super-)SMs keep the
+ * state small, so trade registers for occupancy (measured). */
+template <int SMAX>
+struct MinBlocks {
+#ifdef RK_EVAL_MIN_BLOCKS
+    static constexpr int value = RK_EVAL_MIN_BLOCKS;
+#else
+    static constexpr int value = SMAX <= 4 ? 2 : 1;
 #endif
+};
 
 template <int SMAX, bool FULL>
-__global__ void __launch_bounds__(kThreads, RK_EVAL_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     rk_eval_kernel(const RkTables* __restrict__ tab, uint32_t first, uint32_t count, const uint64_t* cand_dev,
                    uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter) {
     __shared__ RkTables t;
@@ -541,18 +599,8 @@ __global__ void __launch_bounds__(kThreads, RK_EVAL_MIN_BLOCKS)
     TStats ts;
     ts.init();
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    if (t.g.n >= 3) {
-        const uint32_t rb = lo / 6u, re = (hi + 5u) / 6u;
-        for (uint32_t run = rb + gtid; run < re; run += nth)
-            eval_run<SMAX, FULL>(t, run, lo, hi, cand, keys, first, ts);
-    } else {
-        NoRec nr;
-        for (uint32_t idx = lo + gtid; idx < hi; idx += nth) {
-            const uint64_t K = eval_index<SMAX, FULL>(t, idx, nr);
-            ts.add(K, idx, cand);
-            if (keys) keys[idx - first] = K;
-        }
-    }
+    Leaf leaf{ts, keys, lo, hi, first, cand};
+    eval_space<SMAX, FULL>(t, lo, hi, gtid, nth, leaf);
     const rk_stats r = block_reduce(to_rec(ts));
     commit(r, recs, counter, out);
 }
@@ -560,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, RK_EVAL_MIN_BLOCKS)
 /* C5 batch: blockIdx.y = set, blockIdx.x = chunk of that set's runs.  All sets
  * of one launch share the variant (max super-SM count over the batch). */
 template <int SMAX, bool FULL>
-__global__ void __launch_bounds__(kThreads, RK_EVAL_MIN_BLOCKS)
+__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     rk_batch_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ cand_keys, rk_stats* recs) {
     __shared__ RkTables t;
     const uint32_t set = blockIdx.y;
@@ -570,17 +618,13 @@ __global__ void __launch_bounds__(kThreads, RK_EVAL_MIN_BLOCKS)
     const uint32_t total = t.g.fact[n];
     TStats ts;
     ts.init();
-    if (n >= 3) {
-        const uint32_t runs = total / 6u;
-        const uint32_t per = (runs + gridDim.x - 1) / gridDim.x;
-        const uint32_t rb = blockIdx.x * per, re = min(runs, rb + per);
-        for (uint32_t run = rb + threadIdx.x; run < re; run += blockDim.x)
-            eval_run<SMAX, FULL>(t, run, 0u, total, cand, nullptr, 0u, ts);
-    } else if (blockIdx.x == 0) {
-        NoRec nr;
-        for (uint32_t idx = threadIdx.x; idx < total; idx += blockDim.x)
-            ts.add(eval_index<SMAX, FULL>(t, idx, nr), idx, cand);
-    }
+    /* chunk c of the set's index space, aligned to the run size */
+    const uint32_t R = cfact(n < (uint32_t)Depth<SMAX>::value ? (int)n : Depth<SMAX>::value);
+    const uint32_t runs = (total + R - 1) / R;
+    const uint32_t per = (runs + gridDim.x - 1) / gridDim.x;
+    const uint32_t lo = min(total, blockIdx.x * per * R), hi = min(total, lo + per * R);
+    Leaf leaf{ts, nullptr, lo, hi, 0u, cand};
+    eval_space<SMAX, FULL>(t, lo, hi, threadIdx.x, blockDim.x, leaf);
     const rk_stats r = block_reduce(to_rec(ts));
     if (threadIdx.x == 0) recs[set * gridDim.x + blockIdx.x] = r;
 }
@@ -635,46 +679,97 @@ __global__ void rk_simulate_kernel(const RkTables* __restrict__ tab, const int32
     *n_rounds = rec.r;
 }
 
-/* Fig. 1 histogram: exact integer bins over [kmin, kmax]. */
-__global__ void rk_hist_kernel(const uint64_t* __restrict__ keys, uint64_t count, uint64_t kmin_imm,
-                               uint64_t kmax_imm, const rk_stats* __restrict__ range, uint32_t bins,
-                               uint64_t* __restrict__ hist) {
+/* Fig. 1 histogram: exact integer bins over [kmin, kmax]:
+ * bin = min(B-1, floor((K-kmin)*B / (kmax-kmin))).  HBM-bound pass: each
+ * thread reads 8 consecutive keys (two 32-B vector loads; a warp reads 2 KB
+ * contiguous), run-length merges equal bins (lexicographic neighbours have
+ * close keys) before one shared-memory atomic per run; u64 global atomics at
+ * the end (integer adds: order-free, bit-exact). */
+struct BinCalc {
+    uint64_t kmin, D, inv;
+    uint32_t bins, m32, kmin32, D32;
+    bool fast;   /* D*bins < 2^63: 64-bit products suffice */
+    bool fast32; /* bins <= D < 2^32: 32-bit offset, 32-bit magic, one exact correction */
+    __device__ __forceinline__ uint32_t operator()(uint64_t K) const {
+        if (fast32) {
+            /* x = K - kmin < 2^32 (keys lie in [kmin, kmax]); q0 = hi(x*m32) with
+             * m32 = floor(2^32*bins/D) is floor(x*bins/D) or one less */
+            const uint32_t x = (uint32_t)K - kmin32;
+            uint32_t q = __umulhi(x, m32);
+            const uint64_t p = (uint64_t)x * bins;
+            q += ((uint64_t)(q + 1u) * D32 <= p) ? 1u : 0u;
+            return min(q, bins - 1u);
+        }
+        if (D == 0) return 0;
+        const uint64_t x = K <= kmin ? 0ull : (K - kmin >= D ? D : K - kmin);
+        uint64_t q;
+        if (fast) {
+            const uint64_t p = x * (uint64_t)bins;
+            q = __umul64hi(p, inv); /* <= floor(p/D), at most 2 below */
+            while ((q + 1) * D <= p) q++;
+        } else { /* exact 128-bit: b*D <= x*bins < (b+1)*D */
+            const uint64_t plo = x * (uint64_t)bins, phi = __umul64hi(x, (uint64_t)bins);
+            q = (uint64_t)((double)x * ((double)bins / (double)D));
+            if (q > bins) q = bins;
+            for (;;) {
+                const uint64_t qlo = q * D, qhi = __umul64hi(q, D);
+                if (q > 0 && (qhi > phi || (qhi == phi && qlo > plo))) q--;
+                else break;
+            }
+            for (;;) {
+                const uint64_t b1 = q + 1, qlo = b1 * D, qhi = __umul64hi(b1, D);
+                if (qhi < phi || (qhi == phi && qlo <= plo)) q++;
+                else break;
+            }
+        }
+        return q > bins - 1 ? bins - 1 : (uint32_t)q;
+    }
+};
+
+__global__ void __launch_bounds__(256) rk_hist_kernel(const uint64_t* __restrict__ keys, uint64_t count,
+                                                      uint64_t kmin_imm, uint64_t kmax_imm,
+                                                      const rk_stats* __restrict__ range, uint32_t bins,
+                                                      uint64_t* __restrict__ hist) {
     extern __shared__ uint32_t sh[];
-    const uint64_t kmin = range ? range->key_min : kmin_imm;
+    BinCalc bc;
+    bc.kmin = range ? range->key_min : kmin_imm;
     const uint64_t kmax = range ? range->key_max : kmax_imm;
-    const uint64_t D = kmax - kmin;
+    bc.D = kmax - bc.kmin;
+    bc.bins = bins;
+    bc.fast = bc.D != 0 && bc.D < (1ull << 63) / bins;
+    bc.inv = bc.D ? (~0ull) / bc.D : 0;
+    bc.fast32 = bc.D >= bins && bc.D < (1ull << 32);
+    bc.kmin32 = (uint32_t)bc.kmin;
+    bc.D32 = (uint32_t)bc.D;
+    bc.m32 = bc.fast32 ? (uint32_t)(((uint64_t)bins << 32) / bc.D) : 0u;
     for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    const double scale = D ? (double)bins / (double)D : 0.0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
-        const uint64_t K = keys[i];
-        uint32_t b = 0;
-        if (D) {
-            const uint64_t x = K <= kmin ? 0ull : (K >= kmax ? D : K - kmin);
-            /* estimate, then correct with exact 128-bit compares:
-             * want b = floor(x*bins / D), i.e. b*D <= x*bins < (b+1)*D */
-            double e = (double)x * scale;
-            int64_t bb = (int64_t)e;
-            if (bb < 0) bb = 0;
-            if (bb > (int64_t)bins) bb = bins;
-            const uint64_t plo = x * (uint64_t)bins, phi = __umul64hi(x, (uint64_t)bins);
-            for (;;) { /* b*D > x*bins ? -> b-- */
-                uint64_t qlo = (uint64_t)bb * D, qhi = __umul64hi((uint64_t)bb, D);
-                if (qhi > phi || (qhi == phi && qlo > plo)) bb--;
-                else break;
-            }
-            for (;;) { /* (b+1)*D <= x*bins ? -> b++ */
-                uint64_t b1 = (uint64_t)bb + 1;
-                uint64_t qlo = b1 * D, qhi = __umul64hi(b1, D);
-                if (qhi < phi || (qhi == phi && qlo <= plo)) bb++;
-                else break;
-            }
-            b = (uint32_t)bb;
-            if (b > bins - 1) b = bins - 1;
+    uint32_t cur = 0xFFFFFFFFu, run = 0;
+    auto put = [&](uint32_t b) {
+        if (b == cur) {
+            run++;
+        } else {
+            if (run) atomicAdd(&sh[cur], run);
+            cur = b;
+            run = 1;
         }
-        atomicAdd(&sh[b], 1u);
+    };
+    const uint64_t nchunks = count / 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
+    const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
+    if (aligned) {
+        for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += stride) {
+            const ulonglong2 a = __ldcs(k2 + 4 * c), b = __ldcs(k2 + 4 * c + 1);
+            const ulonglong2 d = __ldcs(k2 + 4 * c + 2), e = __ldcs(k2 + 4 * c + 3);
+            put(bc(a.x)); put(bc(a.y)); put(bc(b.x)); put(bc(b.y));
+            put(bc(d.x)); put(bc(d.y)); put(bc(e.x)); put(bc(e.y));
+        }
     }
+    for (uint64_t i = (aligned ? nchunks * 8 : 0) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += stride)
+        put(bc(keys[i]));
+    if (run) atomicAdd(&sh[cur], run);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x)
         if (sh[i]) atomicAdd((unsigned long long*)&hist[i], (unsigned long long)sh[i]);
@@ -764,7 +859,10 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
                    rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
     cudaStream_t st = (cudaStream_t)stream;
-    const uint64_t units = n >= 3 ? ((first + count + 5) / 6 - first / 6) : count;
+    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : 3u);
+    uint64_t R = 1;
+    for (uint32_t i = 2; i <= (n < dm ? n : dm); i++) R *= i;
+    const uint64_t units = (first + count + R - 1) / R - first / R;
     uint64_t ctas = (units + kThreads - 1) / kThreads;
     const uint64_t cap = (uint64_t)rk_eval_max_ctas(S, 0);
     if (ctas > cap) ctas = cap;
@@ -785,7 +883,7 @@ int rk_launch_merge(const rk_stats* in_dev, uint32_t n_records, rk_stats* out_de
 int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
                         const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream,
                         uint32_t* launches) {
-    uint64_t ctas = (count + 1023) / 1024;
+    uint64_t ctas = (count / 8 + 255) / 256;
     const uint64_t cap = (uint64_t)num_sms() * 8;
     if (ctas > cap) ctas = cap;
     if (ctas < 1) ctas = 1;
@@ -837,7 +935,7 @@ int rk_batch_chunks_per_set(uint32_t n) {
     if (n < 3) return 1;
     uint64_t f = 1;
     for (uint32_t i = 2; i <= n; i++) f *= i;
-    const uint64_t runs = f / 6;
+    const uint64_t runs = f / 24; /* typical run size (depth 4) */
     uint64_t chunks = (runs + kThreads * 4 - 1) / (kThreads * 4); /* ~4 runs per thread */
     if (chunks < 1) chunks = 1;
     if (chunks > 65535) chunks = 65535;
