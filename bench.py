@@ -180,8 +180,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=120)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--bins", type=int, default=256)
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -276,7 +276,7 @@ def main():
     assert hist_mass == N and (world > 1 or evaluated == N), (hist_mass, evaluated)
 
     # e2e: the public API with host buffers (Sweeper.run: H2D tables, D2H report)
-    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    e2e_steps = args.e2e_steps or max(3, min(30, args.steps // 2))
     for _ in range(2):
         sw.run(ks)
     if world > 1:

@@ -130,7 +130,7 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
         gb = std::gcd(gb, (uint64_t)ks[i].grid_blocks);
         amax = std::max<uint64_t>(amax, std::max(ks[i].inst_per_block, ks[i].mem_per_block));
     }
-    while (gb > 1 && amax * gb > 0xFFFFFFFFull) { /* scaled A, M must stay u32: use a divisor of g */
+    while (gb > 1 && (u128)amax * gb * std::max(p.rb_num, p.rb_den) >= ((u128)1 << 63)) { /* keep den*A*g < 2^63 */
         uint64_t d = 2;
         while (gb % d) d++;
         gb /= d;
@@ -168,9 +168,9 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
         uint32_t mag[3], add[3];
         uint64_t C = p.max_blocks_per_sm;
         for (int r = 0; r < 3; r++) {
-            if (dem[r] == 0) {
-                mag[r] = 0;
-                add[r] = 0xFFFFu;
+            if (dem[r] == 0) { /* numerator forced >= 2^30: quotient exceeds any cap */
+                mag[r] = 0xFFFFFFFFu;
+                add[r] = r == 0 ? 0x7FFF0000u : 0x7FFFu;
                 continue;
             }
             C = std::min<uint64_t>(C, caps[r] / dem[r]);
@@ -191,14 +191,19 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
         k.mw = mag[2];
         k.zr = add[0];
         k.zs = add[1];
-        k.zw = add[2];
         k.dA = (uint32_t)(2 * dem[0]) | (uint32_t)(2 * dem[1]) << 16;
         k.dB = (uint32_t)(2 * dem[2]) | 2u << 16;
-        k.A = (uint32_t)(ks[i].inst_per_block * gb);
-        k.M = (uint32_t)(ks[i].mem_per_block * gb);
+        const uint64_t Ared = (uint64_t)ks[i].inst_per_block * gb, Mred = (uint64_t)ks[i].mem_per_block * gb;
+        k.cA = Ared * p.rb_den; /* < 2^63 by the key bound */
+        k.cM = Mred * p.rb_num;
         k.C = (uint32_t)C;
         k.SC = (uint32_t)(C * Sred);
-        const u128 ci = (u128)k.SC * k.A * p.rb_den, cm = (u128)k.SC * k.M * p.rb_num;
+        k.scm = 0;
+        if (k.SC >= 2) { /* floor(x/SC) = hi(x*scm) for x < T: verified bound x*e < 2^32 */
+            const uint64_t m = ((1ull << 32) + k.SC - 1) / k.SC, e = m * k.SC - (1ull << 32);
+            if ((uint64_t)k.T * e < (1ull << 32)) k.scm = (uint32_t)m;
+        }
+        const u128 ci = (u128)k.SC * k.cA, cm = (u128)k.SC * k.cM;
         const u128 fk = ci >= cm ? ci : cm;
         k.fullkey = fk >> 64 ? ~0ull : (uint64_t)fk; /* only used when T > SC, then bounded */
     }

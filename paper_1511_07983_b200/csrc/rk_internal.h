@@ -24,16 +24,18 @@
 #define RK_MAX_N 12
 #define RK_SMAX 32
 
-struct RkKTab {        /* one kernel; 64 B */
+struct RkKTab {        /* one kernel; 72 B */
     uint32_t T;        /* N_tblk */
-    uint32_t mr, ms, mw;   /* magic multipliers for floor((2x+1)/(2d)); 0 if d == 0 */
-    uint32_t zr, zs, zw;   /* addends: 0, or 0xFF (>= any cap) if d == 0 */
+    uint32_t mr, ms, mw;   /* magic multipliers for floor((2x+1)/(2d)); 0xFFFFFFFF if d == 0 */
+    uint32_t zr;           /* regs numerator OR-mask: 0, or 0x7FFF0000 if d == 0 (quotient >> any cap) */
+    uint32_t zs;           /* shm numerator high word for the funnel shift: 0, or 0x7FFF if d == 0 */
+    uint32_t scm;          /* magic for floor(x / SC), exact for x < T; 0 = use a division */
     uint32_t dA, dB;       /* per-block decrement of fa / fb */
-    uint32_t A, M;         /* inst / mem units per block */
     uint32_t C;            /* blocks per fresh SM */
     uint32_t SC;           /* S * C: blocks per full single-kernel round */
     uint32_t pad;
-    uint64_t fullkey;      /* max(den*SC*A, num*SC*M): key of one full round */
+    uint64_t cA, cM;       /* den * A_i and num * M_i (scaled per-block work, exact) */
+    uint64_t fullkey;      /* max(SC*cA, SC*cM): key of one full round */
 };
 
 struct RkGTab {

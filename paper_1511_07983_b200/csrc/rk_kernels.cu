@@ -39,16 +39,18 @@ __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
     return r;
 }
 
-__device__ __forceinline__ uint64_t round_key(uint64_t I, uint64_t M, uint32_t num, uint32_t den) {
-    uint64_t ci = I * den, cm = M * num; /* max(I_r, R_B M_r) * den, exact */
-    return ci >= cm ? ci : cm;
+/* Round key max(den*I_r, num*M_r) = den * max(I_r, R_B*M_r): the
+ * state accumulates the scaled sums den*I_r and num*M_r directly (per-kernel
+ * den*A_i and num*M_i precomputed), so closing a round is one 64-bit max. */
+__device__ __forceinline__ uint64_t round_key(uint64_t dI, uint64_t nM, uint32_t, uint32_t) {
+    return dI >= nM ? dI : nM;
 }
 
 template <int SMAX>
 struct St {
     uint32_t fa[SMAX], fb[SMAX];
     uint32_t cur;
-    uint64_t I, M, K; /* open round's inst/mem units; closed rounds' key */
+    uint64_t I, M, K; /* open round's den*I_r and num*M_r; closed rounds' key */
 };
 
 /* number of SMs: compile-time when FULL */
@@ -101,14 +103,23 @@ __device__ __forceinline__ void st_fresh(St<SMAX>& s, const RkGTab& g) {
  * (reading L8).  Fields are stored as 2x+1, so floor(x/d) = floor((2x+1)/(2d))
  * = IMAD.HI with a host-verified magic; a zero demand adds 0xFFFF instead. */
 struct CapK {
-    uint32_t mr, ms, mw, zr, zs, zw;
+    uint32_t mr, ms, mw, zr, zs;
 };
-__device__ __forceinline__ CapK capk(const RkKTab& k) { return CapK{k.mr, k.ms, k.mw, k.zr, k.zs, k.zw}; }
+__device__ __forceinline__ CapK capk(const RkKTab& k) { return CapK{k.mr, k.ms, k.mw, k.zr, k.zs}; }
 __device__ __forceinline__ uint32_t cap1(uint32_t fa, uint32_t fb, const CapK& k) {
-    const uint32_t qr = mad_hi(fa & 0xFFFFu, k.mr, k.zr);
-    const uint32_t qs = mad_hi(fa >> 16, k.ms, k.zs);
-    const uint32_t qw = mad_hi(fb & 0xFFFFu, k.mw, k.zw);
+    /* zero demand: the numerator gets bits >= 2^30 (LOP3 OR / funnel shift, no
+     * extra instruction) and the magic 0xFFFFFFFF keeps it >> any cap */
+    const uint32_t qr = __umulhi((fa & 0xFFFFu) | k.zr, k.mr);
+    const uint32_t qs = __umulhi(__funnelshift_r(fa, k.zs, 16), k.ms);
+    const uint32_t qw = __umulhi(fb & 0xFFFFu, k.mw); /* warps demand >= 1 */
     return min(__vimin3_u32(qr, qs, qw), fb >> 17);
+}
+
+/* complete single-kernel rounds among x = n - 1 leftover blocks: floor(x / SC) */
+__device__ __forceinline__ uint32_t full_rounds(uint32_t x, const RkKTab& k) {
+    uint32_t q = __umulhi(x, k.scm); /* exact for x < T (host-verified) */
+    if (k.scm == 0) q = k.SC == 1 ? x : x / k.SC; /* SC == 1 or an unverifiable bound */
+    return q;
 }
 
 /* Ring rotation of an S-bit mask (S <= 32). */
@@ -147,59 +158,33 @@ struct Placed {
     uint64_t I, M, K;
 };
 
-/* Dispatch all T_k blocks of kernel k (PAPER:69-81) on state `in`; the new
- * per-SM words are handed to upd(i, fa, fb) so callers either store them
- * (a new state) or consume them on the fly (the fused last level). */
-template <int SMAX, bool FULL, class R, class U>
-__device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k, uint32_t kid, const RkGTab& g,
-                                             R& rec, U& upd) {
-    const CapK ck = capk(k);
-    uint32_t c[SMAX];
-    uint32_t F = 0;
-#pragma unroll
-    for (int i = 0; i < SMAX; i++) {
-        c[i] = cap1(in.fa[i], in.fb[i], ck);
-        F += c[i];
-    }
-    uint32_t n = k.T;
-    Placed o;
+/* Water-fill of n blocks (1 <= n <= sum c) with capacities c[] on the SM
+ * words (bfa, bfb) from cursor cur: after tlo passes every SM holds
+ * min(c_s, tlo); pass tlo+1 gives one more block to the first r SMs with
+ * c_s > tlo in ring order.  Emits the new words via upd; returns the cursor. */
+template <int SMAX, bool FULL, class U>
+__device__ __forceinline__ uint32_t water_fill(uint32_t n, const uint32_t (&c)[SMAX], const uint32_t (&bfa)[SMAX],
+                                               const uint32_t (&bfb)[SMAX], uint32_t cur, const RkKTab& k,
+                                               const RkGTab& g, U& upd) {
     const uint32_t S = nsm<SMAX, FULL>(g);
-    if (n > F) {
-        /* every SM takes its c_s and the next block fits nowhere: the round
-         * closes; complete single-kernel rounds follow, the rest
-         * opens a fresh round whose blocks go to SMs 0,1,.. in turn (cursor 0). */
-        rec.add(kid, F);
-        rec.close();
-        o.K = in.K + round_key(in.I + (uint64_t)F * k.A, in.M + (uint64_t)F * k.M, g.num, g.den);
-        n -= F;
-        const uint32_t nfull = (n - 1u) / k.SC;
-        o.K += (uint64_t)nfull * k.fullkey;
-        rec.full(kid, nfull, k.SC);
-        n -= nfull * k.SC;
-        uint32_t q, r;
-        if constexpr (FULL) {
-            q = n / (uint32_t)SMAX; /* power of two: a shift */
-            r = n % (uint32_t)SMAX;
-        } else {
-            q = n / S;
-            r = n - q * S;
-        }
+    /* tlo = max{t : f(t) < n}, f(t) = sum_s min(c_s, t); SM pairs in 16x2 SIMD */
+    constexpr int NP = SMAX / 2;
+    uint32_t cp[NP > 0 ? NP : 1];
 #pragma unroll
-        for (int i = 0; i < SMAX; i++) {
-            const uint32_t x = q + ((uint32_t)i < r ? 1u : 0u);
-            if (live_sm<SMAX, FULL>(i, g)) upd(i, g.freshA - x * k.dA, g.freshB - x * k.dB);
-            else upd(i, 0u, 0u);
-        }
-        o.cur = r;
-        o.I = (uint64_t)n * k.A;
-        o.M = (uint64_t)n * k.M;
+    for (int j = 0; j < NP; j++) cp[j] = __byte_perm(c[2 * j], c[2 * j + 1], 0x5410);
+    uint32_t tlo, flo;
+    if constexpr (FULL && SMAX == 1) {
+        tlo = n - 1u; /* f(t) = min(c, t) < n  <=>  t < n (n <= c) */
+        flo = tlo;
+    } else if constexpr (FULL && SMAX == 2) {
+        /* f(t) = 2t up to the smaller cap lo, then lo + t (n <= lo + hi) */
+        const uint32_t lo = min(c[0], c[1]);
+        const bool even = n <= 2u * lo;
+        tlo = even ? (n - 1u) >> 1 : n - 1u - lo;
+        flo = even ? 2u * tlo : n - 1u;
     } else {
-        /* tlo = max{t : f(t) < n}, f(t) = sum_s min(c_s, t); SM pairs in 16x2 SIMD */
-        constexpr int NP = SMAX / 2;
-        uint32_t cp[NP > 0 ? NP : 1];
-#pragma unroll
-        for (int j = 0; j < NP; j++) cp[j] = __byte_perm(c[2 * j], c[2 * j + 1], 0x5410);
-        uint32_t tlo = 0, flo = 0;
+        tlo = 0;
+        flo = 0;
         for (uint32_t b = g.tbits; b; b >>= 1) {
             const uint32_t tt = tlo + b;
             uint32_t f;
@@ -217,34 +202,105 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
                 flo = f;
             }
         }
-        const uint32_t r = n - flo; /* >= 1 blocks of pass tlo+1, to SMs with c_s > tlo in ring order */
-        uint32_t E;
-        if constexpr (NP > 0 && SMAX <= 16) {
-            /* E = {s : c_s > tlo}: per pair min(c, tlo+1) - min(c, tlo) is 0/1 in each half */
-            const uint32_t lo2 = tlo * 0x10001u, hi2 = lo2 + 0x10001u;
-            uint32_t acc = 0;
+    }
+    const uint32_t r = n - flo; /* >= 1 blocks of pass tlo+1, to SMs with c_s > tlo in ring order */
+    uint32_t E;
+    if constexpr (NP > 0 && SMAX <= 16) {
+        /* E = {s : c_s > tlo}: per pair min(c, tlo+1) - min(c, tlo) is 0/1 in each half */
+        const uint32_t lo2 = tlo * 0x10001u, hi2 = lo2 + 0x10001u;
+        uint32_t acc = 0;
 #pragma unroll
-            for (int j = 0; j < NP; j++) acc += (__vminu2(cp[j], hi2) - __vminu2(cp[j], lo2)) << (2 * j);
-            E = (acc & 0x5555u) | ((acc >> 15) & 0xAAAAu);
-        } else {
-            E = 0;
+        for (int j = 0; j < NP; j++) acc += (__vminu2(cp[j], hi2) - __vminu2(cp[j], lo2)) << (2 * j);
+        E = (acc & 0x5555u) | ((acc >> 15) & 0xAAAAu);
+    } else {
+        E = 0;
 #pragma unroll
-            for (int i = 0; i < SMAX; i++) E |= (c[i] > tlo ? 1u : 0u) << i;
-        }
-        const uint32_t Er = rotr_s<SMAX, FULL>(E, in.cur, S);
-        const uint32_t p = select_bit<SMAX>(Er, r);
-        const uint32_t Xr = Er & ((2u << p) - 1u); /* first r eligible SMs from the cursor */
-        const uint32_t X = rotr_s<SMAX, FULL>(Xr, S - in.cur, S);
-        const uint32_t nc = in.cur + p + 1u;
-        o.cur = nc >= S ? nc - S : nc; /* cursor = SM of the last block + 1 */
+        for (int i = 0; i < SMAX; i++) E |= (c[i] > tlo ? 1u : 0u) << i;
+    }
+    const uint32_t Er = rotr_s<SMAX, FULL>(E, cur, S);
+    const uint32_t p = select_bit<SMAX>(Er, r);
+    const uint32_t Xr = Er & ((2u << p) - 1u); /* first r eligible SMs from the cursor */
+    const uint32_t X = rotr_s<SMAX, FULL>(Xr, S - cur, S);
+    const uint32_t nc = cur + p + 1u;
+#pragma unroll
+    for (int i = 0; i < SMAX; i++) {
+        const uint32_t x = min(c[i], tlo) + ((X >> i) & 1u);
+        upd(i, bfa[i] - x * k.dA, bfb[i] - x * k.dB);
+    }
+    return nc >= S ? nc - S : nc; /* cursor = SM of the last block + 1 */
+}
+
+/* Dispatch all T_k blocks of kernel k (PAPER:69-81) on state `in`; the new
+ * per-SM words are handed to upd(i, fa, fb) so callers either store them
+ * (a new state) or consume them on the fly (the fused last level). */
+template <int SMAX, bool FULL, class R, class U>
+__device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k, uint32_t kid, const RkGTab& g,
+                                             R& rec, U& upd) {
+    const CapK ck = capk(k);
+    uint32_t c[SMAX];
+    uint32_t F = 0;
+#pragma unroll
+    for (int i = 0; i < SMAX; i++) {
+        c[i] = cap1(in.fa[i], in.fb[i], ck);
+        F += c[i];
+    }
+    uint32_t n = k.T;
+    Placed o;
+    const bool ovf = n > F;
+    /* n > F: every SM takes its c_s and the next block fits nowhere, so the round
+     * closes; complete single-kernel rounds follow; the rest opens a
+     * fresh round (all SMs fresh, cursor 0) — the same water-fill on fresh inputs. */
+    const uint32_t nfull = full_rounds(ovf ? n - F - 1u : 0u, k);
+    if (ovf) {
+        rec.add(kid, F);
+        rec.close();
+        rec.full(kid, nfull, k.SC);
+    }
+    if constexpr (SMAX <= 4) {
+        /* few SMs: branch-free (lanes disagree on ovf often; selects are cheap) */
+        const uint64_t kc = in.K + round_key(in.I + (uint64_t)F * k.cA, in.M + (uint64_t)F * k.cM, g.num, g.den) +
+                            (uint64_t)nfull * k.fullkey;
+        n = ovf ? n - F - nfull * k.SC : n;
+        o.K = ovf ? kc : in.K;
+        uint32_t bfa[SMAX], bfb[SMAX];
 #pragma unroll
         for (int i = 0; i < SMAX; i++) {
-            const uint32_t x = min(c[i], tlo) + ((X >> i) & 1u);
-            upd(i, in.fa[i] - x * k.dA, in.fb[i] - x * k.dB);
+            const bool live = live_sm<SMAX, FULL>(i, g);
+            bfa[i] = ovf ? (live ? g.freshA : 0u) : in.fa[i];
+            bfb[i] = ovf ? (live ? g.freshB : 0u) : in.fb[i];
+            c[i] = ovf ? (live ? k.C : 0u) : c[i];
         }
-        o.I = in.I + (uint64_t)n * k.A;
-        o.M = in.M + (uint64_t)n * k.M;
-        o.K = in.K;
+        o.cur = water_fill<SMAX, FULL>(n, c, bfa, bfb, ovf ? 0u : in.cur, k, g, upd);
+        o.I = (ovf ? 0ull : in.I) + (uint64_t)n * k.cA;
+        o.M = (ovf ? 0ull : in.M) + (uint64_t)n * k.cM;
+    } else {
+        if (ovf) {
+            o.K = in.K + round_key(in.I + (uint64_t)F * k.cA, in.M + (uint64_t)F * k.cM, g.num, g.den) +
+                  (uint64_t)nfull * k.fullkey;
+            n -= F + nfull * k.SC;
+            uint32_t q, r;
+            if constexpr (FULL) {
+                q = n / (uint32_t)SMAX; /* power of two: a shift */
+                r = n % (uint32_t)SMAX;
+            } else {
+                q = n / g.S;
+                r = n - q * g.S;
+            }
+#pragma unroll
+            for (int i = 0; i < SMAX; i++) {
+                const uint32_t x = q + ((uint32_t)i < r ? 1u : 0u);
+                if (live_sm<SMAX, FULL>(i, g)) upd(i, g.freshA - x * k.dA, g.freshB - x * k.dB);
+                else upd(i, 0u, 0u);
+            }
+            o.cur = r;
+            o.I = (uint64_t)n * k.cA;
+            o.M = (uint64_t)n * k.cM;
+        } else {
+            o.cur = water_fill<SMAX, FULL>(n, c, in.fa, in.fb, in.cur, k, g, upd);
+            o.I = in.I + (uint64_t)n * k.cA;
+            o.M = in.M + (uint64_t)n * k.cM;
+            o.K = in.K;
+        }
     }
     rec.add(kid, n);
     return o;
@@ -285,19 +341,19 @@ __device__ __forceinline__ uint64_t finish_key(uint32_t F, uint64_t I, uint64_t 
     if (n <= F) {
         rec.add(kid, n);
         rec.close();
-        return K + round_key(I + (uint64_t)n * k.A, M + (uint64_t)n * k.M, g.num, g.den);
+        return K + round_key(I + (uint64_t)n * k.cA, M + (uint64_t)n * k.cM, g.num, g.den);
     }
     rec.add(kid, F);
     rec.close();
-    K += round_key(I + (uint64_t)F * k.A, M + (uint64_t)F * k.M, g.num, g.den);
+    K += round_key(I + (uint64_t)F * k.cA, M + (uint64_t)F * k.cM, g.num, g.den);
     n -= F;
-    const uint32_t nfull = (n - 1u) / k.SC;
+    const uint32_t nfull = full_rounds(n - 1u, k);
     K += (uint64_t)nfull * k.fullkey;
     rec.full(kid, nfull, k.SC);
     n -= nfull * k.SC;
     rec.add(kid, n);
     rec.close();
-    return K + round_key((uint64_t)n * k.A, (uint64_t)n * k.M, g.num, g.den);
+    return K + round_key((uint64_t)n * k.cA, (uint64_t)n * k.cM, g.num, g.den);
 }
 
 template <int SMAX, class R>
@@ -369,7 +425,7 @@ struct TStats {
         /* indices arrive in increasing order per thread: strict compares keep
          * the smallest index on ties (reading L12) */
         if (K < kmin) { kmin = K; amin = idx; }
-        if (K > kmax || cnt == 0) { kmax = K; amax = idx; }
+        if (K > kmax) { kmax = K; amax = idx; } /* K >= 1 > initial 0 */
         nlt += (K < cand) ? 1u : 0u;
         neq += (K == cand) ? 1u : 0u;
         cnt += 1u;
