@@ -636,33 +636,46 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
             do_rank(order.data(), n, &idx[q]);
         }
     }
+    /* group the sets by reduced SM count so every launch runs a compile-time variant */
+    std::vector<uint32_t> perm(n_sets);
+    for (uint32_t q = 0; q < n_sets; q++) perm[q] = q;
+    std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return tabs[a].g.S < tabs[b].g.S; });
+    std::vector<RkTables> ptabs(n_sets);
+    std::vector<uint64_t> pidx(n_sets);
+    for (uint32_t q = 0; q < n_sets; q++) {
+        ptabs[q] = tabs[perm[q]];
+        pidx[q] = idx[perm[q]];
+    }
     DeviceGuard dg(c->device);
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
-    const uint32_t chunks = (uint32_t)rk_batch_chunks_per_set(n);
+    uint32_t max_chunks = 0;
+    for (uint32_t q = 0; q < n_sets; q++)
+        max_chunks = std::max(max_chunks, (uint32_t)rk_batch_chunks_per_set(n, ptabs[q].g.S));
     RkTables* tabs_dev = nullptr;
     uint64_t *idx_dev = nullptr, *keys_dev = nullptr;
     rk_stats *recs = nullptr, *out_dev = nullptr;
     int e = cudaMalloc(&tabs_dev, sizeof(RkTables) * n_sets);
     if (!e) e = cudaMalloc(&idx_dev, sizeof(uint64_t) * n_sets);
     if (!e) e = cudaMalloc(&keys_dev, sizeof(uint64_t) * n_sets);
-    if (!e) e = cudaMalloc(&recs, sizeof(rk_stats) * (size_t)n_sets * chunks);
+    if (!e) e = cudaMalloc(&recs, sizeof(rk_stats) * (size_t)n_sets * max_chunks);
     if (!e) e = cudaMalloc(&out_dev, sizeof(rk_stats) * n_sets);
-    if (!e) e = cudaMemcpyAsync(tabs_dev, tabs.data(), sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
-    if (!e) e = cudaMemcpyAsync(idx_dev, idx.data(), sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemcpyAsync(tabs_dev, ptabs.data(), sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemcpyAsync(idx_dev, pidx.data(), sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
     uint32_t smax_k = 0;
-    for (uint32_t q = 0; q < n_sets; q++) smax_k = std::max(smax_k, tabs[q].g.S);
+    for (uint32_t q = 0; q < n_sets; q++) smax_k = std::max(smax_k, ptabs[q].g.S);
     if (!e) e = rk_launch_keys_of(tabs_dev, n, smax_k, idx_dev, n_sets, keys_dev, stream, &c->launches);
-    uint32_t smax = 0;
-    bool uniform = true;
-    for (uint32_t q = 0; q < n_sets; q++) {
-        if (q && tabs[q].g.S != tabs[0].g.S) uniform = false;
-        smax = std::max(smax, tabs[q].g.S);
+    for (uint32_t a = 0; a < n_sets && !e;) {
+        uint32_t b = a;
+        while (b < n_sets && ptabs[b].g.S == ptabs[a].g.S) b++;
+        const uint32_t S = ptabs[a].g.S, chunks = (uint32_t)rk_batch_chunks_per_set(n, S);
+        e = rk_launch_batch(tabs_dev + a, n, S | 0x80000000u, b - a, keys_dev + a, out_dev + a, recs, chunks, stream,
+                            &c->launches);
+        a = b;
     }
-    if (!e) e = rk_launch_batch(tabs_dev, n, smax | (uniform ? 0x80000000u : 0u), n_sets, keys_dev, out_dev, recs,
-                                chunks, stream, &c->launches);
     std::vector<uint64_t> keys(n_sets);
-    if (!e) e = cudaMemcpyAsync(out_host, out_dev, sizeof(rk_stats) * n_sets, cudaMemcpyDeviceToHost, st);
+    std::vector<rk_stats> pout(n_sets);
+    if (!e) e = cudaMemcpyAsync(pout.data(), out_dev, sizeof(rk_stats) * n_sets, cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaMemcpyAsync(keys.data(), keys_dev, sizeof(uint64_t) * n_sets, cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaStreamSynchronize(st);
     cudaFree(tabs_dev);
@@ -671,7 +684,10 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     cudaFree(recs);
     cudaFree(out_dev);
     if (e) return cuda_fail(c, e, "rk_eval_batch");
-    if (cand_key_out) std::memcpy(cand_key_out, keys.data(), sizeof(uint64_t) * n_sets);
+    for (uint32_t q = 0; q < n_sets; q++) {
+        out_host[perm[q]] = pout[q];
+        if (cand_key_out) cand_key_out[perm[q]] = keys[q];
+    }
     return RK_OK;
 }
 

@@ -987,12 +987,14 @@ int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const in
     return (int)cudaGetLastError();
 }
 
-int rk_batch_chunks_per_set(uint32_t n) {
+int rk_batch_chunks_per_set(uint32_t n, uint32_t S) {
     if (n < 3) return 1;
-    uint64_t f = 1;
+    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : 3u);
+    uint64_t f = 1, R = 1;
     for (uint32_t i = 2; i <= n; i++) f *= i;
-    const uint64_t runs = f / 24; /* typical run size (depth 4) */
-    uint64_t chunks = (runs + kThreads * 4 - 1) / (kThreads * 4); /* ~4 runs per thread */
+    for (uint32_t i = 2; i <= (n < dm ? n : dm); i++) R *= i;
+    const uint64_t runs = (f + R - 1) / R;
+    uint64_t chunks = (runs + kThreads * 2 - 1) / (kThreads * 2); /* ~2 runs per thread */
     if (chunks < 1) chunks = 1;
     if (chunks > 65535) chunks = 65535;
     return (int)chunks;
