@@ -31,7 +31,10 @@
 
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef RK_EVAL_THREADS
+#define RK_EVAL_THREADS 256
+#endif
+constexpr int kThreads = RK_EVAL_THREADS;
 
 __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;
