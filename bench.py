@@ -152,7 +152,9 @@ def run_reference(args):
     gpu, ks = W.config(CONFIG_NAME)
     threads = os.cpu_count() or 1
     N = math.factorial(len(ks))
-    per_step_s = float(os.environ.get("RK_REF_STEP_SECONDS", "2.0"))
+    # bounded sample: the whole (warmup + steps) run takes ~RK_REF_TOTAL_SECONDS of host time
+    total_s = float(os.environ.get("RK_REF_TOTAL_SECONDS", "90"))
+    per_step_s = max(0.05, total_s / max(1, args.warmup + args.steps))
     import oracle as O
 
     # size each step (a bounded contiguous sample) from a short calibration

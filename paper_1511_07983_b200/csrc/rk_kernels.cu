@@ -35,6 +35,10 @@ namespace {
 #define RK_EVAL_THREADS 256
 #endif
 constexpr int kThreads = RK_EVAL_THREADS;
+/* branch-free overflow handling up to this many (super-)SMs (measured) */
+#ifndef RK_BF_MAX
+#define RK_BF_MAX 32
+#endif
 
 __device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t r;
@@ -259,8 +263,9 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
         rec.close();
         rec.full(kid, nfull, k.SC);
     }
-    if constexpr (SMAX <= 4) {
-        /* few SMs: branch-free (lanes disagree on ovf often; selects are cheap) */
+    if constexpr (SMAX <= RK_BF_MAX) {
+        /* branch-free: lanes disagree on ovf often; the fresh round is the same
+         * water-fill on fresh words, so select the inputs instead of branching */
         const uint64_t kc = in.K + round_key(in.I + (uint64_t)F * k.cA, in.M + (uint64_t)F * k.cM, g.num, g.den) +
                             (uint64_t)nfull * k.fullkey;
         n = ovf ? n - F - nfull * k.SC : n;
@@ -542,9 +547,12 @@ __device__ void commit(const rk_stats& cta, rk_stats* recs, uint32_t* counter, r
 
 /* Suffix-tree depth per SM-count variant: placements are cheap for few
  * (super-)SMs, so share longer prefixes (DESIGN.md §5 "prefix sharing"). */
+#ifndef RK_DEPTH_LARGE
+#define RK_DEPTH_LARGE 3
+#endif
 template <int SMAX>
 struct Depth {
-    static constexpr int value = SMAX <= 2 ? 5 : (SMAX <= 8 ? 4 : 3);
+    static constexpr int value = SMAX <= 2 ? 5 : (SMAX <= 8 ? 4 : RK_DEPTH_LARGE);
 };
 __host__ __device__ constexpr uint32_t cfact(int m) { return m <= 1 ? 1u : (uint32_t)m * cfact(m - 1); }
 
@@ -918,7 +926,7 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
                    rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
     cudaStream_t st = (cudaStream_t)stream;
-    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : 3u);
+    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t R = 1;
     for (uint32_t i = 2; i <= (n < dm ? n : dm); i++) R *= i;
     const uint64_t units = (first + count + R - 1) / R - first / R;
@@ -992,7 +1000,7 @@ int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const in
 
 int rk_batch_chunks_per_set(uint32_t n, uint32_t S) {
     if (n < 3) return 1;
-    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : 3u);
+    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t f = 1, R = 1;
     for (uint32_t i = 2; i <= n; i++) f *= i;
     for (uint32_t i = 2; i <= (n < dm ? n : dm); i++) R *= i;
