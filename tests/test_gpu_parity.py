@@ -286,3 +286,56 @@ def test_symmetry_reduction_equivalence(ctx):
         sets = W.random_small_sets(rng.next(), 1, 5, 7)
         ks = [(k[0] + (rng.below(7) if rng.below(2) else 0),) + tuple(k[1:]) for k in sets[0]]
         check_full_space(ctx, W.GTX580, ks, bins=(5,))
+
+
+DEGENERATE = {
+    # all R_i >= R_B: every order has the same key (same-side theorem)
+    "same_side": (W.GTX580, [(32, 256, 20, 0, 1110 * 8, 100 * 8), (48, 128, 32, 8192, 2400 * 4, 100 * 4),
+                             (16, 512, 16, 16384, 600 * 16, 100 * 16), (64, 64, 24, 0, 800 * 2, 100 * 2)]),
+    # identical kernels differing only in N_tblk
+    "identical": (W.GTX580, [(t, 256, 24, 12288, 311 * 8, 100 * 8) for t in (16, 48, 80, 128, 32)]),
+    # total blocks <= N_SM: one round for every order
+    "one_round": (W.GTX580, [(3, 256, 24, 0, 311, 100), (5, 128, 20, 4096, 1110, 100), (8, 64, 16, 0, 2400, 100)]),
+    # zero register and zero shared-memory demand (magic / numerator-mask path)
+    "zero_demand": (W.GTX580, [(24, 128, 0, 0, 311, 100), (40, 256, 0, 8192, 1110, 100), (17, 64, 8, 0, 150, 100),
+                               (33, 96, 0, 16384, 2400, 100)]),
+    # one block per SM per kernel and one super-SM: SC == 1 (full-round division fallback)
+    "sc_one": (W.GTX580, [(48, 128, 20, 49152, 311, 100), (32, 128, 20, 40000, 1110, 100),
+                          (64, 1024, 32, 0, 600, 100)]),
+    # N_blk_SM = 1 (no binary search), many rounds, odd grids
+    "one_slot": ((7, 65536, 65536, 64, 1, 3, 2), [(9, 64, 8, 0, 7, 3), (13, 128, 16, 1024, 5, 9), (4, 32, 8, 0, 11, 2),
+                                                  (21, 256, 4, 0, 2, 5)]),
+    # many full single-kernel rounds (nfull > 0) with large grids
+    "long_grids": (W.GTX580, [(2000, 256, 32, 16384, 311, 100), (1600, 128, 20, 0, 1110, 100),
+                              (3000, 512, 16, 4096, 150, 100), (800, 64, 63, 24576, 2400, 100)]),
+}
+
+
+@pytest.mark.parametrize("name", sorted(DEGENERATE))
+def test_degenerate_and_edge_inputs(ctx, name):
+    gpu, ks = DEGENERATE[name]
+    st = check_full_space(ctx, gpu, ks, bins=(1, 3, 256))
+    if name in ("same_side", "identical"):
+        assert st.key_min == st.key_max and st.argmin == 0 and st.argmax == 0
+    if name == "one_round":
+        for p in range(math.factorial(len(ks))):
+            rounds, _ = ctx.rk_simulate_order(O.unrank(p, len(ks)))
+            assert len(rounds) == 1
+
+
+def test_max_n12_many_rounds_one_sm(ctx):
+    # n = 12 on a 1-SM GPU with 2 block slots: sampled indices vs the oracle
+    gpu = (1, 65536, 49152, 48, 2, 1, 1)
+    ks = [(1 + (i % 3), 32 * (1 + i % 4), 8, 1024 * (i % 5), 3 + i, 2 + (7 * i) % 5) for i in range(12)]
+    N = math.factorial(12)
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    keys = torch.empty(N, dtype=torch.int64, device="cuda")
+    st = ctx.rk_eval_range(0, N, 0, keys_dev=keys)
+    assert st.evaluated == N
+    rng = np.random.default_rng(5)
+    idx = np.concatenate([rng.integers(0, N, 3000), [0, N - 1, st.argmin, st.argmax]])
+    kh = keys[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint64)
+    for i, k in zip(idx.tolist(), kh.tolist()):
+        assert O.simulate(gpu, ks, O.unrank(i, 12)).key == k
+    assert int(kh[-2]) == st.key_min and int(kh[-1]) == st.key_max
