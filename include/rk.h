@@ -139,6 +139,20 @@ rk_status rk_histogram(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, ui
 rk_status rk_histogram_async(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, const rk_stats* range_dev,
                              uint32_t bins, uint64_t* hist_dev, void* stream);
 
+/* Order statistics over device keys (SPEC:299-302 SweepReport median = the
+ * lower-middle element, rank (N-1)/2; Fig. 1 PAPER:204 "ranking" curve = keys
+ * at chosen ranks).  keys_out[j] = the ranks[j]-th smallest (0-based) of
+ * keys_dev[0..count); every key must lie in [kmin, kmax] (e.g. a record's
+ * key_min/key_max).  Exact: iterated integer histograms over shrinking key
+ * ranges.  Synchronous.  RK_EINVAL if a rank >= count. */
+rk_status rk_select_keys(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
+                         const uint64_t* ranks, uint32_t m, uint64_t* keys_out, void* stream);
+/* Building block of sharded selection: hist_dev[b] += #{keys in [lo, lo+span) with
+ * floor((K-lo)*bins/span) = b} (half-open equal bins, keys outside ignored).
+ * span >= 1, 1 <= bins <= 65536.  Stream-ordered. */
+rk_status rk_range_histogram(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, uint64_t lo, uint64_t span,
+                             uint32_t bins, uint64_t* hist_dev, void* stream);
+
 /* Algorithm 1 (readings L2, L16-L19), on the
  * host (sequential by nature).  order_out[n] = launch order Rd_1..Rd_r
  * (PAPER:134); round_of_out[n] (nullable) = round of each position;

@@ -559,6 +559,73 @@ rk_status rk_histogram_async(rk_ctx* c, const uint64_t* keys_dev, uint64_t count
     return hist_common(c, keys_dev, count, 0, 0, range_dev, bins, hist_dev, stream);
 }
 
+rk_status rk_range_histogram(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, uint64_t lo, uint64_t span,
+                             uint32_t bins, uint64_t* hist_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (span == 0 || bins < 1 || bins > 65536 || !hist_dev || (count && !keys_dev))
+        return fail(c, RK_EINVAL, "bad range histogram args");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    if (count == 0) return RK_OK;
+    int e = rk_launch_range_histogram(keys_dev, count, lo, span, bins, hist_dev, stream, &c->launches);
+    return e ? cuda_fail(c, e, "range histogram launch") : RK_OK;
+}
+
+rk_status rk_select_keys(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
+                         const uint64_t* ranks, uint32_t m, uint64_t* keys_out, void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (!keys_dev || !ranks || !keys_out || kmax < kmin) return fail(c, RK_EINVAL, "bad select args");
+    for (uint32_t j = 0; j < m; j++)
+        if (ranks[j] >= count) return fail(c, RK_EINVAL, "rank %llu >= count", (unsigned long long)ranks[j]);
+    DeviceGuard dg(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    constexpr uint32_t B = 16384;
+    uint64_t* hd = nullptr;
+    int e = cudaMalloc(&hd, sizeof(uint64_t) * B);
+    std::vector<uint64_t> h(B);
+    uint32_t launches = 0;
+    std::vector<uint64_t> out(m);
+    if (kmax - kmin == ~0ull) return fail(c, RK_EINVAL, "key range must be < 2^64 - 1");
+    for (uint32_t j = 0; j < m && !e; j++) {
+        uint64_t lo = kmin, span = kmax - kmin + 1, r = ranks[j];
+        for (;;) {
+            const uint32_t bins = span <= B ? (uint32_t)span : B;
+            e = cudaMemsetAsync(hd, 0, sizeof(uint64_t) * bins, st);
+            if (!e) e = rk_launch_range_histogram(keys_dev, count, lo, span, bins, hd, stream, &launches);
+            if (!e) e = cudaMemcpyAsync(h.data(), hd, sizeof(uint64_t) * bins, cudaMemcpyDeviceToHost, st);
+            if (!e) e = cudaStreamSynchronize(st);
+            if (e) break;
+            uint64_t cum = 0;
+            uint32_t b = 0;
+            for (; b < bins; b++) {
+                if (r < cum + h[b]) break;
+                cum += h[b];
+            }
+            if (b == bins) { /* keys outside [kmin, kmax]: caller error */
+                e = -1;
+                break;
+            }
+            r -= cum;
+            if (bins == span) { /* unit bins: exact */
+                out[j] = lo + b;
+                break;
+            }
+            /* bin b = keys with x in [ceil(b*span/bins), ceil((b+1)*span/bins)) */
+            const u128 a0 = ((u128)b * span + bins - 1) / bins, a1 = ((u128)(b + 1) * span + bins - 1) / bins;
+            lo += (uint64_t)a0;
+            span = (uint64_t)(a1 - a0);
+        }
+    }
+    cudaFree(hd);
+    c->launches = launches;
+    if (e == -1) return fail(c, RK_EINVAL, "keys outside [kmin, kmax]");
+    if (e) return cuda_fail(c, e, "rk_select_keys");
+    std::memcpy(keys_out, out.data(), sizeof(uint64_t) * m);
+    return RK_OK;
+}
+
 /* key of one index on the device (synchronous) */
 static rk_status key_of_index(rk_ctx* c, uint64_t idx, uint64_t* key, void* stream) {
     DeviceGuard dg(c->device);

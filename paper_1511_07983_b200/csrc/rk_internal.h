@@ -63,6 +63,8 @@ int rk_launch_merge(const rk_stats* in_dev, uint32_t n_records, rk_stats* out_de
 int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
                         const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream,
                         uint32_t* launches);
+int rk_launch_range_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t lo, uint64_t span, uint32_t bins,
+                              uint64_t* hist_dev, void* stream, uint32_t* launches);
 /* keys of explicit indices (1 thread each): out_dev[i] = key(idx_dev[i]) of set (set_dev ? set_dev[i] : 0) */
 int rk_launch_keys_of(const RkTables* tabs_dev, uint32_t n, uint32_t S, const uint64_t* idx_dev,
                       uint32_t m, uint64_t* out_dev, void* stream, uint32_t* launches);

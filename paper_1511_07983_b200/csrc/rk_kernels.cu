@@ -752,11 +752,13 @@ __global__ void rk_simulate_kernel(const RkTables* __restrict__ tab, const int32
  * contiguous), run-length merges equal bins (lexicographic neighbours have
  * close keys) before one shared-memory atomic per run; u64 global atomics at
  * the end (integer adds: order-free, bit-exact). */
+constexpr uint32_t kSmemBins = 32768; /* 128 KB of u32 bins per CTA */
+
 struct BinCalc {
     uint64_t kmin, D, inv;
     uint32_t bins, m32, kmin32, D32;
     bool fast;   /* D*bins < 2^63: 64-bit products suffice */
-    bool fast32; /* bins <= D < 2^32: 32-bit offset, 32-bit magic, one exact correction */
+    bool fast32; /* bins < D < 2^32: 32-bit offset, 32-bit magic, one exact correction */
     __device__ __forceinline__ uint32_t operator()(uint64_t K) const {
         if (fast32) {
             /* x = K - kmin < 2^32 (keys lie in [kmin, kmax]); q0 = hi(x*m32) with
@@ -793,33 +795,49 @@ struct BinCalc {
     }
 };
 
+/* RANGE = false: Fig. 1 bins over [kmin, kmax] (last bin closed).
+ * RANGE = true: order-statistic refinement — `bins` half-open bins over
+ * [kmin_imm, kmin_imm + kmax_imm) (kmax_imm = span), keys outside ignored. */
+template <bool RANGE>
 __global__ void __launch_bounds__(256) rk_hist_kernel(const uint64_t* __restrict__ keys, uint64_t count,
                                                       uint64_t kmin_imm, uint64_t kmax_imm,
                                                       const rk_stats* __restrict__ range, uint32_t bins,
                                                       uint64_t* __restrict__ hist) {
     extern __shared__ uint32_t sh[];
+    const bool smem_bins = bins <= kSmemBins; /* else accumulate straight into global u64 bins */
     BinCalc bc;
     bc.kmin = range ? range->key_min : kmin_imm;
     const uint64_t kmax = range ? range->key_max : kmax_imm;
-    bc.D = kmax - bc.kmin;
+    bc.D = RANGE ? kmax_imm : kmax - bc.kmin;
     bc.bins = bins;
     bc.fast = bc.D != 0 && bc.D < (1ull << 63) / bins;
     bc.inv = bc.D ? (~0ull) / bc.D : 0;
-    bc.fast32 = bc.D >= bins && bc.D < (1ull << 32);
+    bc.fast32 = bc.D > bins && bc.D < (1ull << 32); /* m32 < 2^32 needs D > bins */
     bc.kmin32 = (uint32_t)bc.kmin;
     bc.D32 = (uint32_t)bc.D;
     bc.m32 = bc.fast32 ? (uint32_t)(((uint64_t)bins << 32) / bc.D) : 0u;
-    for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) sh[i] = 0;
+    if (smem_bins)
+        for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
     uint32_t cur = 0xFFFFFFFFu, run = 0;
+    auto flush = [&]() {
+        if (!run) return;
+        if (smem_bins) atomicAdd(&sh[cur], run);
+        else atomicAdd((unsigned long long*)&hist[cur], (unsigned long long)run);
+    };
     auto put = [&](uint32_t b) {
+        if (RANGE && b == 0xFFFFFFFFu) return; /* outside the refinement range */
         if (b == cur) {
             run++;
         } else {
-            if (run) atomicAdd(&sh[cur], run);
+            flush();
             cur = b;
             run = 1;
         }
+    };
+    auto binof = [&](uint64_t K) -> uint32_t {
+        if (RANGE && K - bc.kmin >= bc.D) return 0xFFFFFFFFu;
+        return bc(K);
     };
     const uint64_t nchunks = count / 8;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -829,14 +847,15 @@ __global__ void __launch_bounds__(256) rk_hist_kernel(const uint64_t* __restrict
         for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += stride) {
             const ulonglong2 a = __ldcs(k2 + 4 * c), b = __ldcs(k2 + 4 * c + 1);
             const ulonglong2 d = __ldcs(k2 + 4 * c + 2), e = __ldcs(k2 + 4 * c + 3);
-            put(bc(a.x)); put(bc(a.y)); put(bc(b.x)); put(bc(b.y));
-            put(bc(d.x)); put(bc(d.y)); put(bc(e.x)); put(bc(e.y));
+            put(binof(a.x)); put(binof(a.y)); put(binof(b.x)); put(binof(b.y));
+            put(binof(d.x)); put(binof(d.y)); put(binof(e.x)); put(binof(e.y));
         }
     }
     for (uint64_t i = (aligned ? nchunks * 8 : 0) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += stride)
-        put(bc(keys[i]));
-    if (run) atomicAdd(&sh[cur], run);
+        put(binof(keys[i]));
+    flush();
+    if (!smem_bins) return;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x)
         if (sh[i]) atomicAdd((unsigned long long*)&hist[i], (unsigned long long)sh[i]);
@@ -954,11 +973,26 @@ int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin,
     const uint64_t cap = (uint64_t)num_sms() * 8;
     if (ctas > cap) ctas = cap;
     if (ctas < 1) ctas = 1;
-    const size_t smem = (size_t)bins * 4;
+    const size_t smem = bins <= kSmemBins ? (size_t)bins * 4 : 0;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(rk_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rk_hist_kernel<<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, kmin, kmax, range_dev, bins,
-                                                                          hist_dev);
+        cudaFuncSetAttribute(rk_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rk_hist_kernel<false><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, kmin, kmax, range_dev,
+                                                                                 bins, hist_dev);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_launch_range_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t lo, uint64_t span, uint32_t bins,
+                              uint64_t* hist_dev, void* stream, uint32_t* launches) {
+    uint64_t ctas = (count / 8 + 255) / 256;
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    if (ctas > cap) ctas = cap;
+    if (ctas < 1) ctas = 1;
+    const size_t smem = bins <= kSmemBins ? (size_t)bins * 4 : 0;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rk_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rk_hist_kernel<true><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, lo, span, nullptr,
+                                                                                bins, hist_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

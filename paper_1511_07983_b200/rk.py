@@ -23,7 +23,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 #: every symbol include/rk.h declares (checked by tests/test_abi.py)
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
            "rk_eval_range_async", "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_heuristic_order", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
+           "rk_select_keys", "rk_range_histogram", "rk_heuristic_order", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -78,6 +78,8 @@ def lib():
             "rk_merge_stats_async": ([vp, vp, u32, vp, vp], ctypes.c_int),
             "rk_histogram": ([vp, vp, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_histogram_async": ([vp, vp, u64, vp, u32, vp, vp], ctypes.c_int),
+            "rk_select_keys": ([vp, vp, u64, u64, u64, P(u64), u32, P(u64), vp], ctypes.c_int),
+            "rk_range_histogram": ([vp, vp, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_heuristic_order": ([vp, P(ctypes.c_int32), P(ctypes.c_int32), P(u64), P(u64)], ctypes.c_int),
             "rk_percentile": ([vp, P(ctypes.c_int32), u64, u64, P(u64), P(u64)], ctypes.c_int),
             "rk_eval_batch": ([vp, P(rk_kernel), u32, u32, P(u64), P(rk_stats), P(u64), vp], ctypes.c_int),
@@ -231,6 +233,18 @@ class Context:
     def rk_histogram_async(self, keys_dev, count: int, range_dev, bins: int, hist_dev, stream=None):
         self._chk(self._L.rk_histogram_async(self.h, _ptr(keys_dev), count, _ptr(range_dev), bins, _ptr(hist_dev),
                                              _stream(stream)), "rk_histogram_async")
+
+    def rk_select_keys(self, keys_dev, count: int, kmin: int, kmax: int, ranks, stream=None):
+        m = len(ranks)
+        r = (ctypes.c_uint64 * max(1, m))(*ranks)
+        out = (ctypes.c_uint64 * max(1, m))()
+        self._chk(self._L.rk_select_keys(self.h, _ptr(keys_dev), count, kmin, kmax, r, m, out, _stream(stream)),
+                  "rk_select_keys")
+        return list(out)[:m]
+
+    def rk_range_histogram(self, keys_dev, count: int, lo: int, span: int, bins: int, hist_dev, stream=None):
+        self._chk(self._L.rk_range_histogram(self.h, _ptr(keys_dev), count, lo, span, bins, _ptr(hist_dev),
+                                             _stream(stream)), "rk_range_histogram")
 
     def rk_heuristic_order(self, with_key: bool = True):
         """Algorithm 1 -> (order, round_of, index, key-or-None)."""

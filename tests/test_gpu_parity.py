@@ -339,3 +339,67 @@ def test_max_n12_many_rounds_one_sm(ctx):
     for i, k in zip(idx.tolist(), kh.tolist()):
         assert O.simulate(gpu, ks, O.unrank(i, 12)).key == k
     assert int(kh[-2]) == st.key_min and int(kh[-1]) == st.key_max
+
+
+def test_order_statistics_median_and_ranks(ctx):
+    """median = lower-middle of the sorted times; Fig. 1 ranking curve =
+    keys at chosen ranks.  rk_select_keys vs a library sort of the oracle keys."""
+    g = _gold("w4.json")
+    st, keys = gpu_keys(ctx, g["gpu"], g["kernels"])
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    # hand distribution {126464:16, 129664:2, 131264:2, 132864:4}: ranks 11 (median), 16, 18, 20, 23
+    got = ctx.rk_select_keys(kd, 24, st.key_min, st.key_max, [11, 15, 16, 18, 20, 23, 0])
+    assert got == [100 * t for t in (126464, 126464, 129664, 131264, 132864, 132864, 126464)]
+    for name in ("C2", "C3"):
+        gpu, ks = W.config(name)
+        st, keys = gpu_keys(ctx, gpu, ks)
+        _, okeys = O.sweep(gpu, ks, threads=NCPU, keys=True)
+        srt = np.sort(okeys)
+        N = len(srt)
+        ranks = [0, N - 1, (N - 1) // 2, N // 3, 7 * N // 9, 1, N - 2] + [int(x) for x in
+                                                                           np.random.default_rng(3).integers(0, N, 20)]
+        kd = torch.from_numpy(keys.view(np.int64)).cuda()
+        assert ctx.rk_select_keys(kd, N, st.key_min, st.key_max, ranks) == [int(srt[r]) for r in ranks]
+        # the range-histogram building block: counts in [lo, lo+span) match a direct count
+        lo, span = int(srt[N // 4]), int(srt[3 * N // 4] - srt[N // 4]) + 1
+        h = torch.zeros(64, dtype=torch.int64, device="cuda")
+        ctx.rk_range_histogram(kd, N, lo, span, 64, h)
+        torch.cuda.synchronize()
+        inside = okeys[(okeys >= lo) & (okeys < lo + span)]
+        assert int(h.sum().item()) == len(inside)
+
+
+def test_histogram_bin_count_equals_key_span(ctx):
+    """Regression: bins == kmax - kmin (the 32-bit magic would be 2^32)."""
+    gpu, ks = W.config("C2")
+    st, keys = gpu_keys(ctx, gpu, ks)
+    _, okeys = O.sweep(gpu, ks, threads=NCPU, keys=True)
+    D = st.key_max - st.key_min
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    lo = int(np.sort(okeys)[100])
+    sub = okeys[okeys >= lo]
+    for B in (D, D - 1, D + 1) if D <= 65536 else ():
+        h = torch.zeros(B, dtype=torch.int64, device="cuda")
+        ctx.rk_histogram(kd, len(keys), st.key_min, st.key_max, B, h)
+        assert h.cpu().tolist() == O.histogram(okeys, st.key_min, st.key_max, B)
+    # unit-width range bins: span == bins
+    span = 4096
+    h = torch.zeros(span, dtype=torch.int64, device="cuda")
+    ctx.rk_range_histogram(kd, len(keys), lo, span, span, h)
+    want = np.bincount((sub[sub < lo + span] - np.uint64(lo)).astype(np.int64), minlength=span)
+    assert h.cpu().numpy().tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("D,B", [(1000, 1000), (999, 1000), (1001, 1000), (5, 256), (1 << 33, 256), (1 << 40, 4096),
+                                 ((1 << 62) + 12345, 7), (65536, 65536)])
+def test_histogram_exact_on_synthetic_keys(ctx, D, B):
+    """rk_histogram on arbitrary key arrays (every BinCalc path: 32-bit magic,
+    64-bit reciprocal, 128-bit) vs the oracle's integer formula (O7)."""
+    rng = np.random.default_rng(D % 1000 + B)
+    kmin = 10 ** 9 + 17
+    keys = (np.uint64(kmin) + rng.integers(0, D + 1, 100000, dtype=np.uint64)).astype(np.uint64)
+    keys[:3] = [kmin, kmin + D, kmin + D // 2]
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    h = torch.zeros(B, dtype=torch.int64, device="cuda")
+    ctx.rk_histogram(kd, len(keys), kmin, kmin + D, B, h)
+    assert h.cpu().tolist() == O.histogram(keys, kmin, kmin + D, B)
