@@ -49,3 +49,37 @@ def max_over_ranks(x: float, device, group=None) -> float:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def select_keys_sharded(count_fn, kmin: int, kmax: int, ranks, bins: int = 16384, group=None, device=None):
+    """Exact order statistics over keys sharded across ranks (SPEC:302 median =
+    rank (N-1)//2 of the sorted times; Fig. 1 ranking points).
+
+    count_fn(lo, span, bins) -> int64 tensor[bins]: this rank's counts of keys in
+    [lo, lo+span) per half-open equal bin (on GPU: Context.rk_range_histogram
+    over the rank's keys).  The per-bin counts are summed over ranks
+    (all_reduce), every rank picks the same bin, and the range shrinks until
+    the bins are single key values.  Returns the selected keys (same on every
+    rank)."""
+    out = []
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    for r in ranks:
+        lo, span, r = int(kmin), int(kmax) - int(kmin) + 1, int(r)
+        while True:
+            nb = span if span <= bins else bins
+            h = count_fn(lo, span, nb)
+            if multi:
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+            c = torch.cumsum(h.to("cpu", torch.int64), 0)
+            b = int(torch.searchsorted(c, torch.tensor([r], dtype=torch.int64), right=True).item())
+            if b >= nb:
+                raise ValueError("rank outside the keys in [kmin, kmax]")
+            below = int(c[b - 1].item()) if b > 0 else 0
+            r -= below
+            if nb == span:
+                out.append(lo + b)
+                break
+            a0 = -((-b * span) // nb)          # ceil(b*span/nb)
+            a1 = -((-(b + 1) * span) // nb)    # ceil((b+1)*span/nb)
+            lo, span = lo + a0, a1 - a0
+    return out

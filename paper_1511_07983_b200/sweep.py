@@ -34,6 +34,7 @@ class Report:
     n_gt: int
     hist: list
     rb_den: int
+    median_key: int | None = None  # lower-middle of the sorted keys
 
     @property
     def percentile(self) -> float:  # ties count for the candidate
@@ -108,17 +109,34 @@ class Sweeper:
         order, _, idx, _ = self.ctx.rk_heuristic_order(with_key=False)  # Algorithm 1 on the host
         return order, idx
 
-    def run(self, kernels) -> Report:
-        """End to end: host profiles in (H2D), report out (D2H)."""
+    def run(self, kernels, median: bool = False) -> Report:
+        """End to end: host profiles in (H2D), report out (D2H).  median=True adds
+        the exact median key (a few extra passes over the keys)."""
         self.set_kernels(kernels)
         order, idx = self.heuristic()
         self.step_device(idx)
         out = torch.cat([(self.glob if self.world > 1 else self.rec), self.cand, self.hist]).cpu()
         st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(out[:REC_WORDS].numpy().tobytes()))
-        return Report(n_orders=self.total, best_key=st.key_min, best_index=st.argmin, worst_key=st.key_max,
-                      worst_index=st.argmax, cand_order=order, cand_index=idx,
-                      cand_key=int(out[REC_WORDS].item()) & ((1 << 64) - 1), n_lt=st.n_lt, n_eq=st.n_eq,
-                      n_gt=st.n_gt, hist=[int(x) for x in out[REC_WORDS + 1:].tolist()], rb_den=self.gpu[6])
+        rep = Report(n_orders=self.total, best_key=st.key_min, best_index=st.argmin, worst_key=st.key_max,
+                     worst_index=st.argmax, cand_order=order, cand_index=idx,
+                     cand_key=int(out[REC_WORDS].item()) & ((1 << 64) - 1), n_lt=st.n_lt, n_eq=st.n_eq,
+                     n_gt=st.n_gt, hist=[int(x) for x in out[REC_WORDS + 1:].tolist()], rb_den=self.gpu[6])
+        if median:
+            rep.median_key = self.select([(self.total - 1) // 2], st.key_min, st.key_max)[0]
+        return rep
+
+    def select(self, ranks, kmin: int, kmax: int):
+        """Exact order statistics over all ranks' keys (after a step)."""
+        if self.world == 1:
+            return self.ctx.rk_select_keys(self.keys, self.count, kmin, kmax, ranks)
+
+        def count_fn(lo, span, nb):
+            h = torch.zeros(nb, dtype=torch.int64, device=self.dev)
+            self.ctx.rk_range_histogram(self.keys, self.count, lo, span, nb, h)
+            return h
+
+        from .dist import select_keys_sharded
+        return select_keys_sharded(count_fn, kmin, kmax, ranks, group=self.group)
 
     @property
     def h2d_bytes(self) -> int:

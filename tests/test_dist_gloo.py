@@ -107,3 +107,49 @@ def test_shard_bounds_partition():
             for (f0, c0), (f1, _) in zip(b, b[1:]):
                 assert f0 + c0 == f1
             assert max(c for _, c in b) - min(c for _, c in b) <= 1
+
+
+def _sel_worker(rank, world, port, q):
+    import numpy as np
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(7)
+    allkeys = rng.integers(10 ** 10, 10 ** 10 + 10 ** 7, 50000).astype(np.int64)
+    allkeys[:5] = [10 ** 10, 10 ** 10 + 10 ** 7 - 1, 10 ** 10 + 3, 10 ** 10 + 3, 10 ** 10 + 3]
+    first, count = D.shard_bounds(len(allkeys), world, rank)
+    mine = allkeys[first:first + count]
+
+    def count_fn(lo, span, nb):  # test-side counter (the GPU uses rk_range_histogram)
+        x = mine[(mine >= lo) & (mine < lo + span)] - lo
+        return torch.from_numpy(np.bincount((x * nb) // span, minlength=nb).astype(np.int64))
+
+    ranks = [0, len(allkeys) - 1, (len(allkeys) - 1) // 2, 1, 2, 3, 12345]
+    got = D.select_keys_sharded(count_fn, int(allkeys.min()), int(allkeys.max()), ranks, bins=64)
+    if rank == 0:
+        q.put((got, [int(v) for v in np.sort(allkeys)[ranks]]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_sharded_order_statistics_over_gloo(world):
+    import queue
+    import time
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sel_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    t0 = time.time()
+    while True:
+        try:
+            got, want = q.get(timeout=2)
+            break
+        except queue.Empty:
+            assert not any(p.exitcode not in (None, 0) for p in procs), "a rank failed"
+            assert time.time() - t0 < 240, "timeout"
+    for p in procs:
+        p.join(timeout=60)
+    assert got == want

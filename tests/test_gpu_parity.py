@@ -403,3 +403,23 @@ def test_histogram_exact_on_synthetic_keys(ctx, D, B):
     h = torch.zeros(B, dtype=torch.int64, device="cuda")
     ctx.rk_histogram(kd, len(keys), kmin, kmin + D, B, h)
     assert h.cpu().tolist() == O.histogram(keys, kmin, kmin + D, B)
+
+
+def test_public_sweeper_report_vs_oracle():
+    """The user-level call (Sweeper.run: host profiles in, Table-3 report out)."""
+    from paper_1511_07983_b200.sweep import Sweeper
+    for name in ("C2", "C3"):
+        gpu, ks = W.config(name)
+        rep = Sweeper(gpu, bins=64).run(ks, median=True)
+        order, _ = O.heuristic(gpu, ks)
+        cand = O.simulate(gpu, ks, order).key
+        st, keys = O.sweep(gpu, ks, cand_key=cand, threads=NCPU, keys=True)
+        N = len(keys)
+        assert (rep.best_key, rep.best_index, rep.worst_key, rep.worst_index) == (st.key_min, st.argmin, st.key_max,
+                                                                                st.argmax)
+        assert rep.cand_order == order and rep.cand_key == cand and rep.cand_index == O.rank(order)
+        assert (rep.n_lt, rep.n_eq, rep.n_gt) == (st.n_lt, st.n_eq, st.n_gt)
+        assert rep.hist == O.histogram(keys, st.key_min, st.key_max, 64)
+        assert rep.median_key == int(np.sort(keys)[(N - 1) // 2])  # SPEC:302 lower-middle
+        assert abs(rep.percentile - 100.0 * (st.n_eq + st.n_gt) / N) < 1e-12
+        assert rep.speedup_over_worst == st.key_max / cand
