@@ -121,6 +121,20 @@ rk_status rk_eval_range_async(rk_ctx* ctx, uint64_t first, uint64_t count, const
  * candidate order inside a device pipeline).  index < n!. */
 rk_status rk_eval_index_async(rk_ctx* ctx, uint64_t index, uint64_t* key_dev, void* stream);
 
+/* Compact-key variant: keys32_dev[j] = K(first+j) - key_base as
+ * u32, halving the key traffic.  key_base must not exceed any key of the range
+ * (e.g. rk_key_lower_bound).  If some K - key_base >= 2^32 the kernel ORs 1
+ * into *ovf_dev (caller-zeroed u32) and that entry is truncated: re-run with
+ * rk_eval_range_async.  Stats are exact either way.  Only enqueues. */
+rk_status rk_eval_range32_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                                rk_stats* stats_dev, uint32_t* keys32_dev, uint64_t key_base, uint32_t* ovf_dev,
+                                void* stream);
+
+/* Exact lower bound of every order's key for the current kernel set:
+ * max(den*sum_i T_i A_i, num*sum_i T_i M_i) ("sum of maxima >= maximum
+ * of sums").  Host only. */
+rk_status rk_key_lower_bound(rk_ctx* ctx, uint64_t* lb_out);
+
 /* Deterministic merge of n_records device records (e.g. all-gathered per-rank
  * records) into out_dev: min/max with smallest-index ties, counts summed.
  * The result is independent of record order.  Only enqueues. */
@@ -139,6 +153,10 @@ rk_status rk_histogram(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, ui
 rk_status rk_histogram_async(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, const rk_stats* range_dev,
                              uint32_t bins, uint64_t* hist_dev, void* stream);
 
+/* rk_histogram_async over compact keys: K = key_base + keys32_dev[j]. */
+rk_status rk_histogram32_async(rk_ctx* ctx, const uint32_t* keys32_dev, uint64_t count, uint64_t key_base,
+                               const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream);
+
 /* Order statistics over device keys (SPEC:299-302 SweepReport median = the
  * lower-middle element, rank (N-1)/2; Fig. 1 PAPER:204 "ranking" curve = keys
  * at chosen ranks).  keys_out[j] = the ranks[j]-th smallest (0-based) of
@@ -152,6 +170,12 @@ rk_status rk_select_keys(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, 
  * span >= 1, 1 <= bins <= 65536.  Stream-ordered. */
 rk_status rk_range_histogram(rk_ctx* ctx, const uint64_t* keys_dev, uint64_t count, uint64_t lo, uint64_t span,
                              uint32_t bins, uint64_t* hist_dev, void* stream);
+
+/* The same two calls over compact keys K = key_base + keys32_dev[j]. */
+rk_status rk_select_keys32(rk_ctx* ctx, const uint32_t* keys32_dev, uint64_t key_base, uint64_t count, uint64_t kmin,
+                           uint64_t kmax, const uint64_t* ranks, uint32_t m, uint64_t* keys_out, void* stream);
+rk_status rk_range_histogram32(rk_ctx* ctx, const uint32_t* keys32_dev, uint64_t key_base, uint64_t count,
+                               uint64_t lo, uint64_t span, uint32_t bins, uint64_t* hist_dev, void* stream);
 
 /* Algorithm 1 (readings L2, L16-L19), on the
  * host (sequential by nature).  order_out[n] = launch order Rd_1..Rd_r

@@ -524,6 +524,48 @@ rk_status rk_eval_index_async(rk_ctx* c, uint64_t index, uint64_t* key_dev, void
 
 uint32_t rk_table_bytes(void) { return (uint32_t)sizeof(RkTables); }
 
+rk_status rk_eval_range32_async(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                                rk_stats* stats_dev, uint32_t* keys32_dev, uint64_t key_base, uint32_t* ovf_dev,
+                                void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!stats_dev || !keys32_dev || !ovf_dev) return fail(c, RK_EINVAL, "stats_dev, keys32_dev, ovf_dev required");
+    if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, cand_key_dev, 0, stats_dev, nullptr,
+                           c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches, keys32_dev, key_base,
+                           ovf_dev);
+    return e ? cuda_fail(c, e, "rk_eval_kernel launch") : RK_OK;
+}
+
+rk_status rk_key_lower_bound(rk_ctx* c, uint64_t* lb_out) {
+    if (!c || !lb_out) return RK_EINVAL;
+    rk_status s = need_kernels(c);
+    if (s) return s;
+    u128 sI = 0, sM = 0;
+    for (const rk_kernel& k : c->ks) {
+        sI += (u128)k.grid_blocks * k.inst_per_block;
+        sM += (u128)k.grid_blocks * k.mem_per_block;
+    }
+    const u128 a = sI * c->gp.rb_den, b = sM * c->gp.rb_num;
+    *lb_out = (uint64_t)(a >= b ? a : b); /* < 2^63 by the key bound */
+    return RK_OK;
+}
+
+rk_status rk_histogram32_async(rk_ctx* c, const uint32_t* keys32_dev, uint64_t count, uint64_t key_base,
+                               const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (bins < 1 || bins > 65536 || !hist_dev || !range_dev || (count && !keys32_dev))
+        return fail(c, RK_EINVAL, "bad histogram args");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    if (count == 0) return RK_OK;
+    int e = rk_launch_histogram32(keys32_dev, count, key_base, range_dev, bins, hist_dev, stream, &c->launches);
+    return e ? cuda_fail(c, e, "histogram32 launch") : RK_OK;
+}
+
 rk_status rk_merge_stats_async(rk_ctx* c, const rk_stats* in_dev, uint32_t n_records, rk_stats* out_dev,
                                void* stream) {
     rk_status s = need_device(c);
@@ -572,8 +614,9 @@ rk_status rk_range_histogram(rk_ctx* c, const uint64_t* keys_dev, uint64_t count
     return e ? cuda_fail(c, e, "range histogram launch") : RK_OK;
 }
 
-rk_status rk_select_keys(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
-                         const uint64_t* ranks, uint32_t m, uint64_t* keys_out, void* stream) {
+static rk_status select_common(rk_ctx* c, const void* keys_dev, bool k32, uint64_t key_base, uint64_t count,
+                               uint64_t kmin, uint64_t kmax, const uint64_t* ranks, uint32_t m, uint64_t* keys_out,
+                               void* stream) {
     rk_status s = need_device(c);
     if (s) return s;
     if (!keys_dev || !ranks || !keys_out || kmax < kmin) return fail(c, RK_EINVAL, "bad select args");
@@ -593,7 +636,11 @@ rk_status rk_select_keys(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, ui
         for (;;) {
             const uint32_t bins = span <= B ? (uint32_t)span : B;
             e = cudaMemsetAsync(hd, 0, sizeof(uint64_t) * bins, st);
-            if (!e) e = rk_launch_range_histogram(keys_dev, count, lo, span, bins, hd, stream, &launches);
+            if (!e)
+                e = k32 ? rk_launch_range_histogram32((const uint32_t*)keys_dev, count, key_base, lo, span, bins, hd,
+                                                      stream, &launches)
+                        : rk_launch_range_histogram((const uint64_t*)keys_dev, count, lo, span, bins, hd, stream,
+                                                    &launches);
             if (!e) e = cudaMemcpyAsync(h.data(), hd, sizeof(uint64_t) * bins, cudaMemcpyDeviceToHost, st);
             if (!e) e = cudaStreamSynchronize(st);
             if (e) break;
@@ -624,6 +671,29 @@ rk_status rk_select_keys(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, ui
     if (e) return cuda_fail(c, e, "rk_select_keys");
     std::memcpy(keys_out, out.data(), sizeof(uint64_t) * m);
     return RK_OK;
+}
+
+rk_status rk_select_keys(rk_ctx* c, const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
+                         const uint64_t* ranks, uint32_t m, uint64_t* keys_out, void* stream) {
+    return select_common(c, keys_dev, false, 0, count, kmin, kmax, ranks, m, keys_out, stream);
+}
+
+rk_status rk_select_keys32(rk_ctx* c, const uint32_t* keys32_dev, uint64_t key_base, uint64_t count, uint64_t kmin,
+                           uint64_t kmax, const uint64_t* ranks, uint32_t m, uint64_t* keys_out, void* stream) {
+    return select_common(c, keys32_dev, true, key_base, count, kmin, kmax, ranks, m, keys_out, stream);
+}
+
+rk_status rk_range_histogram32(rk_ctx* c, const uint32_t* keys32_dev, uint64_t key_base, uint64_t count, uint64_t lo,
+                               uint64_t span, uint32_t bins, uint64_t* hist_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (span == 0 || bins < 1 || bins > 65536 || !hist_dev || (count && !keys32_dev))
+        return fail(c, RK_EINVAL, "bad range histogram args");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    if (count == 0) return RK_OK;
+    int e = rk_launch_range_histogram32(keys32_dev, count, key_base, lo, span, bins, hist_dev, stream, &c->launches);
+    return e ? cuda_fail(c, e, "range histogram32 launch") : RK_OK;
 }
 
 /* key of one index on the device (synchronous) */

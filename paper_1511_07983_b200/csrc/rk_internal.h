@@ -58,7 +58,12 @@ struct RkTables {
 int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t first, uint64_t count,
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
                    rk_stats* scratch_recs, uint32_t* scratch_counter, uint32_t max_ctas, void* stream,
-                   uint32_t* launches);
+                   uint32_t* launches, uint32_t* keys32_dev = nullptr, uint64_t key_base = 0,
+                   uint32_t* ovf_dev = nullptr);
+int rk_launch_range_histogram32(const uint32_t* keys_dev, uint64_t count, uint64_t key_base, uint64_t lo,
+                                uint64_t span, uint32_t bins, uint64_t* hist_dev, void* stream, uint32_t* launches);
+int rk_launch_histogram32(const uint32_t* keys_dev, uint64_t count, uint64_t key_base, const rk_stats* range_dev,
+                          uint32_t bins, uint64_t* hist_dev, void* stream, uint32_t* launches);
 int rk_launch_merge(const rk_stats* in_dev, uint32_t n_records, rk_stats* out_dev, void* stream, uint32_t* launches);
 int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin, uint64_t kmax,
                         const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream,

@@ -558,13 +558,21 @@ __host__ __device__ constexpr uint32_t cfact(int m) { return m <= 1 ? 1u : (uint
 
 struct Leaf { /* one evaluated order: statistics + optional key store */
     TStats& ts;
-    uint64_t* keys;
+    uint64_t* keys;   /* u64 keys, or */
+    uint32_t* keys32; /* compact u32 offsets K - base (ovf set if one does not fit) */
+    uint64_t base;
+    uint32_t ovf;
     uint32_t lo, hi, first;
     uint64_t cand;
     __device__ __forceinline__ void operator()(uint32_t idx, uint64_t K) {
         if (idx >= lo && idx < hi) {
             ts.add(K, idx, cand);
             if (keys) keys[idx - first] = K;
+            if (keys32) {
+                const uint64_t x = K - base;
+                ovf |= (x >> 32) != 0 ? 1u : 0u;
+                keys32[idx - first] = (uint32_t)x;
+            }
         }
     }
 };
@@ -658,7 +666,8 @@ struct MinBlocks {
 template <int SMAX, bool FULL>
 __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     rk_eval_kernel(const RkTables* __restrict__ tab, uint32_t first, uint32_t count, const uint64_t* cand_dev,
-                   uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter) {
+                   uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter,
+                   uint32_t* keys32, uint64_t key_base, uint32_t* ovf_dev) {
     __shared__ RkTables t;
     load_tables(t, tab);
     const uint64_t cand = cand_dev ? *cand_dev : cand_imm;
@@ -666,8 +675,9 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     TStats ts;
     ts.init();
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    Leaf leaf{ts, keys, lo, hi, first, cand};
+    Leaf leaf{ts, keys, keys32, key_base, 0u, lo, hi, first, cand};
     eval_space<SMAX, FULL>(t, lo, hi, gtid, nth, leaf);
+    if (leaf.ovf) atomicOr(ovf_dev, 1u);
     const rk_stats r = block_reduce(to_rec(ts));
     commit(r, recs, counter, out);
 }
@@ -690,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     const uint32_t runs = (total + R - 1) / R;
     const uint32_t per = (runs + gridDim.x - 1) / gridDim.x;
     const uint32_t lo = min(total, blockIdx.x * per * R), hi = min(total, lo + per * R);
-    Leaf leaf{ts, nullptr, lo, hi, 0u, cand};
+    Leaf leaf{ts, nullptr, nullptr, 0ull, 0u, lo, hi, 0u, cand};
     eval_space<SMAX, FULL>(t, lo, hi, threadIdx.x, blockDim.x, leaf);
     const rk_stats r = block_reduce(to_rec(ts));
     if (threadIdx.x == 0) recs[set * gridDim.x + blockIdx.x] = r;
@@ -798,11 +808,11 @@ struct BinCalc {
 /* RANGE = false: Fig. 1 bins over [kmin, kmax] (last bin closed).
  * RANGE = true: order-statistic refinement — `bins` half-open bins over
  * [kmin_imm, kmin_imm + kmax_imm) (kmax_imm = span), keys outside ignored. */
-template <bool RANGE>
-__global__ void __launch_bounds__(256) rk_hist_kernel(const uint64_t* __restrict__ keys, uint64_t count,
+template <bool RANGE, class KT>
+__global__ void __launch_bounds__(256) rk_hist_kernel(const KT* __restrict__ keys, uint64_t count,
                                                       uint64_t kmin_imm, uint64_t kmax_imm,
                                                       const rk_stats* __restrict__ range, uint32_t bins,
-                                                      uint64_t* __restrict__ hist) {
+                                                      uint64_t* __restrict__ hist, uint64_t key_base) {
     extern __shared__ uint32_t sh[];
     const bool smem_bins = bins <= kSmemBins; /* else accumulate straight into global u64 bins */
     BinCalc bc;
@@ -835,20 +845,30 @@ __global__ void __launch_bounds__(256) rk_hist_kernel(const uint64_t* __restrict
             run = 1;
         }
     };
-    auto binof = [&](uint64_t K) -> uint32_t {
+    auto binof = [&](uint64_t Kraw) -> uint32_t {
+        const uint64_t K = sizeof(KT) == 4 ? key_base + Kraw : Kraw; /* u32 keys are offsets */
         if (RANGE && K - bc.kmin >= bc.D) return 0xFFFFFFFFu;
         return bc(K);
     };
     const uint64_t nchunks = count / 8;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
     const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
     if (aligned) {
-        for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += stride) {
-            const ulonglong2 a = __ldcs(k2 + 4 * c), b = __ldcs(k2 + 4 * c + 1);
-            const ulonglong2 d = __ldcs(k2 + 4 * c + 2), e = __ldcs(k2 + 4 * c + 3);
-            put(binof(a.x)); put(binof(a.y)); put(binof(b.x)); put(binof(b.y));
-            put(binof(d.x)); put(binof(d.y)); put(binof(e.x)); put(binof(e.y));
+        if constexpr (sizeof(KT) == 8) {
+            const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
+            for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += stride) {
+                const ulonglong2 a = __ldcs(k2 + 4 * c), b = __ldcs(k2 + 4 * c + 1);
+                const ulonglong2 d = __ldcs(k2 + 4 * c + 2), e = __ldcs(k2 + 4 * c + 3);
+                put(binof(a.x)); put(binof(a.y)); put(binof(b.x)); put(binof(b.y));
+                put(binof(d.x)); put(binof(d.y)); put(binof(e.x)); put(binof(e.y));
+            }
+        } else {
+            const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+            for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += stride) {
+                const uint4 a = __ldcs(k4 + 2 * c), b = __ldcs(k4 + 2 * c + 1);
+                put(binof(a.x)); put(binof(a.y)); put(binof(a.z)); put(binof(a.w));
+                put(binof(b.x)); put(binof(b.y)); put(binof(b.z)); put(binof(b.w));
+            }
         }
     }
     for (uint64_t i = (aligned ? nchunks * 8 : 0) + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
@@ -943,7 +963,8 @@ int rk_eval_max_ctas(uint32_t S, int) {
 
 int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t first, uint64_t count,
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
-                   rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
+                   rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches,
+                   uint32_t* keys32_dev, uint64_t key_base, uint32_t* ovf_dev) {
     cudaStream_t st = (cudaStream_t)stream;
     const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t R = 1;
@@ -955,7 +976,8 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
     if (ctas > max_ctas) ctas = max_ctas;
     if (ctas < 1) ctas = 1;
     RK_DISPATCH(S, rk_eval_kernel, RK_CFG((unsigned)ctas, kThreads, 0, st), tab_dev, (uint32_t)first,
-                (uint32_t)count, cand_key_dev, cand_key_imm, stats_dev, keys_dev, recs, counter);
+                (uint32_t)count, cand_key_dev, cand_key_imm, stats_dev, keys_dev, recs, counter, keys32_dev, key_base,
+                ovf_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -975,9 +997,10 @@ int rk_launch_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t kmin,
     if (ctas < 1) ctas = 1;
     const size_t smem = bins <= kSmemBins ? (size_t)bins * 4 : 0;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(rk_hist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rk_hist_kernel<false><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, kmin, kmax, range_dev,
-                                                                                 bins, hist_dev);
+        cudaFuncSetAttribute(rk_hist_kernel<false, uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    rk_hist_kernel<false, uint64_t><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(
+        keys_dev, count, kmin, kmax, range_dev, bins, hist_dev, 0ull);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -990,9 +1013,41 @@ int rk_launch_range_histogram(const uint64_t* keys_dev, uint64_t count, uint64_t
     if (ctas < 1) ctas = 1;
     const size_t smem = bins <= kSmemBins ? (size_t)bins * 4 : 0;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(rk_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rk_hist_kernel<true><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, lo, span, nullptr,
-                                                                                bins, hist_dev);
+        cudaFuncSetAttribute(rk_hist_kernel<true, uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rk_hist_kernel<true, uint64_t><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, lo, span,
+                                                                                          nullptr, bins, hist_dev, 0ull);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_launch_range_histogram32(const uint32_t* keys_dev, uint64_t count, uint64_t key_base, uint64_t lo,
+                                uint64_t span, uint32_t bins, uint64_t* hist_dev, void* stream, uint32_t* launches) {
+    uint64_t ctas = (count / 8 + 255) / 256;
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    if (ctas > cap) ctas = cap;
+    if (ctas < 1) ctas = 1;
+    const size_t smem = bins <= kSmemBins ? (size_t)bins * 4 : 0;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rk_hist_kernel<true, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rk_hist_kernel<true, uint32_t><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(keys_dev, count, lo, span,
+                                                                                          nullptr, bins, hist_dev,
+                                                                                          key_base);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_launch_histogram32(const uint32_t* keys_dev, uint64_t count, uint64_t key_base, const rk_stats* range_dev,
+                          uint32_t bins, uint64_t* hist_dev, void* stream, uint32_t* launches) {
+    uint64_t ctas = (count / 8 + 255) / 256;
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    if (ctas > cap) ctas = cap;
+    if (ctas < 1) ctas = 1;
+    const size_t smem = bins <= kSmemBins ? (size_t)bins * 4 : 0;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rk_hist_kernel<false, uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    rk_hist_kernel<false, uint32_t><<<(unsigned)ctas, 256, smem, (cudaStream_t)stream>>>(
+        keys_dev, count, 0ull, 0ull, range_dev, bins, hist_dev, key_base);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

@@ -22,8 +22,9 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 
 #: every symbol include/rk.h declares (checked by tests/test_abi.py)
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
-           "rk_eval_range_async", "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_select_keys", "rk_range_histogram", "rk_heuristic_order", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
+           "rk_eval_range_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
+           "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
+           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -74,12 +75,17 @@ def lib():
             "rk_eval_range": ([vp, u64, u64, u64, P(rk_stats), vp, vp], ctypes.c_int),
             "rk_eval_range_async": ([vp, u64, u64, vp, vp, vp, vp], ctypes.c_int),
             "rk_eval_index_async": ([vp, u64, vp, vp], ctypes.c_int),
+            "rk_eval_range32_async": ([vp, u64, u64, vp, vp, vp, u64, vp, vp], ctypes.c_int),
+            "rk_key_lower_bound": ([vp, P(u64)], ctypes.c_int),
+            "rk_histogram32_async": ([vp, vp, u64, u64, vp, u32, vp, vp], ctypes.c_int),
             "rk_table_bytes": ([], u32),
             "rk_merge_stats_async": ([vp, vp, u32, vp, vp], ctypes.c_int),
             "rk_histogram": ([vp, vp, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_histogram_async": ([vp, vp, u64, vp, u32, vp, vp], ctypes.c_int),
             "rk_select_keys": ([vp, vp, u64, u64, u64, P(u64), u32, P(u64), vp], ctypes.c_int),
             "rk_range_histogram": ([vp, vp, u64, u64, u64, u32, vp, vp], ctypes.c_int),
+            "rk_select_keys32": ([vp, vp, u64, u64, u64, u64, P(u64), u32, P(u64), vp], ctypes.c_int),
+            "rk_range_histogram32": ([vp, vp, u64, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_heuristic_order": ([vp, P(ctypes.c_int32), P(ctypes.c_int32), P(u64), P(u64)], ctypes.c_int),
             "rk_percentile": ([vp, P(ctypes.c_int32), u64, u64, P(u64), P(u64)], ctypes.c_int),
             "rk_eval_batch": ([vp, P(rk_kernel), u32, u32, P(u64), P(rk_stats), P(u64), vp], ctypes.c_int),
@@ -219,6 +225,22 @@ class Context:
         self._chk(self._L.rk_eval_range_async(self.h, first, count, _ptr(cand_key_dev), _ptr(stats_dev),
                                               _ptr(keys_dev), _stream(stream)), "rk_eval_range_async")
 
+    def rk_eval_range32_async(self, first: int, count: int, cand_key_dev, stats_dev, keys32_dev, key_base: int,
+                              ovf_dev, stream=None):
+        self._chk(self._L.rk_eval_range32_async(self.h, first, count, _ptr(cand_key_dev), _ptr(stats_dev),
+                                                _ptr(keys32_dev), key_base, _ptr(ovf_dev), _stream(stream)),
+                  "rk_eval_range32_async")
+
+    def rk_key_lower_bound(self) -> int:
+        v = ctypes.c_uint64()
+        self._chk(self._L.rk_key_lower_bound(self.h, ctypes.byref(v)), "rk_key_lower_bound")
+        return v.value
+
+    def rk_histogram32_async(self, keys32_dev, count: int, key_base: int, range_dev, bins: int, hist_dev,
+                             stream=None):
+        self._chk(self._L.rk_histogram32_async(self.h, _ptr(keys32_dev), count, key_base, _ptr(range_dev), bins,
+                                               _ptr(hist_dev), _stream(stream)), "rk_histogram32_async")
+
     def rk_eval_index_async(self, index: int, key_dev, stream=None):
         self._chk(self._L.rk_eval_index_async(self.h, index, _ptr(key_dev), _stream(stream)), "rk_eval_index_async")
 
@@ -245,6 +267,19 @@ class Context:
     def rk_range_histogram(self, keys_dev, count: int, lo: int, span: int, bins: int, hist_dev, stream=None):
         self._chk(self._L.rk_range_histogram(self.h, _ptr(keys_dev), count, lo, span, bins, _ptr(hist_dev),
                                              _stream(stream)), "rk_range_histogram")
+
+    def rk_select_keys32(self, keys32_dev, key_base: int, count: int, kmin: int, kmax: int, ranks, stream=None):
+        m = len(ranks)
+        r = (ctypes.c_uint64 * max(1, m))(*ranks)
+        out = (ctypes.c_uint64 * max(1, m))()
+        self._chk(self._L.rk_select_keys32(self.h, _ptr(keys32_dev), key_base, count, kmin, kmax, r, m, out,
+                                           _stream(stream)), "rk_select_keys32")
+        return list(out)[:m]
+
+    def rk_range_histogram32(self, keys32_dev, key_base: int, count: int, lo: int, span: int, bins: int, hist_dev,
+                             stream=None):
+        self._chk(self._L.rk_range_histogram32(self.h, _ptr(keys32_dev), key_base, count, lo, span, bins,
+                                               _ptr(hist_dev), _stream(stream)), "rk_range_histogram32")
 
     def rk_heuristic_order(self, with_key: bool = True):
         """Algorithm 1 -> (order, round_of, index, key-or-None)."""

@@ -53,7 +53,7 @@ class Report:
 
 
 class Sweeper:
-    def __init__(self, gpu, device: int | None = None, bins: int = 256, group=None):
+    def __init__(self, gpu, device: int | None = None, bins: int = 256, group=None, compact_keys: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("Sweeper needs a CUDA device (no CPU fallback)")
         self.group = group
@@ -68,6 +68,9 @@ class Sweeper:
         self.bins = bins
         self.n = 0
         self.keys = None
+        self.keys32 = None
+        self.ovf = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.compact_keys = compact_keys  # u32 offsets: half the key bytes (measured: no net gain on C4)
         self.rec = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
         self.glob = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
         self.cand = torch.zeros(1, dtype=torch.int64, device=self.dev)
@@ -79,17 +82,44 @@ class Sweeper:
         self.n = len(kernels)
         self.total = math.factorial(self.n)
         self.first, self.count = shard_bounds(self.total, self.world, self.rank)
+        # compact keys (u32 offsets from the exact lower bound) unless a
+        # previous pass on this set overflowed; then u64 keys
+        self.base = self.ctx.rk_key_lower_bound()
+        self.ovf.zero_()
+        if self.compact_keys:
+            self.compact = True
+            if self.keys32 is None or self.keys32.numel() < self.count:
+                self.keys32 = torch.empty(max(1, self.count), dtype=torch.int32, device=self.dev)
+        else:
+            self._use_wide_keys()
+
+    def _use_wide_keys(self):
+        self.compact = False
         if self.keys is None or self.keys.numel() < self.count:
             self.keys = torch.empty(max(1, self.count), dtype=torch.int64, device=self.dev)
 
-    def step_device(self, cand_index: int, stream=None):
-        """Enqueue one pass of the hot path; no host sync.  Returns #our launches."""
+    def step_device(self, cand_index: int, stream=None, events=None):
+        """Enqueue one pass of the hot path; no host sync.  Returns #our launches.
+        events (optional dict) receives CUDA event pairs around the eval and
+        histogram kernels."""
         c = self.ctx
         L = 0
         c.rk_eval_index_async(cand_index, self.cand, stream)                                  # a5 candidate key
         L += c.launches
-        c.rk_eval_range_async(self.first, self.count, self.cand, self.rec, self.keys, stream)  # a1-a4
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if events is not None else None
+        st = torch.cuda.current_stream() if stream is None else stream
+        if ev:
+            e0, e1 = ev(), ev()
+            e0.record(st)
+        if self.compact:                                                                       # a1-a4
+            c.rk_eval_range32_async(self.first, self.count, self.cand, self.rec, self.keys32, self.base, self.ovf,
+                                    stream)
+        else:
+            c.rk_eval_range_async(self.first, self.count, self.cand, self.rec, self.keys, stream)
         L += c.launches
+        if ev:
+            e1.record(st)
+            events.setdefault("eval", []).append((e0, e1))
         if self.world > 1:                                                                      # a6 combine
             recs = all_gather_records(self.rec, self.group)
             c.rk_merge_stats_async(recs, self.world, self.glob, stream)
@@ -98,12 +128,28 @@ class Sweeper:
         else:
             rng = self.rec
         self.hist.zero_()
-        c.rk_histogram_async(self.keys, self.count, rng, self.bins, self.hist, stream)          # a4 histogram
+        if ev:
+            h0, h1 = ev(), ev()
+            h0.record(st)
+        if self.compact:                                                                       # a4 histogram
+            c.rk_histogram32_async(self.keys32, self.count, self.base, rng, self.bins, self.hist, stream)
+        else:
+            c.rk_histogram_async(self.keys, self.count, rng, self.bins, self.hist, stream)
         L += c.launches
+        if ev:
+            h1.record(st)
+            events.setdefault("hist", []).append((h0, h1))
         if self.world > 1:
             all_reduce_hist(self.hist, self.group)
         self.launches = L
         return L
+
+    def overflowed(self) -> bool:
+        """Did a compact-key pass see a key >= base + 2^32 (on any rank)?"""
+        f = self.ovf.clone()
+        if self.world > 1:
+            dist.all_reduce(f, op=dist.ReduceOp.MAX, group=self.group)
+        return bool(f.item())
 
     def heuristic(self):
         order, _, idx, _ = self.ctx.rk_heuristic_order(with_key=False)  # Algorithm 1 on the host
@@ -115,6 +161,9 @@ class Sweeper:
         self.set_kernels(kernels)
         order, idx = self.heuristic()
         self.step_device(idx)
+        if self.compact and self.overflowed():  # rare: keys span >= 2^32 above the bound
+            self._use_wide_keys()
+            self.step_device(idx)
         out = torch.cat([(self.glob if self.world > 1 else self.rec), self.cand, self.hist]).cpu()
         st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(out[:REC_WORDS].numpy().tobytes()))
         rep = Report(n_orders=self.total, best_key=st.key_min, best_index=st.argmin, worst_key=st.key_max,
@@ -128,11 +177,16 @@ class Sweeper:
     def select(self, ranks, kmin: int, kmax: int):
         """Exact order statistics over all ranks' keys (after a step)."""
         if self.world == 1:
+            if self.compact:
+                return self.ctx.rk_select_keys32(self.keys32, self.base, self.count, kmin, kmax, ranks)
             return self.ctx.rk_select_keys(self.keys, self.count, kmin, kmax, ranks)
 
         def count_fn(lo, span, nb):
             h = torch.zeros(nb, dtype=torch.int64, device=self.dev)
-            self.ctx.rk_range_histogram(self.keys, self.count, lo, span, nb, h)
+            if self.compact:
+                self.ctx.rk_range_histogram32(self.keys32, self.base, self.count, lo, span, nb, h)
+            else:
+                self.ctx.rk_range_histogram(self.keys, self.count, lo, span, nb, h)
             return h
 
         from .dist import select_keys_sharded

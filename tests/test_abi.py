@@ -24,7 +24,7 @@ def built():
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "rk.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rk_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(rk_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declarations_match_binding_exports():

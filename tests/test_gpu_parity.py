@@ -423,3 +423,42 @@ def test_public_sweeper_report_vs_oracle():
         assert rep.median_key == int(np.sort(keys)[(N - 1) // 2])  # SPEC:302 lower-middle
         assert abs(rep.percentile - 100.0 * (st.n_eq + st.n_gt) / N) < 1e-12
         assert rep.speedup_over_worst == st.key_max / cand
+
+
+def test_compact_keys_histogram32_select32_and_overflow_flag(ctx):
+    gpu, ks = W.config("C3")
+    st, keys = gpu_keys(ctx, gpu, ks)
+    N = len(keys)
+    base = ctx.rk_key_lower_bound()
+    sI = sum(k[0] * k[4] for k in ks)
+    sM = sum(k[0] * k[5] for k in ks)
+    assert base == max(gpu[6] * sI, gpu[5] * sM) <= st.key_min
+    k32 = torch.empty(N, dtype=torch.int32, device="cuda")
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+    ctx.rk_eval_range32_async(0, N, None, rec, k32, base, ovf)
+    torch.cuda.synchronize()
+    assert int(ovf.item()) == 0
+    got = k32.cpu().numpy().view(np.uint32).astype(np.uint64) + np.uint64(base)
+    assert np.array_equal(got, keys)
+    assert rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes())).as_tuple()[:4] == \
+        st.as_tuple()[:4]
+    h = torch.zeros(256, dtype=torch.int64, device="cuda")
+    ctx.rk_histogram32_async(k32, N, base, rec, 256, h)
+    assert h.cpu().tolist() == O.histogram(keys, st.key_min, st.key_max, 256)
+    srt = np.sort(keys)
+    ranks = [0, N - 1, (N - 1) // 2, 12345]
+    assert ctx.rk_select_keys32(k32, base, N, st.key_min, st.key_max, ranks) == [int(srt[r]) for r in ranks]
+    # a base too far below the keys must raise the overflow flag
+    ovf.zero_()
+    ctx.rk_eval_range32_async(0, N, None, rec, k32, st.key_max - (1 << 32), ovf)
+    torch.cuda.synchronize()
+    assert int(ovf.item()) == 1
+
+
+def test_public_sweeper_compact_keys_mode():
+    from paper_1511_07983_b200.sweep import Sweeper
+    gpu, ks = W.config("C2")
+    a = Sweeper(gpu, bins=32).run(ks, median=True)
+    b = Sweeper(gpu, bins=32, compact_keys=True).run(ks, median=True)
+    assert a == b
