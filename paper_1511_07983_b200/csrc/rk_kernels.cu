@@ -211,6 +211,22 @@ __device__ __forceinline__ uint32_t water_fill(uint32_t n, const uint32_t (&c)[S
         }
     }
     const uint32_t r = n - flo; /* >= 1 blocks of pass tlo+1, to SMs with c_s > tlo in ring order */
+    if constexpr (FULL && SMAX == 1) {
+        upd(0, bfa[0] - n * k.dA, bfb[0] - n * k.dB); /* one SM takes all n (n <= c) */
+        return 0u;
+    } else if constexpr (FULL && SMAX == 2) {
+        /* ring order from the cursor: SM a = cur, then SM b.  r == 2: both get
+         * pass tlo+1 (both eligible), the last lands on b, cursor stays;
+         * r == 1: the first eligible of (a, b) gets it, cursor = the other. */
+        const uint32_t a = cur, ca = a ? c[1] : c[0], cb = a ? c[0] : c[1];
+        const bool ea = ca > tlo, two = r == 2u;
+        const uint32_t xa = min(ca, tlo) + ((two || ea) ? 1u : 0u);
+        const uint32_t xb = min(cb, tlo) + ((two || !ea) ? 1u : 0u);
+        const uint32_t x0 = a ? xb : xa, x1 = a ? xa : xb;
+        upd(0, bfa[0] - x0 * k.dA, bfb[0] - x0 * k.dB);
+        upd(1, bfa[1] - x1 * k.dA, bfb[1] - x1 * k.dB);
+        return (two || !ea) ? a : 1u - a;
+    }
     uint32_t E;
     if constexpr (NP > 0 && SMAX <= 16) {
         /* E = {s : c_s > tlo}: per pair min(c, tlo+1) - min(c, tlo) is 0/1 in each half */
