@@ -8,7 +8,7 @@ Generator G (seed 0x0151107983000004) on the GTX580 model parameters, the full
 12! = 479,001,600 launch-order space.  One step = one pass of the whole hot
 path: Algorithm 1 candidate (host) + its key
 (device), unrank/pack/score/reduce over the rank's index shard with keys kept
-in HBM, [N>1: NCCL all_gather of the 56-B records + device merge], the exact
+in HBM, [N>1: NCCL all_gather of the 64-B records + device merge], the exact
 256-bin histogram over the global [min,max], [N>1: NCCL all_reduce].  Total
 work per step is fixed (12!), shards are contiguous index ranges: strong
 scaling.  For N>1 launch with torchrun (one rank per GPU).
@@ -253,8 +253,8 @@ def main():
 
     # correctness of the timed pipeline's result (global record, histogram mass)
     out = torch.cat([sw.glob if world > 1 else sw.rec, sw.hist]).cpu()
-    evaluated = int(out[6].item())
-    hist_mass = int(out[7:].sum().item())
+    evaluated = int(out[7].item())
+    hist_mass = int(out[8:].sum().item())
     assert hist_mass == N and (world > 1 or evaluated == N), (hist_mass, evaluated)
 
     # e2e: the public API with host buffers (Sweeper.run: H2D tables, D2H report)
@@ -282,7 +282,7 @@ def main():
         del os.environ["RK_NO_REDUCE"]
         c2.rk_set_gpu_params(gpu)
         c2.rk_set_kernels(ks)
-        rec2 = torch.zeros(7, dtype=torch.int64, device=sw.dev)
+        rec2 = torch.zeros(8, dtype=torch.int64, device=sw.dev)
         for _ in range(2):
             c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, sw.keys, stream)
         torch.cuda.synchronize()

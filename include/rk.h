@@ -36,7 +36,7 @@ typedef enum {
     RK_OK = 0,
     RK_EINVAL = 1,         /* invalid argument / profile (SPEC:359 ValidationError)           */
     RK_EINFEASIBLE = 2,    /* a single block exceeds an SM limit      */
-    RK_ETOOMANY = 3,       /* n > 12: index no longer fits u32                */
+    RK_ETOOMANY = 3,       /* n > 16 (indices are u64, kernel ids 4-bit)       */
     RK_EMISSINGRATIO = 4,  /* mem_per_block == 0: R_i undefined                 */
     RK_EOVERFLOW = 5,      /* exact key bound sum_i T_i(den*A_i + num*M_i) >= 2^63            */
     RK_ESTATE = 6,         /* call order (params/kernels not set)                              */
@@ -81,7 +81,7 @@ typedef struct {
     uint32_t inst_per_block, mem_per_block;
 } rk_kernel;
 
-/* Copy and validate n kernels (1 <= n <= 12) and upload the device tables.
+/* Copy and validate n kernels (1 <= n <= 16) and upload the device tables.
  * Errors: RK_ESTATE (no gpu params), RK_EINVAL, RK_EINFEASIBLE,
  * RK_ETOOMANY, RK_EMISSINGRATIO, RK_EOVERFLOW, RK_EUNSUPPORTED, RK_ECUDA. */
 rk_status rk_set_kernels(rk_ctx* ctx, const rk_kernel* k, uint32_t n);
@@ -90,10 +90,10 @@ rk_status rk_set_kernels(rk_ctx* ctx, const rk_kernel* k, uint32_t n);
  * SPEC:281-286).  Keys are exact: K = sum_r max(rb_den*I_r, rb_num*M_r) =
  * rb_den * T (O4), so T = K / rb_den.  argmin/argmax = smallest lexicographic
  * index attaining the extreme (reading L12).  n_lt/n_eq/n_gt count keys
- * below/equal/above the candidate key.  56 bytes, no padding. */
+ * below/equal/above the candidate key.  64 bytes, no padding. */
 typedef struct {
     uint64_t key_min, key_max;
-    uint32_t argmin, argmax;
+    uint64_t argmin, argmax;
     uint64_t n_lt, n_eq, n_gt;
     uint64_t evaluated;
 } rk_stats;
@@ -115,6 +115,16 @@ rk_status rk_eval_range(rk_ctx* ctx, uint64_t first, uint64_t count, uint64_t ca
  * Only enqueues. */
 rk_status rk_eval_range_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
                               rk_stats* stats_dev, uint64_t* keys_dev, void* stream);
+
+/* Second pass for spaces too large to keep keys (n >= 13: 13! keys = 50 GB):
+ * re-evaluates [first, first+count) and bins every key straight into `bins`
+ * Fig. 1 bins over [range_dev->key_min, key_max] (the first pass's global
+ * record) in shared memory; hist_dev (device u64[bins]) is accumulated.  Also
+ * writes the range's record to stats_dev (nullable).  1 <= bins <= 32768.
+ * Only enqueues. */
+rk_status rk_eval_range_hist_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                                   rk_stats* stats_dev, const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev,
+                                   void* stream);
 
 /* Exact key of the single launch order with lexicographic index `index`,
  * written to key_dev (device u64).  Stream-ordered, no host sync (used for the

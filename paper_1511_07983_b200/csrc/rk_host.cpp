@@ -103,7 +103,7 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
     rk_status s = check_params(c, p);
     if (s) return s;
     if (n == 0) return fail(c, RK_EINVAL, "need at least one kernel");
-    if (n > RK_MAX_N) return fail(c, RK_ETOOMANY, "n = %u > %d: index space exceeds u32", n, RK_MAX_N);
+    if (n > RK_MAX_N) return fail(c, RK_ETOOMANY, "n = %u > %d kernels", n, RK_MAX_N);
     u128 bound = 0;
     uint64_t gr = p.regs_per_sm, gs = p.shm_bytes_per_sm;
     std::vector<Derived> d(n);
@@ -161,7 +161,7 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
     }
     g.tbits = tb;
     g.n = n;
-    for (uint32_t i = 0; i <= RK_MAX_N; i++) g.fact[i] = (uint32_t)fact64(i);
+    for (uint32_t i = 0; i <= RK_MAX_N; i++) g.fact[i] = fact64(i);
     const uint64_t caps[3] = {R, Sh, p.max_warps_per_sm};
     for (uint32_t i = 0; i < n; i++) {
         const uint64_t dem[3] = {d[i].regs / gr, d[i].shm / gs, d[i].warps};
@@ -537,6 +537,22 @@ rk_status rk_eval_range32_async(rk_ctx* c, uint64_t first, uint64_t count, const
                            c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches, keys32_dev, key_base,
                            ovf_dev);
     return e ? cuda_fail(c, e, "rk_eval_kernel launch") : RK_OK;
+}
+
+rk_status rk_eval_range_hist_async(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                                   rk_stats* stats_dev, const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev,
+                                   void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!range_dev || !hist_dev || bins < 1 || bins > 32768) return fail(c, RK_EINVAL, "bad fused histogram args");
+    if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    rk_stats* out = stats_dev ? stats_dev : c->stats_dev;
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, cand_key_dev, 0, out, nullptr,
+                           c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches, nullptr, 0, nullptr,
+                           range_dev, bins, hist_dev);
+    return e ? cuda_fail(c, e, "rk_eval_kernel (fused histogram) launch") : RK_OK;
 }
 
 rk_status rk_key_lower_bound(rk_ctx* c, uint64_t* lb_out) {

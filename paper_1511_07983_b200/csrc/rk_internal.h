@@ -21,7 +21,7 @@
 #include <stdint.h>
 #include "rk.h"
 
-#define RK_MAX_N 12
+#define RK_MAX_N 16
 #define RK_SMAX 32
 
 struct RkKTab {        /* one kernel; 72 B */
@@ -46,7 +46,7 @@ struct RkGTab {
     uint32_t smagic;       /* ceil(2^32 / S) */
     uint32_t tbits;        /* highest power of two <= max_blocks_per_sm (binary search) */
     uint32_t n;            /* number of kernels */
-    uint32_t fact[RK_MAX_N + 1];
+    uint64_t fact[RK_MAX_N + 1];
 };
 
 struct RkTables {
@@ -59,7 +59,8 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
                    rk_stats* scratch_recs, uint32_t* scratch_counter, uint32_t max_ctas, void* stream,
                    uint32_t* launches, uint32_t* keys32_dev = nullptr, uint64_t key_base = 0,
-                   uint32_t* ovf_dev = nullptr);
+                   uint32_t* ovf_dev = nullptr, const rk_stats* hist_range = nullptr, uint32_t bins = 0,
+                   uint64_t* hist_dev = nullptr);
 int rk_launch_range_histogram32(const uint32_t* keys_dev, uint64_t count, uint64_t key_base, uint64_t lo,
                                 uint64_t span, uint32_t bins, uint64_t* hist_dev, void* stream, uint32_t* launches);
 int rk_launch_histogram32(const uint32_t* keys_dev, uint64_t count, uint64_t key_base, const rk_stats* range_dev,

@@ -40,18 +40,69 @@ constexpr int kThreads = RK_EVAL_THREADS;
 #define RK_BF_MAX 32
 #endif
 
-__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t r;
-    asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-}
-
 /* Round key max(den*I_r, num*M_r) = den * max(I_r, R_B*M_r): the
  * state accumulates the scaled sums den*I_r and num*M_r directly (per-kernel
  * den*A_i and num*M_i precomputed), so closing a round is one 64-bit max. */
 __device__ __forceinline__ uint64_t round_key(uint64_t dI, uint64_t nM, uint32_t, uint32_t) {
     return dI >= nM ? dI : nM;
 }
+
+constexpr uint32_t kSmemBins = 32768; /* 128 KB of u32 bins per CTA */
+
+struct BinCalc {
+    uint64_t kmin, D, inv;
+    uint32_t bins, m32, kmin32, D32;
+    bool fast;   /* D*bins < 2^63: 64-bit products suffice */
+    bool fast32; /* bins < D < 2^32: 32-bit offset, 32-bit magic, one exact correction */
+    /* Fig. 1 bins over [kmin, kmax] (last bin closed) */
+    __device__ __forceinline__ void init(uint64_t lo, uint64_t hi, uint32_t nb) { init_span(lo, hi - lo, nb); }
+    /* floor((K - lo) * nb / span) */
+    __device__ __forceinline__ void init_span(uint64_t lo, uint64_t span, uint32_t nb) {
+        kmin = lo;
+        D = span;
+        bins = nb;
+        fast = D != 0 && D < (1ull << 63) / nb;
+        inv = D ? (~0ull) / D : 0;
+        fast32 = D > nb && D < (1ull << 32); /* m32 < 2^32 needs D > bins */
+        kmin32 = (uint32_t)kmin;
+        D32 = (uint32_t)D;
+        m32 = fast32 ? (uint32_t)(((uint64_t)nb << 32) / D) : 0u;
+    }
+    __device__ __forceinline__ uint32_t operator()(uint64_t K) const {
+        if (fast32) {
+            /* x = K - kmin < 2^32 (keys lie in [kmin, kmax]); q0 = hi(x*m32) with
+             * m32 = floor(2^32*bins/D) is floor(x*bins/D) or one less */
+            const uint32_t x = (uint32_t)K - kmin32;
+            uint32_t q = __umulhi(x, m32);
+            const uint64_t p = (uint64_t)x * bins;
+            q += ((uint64_t)(q + 1u) * D32 <= p) ? 1u : 0u;
+            return min(q, bins - 1u);
+        }
+        if (D == 0) return 0;
+        const uint64_t x = K <= kmin ? 0ull : (K - kmin >= D ? D : K - kmin);
+        uint64_t q;
+        if (fast) {
+            const uint64_t p = x * (uint64_t)bins;
+            q = __umul64hi(p, inv); /* <= floor(p/D), at most 2 below */
+            while ((q + 1) * D <= p) q++;
+        } else { /* exact 128-bit: b*D <= x*bins < (b+1)*D */
+            const uint64_t plo = x * (uint64_t)bins, phi = __umul64hi(x, (uint64_t)bins);
+            q = (uint64_t)((double)x * ((double)bins / (double)D));
+            if (q > bins) q = bins;
+            for (;;) {
+                const uint64_t qlo = q * D, qhi = __umul64hi(q, D);
+                if (q > 0 && (qhi > phi || (qhi == phi && qlo > plo))) q--;
+                else break;
+            }
+            for (;;) {
+                const uint64_t b1 = q + 1, qlo = b1 * D, qhi = __umul64hi(b1, D);
+                if (qhi < phi || (qhi == phi && qlo <= plo)) q++;
+                else break;
+            }
+        }
+        return q > bins - 1 ? bins - 1 : (uint32_t)q;
+    }
+};
 
 template <int SMAX>
 struct St {
@@ -405,7 +456,8 @@ __device__ __forceinline__ uint32_t take_nibble(uint64_t& L, uint32_t d) {
     const uint32_t sh = 4u * d;
     const uint32_t v = (uint32_t)(L >> sh) & 15u;
     const uint64_t low = L & ((1ull << sh) - 1ull);
-    L = low | ((L >> (sh + 4u)) << sh);
+    const uint64_t high = sh + 4u >= 64u ? 0ull : (L >> (sh + 4u)) << sh;
+    L = low | high;
     return v;
 }
 __device__ __forceinline__ uint64_t identity_list(uint32_t n) {
@@ -416,17 +468,17 @@ __device__ __forceinline__ uint64_t identity_list(uint32_t n) {
 
 /* Key of one lexicographic index, from scratch (candidate, samples, n < 3). */
 template <int SMAX, bool FULL, class R>
-__device__ uint64_t eval_index(const RkTables& t, uint32_t idx, R& rec) {
+__device__ uint64_t eval_index(const RkTables& t, uint64_t idx, R& rec) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
     St<SMAX> s;
     st_fresh<SMAX, FULL>(s, g);
     uint64_t L = identity_list(n);
-    uint32_t rem = idx;
+    uint64_t rem = idx;
     for (uint32_t j = 0; j + 1 < n; j++) {
-        const uint32_t f = g.fact[n - 1 - j];
-        const uint32_t d = rem / f;
-        rem -= d * f;
+        const uint64_t f = g.fact[n - 1 - j];
+        const uint32_t d = (uint32_t)(rem / f);
+        rem -= (uint64_t)d * f;
         const uint32_t k = take_nibble(L, d);
         St<SMAX> s2;
         place<SMAX, FULL>(s, s2, t.k[k], k, g, rec);
@@ -437,23 +489,15 @@ __device__ uint64_t eval_index(const RkTables& t, uint32_t idx, R& rec) {
 }
 
 struct TStats {
-    uint64_t kmin, kmax;
-    uint32_t amin, amax, nlt, neq, cnt;
+    uint64_t kmin, kmax, amin, amax;
+    uint32_t nlt, neq, cnt; /* per thread (< 2^32 orders per thread) */
     __device__ __forceinline__ void init() {
         kmin = ~0ull;
         kmax = 0;
-        amin = amax = 0xFFFFFFFFu;
+        amin = amax = ~0ull;
         nlt = neq = cnt = 0;
     }
-    __device__ __forceinline__ void add(uint64_t K, uint32_t idx, uint64_t cand) {
-        /* indices arrive in increasing order per thread: strict compares keep
-         * the smallest index on ties (reading L12) */
-        if (K < kmin) { kmin = K; amin = idx; }
-        if (K > kmax) { kmax = K; amax = idx; } /* K >= 1 > initial 0 */
-        nlt += (K < cand) ? 1u : 0u;
-        neq += (K == cand) ? 1u : 0u;
-        cnt += 1u;
-    }
+    /* updated per run by Leaf::end_run (reading L12: smallest index on ties) */
 };
 
 __device__ __forceinline__ void merge_into(rk_stats& a, const rk_stats& b) {
@@ -572,35 +616,91 @@ struct Depth {
 };
 __host__ __device__ constexpr uint32_t cfact(int m) { return m <= 1 ? 1u : (uint32_t)m * cfact(m - 1); }
 
-struct Leaf { /* one evaluated order: statistics + optional key store */
+/* One evaluated order.  Leaves are visited run by run; inside a run by a u32
+ * offset (the run's first index run0 is u64).  Per-run extremes and counts are
+ * folded into the thread's TStats at the run's end (offsets increase inside a
+ * run and runs increase per thread, so strict compares keep the smallest index
+ * on ties).  EXTRA adds the compact-key and fused-histogram outputs. */
+template <bool EXTRA>
+struct Leaf {
     TStats& ts;
-    uint64_t* keys;   /* u64 keys, or */
-    uint32_t* keys32; /* compact u32 offsets K - base (ovf set if one does not fit) */
+    uint64_t* keys;   /* u64 keys (nullable) */
+    uint32_t* keys32; /* EXTRA: compact u32 offsets K - base (ovf set if one does not fit) */
     uint64_t base;
     uint32_t ovf;
-    uint32_t lo, hi, first;
+    uint64_t lo, hi, first;
     uint64_t cand;
-    __device__ __forceinline__ void operator()(uint32_t idx, uint64_t K) {
-        if (idx >= lo && idx < hi) {
-            ts.add(K, idx, cand);
-            if (keys) keys[idx - first] = K;
-            if (keys32) {
-                const uint64_t x = K - base;
-                ovf |= (x >> 32) != 0 ? 1u : 0u;
-                keys32[idx - first] = (uint32_t)x;
+    uint32_t* shist; /* EXTRA: fused Fig. 1 binning (second pass without stored keys) */
+    BinCalc bc;
+    uint32_t hcur, hrun;
+    /* per run */
+    uint64_t run0;
+    uint32_t olo, ohi;
+    uint64_t* kout;
+    uint32_t* kout32;
+    uint64_t rmin, rmax;
+    uint32_t omin, omax, rlt, req;
+
+    __device__ __forceinline__ void begin_run(uint64_t r0, uint32_t R) {
+        run0 = r0;
+        olo = lo > r0 ? (uint32_t)(lo - r0) : 0u;
+        ohi = hi < r0 + R ? (uint32_t)(hi - r0) : R;
+        kout = keys ? keys + (r0 - first) : nullptr;
+        if (EXTRA) kout32 = keys32 ? keys32 + (r0 - first) : nullptr;
+        rmin = ~0ull;
+        rmax = 0;
+        omin = omax = 0;
+        rlt = req = 0;
+    }
+    __device__ __forceinline__ void operator()(uint32_t off, uint64_t K) {
+        if (off >= olo && off < ohi) {
+            if (K < rmin) { rmin = K; omin = off; }
+            if (K > rmax) { rmax = K; omax = off; } /* K >= 1 > 0 */
+            rlt += (K < cand) ? 1u : 0u;
+            req += (K == cand) ? 1u : 0u;
+            if (kout) kout[off] = K;
+            if constexpr (EXTRA) {
+                if (kout32) {
+                    const uint64_t x = K - base;
+                    ovf |= (x >> 32) != 0 ? 1u : 0u;
+                    kout32[off] = (uint32_t)x;
+                }
+                if (shist) {
+                    const uint32_t b = bc(K);
+                    if (b == hcur) {
+                        hrun++;
+                    } else {
+                        if (hrun) atomicAdd(&shist[hcur], hrun);
+                        hcur = b;
+                        hrun = 1;
+                    }
+                }
             }
         }
+    }
+    __device__ __forceinline__ void end_run() {
+        if (ohi <= olo) return;
+        if (rmin < ts.kmin) { ts.kmin = rmin; ts.amin = run0 + omin; }
+        if (rmax > ts.kmax) { ts.kmax = rmax; ts.amax = run0 + omax; }
+        ts.nlt += rlt;
+        ts.neq += req;
+        ts.cnt += ohi - olo;
+    }
+    __device__ __forceinline__ void flush() {
+        if constexpr (EXTRA)
+            if (shist && hrun) atomicAdd(&shist[hcur], hrun);
+        hrun = 0;
     }
 };
 
 /* The D kernels left after a prefix are the low D nibbles of `rem` (ascending);
- * visit their D! orders in lexicographic order, leaf index idx.. idx+D!-1. */
-template <int SMAX, bool FULL, int D>
-__device__ __forceinline__ void dfs(const RkTables& t, const St<SMAX>& s, uint32_t rem, uint32_t idx, Leaf& leaf) {
+ * visit their D! orders in lexicographic order, leaf offsets off .. off+D!-1. */
+template <int SMAX, bool FULL, int D, class LF>
+__device__ __forceinline__ void dfs(const RkTables& t, const St<SMAX>& s, uint32_t rem, uint32_t off, LF& leaf) {
     if constexpr (D == 2) {
         const uint32_t x = rem & 15u, y = (rem >> 4) & 15u;
-        leaf(idx, place_finish<SMAX, FULL>(s, t.k[x], x, t.k[y], y, t.g));
-        leaf(idx + 1u, place_finish<SMAX, FULL>(s, t.k[y], y, t.k[x], x, t.g));
+        leaf(off, place_finish<SMAX, FULL>(s, t.k[x], x, t.k[y], y, t.g));
+        leaf(off + 1u, place_finish<SMAX, FULL>(s, t.k[y], y, t.k[x], x, t.g));
     } else {
         NoRec nr;
 #pragma unroll 1
@@ -610,45 +710,52 @@ __device__ __forceinline__ void dfs(const RkTables& t, const St<SMAX>& s, uint32
             const uint32_t rest = (rem & ((1u << sh) - 1u)) | ((rem >> (sh + 4u)) << sh);
             St<SMAX> s1;
             place<SMAX, FULL>(s, s1, t.k[ka], ka, t.g, nr);
-            dfs<SMAX, FULL, D - 1>(t, s1, rest, idx + a * cfact(D - 1), leaf);
+            dfs<SMAX, FULL, D - 1>(t, s1, rest, off + a * cfact(D - 1), leaf);
         }
     }
 }
 
 /* A run = the D! consecutive indices sharing an (n-D)-prefix. */
-template <int SMAX, bool FULL, int D>
-__device__ __forceinline__ void eval_run(const RkTables& t, uint32_t run, Leaf& leaf) {
+template <int SMAX, bool FULL, int D, class LF>
+__device__ __forceinline__ void eval_run(const RkTables& t, uint64_t run, LF& leaf) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
     NoRec nr;
-    const uint32_t idx0 = run * cfact(D);
+    const uint64_t idx0 = run * cfact(D);
+    leaf.begin_run(idx0, cfact(D));
     St<SMAX> s0;
     st_fresh<SMAX, FULL>(s0, g);
     uint64_t L = identity_list(n);
-    uint32_t rem = idx0;
+    uint64_t rem = idx0;
     for (uint32_t j = 0; j + D < n; j++) { /* shared (n-D)-prefix */
-        const uint32_t f = g.fact[n - 1 - j];
-        const uint32_t d = rem / f;
-        rem -= d * f;
+        const uint64_t f = g.fact[n - 1 - j];
+        uint32_t d;
+        if (rem < (1ull << 32) && f < (1ull << 32)) { /* 32-bit division when it fits (n <= 12) */
+            d = (uint32_t)rem / (uint32_t)f;
+        } else {
+            d = (uint32_t)(rem / f);
+        }
+        rem -= (uint64_t)d * f;
         const uint32_t k = take_nibble(L, d);
         place<SMAX, FULL>(s0, s0, t.k[k], k, g, nr);
     }
-    dfs<SMAX, FULL, D>(t, s0, (uint32_t)L, idx0, leaf);
+    dfs<SMAX, FULL, D>(t, s0, (uint32_t)L, 0u, leaf);
+    leaf.end_run();
 }
 
 /* All runs of [lo, hi) handled by this thread (stride over the grid). */
-template <int SMAX, bool FULL, int D>
-__device__ __forceinline__ void eval_runs(const RkTables& t, uint32_t lo, uint32_t hi, uint32_t tid, uint32_t nth,
-                                          Leaf& leaf) {
-    constexpr uint32_t R = cfact(D);
-    const uint32_t rb = lo / R, re = (hi + R - 1u) / R;
-    for (uint32_t run = rb + tid; run < re; run += nth) eval_run<SMAX, FULL, D>(t, run, leaf);
+template <int SMAX, bool FULL, int D, class LF>
+__device__ __forceinline__ void eval_runs(const RkTables& t, uint64_t lo, uint64_t hi, uint32_t tid, uint32_t nth,
+                                          LF& leaf) {
+    constexpr uint64_t R = cfact(D);
+    const uint64_t rb = lo / R, re = (hi + R - 1u) / R;
+    for (uint64_t run = rb + tid; run < re; run += nth) eval_run<SMAX, FULL, D>(t, run, leaf);
 }
 
 /* n-dependent depth: D = min(n, Depth<SMAX>); n == 1 evaluates the single order. */
-template <int SMAX, bool FULL>
-__device__ __forceinline__ void eval_space(const RkTables& t, uint32_t lo, uint32_t hi, uint32_t tid, uint32_t nth,
-                                           Leaf& leaf) {
+template <int SMAX, bool FULL, class LF>
+__device__ __forceinline__ void eval_space(const RkTables& t, uint64_t lo, uint64_t hi, uint32_t tid, uint32_t nth,
+                                           LF& leaf) {
     constexpr int DM = Depth<SMAX>::value;
     const uint32_t n = t.g.n;
     if (n >= (uint32_t)DM) eval_runs<SMAX, FULL, DM>(t, lo, hi, tid, nth, leaf);
@@ -657,7 +764,9 @@ __device__ __forceinline__ void eval_space(const RkTables& t, uint32_t lo, uint3
     else if (n == 2) eval_runs<SMAX, FULL, 2>(t, lo, hi, tid, nth, leaf);
     else if (tid == 0 && lo < hi) {
         NoRec nr;
-        leaf(0, eval_index<SMAX, FULL>(t, 0, nr));
+        leaf.begin_run(0ull, 1u);
+        leaf(0u, eval_index<SMAX, FULL>(t, 0, nr));
+        leaf.end_run();
     }
 }
 
@@ -679,23 +788,60 @@ struct MinBlocks {
 #endif
 };
 
-template <int SMAX, bool FULL>
-__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
-    rk_eval_kernel(const RkTables* __restrict__ tab, uint32_t first, uint32_t count, const uint64_t* cand_dev,
-                   uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter,
-                   uint32_t* keys32, uint64_t key_base, uint32_t* ovf_dev) {
+template <int SMAX, bool FULL, bool EXTRA>
+__device__ __forceinline__ void eval_body(const RkTables* __restrict__ tab, uint64_t first, uint64_t count,
+                                          const uint64_t* cand_dev, uint64_t cand_imm, rk_stats* out, uint64_t* keys,
+                                          rk_stats* recs, uint32_t* counter, uint32_t* keys32, uint64_t key_base,
+                                          uint32_t* ovf_dev, const rk_stats* hist_range, uint32_t bins,
+                                          uint64_t* hist) {
     __shared__ RkTables t;
-    load_tables(t, tab);
+    extern __shared__ uint32_t shist[];
+    if (EXTRA && hist)
+        for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) shist[i] = 0;
+    load_tables(t, tab); /* (includes the barrier) */
     const uint64_t cand = cand_dev ? *cand_dev : cand_imm;
-    const uint32_t lo = first, hi = first + count;
+    const uint64_t lo = first, hi = first + count;
     TStats ts;
     ts.init();
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    Leaf leaf{ts, keys, keys32, key_base, 0u, lo, hi, first, cand};
+    Leaf<EXTRA> leaf{ts, keys, keys32, key_base, 0u, lo, hi, first, cand, (EXTRA && hist) ? shist : nullptr};
+    leaf.hcur = 0xFFFFFFFFu;
+    leaf.hrun = 0;
+    if (EXTRA && hist) leaf.bc.init(hist_range->key_min, hist_range->key_max, bins);
     eval_space<SMAX, FULL>(t, lo, hi, gtid, nth, leaf);
-    if (leaf.ovf) atomicOr(ovf_dev, 1u);
+    if constexpr (EXTRA) {
+        leaf.flush();
+        if (leaf.ovf) atomicOr(ovf_dev, 1u);
+        if (hist) {
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x)
+                if (shist[i]) atomicAdd((unsigned long long*)&hist[i], (unsigned long long)shist[i]);
+        }
+    }
     const rk_stats r = block_reduce(to_rec(ts));
     commit(r, recs, counter, out);
+}
+
+/* the hot path: statistics + optional u64 keys */
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
+    rk_eval_kernel(const RkTables* __restrict__ tab, uint64_t first, uint64_t count, const uint64_t* cand_dev,
+                   uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter,
+                   uint32_t* keys32, uint64_t key_base, uint32_t* ovf_dev, const rk_stats* hist_range,
+                   uint32_t bins, uint64_t* hist) {
+    eval_body<SMAX, FULL, false>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, nullptr, 0, nullptr,
+                                 nullptr, 0, nullptr);
+}
+
+/* + compact keys / fused histogram */
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
+    rk_eval_x_kernel(const RkTables* __restrict__ tab, uint64_t first, uint64_t count, const uint64_t* cand_dev,
+                     uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter,
+                     uint32_t* keys32, uint64_t key_base, uint32_t* ovf_dev, const rk_stats* hist_range,
+                     uint32_t bins, uint64_t* hist) {
+    eval_body<SMAX, FULL, true>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, keys32, key_base,
+                                ovf_dev, hist_range, bins, hist);
 }
 
 /* C5 batch: blockIdx.y = set, blockIdx.x = chunk of that set's runs.  All sets
@@ -708,15 +854,15 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     load_tables(t, tabs + set);
     const uint64_t cand = cand_keys[set];
     const uint32_t n = t.g.n;
-    const uint32_t total = t.g.fact[n];
+    const uint64_t total = t.g.fact[n];
     TStats ts;
     ts.init();
     /* chunk c of the set's index space, aligned to the run size */
-    const uint32_t R = cfact(n < (uint32_t)Depth<SMAX>::value ? (int)n : Depth<SMAX>::value);
-    const uint32_t runs = (total + R - 1) / R;
-    const uint32_t per = (runs + gridDim.x - 1) / gridDim.x;
-    const uint32_t lo = min(total, blockIdx.x * per * R), hi = min(total, lo + per * R);
-    Leaf leaf{ts, nullptr, nullptr, 0ull, 0u, lo, hi, 0u, cand};
+    const uint64_t R = cfact(n < (uint32_t)Depth<SMAX>::value ? (int)n : Depth<SMAX>::value);
+    const uint64_t runs = (total + R - 1) / R;
+    const uint64_t per = (runs + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = min(total, (uint64_t)blockIdx.x * per * R), hi = min(total, lo + per * R);
+    Leaf<false> leaf{ts, nullptr, nullptr, 0ull, 0u, lo, hi, 0ull, cand, nullptr};
     eval_space<SMAX, FULL>(t, lo, hi, threadIdx.x, blockDim.x, leaf);
     const rk_stats r = block_reduce(to_rec(ts));
     if (threadIdx.x == 0) recs[set * gridDim.x + blockIdx.x] = r;
@@ -745,11 +891,11 @@ __global__ void rk_keys_of_kernel(const RkTables* __restrict__ tabs, const uint6
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     NoRec nr;
-    out[i] = eval_index<SMAX, FULL>(tabs[per_set ? i : 0], (uint32_t)idx[i], nr);
+    out[i] = eval_index<SMAX, FULL>(tabs[per_set ? i : 0], idx[i], nr);
 }
 
 template <int SMAX, bool FULL>
-__global__ void rk_key_of_index_kernel(const RkTables* __restrict__ tab, uint32_t index, uint64_t* __restrict__ out) {
+__global__ void rk_key_of_index_kernel(const RkTables* __restrict__ tab, uint64_t index, uint64_t* __restrict__ out) {
     __shared__ RkTables t;
     load_tables(t, tab);
     if (threadIdx.x == 0) {
@@ -778,49 +924,6 @@ __global__ void rk_simulate_kernel(const RkTables* __restrict__ tab, const int32
  * contiguous), run-length merges equal bins (lexicographic neighbours have
  * close keys) before one shared-memory atomic per run; u64 global atomics at
  * the end (integer adds: order-free, bit-exact). */
-constexpr uint32_t kSmemBins = 32768; /* 128 KB of u32 bins per CTA */
-
-struct BinCalc {
-    uint64_t kmin, D, inv;
-    uint32_t bins, m32, kmin32, D32;
-    bool fast;   /* D*bins < 2^63: 64-bit products suffice */
-    bool fast32; /* bins < D < 2^32: 32-bit offset, 32-bit magic, one exact correction */
-    __device__ __forceinline__ uint32_t operator()(uint64_t K) const {
-        if (fast32) {
-            /* x = K - kmin < 2^32 (keys lie in [kmin, kmax]); q0 = hi(x*m32) with
-             * m32 = floor(2^32*bins/D) is floor(x*bins/D) or one less */
-            const uint32_t x = (uint32_t)K - kmin32;
-            uint32_t q = __umulhi(x, m32);
-            const uint64_t p = (uint64_t)x * bins;
-            q += ((uint64_t)(q + 1u) * D32 <= p) ? 1u : 0u;
-            return min(q, bins - 1u);
-        }
-        if (D == 0) return 0;
-        const uint64_t x = K <= kmin ? 0ull : (K - kmin >= D ? D : K - kmin);
-        uint64_t q;
-        if (fast) {
-            const uint64_t p = x * (uint64_t)bins;
-            q = __umul64hi(p, inv); /* <= floor(p/D), at most 2 below */
-            while ((q + 1) * D <= p) q++;
-        } else { /* exact 128-bit: b*D <= x*bins < (b+1)*D */
-            const uint64_t plo = x * (uint64_t)bins, phi = __umul64hi(x, (uint64_t)bins);
-            q = (uint64_t)((double)x * ((double)bins / (double)D));
-            if (q > bins) q = bins;
-            for (;;) {
-                const uint64_t qlo = q * D, qhi = __umul64hi(q, D);
-                if (q > 0 && (qhi > phi || (qhi == phi && qlo > plo))) q--;
-                else break;
-            }
-            for (;;) {
-                const uint64_t b1 = q + 1, qlo = b1 * D, qhi = __umul64hi(b1, D);
-                if (qhi < phi || (qhi == phi && qlo <= plo)) q++;
-                else break;
-            }
-        }
-        return q > bins - 1 ? bins - 1 : (uint32_t)q;
-    }
-};
-
 /* RANGE = false: Fig. 1 bins over [kmin, kmax] (last bin closed).
  * RANGE = true: order-statistic refinement — `bins` half-open bins over
  * [kmin_imm, kmin_imm + kmax_imm) (kmax_imm = span), keys outside ignored. */
@@ -832,16 +935,8 @@ __global__ void __launch_bounds__(256) rk_hist_kernel(const KT* __restrict__ key
     extern __shared__ uint32_t sh[];
     const bool smem_bins = bins <= kSmemBins; /* else accumulate straight into global u64 bins */
     BinCalc bc;
-    bc.kmin = range ? range->key_min : kmin_imm;
-    const uint64_t kmax = range ? range->key_max : kmax_imm;
-    bc.D = RANGE ? kmax_imm : kmax - bc.kmin;
-    bc.bins = bins;
-    bc.fast = bc.D != 0 && bc.D < (1ull << 63) / bins;
-    bc.inv = bc.D ? (~0ull) / bc.D : 0;
-    bc.fast32 = bc.D > bins && bc.D < (1ull << 32); /* m32 < 2^32 needs D > bins */
-    bc.kmin32 = (uint32_t)bc.kmin;
-    bc.D32 = (uint32_t)bc.D;
-    bc.m32 = bc.fast32 ? (uint32_t)(((uint64_t)bins << 32) / bc.D) : 0u;
+    if (RANGE) bc.init_span(kmin_imm, kmax_imm, bins);
+    else bc.init(range ? range->key_min : kmin_imm, range ? range->key_max : kmax_imm, bins);
     if (smem_bins)
         for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -980,7 +1075,8 @@ int rk_eval_max_ctas(uint32_t S, int) {
 int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t first, uint64_t count,
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,
                    rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches,
-                   uint32_t* keys32_dev, uint64_t key_base, uint32_t* ovf_dev) {
+                   uint32_t* keys32_dev, uint64_t key_base, uint32_t* ovf_dev, const rk_stats* hist_range,
+                   uint32_t bins, uint64_t* hist_dev) {
     cudaStream_t st = (cudaStream_t)stream;
     const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t R = 1;
@@ -991,9 +1087,28 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
     if (ctas > cap) ctas = cap;
     if (ctas > max_ctas) ctas = max_ctas;
     if (ctas < 1) ctas = 1;
-    RK_DISPATCH(S, rk_eval_kernel, RK_CFG((unsigned)ctas, kThreads, 0, st), tab_dev, (uint32_t)first,
-                (uint32_t)count, cand_key_dev, cand_key_imm, stats_dev, keys_dev, recs, counter, keys32_dev, key_base,
-                ovf_dev);
+    const size_t smem = hist_dev ? (size_t)bins * 4 : 0;
+    if (keys32_dev || hist_dev) {
+        if (smem > 48 * 1024) {
+            cudaFuncSetAttribute(rk_eval_x_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        }
+        RK_DISPATCH(S, rk_eval_x_kernel, RK_CFG((unsigned)ctas, kThreads, smem, st), tab_dev, first, count,
+                    cand_key_dev, cand_key_imm, stats_dev, keys_dev, recs, counter, keys32_dev, key_base, ovf_dev,
+                    hist_range, bins, hist_dev);
+        if (launches) (*launches)++;
+        return (int)cudaGetLastError();
+    }
+    RK_DISPATCH(S, rk_eval_kernel, RK_CFG((unsigned)ctas, kThreads, 0, st), tab_dev, first, count, cand_key_dev,
+                cand_key_imm, stats_dev, keys_dev, recs, counter, nullptr, 0ull, nullptr, nullptr, 0u, nullptr);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -1087,7 +1202,7 @@ int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* 
 
 int rk_launch_key_of_index(const RkTables* tab_dev, uint32_t S, uint64_t index, uint64_t* out_dev, void* stream,
                            uint32_t* launches) {
-    RK_DISPATCH_GENERIC(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, (uint32_t)index,
+    RK_DISPATCH_GENERIC(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, index,
                 out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();

@@ -3,7 +3,7 @@
 One process per GPU (torchrun), ``torch.distributed`` with NCCL over NVLink 5 /
 NVSwitch for the two real exchange steps of the path:
 
-1. ``all_gather_into_tensor`` of one 56-byte ``rk_stats`` record per rank, then
+1. ``all_gather_into_tensor`` of one 64-byte ``rk_stats`` record per rank, then
    the deterministic device merge (``rk_merge_stats_async``) — every rank gets
    the global min/argmin, max/argmax and candidate counts.  Equal-width bins
    over [best, worst] need these extremes before any key is binned.
@@ -20,7 +20,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-REC_WORDS = 7  # rk_stats = 56 bytes = 7 x int64
+REC_WORDS = 8  # rk_stats = 64 bytes = 8 x int64
 
 
 def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -31,7 +31,7 @@ def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def all_gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
-    """rec: int64[7] (one rk_stats) -> int64[world, 7] on every rank."""
+    """rec: int64[8] (one rk_stats) -> int64[world, 8] on every rank."""
     world = dist.get_world_size(group)
     out = torch.empty((world, REC_WORDS), dtype=torch.int64, device=rec.device)
     dist.all_gather_into_tensor(out, rec.view(1, REC_WORDS), group=group)

@@ -22,7 +22,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 
 #: every symbol include/rk.h declares (checked by tests/test_abi.py)
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
-           "rk_eval_range_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
+           "rk_eval_range_async", "rk_eval_range_hist_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
            "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
            "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
@@ -41,8 +41,8 @@ class rk_kernel(ctypes.Structure):
 
 
 class rk_stats(ctypes.Structure):
-    _fields_ = [("key_min", ctypes.c_uint64), ("key_max", ctypes.c_uint64), ("argmin", ctypes.c_uint32),
-                ("argmax", ctypes.c_uint32), ("n_lt", ctypes.c_uint64), ("n_eq", ctypes.c_uint64),
+    _fields_ = [("key_min", ctypes.c_uint64), ("key_max", ctypes.c_uint64), ("argmin", ctypes.c_uint64),
+                ("argmax", ctypes.c_uint64), ("n_lt", ctypes.c_uint64), ("n_eq", ctypes.c_uint64),
                 ("n_gt", ctypes.c_uint64), ("evaluated", ctypes.c_uint64)]
 
     def as_tuple(self):
@@ -50,8 +50,8 @@ class rk_stats(ctypes.Structure):
                 self.evaluated)
 
 
-assert ctypes.sizeof(rk_stats) == 56
-STATS_BYTES = 56
+assert ctypes.sizeof(rk_stats) == 64
+STATS_BYTES = 64
 
 _lib = None
 
@@ -75,6 +75,7 @@ def lib():
             "rk_eval_range": ([vp, u64, u64, u64, P(rk_stats), vp, vp], ctypes.c_int),
             "rk_eval_range_async": ([vp, u64, u64, vp, vp, vp, vp], ctypes.c_int),
             "rk_eval_index_async": ([vp, u64, vp, vp], ctypes.c_int),
+            "rk_eval_range_hist_async": ([vp, u64, u64, vp, vp, vp, u32, vp, vp], ctypes.c_int),
             "rk_eval_range32_async": ([vp, u64, u64, vp, vp, vp, u64, vp, vp], ctypes.c_int),
             "rk_key_lower_bound": ([vp, P(u64)], ctypes.c_int),
             "rk_histogram32_async": ([vp, vp, u64, u64, vp, u32, vp, vp], ctypes.c_int),
@@ -224,6 +225,12 @@ class Context:
     def rk_eval_range_async(self, first: int, count: int, cand_key_dev, stats_dev, keys_dev=None, stream=None):
         self._chk(self._L.rk_eval_range_async(self.h, first, count, _ptr(cand_key_dev), _ptr(stats_dev),
                                               _ptr(keys_dev), _stream(stream)), "rk_eval_range_async")
+
+    def rk_eval_range_hist_async(self, first: int, count: int, cand_key_dev, stats_dev, range_dev, bins: int,
+                                 hist_dev, stream=None):
+        self._chk(self._L.rk_eval_range_hist_async(self.h, first, count, _ptr(cand_key_dev), _ptr(stats_dev),
+                                                   _ptr(range_dev), bins, _ptr(hist_dev), _stream(stream)),
+                  "rk_eval_range_hist_async")
 
     def rk_eval_range32_async(self, first: int, count: int, cand_key_dev, stats_dev, keys32_dev, key_base: int,
                               ovf_dev, stream=None):

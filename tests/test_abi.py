@@ -86,7 +86,7 @@ CASES = [
     ([(16, 32, 1, 0, 1, 0)], O.OR_EMISSINGRATIO),
     ([(16, 1024, 33, 0, 1, 1)], O.OR_EINFEASIBLE),
     ([(16, 128, 20, 65536, 311, 100)], O.OR_EINFEASIBLE),
-    ([(16, 128, 20, 0, 311, 100)] * 13, O.OR_ETOOMANY),
+    ([(16, 128, 20, 0, 311, 100)] * 17, O.OR_ETOOMANY),
     ([(1 << 31, 32, 1, 0, 1 << 31, 1)], O.OR_EOVERFLOW),
 ]
 

@@ -24,15 +24,12 @@ def _free_port():
 
 
 def _pack(t):
-    """oracle Stats tuple -> the 7 int64 words of an rk_stats record (56 B)."""
-    kmin, kmax, amin, amax, lt, eq, gt, ev = t
-    w = [kmin, kmax, amin | (amax << 32), lt, eq, gt, ev]
-    return [x if x < (1 << 63) else x - (1 << 64) for x in w]
+    """oracle Stats tuple -> the 8 int64 words of an rk_stats record (64 B)."""
+    return [x if x < (1 << 63) else x - (1 << 64) for x in t]
 
 
 def _unpack(w):
-    w = [x & ((1 << 64) - 1) for x in w]
-    return (w[0], w[1], w[2] & 0xFFFFFFFF, w[2] >> 32, w[3], w[4], w[5], w[6])
+    return tuple(x & ((1 << 64) - 1) for x in w)
 
 
 def _merge(records):

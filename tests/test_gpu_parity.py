@@ -186,12 +186,12 @@ def test_ranges_edges_and_sharding(ctx):
             assert st.evaluated == 0
     # G shards merged on the device == unsharded (deterministic merge)
     for G in (2, 3, 8):
-        recs = torch.zeros((G, 7), dtype=torch.int64, device="cuda")  # 56 B per record
+        recs = torch.zeros((G, 8), dtype=torch.int64, device="cuda")  # 64 B per record
         bounds = [N * g // G for g in range(G + 1)]
         cand = torch.tensor([12130259200], dtype=torch.int64, device="cuda")
         for g in range(G):
             ctx.rk_eval_range_async(bounds[g], bounds[g + 1] - bounds[g], cand, recs[g])
-        out = torch.zeros(7, dtype=torch.int64, device="cuda")
+        out = torch.zeros(8, dtype=torch.int64, device="cuda")
         ctx.rk_merge_stats_async(recs, G, out)
         torch.cuda.synchronize()
         assert rk.Stats.from_c(rk.rk_stats.from_buffer_copy(out.cpu().numpy().tobytes())).as_tuple() == full.as_tuple()
@@ -435,7 +435,7 @@ def test_compact_keys_histogram32_select32_and_overflow_flag(ctx):
     assert base == max(gpu[6] * sI, gpu[5] * sM) <= st.key_min
     k32 = torch.empty(N, dtype=torch.int32, device="cuda")
     ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
-    rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
     ctx.rk_eval_range32_async(0, N, None, rec, k32, base, ovf)
     torch.cuda.synchronize()
     assert int(ovf.item()) == 0
@@ -462,3 +462,91 @@ def test_public_sweeper_compact_keys_mode():
     a = Sweeper(gpu, bins=32).run(ks, median=True)
     b = Sweeper(gpu, bins=32, compact_keys=True).run(ks, median=True)
     assert a == b
+
+
+def _set13():
+    return W.gen_g(W.SplitMix64(W.SEED_BASE + 13), 13)
+
+
+def test_n13_u64_indices_around_2_pow_32(ctx):
+    """13! = 6.2e9 orders needs u64 indices."""
+    gpu, ks = W.GTX580, _set13()
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    first, count = (1 << 32) - 3001, 6007
+    keys = torch.empty(count, dtype=torch.int64, device="cuda")
+    cand = O.simulate(gpu, ks, O.unrank(1 << 32, 13)).key
+    st = ctx.rk_eval_range(first, count, cand, keys_dev=keys)
+    ost, okeys = O.sweep(gpu, ks, first, count, cand_key=cand, threads=NCPU, keys=True)
+    assert np.array_equal(keys.cpu().numpy().view(np.uint64), okeys)
+    assert st.as_tuple() == ost.as_tuple() and st.argmin >= first
+
+
+def test_n13_full_space_two_pass_histogram(ctx):
+    gpu, ks = W.GTX580, _set13()
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(13)
+    order, _, idx, key = ctx.rk_heuristic_order()
+    assert key == O.simulate(gpu, ks, order).key
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    cd = torch.tensor([key], dtype=torch.int64, device="cuda")
+    ctx.rk_eval_range_async(0, N, cd, rec)  # pass 1: no keys stored (50 GB)
+    hist = torch.zeros(256, dtype=torch.int64, device="cuda")
+    rec2 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ctx.rk_eval_range_hist_async(0, N, cd, rec2, rec, 256, hist)  # pass 2: fused binning
+    torch.cuda.synchronize()
+    st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
+    assert torch.equal(rec, rec2)
+    assert st.evaluated == N == st.n_lt + st.n_eq + st.n_gt and st.n_eq >= 1
+    assert int(hist.sum().item()) == N
+    # the extremes are real orders with exactly those keys (oracle, one by one)
+    assert O.simulate(gpu, ks, O.unrank(st.argmin, 13)).key == st.key_min
+    assert O.simulate(gpu, ks, O.unrank(st.argmax, 13)).key == st.key_max
+    # no sampled order beats the minimum or exceeds the maximum
+    rng = np.random.default_rng(13)
+    for i in rng.integers(0, N, 300).tolist():
+        assert st.key_min <= O.simulate(gpu, ks, O.unrank(i, 13)).key <= st.key_max
+    # sharded (3 contiguous shards, device merge) == unsharded
+    recs = torch.zeros((3, 8), dtype=torch.int64, device="cuda")
+    for g in range(3):
+        ctx.rk_eval_range_async(N * g // 3, N * (g + 1) // 3 - N * g // 3, cd, recs[g])
+    out = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ctx.rk_merge_stats_async(recs, 3, out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, rec)
+
+
+def test_fused_histogram_pass_matches_oracle(ctx):
+    gpu, ks = W.config("C3")
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(10)
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ctx.rk_eval_range_async(0, N, None, rec)
+    _, okeys = O.sweep(gpu, ks, threads=NCPU, keys=True)
+    st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
+    for B in (1, 7, 256, 32768):
+        hist = torch.zeros(B, dtype=torch.int64, device="cuda")
+        ctx.rk_eval_range_hist_async(0, N, None, None, rec, B, hist)
+        torch.cuda.synchronize()
+        assert hist.cpu().tolist() == O.histogram(okeys, st.key_min, st.key_max, B)
+    # a sub-range accumulates only its own orders
+    hist = torch.zeros(64, dtype=torch.int64, device="cuda")
+    ctx.rk_eval_range_hist_async(1000, 5000, None, None, rec, 64, hist)
+    torch.cuda.synchronize()
+    assert hist.cpu().tolist() == O.histogram(okeys[1000:6000], st.key_min, st.key_max, 64)
+
+
+def test_n16_tail_of_the_space(ctx):
+    gpu = W.GTX580
+    ks = W.gen_g(W.SplitMix64(W.SEED_BASE + 16), 16)
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(16)
+    for first in (N - 2500, (N // 7) * 3):
+        keys = torch.empty(2500, dtype=torch.int64, device="cuda")
+        st = ctx.rk_eval_range(first, 2500, 0, keys_dev=keys)
+        ost, okeys = O.sweep(gpu, ks, first, 2500, threads=NCPU, keys=True)
+        assert np.array_equal(keys.cpu().numpy().view(np.uint64), okeys)
+        assert st.as_tuple() == ost.as_tuple()

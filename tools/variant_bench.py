@@ -13,7 +13,7 @@ c.rk_set_kernels(ks)
 N = math.factorial(12)
 keys = torch.empty(N, dtype=torch.int64, device="cuda")
 cand = torch.tensor([g["cand_key"]], dtype=torch.int64, device="cuda")
-rec = torch.zeros(7, dtype=torch.int64, device="cuda")
+rec = torch.zeros(8, dtype=torch.int64, device="cuda")
 with_keys = os.environ.get("NOKEYS") is None
 for _ in range(3):
     c.rk_eval_range_async(0, N, cand, rec, keys if with_keys else None)
