@@ -33,6 +33,14 @@ def one_config(name, threads, bins=256):
     s, keys = O.sweep(gpu, ks, cand_key=cand_key, threads=threads, keys=True)
     dt = time.time() - t0
     hist = O.histogram(keys, s.key_min, s.key_max, bins)
+    # order statistics (SPEC:302 median = lower-middle; Fig. 1 ranking points):
+    # a library sort of the oracle's keys
+    import numpy as np
+    N = len(keys)
+    ranks = sorted({0, N - 1, (N - 1) // 2} | {N * q // 10 for q in range(1, 10)})
+    srt = np.sort(keys)
+    order_stats = {str(r): int(srt[r]) for r in ranks}
+    del srt
     return {
         "_source": f"oracle/rk_oracle.cpp via tests/golden/make_goldens.py ({threads} threads, {dt:.1f} s, "
                    f"{platform.processor() or platform.machine()})",
@@ -42,6 +50,7 @@ def one_config(name, threads, bins=256):
                   "n_lt": s.n_lt, "n_eq": s.n_eq, "n_gt": s.n_gt, "evaluated": s.evaluated},
         "max_rel_err_naive_double": s.max_rel_err,
         "bins": bins, "hist": hist,
+        "median_rank": (N - 1) // 2, "order_stats": order_stats,
     }
 
 
@@ -53,7 +62,7 @@ def c5(threads, n_sets):
     dt = time.time() - t0
     return {
         "_source": f"oracle/rk_oracle.cpp via tests/golden/make_goldens.py ({threads} threads, {dt:.1f} s); "
-                   f"first {n_sets} of the 4096 C5 sets (labelled subset)",
+                   (f"first {n_sets} of the 4096 C5 sets (labelled subset)" if n_sets < 4096 else "all 4096 C5 sets"),
         "config": "C5", "n_sets": n_sets, "n": 9, "gpu": list(gpu),
         "sets": [{"stats": list(st.as_tuple()), "cand_index": ci, "cand_key": ck} for st, ci, ck in res],
     }

@@ -550,3 +550,19 @@ def test_n16_tail_of_the_space(ctx):
         ost, okeys = O.sweep(gpu, ks, first, 2500, threads=NCPU, keys=True)
         assert np.array_equal(keys.cpu().numpy().view(np.uint64), okeys)
         assert st.as_tuple() == ost.as_tuple()
+
+
+def test_c4_order_statistics_vs_oracle_golden(ctx):
+    g = _gold("c4_oracle.json")
+    if "order_stats" not in g:
+        pytest.skip("golden predates order statistics")
+    gpu, ks = W.config("C4")
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(12)
+    keys = torch.empty(N, dtype=torch.int64, device="cuda")
+    st = ctx.rk_eval_range(0, N, 0, keys_dev=keys)
+    ranks = [int(r) for r in g["order_stats"]]
+    got = ctx.rk_select_keys(keys, N, st.key_min, st.key_max, ranks)
+    assert got == [g["order_stats"][str(r)] for r in ranks]
+    assert g["median_rank"] == (N - 1) // 2
