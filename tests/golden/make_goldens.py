@@ -61,7 +61,7 @@ def c5(threads, n_sets):
     res = O.sweep_sets(gpu, sets, threads=threads)
     dt = time.time() - t0
     return {
-        "_source": f"oracle/rk_oracle.cpp via tests/golden/make_goldens.py ({threads} threads, {dt:.1f} s); "
+        "_source": f"oracle/rk_oracle.cpp via tests/golden/make_goldens.py ({threads} threads, {dt:.1f} s); " +
                    (f"first {n_sets} of the 4096 C5 sets (labelled subset)" if n_sets < 4096 else "all 4096 C5 sets"),
         "config": "C5", "n_sets": n_sets, "n": 9, "gpu": list(gpu),
         "sets": [{"stats": list(st.as_tuple()), "cand_index": ci, "cand_key": ck} for st, ci, ck in res],
