@@ -640,12 +640,14 @@ struct Leaf {
     uint32_t* kout32;
     uint64_t rmin, rmax;
     uint32_t omin, omax, rlt, req;
+    bool pair_ok; /* kout 16-byte aligned for pair stores */
 
     __device__ __forceinline__ void begin_run(uint64_t r0, uint32_t R) {
         run0 = r0;
         olo = lo > r0 ? (uint32_t)(lo - r0) : 0u;
         ohi = hi < r0 + R ? (uint32_t)(hi - r0) : R;
         kout = keys ? keys + (r0 - first) : nullptr;
+        pair_ok = (reinterpret_cast<uintptr_t>(kout) & 15u) == 0;
         if (EXTRA) kout32 = keys32 ? keys32 + (r0 - first) : nullptr;
         rmin = ~0ull;
         rmax = 0;
@@ -678,6 +680,23 @@ struct Leaf {
             }
         }
     }
+    /* the two leaves of a depth-2 node: offsets off, off+1 (off even) */
+    __device__ __forceinline__ void pair(uint32_t off, uint64_t K0, uint64_t K1) {
+        if (!EXTRA && kout && off >= olo && off + 1u < ohi && pair_ok) {
+            /* both in range: statistics, then one 16-byte store (fuller sectors) */
+            const uint32_t o1 = off + 1u;
+            if (K0 < rmin) { rmin = K0; omin = off; }
+            if (K1 < rmin) { rmin = K1; omin = o1; }
+            if (K0 > rmax) { rmax = K0; omax = off; }
+            if (K1 > rmax) { rmax = K1; omax = o1; }
+            rlt += ((K0 < cand) ? 1u : 0u) + ((K1 < cand) ? 1u : 0u);
+            req += ((K0 == cand) ? 1u : 0u) + ((K1 == cand) ? 1u : 0u);
+            *reinterpret_cast<ulonglong2*>(kout + off) = make_ulonglong2(K0, K1);
+            return;
+        }
+        (*this)(off, K0);
+        (*this)(off + 1u, K1);
+    }
     __device__ __forceinline__ void end_run() {
         if (ohi <= olo) return;
         if (rmin < ts.kmin) { ts.kmin = rmin; ts.amin = run0 + omin; }
@@ -699,8 +718,9 @@ template <int SMAX, bool FULL, int D, class LF>
 __device__ __forceinline__ void dfs(const RkTables& t, const St<SMAX>& s, uint32_t rem, uint32_t off, LF& leaf) {
     if constexpr (D == 2) {
         const uint32_t x = rem & 15u, y = (rem >> 4) & 15u;
-        leaf(off, place_finish<SMAX, FULL>(s, t.k[x], x, t.k[y], y, t.g));
-        leaf(off + 1u, place_finish<SMAX, FULL>(s, t.k[y], y, t.k[x], x, t.g));
+        const uint64_t K0 = place_finish<SMAX, FULL>(s, t.k[x], x, t.k[y], y, t.g);
+        const uint64_t K1 = place_finish<SMAX, FULL>(s, t.k[y], y, t.k[x], x, t.g);
+        leaf.pair(off, K0, K1);
     } else {
         NoRec nr;
 #pragma unroll 1
