@@ -195,6 +195,14 @@ rk_status rk_range_histogram32(rk_ctx* ctx, const uint32_t* keys32_dev, uint64_t
 rk_status rk_heuristic_order(rk_ctx* ctx, int32_t* order_out, int32_t* round_of_out, uint64_t* index_out,
                              uint64_t* key_out);
 
+/* Algorithm 1 for n_sets independent kernel sets on the device (SURVEY §8(f)
+ * f4), one thread per set, bit-identical to rk_heuristic_order (same readings,
+ * same explicitly rounded double operations).  orders_out (nullable host
+ * int32[n_sets*n]) and index_out (host u64[n_sets]: lexicographic index).
+ * Uses the ctx's gpu params.  Synchronous. */
+rk_status rk_heuristic_batch(rk_ctx* ctx, const rk_kernel* sets, uint32_t n, uint32_t n_sets, int32_t* orders_out,
+                             uint64_t* index_out, void* stream);
+
 /* Percentile support (Table 3 "Percentile rank"):
  * key of `order` and the number of indices in [first, first+count) whose key
  * is >= it (ties count for the candidate, reading L13).  Shard-aware: sum

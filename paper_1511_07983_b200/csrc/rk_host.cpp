@@ -749,6 +749,40 @@ rk_status rk_heuristic_order(rk_ctx* c, int32_t* order_out, int32_t* round_of_ou
     return RK_OK;
 }
 
+rk_status rk_heuristic_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n_sets, int32_t* orders_out,
+                             uint64_t* index_out, void* stream) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (!c->has_params) return fail(c, RK_ESTATE, "rk_set_gpu_params first");
+    if (!sets || !index_out || n_sets == 0) return fail(c, RK_EINVAL, "bad heuristic batch arguments");
+    if (n == 0 || n > RK_MAX_N) return fail(c, n ? RK_ETOOMANY : RK_EINVAL, "n out of range");
+    RkTables tmp;
+    for (uint32_t q = 0; q < n_sets; q++) /* same validation as rk_set_kernels */
+        if ((s = build_tables(c, c->gp, sets + (size_t)q * n, n, tmp))) {
+            c->err = "set " + std::to_string(q) + ": " + c->err;
+            return s;
+        }
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    rk_kernel* sets_dev = nullptr;
+    int32_t* ord_dev = nullptr;
+    uint64_t* idx_dev = nullptr;
+    int e = cudaMalloc(&sets_dev, sizeof(rk_kernel) * (size_t)n * n_sets);
+    if (!e) e = cudaMalloc(&ord_dev, sizeof(int32_t) * (size_t)n * n_sets);
+    if (!e) e = cudaMalloc(&idx_dev, sizeof(uint64_t) * n_sets);
+    if (!e) e = cudaMemcpyAsync(sets_dev, sets, sizeof(rk_kernel) * (size_t)n * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = rk_launch_heuristic(sets_dev, n, n_sets, &c->gp, ord_dev, idx_dev, stream, &c->launches);
+    if (!e) e = cudaMemcpyAsync(index_out, idx_dev, sizeof(uint64_t) * n_sets, cudaMemcpyDeviceToHost, st);
+    if (!e && orders_out)
+        e = cudaMemcpyAsync(orders_out, ord_dev, sizeof(int32_t) * (size_t)n * n_sets, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    cudaFree(sets_dev);
+    cudaFree(ord_dev);
+    cudaFree(idx_dev);
+    return e ? cuda_fail(c, e, "rk_heuristic_batch") : RK_OK;
+}
+
 rk_status rk_percentile(rk_ctx* c, const int32_t* order, uint64_t first, uint64_t count, uint64_t* n_ge_out,
                         uint64_t* key_out) {
     rk_status s = need_device(c);
@@ -775,7 +809,6 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     if (!sets || !out_host || n_sets == 0) return fail(c, RK_EINVAL, "bad batch arguments");
     std::vector<RkTables> tabs(n_sets);
     std::vector<uint64_t> idx(n_sets);
-    std::vector<int32_t> order(n);
     for (uint32_t q = 0; q < n_sets; q++) {
         if ((s = build_tables(c, c->gp, sets + (size_t)q * n, n, tabs[q]))) {
             c->err = "set " + std::to_string(q) + ": " + c->err;
@@ -784,11 +817,9 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
         if (cand_index) {
             if (cand_index[q] >= fact64(n)) return fail(c, RK_EINVAL, "set %u: candidate index >= n!", q);
             idx[q] = cand_index[q];
-        } else {
-            Alg1(c->gp).run(sets + (size_t)q * n, n, order.data(), nullptr);
-            do_rank(order.data(), n, &idx[q]);
         }
     }
+    if (!cand_index && (s = rk_heuristic_batch(c, sets, n, n_sets, nullptr, idx.data(), stream))) return s;
     /* group the sets by reduced SM count so every launch runs a compile-time variant */
     std::vector<uint32_t> perm(n_sets);
     for (uint32_t q = 0; q < n_sets; q++) perm[q] = q;

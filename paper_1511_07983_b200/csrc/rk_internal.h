@@ -86,6 +86,9 @@ int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const in
 int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n_sets, const uint64_t* cand_keys_dev,
                     rk_stats* out_dev, rk_stats* scratch_recs, uint32_t chunks_per_set, void* stream,
                     uint32_t* launches);
+/* Algorithm 1 on the device, one thread per set */
+int rk_launch_heuristic(const rk_kernel* sets_dev, uint32_t n, uint32_t n_sets, const rk_gpu_params* p,
+                        int32_t* orders_dev, uint64_t* index_dev, void* stream, uint32_t* launches);
 int rk_batch_chunks_per_set(uint32_t n, uint32_t S);
 int rk_eval_max_ctas(uint32_t S, int device);
 

@@ -1012,6 +1012,129 @@ __global__ void __launch_bounds__(256) rk_hist_kernel(const KT* __restrict__ key
         if (sh[i]) atomicAdd((unsigned long long*)&hist[i], (unsigned long long)sh[i]);
 }
 
+/* ==================== Algorithm 1 on the device ====================
+ * One thread per kernel set: the paper's greedy launch-order algorithm
+ * with the readings of DESIGN.md §3, in the same fixed double
+ * operation order as the host implementation (every operation an explicitly
+ * rounded IEEE op, no contraction), so orders are bit-identical. */
+struct DProf {
+    uint64_t shm, regs, warps, blocks;
+    double inst, ratio;
+};
+
+__device__ __forceinline__ DProf d_combine(const DProf& a, const DProf& b) {
+    DProf c;
+    c.shm = a.shm + b.shm;
+    c.regs = a.regs + b.regs;
+    c.warps = a.warps + b.warps;
+    c.blocks = a.blocks + b.blocks;
+    c.inst = __dadd_rn(a.inst, b.inst);
+    c.ratio = __ddiv_rn(__dadd_rn(a.inst, b.inst), __dadd_rn(__ddiv_rn(a.inst, a.ratio), __ddiv_rn(b.inst, b.ratio)));
+    return c;
+}
+__device__ __forceinline__ bool d_fits(const rk_gpu_params& p, const DProf& a, const DProf& b) {
+    return a.shm + b.shm <= p.shm_bytes_per_sm && a.regs + b.regs <= p.regs_per_sm &&
+           a.warps + b.warps <= p.max_warps_per_sm && a.blocks + b.blocks <= p.max_blocks_per_sm;
+}
+__device__ __forceinline__ double d_slack(uint64_t cap, uint64_t x, uint64_t y) {
+    const double v = __ddiv_rn((double)((int64_t)cap - (int64_t)x - (int64_t)y), (double)cap);
+    return v > 0.0 ? v : 0.0;
+}
+__device__ __forceinline__ double d_score(const rk_gpu_params& p, double RB, const DProf& a, const DProf& b) {
+    double s = 0.0;
+    s = __dadd_rn(s, d_slack(p.shm_bytes_per_sm, a.shm, b.shm));
+    s = __dadd_rn(s, d_slack(p.regs_per_sm, a.regs, b.regs));
+    s = __dadd_rn(s, d_slack(p.max_warps_per_sm, a.warps, b.warps));
+    if ((a.ratio <= RB && RB <= b.ratio) || (b.ratio <= RB && RB <= a.ratio)) {
+        const double rc =
+            __ddiv_rn(__dadd_rn(a.inst, b.inst), __dadd_rn(__ddiv_rn(a.inst, a.ratio), __ddiv_rn(b.inst, b.ratio)));
+        const double bonus = __dsub_rn(1.0, __ddiv_rn(fabs(__dsub_rn(rc, RB)), RB));
+        s = __dadd_rn(s, bonus > 0.0 ? bonus : 0.0);
+    }
+    return s;
+}
+
+__global__ void rk_heuristic_kernel(const rk_kernel* __restrict__ sets, uint32_t n, uint32_t n_sets,
+                                    rk_gpu_params p, int32_t* __restrict__ orders, uint64_t* __restrict__ index) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n_sets) return;
+    const rk_kernel* ks = sets + (size_t)q * n;
+    const double RB = __ddiv_rn((double)p.rb_num, (double)p.rb_den);
+    DProf f[RK_MAX_N];
+    for (uint32_t i = 0; i < n; i++) {
+        const uint64_t per_sm = (ks[i].grid_blocks + p.n_sm - 1) / p.n_sm; /* ceil(N_tblk/N_SM) */
+        f[i].shm = (uint64_t)ks[i].shm_bytes_per_block * per_sm;
+        f[i].regs = (uint64_t)ks[i].regs_per_thread * ks[i].threads_per_block * per_sm;
+        f[i].warps = (uint64_t)((ks[i].threads_per_block + 31u) / 32u) * per_sm;
+        f[i].blocks = per_sm;
+        f[i].inst = __dmul_rn((double)ks[i].grid_blocks, (double)ks[i].inst_per_block);
+        f[i].ratio = __ddiv_rn((double)ks[i].inst_per_block, (double)ks[i].mem_per_block);
+    }
+    uint32_t used = 0, pos = 0;
+    int32_t out[RK_MAX_N];
+    while (pos < n) {
+        if (pos + 1 == n) { /* lone kernel: singleton round */
+            for (uint32_t i = 0; i < n; i++)
+                if (!(used >> i & 1u)) out[pos++] = (int32_t)i;
+            break;
+        }
+        int ba = -1, bb = -1;
+        double bs = 0.0;
+        for (uint32_t a = 0; a < n; a++) {
+            if (used >> a & 1u) continue;
+            for (uint32_t b = a + 1; b < n; b++) {
+                if ((used >> b & 1u) || !d_fits(p, f[a], f[b])) continue;
+                const double sc = d_score(p, RB, f[a], f[b]);
+                if (ba < 0 || sc > bs) { ba = (int)a; bb = (int)b; bs = sc; }
+            }
+        }
+        if (ba < 0) { /* no feasible pair: singletons by decreasing shm, index order on ties */
+            while (pos < n) {
+                int best = -1;
+                for (uint32_t i = 0; i < n; i++)
+                    if (!(used >> i & 1u) && (best < 0 || f[i].shm > f[best].shm)) best = (int)i;
+                used |= 1u << best;
+                out[pos++] = best;
+            }
+            break;
+        }
+        int32_t rd[RK_MAX_N];
+        uint32_t m = 2;
+        if (f[bb].shm > f[ba].shm) { rd[0] = bb; rd[1] = ba; }
+        else { rd[0] = ba; rd[1] = bb; }
+        used |= (1u << ba) | (1u << bb);
+        DProf comb = d_combine(f[ba], f[bb]);
+        for (;;) {
+            int bc = -1;
+            double cs = 0.0;
+            for (uint32_t x = 0; x < n; x++) {
+                if ((used >> x & 1u) || !d_fits(p, comb, f[x])) continue;
+                const double sc = d_score(p, RB, comb, f[x]);
+                if (bc < 0 || sc > cs) { bc = (int)x; cs = sc; }
+            }
+            if (bc < 0) break;
+            uint32_t at = 0; /* stable decreasing-shm insertion (reading L17) */
+            while (at < m && f[rd[at]].shm >= f[bc].shm) at++;
+            for (uint32_t j = m; j > at; j--) rd[j] = rd[j - 1];
+            rd[at] = bc;
+            m++;
+            comb = d_combine(comb, f[bc]);
+            used |= 1u << bc;
+        }
+        for (uint32_t j = 0; j < m; j++) out[pos++] = rd[j];
+    }
+    /* lexicographic rank of the order (factorial number system) */
+    uint64_t idx = 0;
+    uint32_t seen = 0;
+    for (uint32_t j = 0; j < n; j++) {
+        const uint32_t x = (uint32_t)out[j];
+        idx = idx * (n - j) + (uint32_t)__popc(~seen & ((1u << x) - 1u));
+        seen |= 1u << x;
+        if (orders) orders[(size_t)q * n + j] = out[j];
+    }
+    index[q] = idx;
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (!g_num_sms) {
@@ -1271,6 +1394,14 @@ int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n
     if (e) return e;
     const unsigned blocks = (n_sets * 32 + 255) / 256;
     rk_merge_groups_kernel<<<blocks, 256, 0, st>>>(recs, n_sets, chunks, out_dev);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_launch_heuristic(const rk_kernel* sets_dev, uint32_t n, uint32_t n_sets, const rk_gpu_params* p,
+                        int32_t* orders_dev, uint64_t* index_dev, void* stream, uint32_t* launches) {
+    const unsigned blocks = (n_sets + 127) / 128;
+    rk_heuristic_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(sets_dev, n, n_sets, *p, orders_dev, index_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

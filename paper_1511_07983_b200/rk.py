@@ -24,7 +24,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
            "rk_eval_range_async", "rk_eval_range_hist_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
            "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
+           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -88,6 +88,7 @@ def lib():
             "rk_select_keys32": ([vp, vp, u64, u64, u64, u64, P(u64), u32, P(u64), vp], ctypes.c_int),
             "rk_range_histogram32": ([vp, vp, u64, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_heuristic_order": ([vp, P(ctypes.c_int32), P(ctypes.c_int32), P(u64), P(u64)], ctypes.c_int),
+            "rk_heuristic_batch": ([vp, P(rk_kernel), u32, u32, P(ctypes.c_int32), P(u64), vp], ctypes.c_int),
             "rk_percentile": ([vp, P(ctypes.c_int32), u64, u64, P(u64), P(u64)], ctypes.c_int),
             "rk_eval_batch": ([vp, P(rk_kernel), u32, u32, P(u64), P(rk_stats), P(u64), vp], ctypes.c_int),
             "rk_simulate_order": ([vp, P(ctypes.c_int32), P(u32), u32, P(u32), P(u64)], ctypes.c_int),
@@ -298,6 +299,17 @@ class Context:
         self._chk(self._L.rk_heuristic_order(self.h, o, r, ctypes.byref(idx), ctypes.byref(key) if with_key else None),
                   "rk_heuristic_order")
         return list(o), list(r), idx.value, (key.value if with_key else None)
+
+    def rk_heuristic_batch(self, sets, stream=None):
+        """Algorithm 1 on the device for many sets -> (orders, indices)."""
+        n = len(sets[0])
+        flat = [k for s in sets for k in s]
+        arr = kernels_array(flat)
+        ns = len(sets)
+        orders = (ctypes.c_int32 * (ns * n))()
+        idx = (ctypes.c_uint64 * ns)()
+        self._chk(self._L.rk_heuristic_batch(self.h, arr, n, ns, orders, idx, _stream(stream)), "rk_heuristic_batch")
+        return [list(orders[q * n:(q + 1) * n]) for q in range(ns)], list(idx)
 
     def rk_percentile(self, order, first: int, count: int):
         o = (ctypes.c_int32 * len(order))(*order)

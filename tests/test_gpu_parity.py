@@ -566,3 +566,30 @@ def test_c4_order_statistics_vs_oracle_golden(ctx):
     got = ctx.rk_select_keys(keys, N, st.key_min, st.key_max, ranks)
     assert got == [g["order_stats"][str(r)] for r in ranks]
     assert g["median_rank"] == (N - 1) // 2
+
+
+@pytest.mark.parametrize("gi", range(4))
+def test_device_algorithm1_matches_oracle(ctx, gi):
+    """Algorithm 1 on the GPU (one thread per set) == the oracle's."""
+    gpu = [W.GTX580, (8, 65536, 102400, 64, 16, 7, 2), (24, 32768, 49152, 48, 8, 311, 100),
+           (16, 32768, 49152, 48, 8, 411, 100)][gi]
+    ctx.rk_set_gpu_params(gpu)
+    for n in (1, 2, 3, 5, 8, 9, 12, 16):
+        sets = [ks for ks in W.random_small_sets(0xF4 + 100 * gi + n, 60, n, n, gpu=gpu)
+                if all(W.feasible(gpu, k) for k in ks)]
+        if not sets:
+            continue
+        orders, idx = ctx.rk_heuristic_batch(sets)
+        for ks, o, i in zip(sets, orders, idx):
+            want, _ = O.heuristic(gpu, ks)
+            assert o == want and i == O.rank(want)
+
+
+def test_device_algorithm1_c5_and_configs(ctx):
+    ctx.rk_set_gpu_params(W.GTX580)
+    sets = W.c5_sets(4096)
+    orders, idx = ctx.rk_heuristic_batch(sets)
+    g = _gold("c5_oracle.json")
+    assert idx[:g["n_sets"]] == [s["cand_index"] for s in g["sets"]]
+    for ks, o in list(zip(sets, orders))[:512]:
+        assert o == O.heuristic(W.GTX580, ks)[0]
