@@ -1345,7 +1345,7 @@ int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* 
 
 int rk_launch_key_of_index(const RkTables* tab_dev, uint32_t S, uint64_t index, uint64_t* out_dev, void* stream,
                            uint32_t* launches) {
-    RK_DISPATCH_GENERIC(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, index,
+    RK_DISPATCH(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, index,
                 out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
