@@ -986,12 +986,23 @@ __global__ void __launch_bounds__(256) rk_hist_kernel(const KT* __restrict__ key
     const bool aligned = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
     if (aligned) {
         if constexpr (sizeof(KT) == 8) {
+            /* software-pipelined: the next chunk's 64 B are in flight while this one is binned */
             const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys);
-            for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += stride) {
-                const ulonglong2 a = __ldcs(k2 + 4 * c), b = __ldcs(k2 + 4 * c + 1);
-                const ulonglong2 d = __ldcs(k2 + 4 * c + 2), e = __ldcs(k2 + 4 * c + 3);
-                put(binof(a.x)); put(binof(a.y)); put(binof(b.x)); put(binof(b.y));
-                put(binof(d.x)); put(binof(d.y)); put(binof(e.x)); put(binof(e.y));
+            uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+            ulonglong2 a, b, d, e;
+            if (c < nchunks) {
+                a = __ldcs(k2 + 4 * c); b = __ldcs(k2 + 4 * c + 1);
+                d = __ldcs(k2 + 4 * c + 2); e = __ldcs(k2 + 4 * c + 3);
+            }
+            for (; c < nchunks; c += stride) {
+                const ulonglong2 a0 = a, b0 = b, d0 = d, e0 = e;
+                const uint64_t cn = c + stride;
+                if (cn < nchunks) {
+                    a = __ldcs(k2 + 4 * cn); b = __ldcs(k2 + 4 * cn + 1);
+                    d = __ldcs(k2 + 4 * cn + 2); e = __ldcs(k2 + 4 * cn + 3);
+                }
+                put(binof(a0.x)); put(binof(a0.y)); put(binof(b0.x)); put(binof(b0.y));
+                put(binof(d0.x)); put(binof(d0.y)); put(binof(e0.x)); put(binof(e0.y));
             }
         } else {
             const uint4* k4 = reinterpret_cast<const uint4*>(keys);
