@@ -176,11 +176,15 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
             C = std::min<uint64_t>(C, caps[r] / dem[r]);
             const uint64_t D = 2 * dem[r];
             const uint64_t m = ((1ull << 32) + D - 1) / D; /* ceil(2^32 / 2d) <= 2^31 */
-            /* exhaustive exactness check of floor((2x+1)*m / 2^32) == floor(x/d) */
-            for (uint64_t x = 0; x <= caps[r]; x++)
-                if ((((2 * x + 1) * m) >> 32) != x / dem[r])
-                    return fail(c, RK_EUNSUPPORTED, "kernel %u: no exact 32-bit magic for demand %llu", i,
-                                (unsigned long long)dem[r]);
+            /* floor((2x+1)*m / 2^32) == floor(x/d) for all x <= cap: guaranteed when
+             * (2cap+1)*e < 2^32 (e = m*2d - 2^32; the odd numerator keeps frac <=
+             * (2d-1)/2d), otherwise checked exhaustively */
+            const uint64_t e = m * D - (1ull << 32);
+            if ((2 * caps[r] + 1) * e >= (1ull << 32))
+                for (uint64_t x = 0; x <= caps[r]; x++)
+                    if ((((2 * x + 1) * m) >> 32) != x / dem[r])
+                        return fail(c, RK_EUNSUPPORTED, "kernel %u: no exact 32-bit magic for demand %llu", i,
+                                    (unsigned long long)dem[r]);
             mag[r] = (uint32_t)m;
             add[r] = 0;
         }

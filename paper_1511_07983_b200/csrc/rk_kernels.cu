@@ -610,9 +610,12 @@ __device__ void commit(const rk_stats& cta, rk_stats* recs, uint32_t* counter, r
 #ifndef RK_DEPTH_LARGE
 #define RK_DEPTH_LARGE 3
 #endif
+#ifndef RK_DEPTH_SMALL
+#define RK_DEPTH_SMALL 5
+#endif
 template <int SMAX>
 struct Depth {
-    static constexpr int value = SMAX <= 2 ? 5 : (SMAX <= 8 ? 4 : RK_DEPTH_LARGE);
+    static constexpr int value = SMAX <= 2 ? RK_DEPTH_SMALL : (SMAX <= 8 ? 4 : RK_DEPTH_LARGE);
 };
 __host__ __device__ constexpr uint32_t cfact(int m) { return m <= 1 ? 1u : (uint32_t)m * cfact(m - 1); }
 
@@ -1232,7 +1235,7 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
                    uint32_t* keys32_dev, uint64_t key_base, uint32_t* ovf_dev, const rk_stats* hist_range,
                    uint32_t bins, uint64_t* hist_dev) {
     cudaStream_t st = (cudaStream_t)stream;
-    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
+    const uint32_t dm = S <= 2 ? (uint32_t)RK_DEPTH_SMALL : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t R = 1;
     for (uint32_t i = 2; i <= (n < dm ? n : dm); i++) R *= i;
     const uint64_t units = (first + count + R - 1) / R - first / R;
@@ -1374,7 +1377,7 @@ int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const in
 
 int rk_batch_chunks_per_set(uint32_t n, uint32_t S) {
     if (n < 3) return 1;
-    const uint32_t dm = S <= 2 ? 5u : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
+    const uint32_t dm = S <= 2 ? (uint32_t)RK_DEPTH_SMALL : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t f = 1, R = 1;
     for (uint32_t i = 2; i <= n; i++) f *= i;
     for (uint32_t i = 2; i <= (n < dm ? n : dm); i++) R *= i;

@@ -125,11 +125,24 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)  # torch.cuda.Stream
 
 
+class _KArr:
+    """Contiguous rk_kernel array backed by numpy (keeps the buffer alive)."""
+
+    def __init__(self, kernels):
+        import numpy as np
+
+        from itertools import chain
+
+        a = (np.fromiter(chain.from_iterable(kernels), dtype=np.uint64, count=6 * len(kernels)).reshape(-1, 6)
+             if len(kernels) else np.zeros((1, 6), np.uint64))
+        if a.size and (a.max() > 0xFFFFFFFF):
+            raise RkError(RK_EINVAL, "kernel field exceeds u32")
+        self.buf = np.ascontiguousarray(a.astype(np.uint32))
+        self._as_parameter_ = self.buf.ctypes.data_as(ctypes.POINTER(rk_kernel))
+
+
 def kernels_array(kernels):
-    arr = (rk_kernel * max(1, len(kernels)))()
-    for i, k in enumerate(kernels):
-        arr[i] = rk_kernel(*[int(x) for x in k])
-    return arr
+    return _KArr(kernels)
 
 
 def rk_table_bytes() -> int:

@@ -21,7 +21,7 @@ pct = sorted(100.0 * (st.n_eq + st.n_gt) / F for st, _ in res)
 q = lambda p: pct[min(len(pct) - 1, int(p * len(pct)))]
 print(json.dumps({"config": "C5", "sets": len(sets), "evaluations": len(sets) * F,
                   "seconds": min(times), "evals_per_s": len(sets) * F / min(times),
-                  "note": "synchronous rk_eval_batch incl. host Algorithm 1 per set, table upload, D2H",
+                  "note": "synchronous rk_eval_batch incl. host validation + table packing, device Algorithm 1 per set, upload, D2H",
                   "heuristic_percentile": {"min": pct[0], "p10": q(0.1), "median": q(0.5), "p90": q(0.9),
                                            "max": pct[-1], "mean": sum(pct) / len(pct),
                                            "frac_ge_90": sum(p >= 90 for p in pct) / len(pct)}}))
