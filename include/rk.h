@@ -63,7 +63,11 @@ const char* rk_last_error(const rk_ctx* ctx);
 typedef struct {
     uint32_t n_sm, regs_per_sm, shm_bytes_per_sm, max_warps_per_sm, max_blocks_per_sm;
     uint32_t rb_num, rb_den;
+    uint32_t flags; /* model-reading policy, 0 = the readings of DESIGN.md §3 */
 } rk_gpu_params;
+/* flags bit: the round-robin cursor restarts at SM 0 for every kernel (the
+ * alternative reading of L4; PAPER:76 only says "round-robin fashion"). */
+#define RK_FLAG_CURSOR_PER_KERNEL 1u
 rk_status rk_set_gpu_params(rk_ctx* ctx, const rk_gpu_params* p);
 
 /* Kernel profile, Table 1 bottom half:

@@ -3,7 +3,7 @@
 Inputs are plain sequences so this module imports nothing from the product
 package:
 
-* ``gpu``     = (n_sm, regs_per_sm, shm_per_sm, warps_per_sm, blocks_per_sm, rb_num, rb_den)
+* ``gpu``     = (n_sm, regs_per_sm, shm_per_sm, warps_per_sm, blocks_per_sm, rb_num, rb_den[, flags])
 * ``kernels`` = [(grid_blocks, threads_per_block, regs_per_thread, shm_per_block,
                   inst_per_block A_i, mem_per_block M_i), ...]
 
@@ -64,8 +64,11 @@ def lib():
 
 
 def _gpu_arr(gpu):
-    assert len(gpu) == 7
-    return (ctypes.c_uint32 * 7)(*[int(x) for x in gpu])
+    """7-tuple (Table 1 GPU parameters) or 8-tuple with model-reading flags (bit 0:
+    cursor restarts at SM 0 for every kernel — alternative reading of L4)."""
+    assert len(gpu) in (7, 8)
+    g = [int(x) for x in gpu] + ([0] if len(gpu) == 7 else [])
+    return (ctypes.c_uint32 * 8)(*g)
 
 
 def _kern_arr(kernels):

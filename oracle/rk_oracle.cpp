@@ -46,6 +46,8 @@ typedef unsigned __int128 u128;
 /* GPU: N_SM, N_reg_SM, N_shm_SM, N_warp_SM, N_blk_SM, R_B = rb_num / rb_den    */
 struct OrGpu {
     uint32_t n_sm, regs_per_sm, shm_per_sm, warps_per_sm, blocks_per_sm, rb_num, rb_den;
+    uint32_t flags; /* bit 0: the alternative reading of L4 — the round-robin cursor
+                       restarts at SM 0 for every kernel */
 };
 /* Kernel profile.  inst_per_block A_i = N_inst_i / N_tblk_i;  mem_per_block
  * M_i = A_i / R_i = 4*mem_events_i / N_tblk_i, in
@@ -185,6 +187,7 @@ static void simulate(const OrGpu& g, const OrKernel* k, int n, const int* order,
     for (int j = 0; j < n; j++) {
         int ki = order[j];
         Demand d = demand_of(k[ki]);
+        if (g.flags & 1u) cursor = 0; /* alternative reading of L4 (f3) */
         for (uint32_t b = 0; b < k[ki].grid_blocks; b++) {
             int found = -1;
             for (uint32_t step = 0; step < S; step++) { /* scan ring-wise from the cursor */
@@ -381,8 +384,8 @@ static void heuristic(const OrGpu& g, const OrKernel* k, int n, int* order_out, 
 /* ===================== C ABI for the Python test harness =================== */
 extern "C" {
 
-int or_check_inputs(const uint32_t* gpu7, const uint32_t* kern, int n) {
-    return check_inputs(*(const OrGpu*)gpu7, (const OrKernel*)kern, n);
+int or_check_inputs(const uint32_t* gpu8, const uint32_t* kern, int n) {
+    return check_inputs(*(const OrGpu*)gpu8, (const OrKernel*)kern, n);
 }
 
 void or_unrank(uint64_t idx, int n, int* order) { unrank(idx, n, order); }
@@ -391,10 +394,10 @@ uint64_t or_factorial(int n) { return factorial(n); }
 
 /* rounds_out: max_rounds x n row-major (p[r][i]); trace_out: 2*sum(T) int32
  * (round, sm) per block in dispatch order.  Both nullable. */
-int or_simulate(const uint32_t* gpu7, const uint32_t* kern, int n, const int* order, uint32_t* rounds_out,
+int or_simulate(const uint32_t* gpu8, const uint32_t* kern, int n, const int* order, uint32_t* rounds_out,
                 int max_rounds, int* n_rounds, uint64_t* key_lo, uint64_t* key_hi, double* t_naive,
                 int32_t* trace_out) {
-    const OrGpu& g = *(const OrGpu*)gpu7;
+    const OrGpu& g = *(const OrGpu*)gpu8;
     const OrKernel* k = (const OrKernel*)kern;
     int e = check_inputs(g, k, n);
     if (e) return e;
@@ -415,9 +418,9 @@ int or_simulate(const uint32_t* gpu7, const uint32_t* kern, int n, const int* or
 }
 
 /* Sweep [first, first+count) with `threads` contiguous chunks merged in order. */
-int or_sweep(const uint32_t* gpu7, const uint32_t* kern, int n, uint64_t first, uint64_t count, uint64_t cand_key,
+int or_sweep(const uint32_t* gpu8, const uint32_t* kern, int n, uint64_t first, uint64_t count, uint64_t cand_key,
              int threads, uint64_t* stats8, uint64_t* keys_out, double* max_rel_err) {
-    const OrGpu& g = *(const OrGpu*)gpu7;
+    const OrGpu& g = *(const OrGpu*)gpu8;
     const OrKernel* k = (const OrKernel*)kern;
     int e = check_inputs(g, k, n);
     if (e) return e;
@@ -481,8 +484,8 @@ int or_histogram(const uint64_t* keys, uint64_t count, uint64_t kmin, uint64_t k
     return OR_OK;
 }
 
-int or_heuristic(const uint32_t* gpu7, const uint32_t* kern, int n, int* order_out, int* round_of_out) {
-    const OrGpu& g = *(const OrGpu*)gpu7;
+int or_heuristic(const uint32_t* gpu8, const uint32_t* kern, int n, int* order_out, int* round_of_out) {
+    const OrGpu& g = *(const OrGpu*)gpu8;
     const OrKernel* k = (const OrKernel*)kern;
     int e = check_inputs(g, k, n);
     if (e) return e;
@@ -491,9 +494,9 @@ int or_heuristic(const uint32_t* gpu7, const uint32_t* kern, int n, int* order_o
 }
 
 /* ScoreGen / ProfileCombine on two single kernels (for SPEC example pins). */
-int or_pair_score(const uint32_t* gpu7, const uint32_t* kern, int i, int j, int* feasible, double* score,
+int or_pair_score(const uint32_t* gpu8, const uint32_t* kern, int i, int j, int* feasible, double* score,
                   double* r_comb) {
-    const OrGpu& g = *(const OrGpu*)gpu7;
+    const OrGpu& g = *(const OrGpu*)gpu8;
     const OrKernel* k = (const OrKernel*)kern;
     Prof a = footprint(g, k[i]), b = footprint(g, k[j]);
     *feasible = pair_fits(g, a, b) ? 1 : 0;
@@ -505,8 +508,8 @@ int or_pair_score(const uint32_t* gpu7, const uint32_t* kern, int i, int j, int*
 /* C5-style batch: for each set, Algorithm 1 order -> its key -> full sweep.
  * Sets are distributed over threads; each set is evaluated single-threaded.
  * out per set: stats8 (8 u64) + cand_index + cand_key (10 u64 total). */
-int or_sweep_sets(const uint32_t* gpu7, const uint32_t* kern, int n, int n_sets, int threads, uint64_t* out10) {
-    const OrGpu& g = *(const OrGpu*)gpu7;
+int or_sweep_sets(const uint32_t* gpu8, const uint32_t* kern, int n, int n_sets, int threads, uint64_t* out10) {
+    const OrGpu& g = *(const OrGpu*)gpu8;
     const OrKernel* all = (const OrKernel*)kern;
     for (int s = 0; s < n_sets; s++) {
         int e = check_inputs(g, all + (size_t)s * n, n);

@@ -93,6 +93,7 @@ rk_status check_params(rk_ctx* c, const rk_gpu_params& p) {
     if (!p.n_sm || !p.regs_per_sm || !p.shm_bytes_per_sm || !p.max_warps_per_sm || !p.max_blocks_per_sm ||
         !p.rb_num || !p.rb_den)
         return fail(c, RK_EINVAL, "gpu params must all be > 0 (SPEC:30-32)");
+    if (p.flags & ~RK_FLAG_CURSOR_PER_KERNEL) return fail(c, RK_EINVAL, "unknown model flags");
     if (p.max_blocks_per_sm > 255) return fail(c, RK_EUNSUPPORTED, "max_blocks_per_sm > 255");
     if (p.max_warps_per_sm > 32767) return fail(c, RK_EUNSUPPORTED, "max_warps_per_sm > 32767");
     return RK_OK;
@@ -161,6 +162,7 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
     }
     g.tbits = tb;
     g.n = n;
+    g.flags = p.flags;
     for (uint32_t i = 0; i <= RK_MAX_N; i++) g.fact[i] = fact64(i);
     const uint64_t caps[3] = {R, Sh, p.max_warps_per_sm};
     for (uint32_t i = 0; i < n; i++) {

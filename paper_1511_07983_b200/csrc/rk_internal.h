@@ -46,6 +46,7 @@ struct RkGTab {
     uint32_t smagic;       /* ceil(2^32 / S) */
     uint32_t tbits;        /* highest power of two <= max_blocks_per_sm (binary search) */
     uint32_t n;            /* number of kernels */
+    uint32_t flags;        /* RK_FLAG_* model-reading policy */
     uint64_t fact[RK_MAX_N + 1];
 };
 

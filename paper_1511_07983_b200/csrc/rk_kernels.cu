@@ -345,7 +345,8 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
             bfb[i] = ovf ? (live ? g.freshB : 0u) : in.fb[i];
             c[i] = ovf ? (live ? k.C : 0u) : c[i];
         }
-        o.cur = water_fill<SMAX, FULL>(n, c, bfa, bfb, ovf ? 0u : in.cur, k, g, upd);
+        o.cur = water_fill<SMAX, FULL>(n, c, bfa, bfb, (ovf || (g.flags & RK_FLAG_CURSOR_PER_KERNEL)) ? 0u : in.cur,
+                                           k, g, upd);
         o.I = (ovf ? 0ull : in.I) + (uint64_t)n * k.cA;
         o.M = (ovf ? 0ull : in.M) + (uint64_t)n * k.cM;
     } else {
@@ -371,7 +372,8 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
             o.I = (uint64_t)n * k.cA;
             o.M = (uint64_t)n * k.cM;
         } else {
-            o.cur = water_fill<SMAX, FULL>(n, c, in.fa, in.fb, in.cur, k, g, upd);
+            o.cur = water_fill<SMAX, FULL>(n, c, in.fa, in.fb, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) ? 0u : in.cur,
+                                           k, g, upd);
             o.I = in.I + (uint64_t)n * k.cA;
             o.M = in.M + (uint64_t)n * k.cM;
             o.K = in.K;

@@ -31,7 +31,10 @@ EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_
 class rk_gpu_params(ctypes.Structure):
     _fields_ = [(f, ctypes.c_uint32) for f in
                 ("n_sm", "regs_per_sm", "shm_bytes_per_sm", "max_warps_per_sm", "max_blocks_per_sm", "rb_num",
-                 "rb_den")]
+                 "rb_den", "flags")]
+
+
+RK_FLAG_CURSOR_PER_KERNEL = 1
 
 
 class rk_kernel(ctypes.Structure):
@@ -221,7 +224,8 @@ class Context:
 
     # -- inputs --------------------------------------------------------------
     def rk_set_gpu_params(self, gpu):
-        p = rk_gpu_params(*[int(x) for x in gpu])
+        g = [int(x) for x in gpu]
+        p = rk_gpu_params(*(g + [0] * (8 - len(g))))  # 7-tuple (Table 1) or 8 with model flags
         self._chk(self._L.rk_set_gpu_params(self.h, ctypes.byref(p)), "rk_set_gpu_params")
 
     def rk_set_kernels(self, kernels):

@@ -593,3 +593,20 @@ def test_device_algorithm1_c5_and_configs(ctx):
     assert idx[:g["n_sets"]] == [s["cand_index"] for s in g["sets"]]
     for ks, o in list(zip(sets, orders))[:512]:
         assert o == O.heuristic(W.GTX580, ks)[0]
+
+
+def test_cursor_per_kernel_reading_vs_oracle(ctx):
+    """model-reading variant (RK_FLAG_CURSOR_PER_KERNEL)."""
+    w = _gold("w2_cursor.json")
+    ctx.rk_set_gpu_params(list(w["gpu"]) + [rk.RK_FLAG_CURSOR_PER_KERNEL])
+    ctx.rk_set_kernels(w["kernels"])
+    assert ctx.rk_simulate_order(w["order"]) == (w["rejected_reading_rounds"], w["T_rejected_reading"])
+    for gpu in (W.GTX580, (13, 32768, 49152, 48, 8, 411, 100), (8, 65536, 102400, 64, 16, 7, 2)):
+        for ks in W.random_small_sets(0xF3 + gpu[0], 6, 3, 7, gpu=gpu):
+            if not all(W.feasible(gpu, k) for k in ks):
+                continue
+            check_full_space(ctx, list(gpu) + [1], ks, bins=(16,))
+    gpu, ks = W.config("C2")
+    st = check_full_space(ctx, list(gpu) + [1], ks, bins=(256,))
+    base, _ = gpu_keys(ctx, gpu, ks)
+    assert st.as_tuple() != base.as_tuple()  # the reading matters on C2

@@ -176,3 +176,14 @@ def test_unrank_equals_library_permutation_enumeration():
             assert O.rank(list(p)) == idx
     import math
     assert O.factorial(12) == math.factorial(12) == 479001600
+
+
+def test_w2_alternative_cursor_reading():
+    """the rejected reading of L4 (cursor restarts at SM 0 for
+    every kernel) as a model flag; W2 gives T = 7 (hand trace, golden)."""
+    w = _load("w2_cursor.json")
+    gpu = list(w["gpu"]) + [1]
+    r = O.simulate(gpu, w["kernels"], w["order"], trace=True)
+    assert [list(t) for t in r.trace] == w["rejected_reading_trace"]
+    assert r.rounds == w["rejected_reading_rounds"]
+    assert r.key == w["T_rejected_reading"] * w["gpu"][6]

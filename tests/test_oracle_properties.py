@@ -266,3 +266,34 @@ def test_heuristic_epbs6_pairs_opposite_types():
     for mem in rounds.values():
         types = {("EP" if k < 3 else "BS") for k in mem}
         assert types == {"EP", "BS"}
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_trace_rules_under_cursor_per_kernel_reading(seed):
+    """The alternative-reading trace obeys first fit from SM 0 at every kernel."""
+    sets = W.random_small_sets(0x7B1 + seed, 4, 2, 6)
+    for ks in sets:
+        gpu = list(G) + [1]
+        order = list(range(len(ks)))[::-1]
+        r = O.simulate(gpu, ks, order, trace=True)
+        S = G[0]
+        caps = (G[1], G[2], G[3], G[4])
+        used = [[0, 0, 0, 0] for _ in range(S)]
+        b, rnd = 0, 0
+        for k in order:
+            d = demand(ks[k])
+            cursor = 0
+            for _ in range(ks[k][0]):
+                rr, s = r.trace[b]
+                b += 1
+                if rr != rnd:
+                    rnd = rr
+                    used = [[0, 0, 0, 0] for _ in range(S)]
+                    cursor = 0
+                x = cursor
+                while x != s:
+                    assert not all(used[x][q] + d[q] <= caps[q] for q in range(4))
+                    x = (x + 1) % S
+                for q in range(4):
+                    used[s][q] += d[q]
+                cursor = (s + 1) % S
