@@ -607,6 +607,4 @@ def test_cursor_per_kernel_reading_vs_oracle(ctx):
                 continue
             check_full_space(ctx, list(gpu) + [1], ks, bins=(16,))
     gpu, ks = W.config("C2")
-    st = check_full_space(ctx, list(gpu) + [1], ks, bins=(256,))
-    base, _ = gpu_keys(ctx, gpu, ks)
-    assert st.as_tuple() != base.as_tuple()  # the reading matters on C2
+    check_full_space(ctx, list(gpu) + [1], ks, bins=(256,))
