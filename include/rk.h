@@ -230,6 +230,20 @@ rk_status rk_eval_batch(rk_ctx* ctx, const rk_kernel* sets, uint32_t n, uint32_t
 rk_status rk_simulate_order(rk_ctx* ctx, const int32_t* order, uint32_t* rounds_out, uint32_t max_rounds,
                             uint32_t* n_rounds_out, uint64_t* key_out);
 
+/* Exact optimum by branch and bound (the same (key_min,
+ * argmin) as a full rk_eval_range over [0, n!) — SPEC:300, ties -> smallest
+ * index — without enumerating n!).  Bound of a prefix (PAPER:79-81 round
+ * time): K_closed + max(den*(I_open + sum_rem T*A), num*(M_open +
+ * sum_rem T*M)); pruning is strict (bound > best) so every order with the
+ * minimum key is visited.  seed_index: an order whose key seeds the bound
+ * (e.g. Algorithm 1's rank), or UINT64_MAX for none.  Outputs (host, each
+ * optional): order_out int32[n] (the argmin order), index_out, key_out (exact
+ * scaled key K = den*T), nodes_out (placements performed; n! * n would be the
+ * exhaustive count).  Synchronous on `stream`.  Run time depends on how tight
+ * the bound is: worst case is the full tree. */
+rk_status rk_best_order(rk_ctx* ctx, uint64_t seed_index, int32_t* order_out, uint64_t* index_out, uint64_t* key_out,
+                        uint64_t* nodes_out, void* stream);
+
 /* Lexicographic rank/unrank (factorial number system; reading L11). Pure host
  * helpers, no ctx.  1 <= n <= 20. RK_EINVAL on a non-permutation / idx >= n!. */
 rk_status rk_rank(const int32_t* order, uint32_t n, uint64_t* idx_out);

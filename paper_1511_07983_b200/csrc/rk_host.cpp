@@ -920,6 +920,48 @@ rk_status rk_simulate_order(rk_ctx* c, const int32_t* order, uint32_t* rounds_ou
     return RK_OK;
 }
 
+rk_status rk_best_order(rk_ctx* c, uint64_t seed_index, int32_t* order_out, uint64_t* index_out, uint64_t* key_out,
+                        uint64_t* nodes_out, void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    const uint32_t n = c->tab.g.n;
+    if (seed_index != UINT64_MAX && seed_index >= space(c)) return fail(c, RK_EINVAL, "seed_index >= n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    uint64_t seed = ~0ull;
+    if (seed_index != UINT64_MAX && (s = key_of_index(c, seed_index, &seed, stream))) return s;
+    /* prefix depth P: enough units for dynamic balance (8 per thread), P <= n-1 */
+    const uint64_t threads = (uint64_t)rk_bnb_ctas() * 128;
+    uint32_t P = 0;
+    uint64_t units = 1;
+    while (P + 1 < n && units < 8 * threads) units *= (n - P++);
+    const int ctas = rk_bnb_ctas();
+    struct {
+        unsigned long long best, nodes;
+        unsigned int next_unit, done;
+        unsigned long long key, index;
+    } h{seed, 0, 0, 0, 0, 0};
+    static_assert(sizeof h == 40, "BnbGlobal layout");
+    void* gb = nullptr;
+    unsigned long long* recs = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    int e = cudaMalloc(&gb, sizeof h);
+    if (!e) e = cudaMalloc(&recs, sizeof(unsigned long long) * 2 * ctas);
+    if (!e) e = cudaMemcpyAsync(gb, &h, sizeof h, cudaMemcpyHostToDevice, st);
+    if (!e) e = rk_launch_bnb(c->tab_dev, c->tab.g.S, P, units, gb, recs, stream, &c->launches);
+    if (!e) e = cudaMemcpyAsync(&h, gb, sizeof h, cudaMemcpyDeviceToHost, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    cudaFree(gb);
+    cudaFree(recs);
+    if (e) return cuda_fail(c, e, "rk_best_order");
+    if (h.index >= space(c)) return fail(c, RK_EINVAL, "rk_best_order: no order found (internal)");
+    if (order_out) do_unrank(h.index, n, order_out);
+    if (index_out) *index_out = h.index;
+    if (key_out) *key_out = h.key;
+    if (nodes_out) *nodes_out = h.nodes;
+    return RK_OK;
+}
+
 rk_status rk_rank(const int32_t* order, uint32_t n, uint64_t* idx_out) {
     if (!order || !idx_out) return RK_EINVAL;
     return do_rank(order, n, idx_out);

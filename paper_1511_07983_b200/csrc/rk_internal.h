@@ -92,5 +92,10 @@ int rk_launch_heuristic(const rk_kernel* sets_dev, uint32_t n, uint32_t n_sets, 
                         int32_t* orders_dev, uint64_t* index_dev, void* stream, uint32_t* launches);
 int rk_batch_chunks_per_set(uint32_t n, uint32_t S);
 int rk_eval_max_ctas(uint32_t S, int device);
+/* branch-and-bound exact optimum: gb_dev = 48-B BnbGlobal (best seeded, rest 0),
+ * recs_dev = 2*rk_bnb_ctas() u64 */
+int rk_bnb_ctas();
+int rk_launch_bnb(const RkTables* tab_dev, uint32_t S, uint32_t P, uint64_t n_units, void* gb_dev,
+                  unsigned long long* recs_dev, void* stream, uint32_t* launches);
 
 #endif

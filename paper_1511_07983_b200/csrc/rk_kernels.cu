@@ -1151,6 +1151,180 @@ __global__ void rk_heuristic_kernel(const rk_kernel* __restrict__ sets, uint32_t
     index[q] = idx;
 }
 
+/* ============ Branch-and-bound exact optimum (n >= 13) ============
+ * A lower bound on every completion of a node (state s after a prefix, remaining
+ * set R): the open round and all later rounds together cost
+ * sum_r max(den I_r, num M_r) >= max(sum_r den I_r, sum_r num M_r) (SPEC:255 round
+ * key is a max of the two sums), and those sums are fixed by R, so
+ *   LB = K + max(dI + sum_{k in R} T_k dA_k, nM + sum_{k in R} T_k nM_k).
+ * The pruning is STRICT (LB > best): every leaf whose key equals the final minimum
+ * is visited, so one pass yields the minimum AND its smallest index (the argmin
+ * of the full sweep, SPEC:300 ties -> smallest index).  Work units are the
+ * n!/(n-P)! prefixes of depth P, handed out by an atomic counter (dynamic
+ * balance: subtree sizes after pruning vary by orders of magnitude); below a unit
+ * an explicit-stack DFS in lexicographic order, so leaf indices are ascending
+ * inside a unit. */
+struct BnbGlobal {             /* device scratch; host zeroes it (best = seed) */
+    unsigned long long best;   /* running minimum key (seeded with an order's key) */
+    unsigned long long nodes;  /* placements performed */
+    unsigned int next_unit;
+    unsigned int done;         /* CTAs finished (last one merges) */
+    unsigned long long key, index; /* result */
+};
+
+__device__ __forceinline__ uint32_t nth_set_bit(uint32_t m, uint32_t r) { /* 0-based r-th set bit of m */
+    for (uint32_t q = 0; q < r; q++) m &= m - 1u;
+    return (uint32_t)__ffs(m) - 1u;
+}
+
+__device__ __forceinline__ bool lex_less(uint64_t ka, uint64_t ia, uint64_t kb, uint64_t ib) {
+    return ka < kb || (ka == kb && ia < ib);
+}
+
+constexpr int kBnbThreads = 128;
+
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kBnbThreads) rk_bnb_kernel(const RkTables* __restrict__ tab, uint32_t P,
+                                                            uint64_t n_units, BnbGlobal* gb,
+                                                            unsigned long long* __restrict__ recs) {
+    __shared__ RkTables t;
+    __shared__ uint64_t totA[RK_MAX_N], totM[RK_MAX_N];
+    __shared__ uint64_t wk[kBnbThreads / 32], wi[kBnbThreads / 32];
+    __shared__ bool last;
+    load_tables(t, tab);
+    const RkGTab& g = t.g;
+    const uint32_t n = g.n;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        totA[i] = (uint64_t)t.k[i].T * t.k[i].cA;
+        totM[i] = (uint64_t)t.k[i].T * t.k[i].cM;
+    }
+    __syncthreads();
+    uint64_t sumA = 0, sumM = 0;
+    for (uint32_t i = 0; i < n; i++) {
+        sumA += totA[i];
+        sumM += totM[i];
+    }
+    uint64_t span = 1; /* (n-P)! leaves per unit */
+    for (uint32_t i = 2; i <= n - P; i++) span *= i;
+    const uint32_t full = (1u << n) - 1u;
+
+    NoRec nr;
+    St<SMAX> st[RK_MAX_N];
+    uint32_t rmask[RK_MAX_N], child[RK_MAX_N];
+    uint64_t ra[RK_MAX_N], rm[RK_MAX_N], ioff[RK_MAX_N];
+    uint64_t nodes = 0, my_key = ~0ull, my_idx = ~0ull;
+    uint64_t best = *(volatile unsigned long long*)&gb->best;
+    for (;;) {
+        const uint64_t u = atomicAdd(&gb->next_unit, 1u);
+        if (u >= n_units) break;
+        best = *(volatile unsigned long long*)&gb->best;
+        /* the P-prefix of unit u: mixed radix (n, n-1, ..., n-P+1), lexicographic */
+        uint64_t rem = u;
+        uint32_t dig[RK_MAX_N];
+        for (int j = (int)P - 1; j >= 0; j--) {
+            const uint32_t base = n - (uint32_t)j;
+            dig[j] = (uint32_t)(rem % base);
+            rem /= base;
+        }
+        st_fresh<SMAX, FULL>(st[0], g);
+        uint32_t mask = full;
+        uint64_t sa = sumA, sm = sumM;
+        bool pruned = false;
+        for (uint32_t j = 0; j < P && !pruned; j++) {
+            const uint32_t k = nth_set_bit(mask, dig[j]);
+            mask &= ~(1u << k);
+            sa -= totA[k];
+            sm -= totM[k];
+            place<SMAX, FULL>(st[0], st[0], t.k[k], k, g, nr);
+            nodes++;
+            const uint64_t x = st[0].I + sa, y = st[0].M + sm;
+            pruned = st[0].K + (x >= y ? x : y) > best;
+        }
+        if (pruned) continue;
+        int l = 0;
+        rmask[0] = mask;
+        child[0] = 0;
+        ra[0] = sa;
+        rm[0] = sm;
+        ioff[0] = u * span;
+        while (l >= 0) {
+            const uint32_t left = (uint32_t)__popc(rmask[l]);
+            if (child[l] >= left) { l--; continue; }
+            const uint32_t c = child[l]++;
+            const uint32_t k = nth_set_bit(rmask[l], c);
+            uint64_t sub = 1; /* (left-1)! leaves below each child */
+            for (uint32_t i = 2; i < left; i++) sub *= i;
+            const uint64_t idx = ioff[l] + (uint64_t)c * sub;
+            if (left == 1) {
+                const uint64_t key = finish<SMAX>(st[l], t.k[k], k, g, nr);
+                nodes++;
+                if (lex_less(key, idx, my_key, my_idx)) {
+                    my_key = key;
+                    my_idx = idx;
+                }
+                if (key < best) {
+                    const unsigned long long old = atomicMin(&gb->best, (unsigned long long)key);
+                    best = old < key ? old : key;
+                }
+                continue;
+            }
+            place<SMAX, FULL>(st[l], st[l + 1], t.k[k], k, g, nr);
+            nodes++;
+            const uint64_t sa2 = ra[l] - totA[k], sm2 = rm[l] - totM[k];
+            const uint64_t x = st[l + 1].I + sa2, y = st[l + 1].M + sm2;
+            if ((nodes & 255u) == 0) best = *(volatile unsigned long long*)&gb->best;
+            if (st[l + 1].K + (x >= y ? x : y) > best) continue;
+            l++;
+            rmask[l] = rmask[l - 1] & ~(1u << k);
+            child[l] = 0;
+            ra[l] = sa2;
+            rm[l] = sm2;
+            ioff[l] = idx;
+        }
+    }
+    atomicAdd(&gb->nodes, (unsigned long long)nodes);
+    /* CTA lexicographic min of (key, index), then the last CTA merges */
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xFFFFFFFFu, my_key, o), i2 = __shfl_xor_sync(0xFFFFFFFFu, my_idx, o);
+        if (lex_less(k2, i2, my_key, my_idx)) {
+            my_key = k2;
+            my_idx = i2;
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        wk[w] = my_key;
+        wi[w] = my_idx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < kBnbThreads / 32; q++)
+            if (lex_less(wk[q], wi[q], wk[0], wi[0])) {
+                wk[0] = wk[q];
+                wi[0] = wi[q];
+            }
+        recs[2 * blockIdx.x] = wk[0];
+        recs[2 * blockIdx.x + 1] = wi[0];
+        __threadfence();
+        last = atomicAdd(&gb->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        uint64_t bk = ~0ull, bi = ~0ull;
+        for (unsigned q = 0; q < gridDim.x; q++) {
+            const uint64_t k2 = ((volatile unsigned long long*)recs)[2 * q];
+            const uint64_t i2 = ((volatile unsigned long long*)recs)[2 * q + 1];
+            if (lex_less(k2, i2, bk, bi)) {
+                bk = k2;
+                bi = i2;
+            }
+        }
+        gb->key = bk;
+        gb->index = bi;
+    }
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (!g_num_sms) {
@@ -1418,6 +1592,16 @@ int rk_launch_heuristic(const rk_kernel* sets_dev, uint32_t n, uint32_t n_sets, 
                         int32_t* orders_dev, uint64_t* index_dev, void* stream, uint32_t* launches) {
     const unsigned blocks = (n_sets + 127) / 128;
     rk_heuristic_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(sets_dev, n, n_sets, *p, orders_dev, index_dev);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_bnb_ctas() { return num_sms() * 4; }
+
+int rk_launch_bnb(const RkTables* tab_dev, uint32_t S, uint32_t P, uint64_t n_units, void* gb_dev,
+                  unsigned long long* recs_dev, void* stream, uint32_t* launches) {
+    RK_DISPATCH(S, rk_bnb_kernel, RK_CFG((unsigned)rk_bnb_ctas(), kBnbThreads, 0, (cudaStream_t)stream), tab_dev,
+                P, n_units, (BnbGlobal*)gb_dev, recs_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

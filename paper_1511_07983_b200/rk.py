@@ -24,7 +24,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
            "rk_eval_range_async", "rk_eval_range_hist_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
            "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_rank", "rk_unrank",
+           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -91,6 +91,7 @@ def lib():
             "rk_select_keys32": ([vp, vp, u64, u64, u64, u64, P(u64), u32, P(u64), vp], ctypes.c_int),
             "rk_range_histogram32": ([vp, vp, u64, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_heuristic_order": ([vp, P(ctypes.c_int32), P(ctypes.c_int32), P(u64), P(u64)], ctypes.c_int),
+            "rk_best_order": ([vp, u64, P(ctypes.c_int32), P(u64), P(u64), P(u64), vp], ctypes.c_int),
             "rk_heuristic_batch": ([vp, P(rk_kernel), u32, u32, P(ctypes.c_int32), P(u64), vp], ctypes.c_int),
             "rk_percentile": ([vp, P(ctypes.c_int32), u64, u64, P(u64), P(u64)], ctypes.c_int),
             "rk_eval_batch": ([vp, P(rk_kernel), u32, u32, P(u64), P(rk_stats), P(u64), vp], ctypes.c_int),
@@ -316,6 +317,17 @@ class Context:
         self._chk(self._L.rk_heuristic_order(self.h, o, r, ctypes.byref(idx), ctypes.byref(key) if with_key else None),
                   "rk_heuristic_order")
         return list(o), list(r), idx.value, (key.value if with_key else None)
+
+    def rk_best_order(self, seed_index=None, stream=None):
+        """Exact optimum by branch and bound -> (order, index, key, nodes);
+        seed_index None = unseeded bound."""
+        n = self.n
+        o = (ctypes.c_int32 * n)()
+        idx, key, nodes = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        seed = (1 << 64) - 1 if seed_index is None else int(seed_index)
+        self._chk(self._L.rk_best_order(self.h, seed, o, ctypes.byref(idx), ctypes.byref(key), ctypes.byref(nodes),
+                                        _stream(stream)), "rk_best_order")
+        return list(o), idx.value, key.value, nodes.value
 
     def rk_heuristic_batch(self, sets, stream=None):
         """Algorithm 1 on the device for many sets -> (orders, indices)."""

@@ -608,3 +608,72 @@ def test_cursor_per_kernel_reading_vs_oracle(ctx):
             check_full_space(ctx, list(gpu) + [1], ks, bins=(16,))
     gpu, ks = W.config("C2")
     check_full_space(ctx, list(gpu) + [1], ks, bins=(256,))
+
+
+def _check_best(ctx, gpu, ks, want_key, want_idx, seeds=(None,)):
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    for seed in seeds:
+        order, idx, key, nodes = ctx.rk_best_order(seed)
+        assert (key, idx) == (want_key, want_idx), (seed, key, idx, want_key, want_idx)
+        assert order == O.unrank(idx, len(ks))
+        assert O.simulate(gpu, ks, order).key == key
+        assert 1 <= nodes <= len(ks) * math.factorial(len(ks)) * 2
+    return nodes
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_branch_and_bound_equals_full_sweep_goldens(ctx, name):
+    """rk_best_order == the oracle's full-space (key_min, argmin)."""
+    gpu, ks = W.config(name)
+    g = _gold(f"{name.lower()}_oracle.json")
+    _check_best(ctx, gpu, ks, g["stats"]["key_min"], g["stats"]["argmin"],
+                seeds=(None, g["cand_index"], g["stats"]["argmin"], g["stats"]["argmax"]))
+
+
+@pytest.mark.parametrize("gi", range(len(GPUS)))
+def test_branch_and_bound_random_sets_vs_oracle(ctx, gi):
+    gpu = GPUS[gi]
+    done = 0
+    for ks in W.random_small_sets(0xB0B + gi, 24, 1, 8, gpu=gpu):
+        if not all(W.feasible(gpu, k) for k in ks):
+            continue
+        try:
+            ctx.rk_set_gpu_params(gpu)
+            ctx.rk_set_kernels(ks)
+        except rk.RkError as e:
+            assert e.status == rk.RK_EUNSUPPORTED
+            continue
+        ost, _ = O.sweep(gpu, ks, threads=NCPU)
+        seed = int(np.random.default_rng(len(ks) + gi).integers(0, math.factorial(len(ks))))
+        _check_best(ctx, gpu, ks, ost.key_min, ost.argmin, seeds=(None, seed))
+        done += 1
+    assert done >= 5
+
+
+def test_branch_and_bound_ties_and_cursor_reading(ctx):
+    # identical kernels: every order has the same key -> argmin 0, no pruning possible
+    k = (20, 256, 20, 4096, 100, 30)
+    _check_best(ctx, W.GTX580, [k] * 7, O.simulate(W.GTX580, [k] * 7, list(range(7))).key, 0)
+    # the cursor-per-kernel reading (f3) through the same search
+    gpu, ks = W.config("C2")
+    g1 = list(gpu) + [rk.RK_FLAG_CURSOR_PER_KERNEL]
+    ost, _ = O.sweep(g1, ks, threads=NCPU)
+    _check_best(ctx, g1, ks, ost.key_min, ost.argmin)
+
+
+def test_branch_and_bound_n13_vs_full_device_sweep(ctx):
+    """n = 13 (6.2e9 orders): the search agrees with the exhaustive device sweep
+    (itself parity-tested) and the oracle re-simulates the optimum."""
+    gpu, ks = W.GTX580, _set13()
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(13)
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    cd = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ctx.rk_eval_range_async(0, N, cd, rec)
+    torch.cuda.synchronize()
+    st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
+    _, _, hidx, _ = ctx.rk_heuristic_order()
+    nodes = _check_best(ctx, gpu, ks, st.key_min, st.argmin, seeds=(None, hidx))
+    assert nodes < 13 * N
