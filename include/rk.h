@@ -58,7 +58,9 @@ const char* rk_last_error(const rk_ctx* ctx);
  * N_warp_SM, N_blk_SM, and the balanced inst/mem ratio R_B
  * as the exact rational rb_num / rb_den (reading L10; GTX580 preset
  * {16, 32768, 49152, 48, 8, 411, 100}).  All fields > 0
- * (SPEC:30-32); n_sm <= 32 and max_blocks_per_sm <= 255 on the device path.
+ * (SPEC:30-32); n_sm <= 65535, max_blocks_per_sm <= 255.  A reduced SM count
+ * S' = n_sm / gcd(n_sm, grids) <= 32 runs on per-SM register state, a larger one
+ * (e.g. the 148-SM B200 preset) on a run-length SM state.
  * Invalidates previously set kernels.  Errors: RK_EINVAL. */
 typedef struct {
     uint32_t n_sm, regs_per_sm, shm_bytes_per_sm, max_warps_per_sm, max_blocks_per_sm;

@@ -36,7 +36,11 @@ struct rk_ctx {
     uint32_t max_ctas = 0;
     uint32_t launches = 0;
     bool no_reduce = false; /* RK_NO_REDUCE=1: disable the symmetry reduction (testing) */
+    bool force_runs = false; /* RK_FORCE_RUNS=1: run-length SM state for every S (testing) */
 };
+
+/* SM count that selects the kernel variant (the table keeps the real S) */
+static uint32_t vS(const rk_ctx* c, uint32_t S) { return c->force_runs ? 65535u : S; }
 
 namespace {
 
@@ -96,6 +100,7 @@ rk_status check_params(rk_ctx* c, const rk_gpu_params& p) {
     if (p.flags & ~RK_FLAG_CURSOR_PER_KERNEL) return fail(c, RK_EINVAL, "unknown model flags");
     if (p.max_blocks_per_sm > 255) return fail(c, RK_EUNSUPPORTED, "max_blocks_per_sm > 255");
     if (p.max_warps_per_sm > 32767) return fail(c, RK_EUNSUPPORTED, "max_warps_per_sm > 32767");
+    if (p.n_sm > 65535) return fail(c, RK_EUNSUPPORTED, "n_sm > 65535");
     return RK_OK;
 }
 
@@ -138,8 +143,7 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
     }
     if (c && c->no_reduce) gb = 1;
     const uint32_t Sred = (uint32_t)(p.n_sm / gb);
-    if (Sred > RK_SMAX)
-        return fail(c, RK_EUNSUPPORTED, "N_SM/gcd(N_SM, grids) = %u > %d (device fast path)", Sred, RK_SMAX);
+    /* Sred <= RK_SMAX: per-SM register state; larger: run-length state (SMAX = 0) */
     const uint64_t R = p.regs_per_sm / gr, Sh = p.shm_bytes_per_sm / gs;
     if (R > 32767 || Sh > 32767)
         return fail(c, RK_EUNSUPPORTED, "scaled regs %llu / shm %llu exceed the 15-bit packing", (unsigned long long)R,
@@ -408,6 +412,8 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
     c->device = cuda_device;
     const char* nr = getenv("RK_NO_REDUCE");
     c->no_reduce = nr && nr[0] == '1';
+    const char* fr = getenv("RK_FORCE_RUNS");
+    c->force_runs = fr && fr[0] == '1';
     if (cuda_device >= 0) {
         int ndev = 0;
         cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -417,7 +423,7 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
         }
         DeviceGuard dg(cuda_device);
         c->max_ctas = 0;
-        for (uint32_t S : {1u, 2u, 3u, 4u, 5u, 8u, 9u, 16u, 17u, 32u})
+        for (uint32_t S : {1u, 2u, 3u, 4u, 5u, 8u, 9u, 16u, 17u, 32u, 33u})
             c->max_ctas = std::max(c->max_ctas, (uint32_t)rk_eval_max_ctas(S, cuda_device));
         if (c->max_ctas < 256) c->max_ctas = 256;
         bool ok = cudaMalloc(&c->tab_dev, sizeof(RkTables)) == cudaSuccess &&
@@ -488,7 +494,7 @@ rk_status rk_eval_range_async(rk_ctx* c, uint64_t first, uint64_t count, const u
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
-    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, cand_key_dev, 0, stats_dev, keys_dev,
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, stats_dev, keys_dev,
                            c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
     return e ? cuda_fail(c, e, "rk_eval_kernel launch") : RK_OK;
 }
@@ -506,7 +512,7 @@ rk_status rk_eval_range(rk_ctx* c, uint64_t first, uint64_t count, uint64_t cand
         std::memset(out_host, 0, sizeof *out_host);
         return RK_OK;
     }
-    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, nullptr, candidate_key, c->stats_dev,
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, nullptr, candidate_key, c->stats_dev,
                            keys_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
     if (e) return cuda_fail(c, e, "rk_eval_kernel launch");
     rk_stats h;
@@ -524,7 +530,7 @@ rk_status rk_eval_index_async(rk_ctx* c, uint64_t index, uint64_t* key_dev, void
     if (index >= space(c)) return fail(c, RK_EINVAL, "index >= n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
-    int e = rk_launch_key_of_index(c->tab_dev, c->tab.g.S, index, key_dev, stream, &c->launches);
+    int e = rk_launch_key_of_index(c->tab_dev, vS(c, c->tab.g.S), index, key_dev, stream, &c->launches);
     return e ? cuda_fail(c, e, "rk_eval_index_async") : RK_OK;
 }
 
@@ -539,7 +545,7 @@ rk_status rk_eval_range32_async(rk_ctx* c, uint64_t first, uint64_t count, const
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
-    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, cand_key_dev, 0, stats_dev, nullptr,
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, stats_dev, nullptr,
                            c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches, keys32_dev, key_base,
                            ovf_dev);
     return e ? cuda_fail(c, e, "rk_eval_kernel launch") : RK_OK;
@@ -555,7 +561,7 @@ rk_status rk_eval_range_hist_async(rk_ctx* c, uint64_t first, uint64_t count, co
     DeviceGuard dg(c->device);
     c->launches = 0;
     rk_stats* out = stats_dev ? stats_dev : c->stats_dev;
-    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, c->tab.g.S, first, count, cand_key_dev, 0, out, nullptr,
+    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, out, nullptr,
                            c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches, nullptr, 0, nullptr,
                            range_dev, bins, hist_dev);
     return e ? cuda_fail(c, e, "rk_eval_kernel (fused histogram) launch") : RK_OK;
@@ -723,7 +729,7 @@ static rk_status key_of_index(rk_ctx* c, uint64_t idx, uint64_t* key, void* stre
     DeviceGuard dg(c->device);
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemcpyAsync(c->u64_dev, &idx, sizeof idx, cudaMemcpyHostToDevice, st);
-    if (!e) e = rk_launch_keys_of_same(c->tab_dev, c->tab.g.S, c->u64_dev, 1, c->u64_dev + 1, stream, &c->launches);
+    if (!e) e = rk_launch_keys_of_same(c->tab_dev, vS(c, c->tab.g.S), c->u64_dev, 1, c->u64_dev + 1, stream, &c->launches);
     uint64_t h = 0;
     if (!e) e = cudaMemcpyAsync(&h, c->u64_dev + 1, sizeof h, cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaStreamSynchronize(st);
@@ -841,7 +847,7 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     cudaStream_t st = (cudaStream_t)stream;
     uint32_t max_chunks = 0;
     for (uint32_t q = 0; q < n_sets; q++)
-        max_chunks = std::max(max_chunks, (uint32_t)rk_batch_chunks_per_set(n, ptabs[q].g.S));
+        max_chunks = std::max(max_chunks, (uint32_t)rk_batch_chunks_per_set(n, vS(c, ptabs[q].g.S)));
     RkTables* tabs_dev = nullptr;
     uint64_t *idx_dev = nullptr, *keys_dev = nullptr;
     rk_stats *recs = nullptr, *out_dev = nullptr;
@@ -853,12 +859,12 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     if (!e) e = cudaMemcpyAsync(tabs_dev, ptabs.data(), sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
     if (!e) e = cudaMemcpyAsync(idx_dev, pidx.data(), sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
     uint32_t smax_k = 0;
-    for (uint32_t q = 0; q < n_sets; q++) smax_k = std::max(smax_k, ptabs[q].g.S);
+    for (uint32_t q = 0; q < n_sets; q++) smax_k = std::max(smax_k, vS(c, ptabs[q].g.S));
     if (!e) e = rk_launch_keys_of(tabs_dev, n, smax_k, idx_dev, n_sets, keys_dev, stream, &c->launches);
     for (uint32_t a = 0; a < n_sets && !e;) {
         uint32_t b = a;
         while (b < n_sets && ptabs[b].g.S == ptabs[a].g.S) b++;
-        const uint32_t S = ptabs[a].g.S, chunks = (uint32_t)rk_batch_chunks_per_set(n, S);
+        const uint32_t S = vS(c, ptabs[a].g.S), chunks = (uint32_t)rk_batch_chunks_per_set(n, S);
         e = rk_launch_batch(tabs_dev + a, n, S | 0x80000000u, b - a, keys_dev + a, out_dev + a, recs, chunks, stream,
                             &c->launches);
         a = b;
@@ -900,7 +906,7 @@ rk_status rk_simulate_order(rk_ctx* c, const int32_t* order, uint32_t* rounds_ou
     if (!e) e = cudaMalloc(&nr_dev, sizeof(uint32_t));
     if (!e) e = cudaMalloc(&key_dev, sizeof(uint64_t));
     if (!e) e = cudaMemcpy(order_dev, order, n * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (!e) e = rk_launch_simulate(c->tab_dev, n, c->tab.g.S, order_dev, rounds_dev, max_rounds, nr_dev, key_dev,
+    if (!e) e = rk_launch_simulate(c->tab_dev, n, vS(c, c->tab.g.S), order_dev, rounds_dev, max_rounds, nr_dev, key_dev,
                                    nullptr, &c->launches);
     uint32_t nr = 0;
     uint64_t key = 0;
@@ -948,7 +954,7 @@ rk_status rk_best_order(rk_ctx* c, uint64_t seed_index, int32_t* order_out, uint
     int e = cudaMalloc(&gb, sizeof h);
     if (!e) e = cudaMalloc(&recs, sizeof(unsigned long long) * 2 * ctas);
     if (!e) e = cudaMemcpyAsync(gb, &h, sizeof h, cudaMemcpyHostToDevice, st);
-    if (!e) e = rk_launch_bnb(c->tab_dev, c->tab.g.S, P, units, gb, recs, stream, &c->launches);
+    if (!e) e = rk_launch_bnb(c->tab_dev, vS(c, c->tab.g.S), P, units, gb, recs, stream, &c->launches);
     if (!e) e = cudaMemcpyAsync(&h, gb, sizeof h, cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaStreamSynchronize(st);
     cudaFree(gb);

@@ -111,6 +111,20 @@ struct St {
     uint64_t I, M, K; /* open round's den*I_r and num*M_r; closed rounds' key */
 };
 
+/* SMAX == 0: run-length SM state for any (super-)SM count S > 32 (e.g. the
+ * 148-SM B200 preset).  Within a round every SM's words are
+ * fixed by how many blocks of each placed kernel it holds; one water-fill
+ * changes that count uniformly except at the cursor and the new cursor, so
+ * run boundaries are a subset of {0} U {cursor after each placement of the
+ * round}: at most 1 + 16 runs (+1 transient). */
+constexpr int RK_RUNS = RK_MAX_N + 2;
+template <>
+struct St<0> {
+    uint32_t fa[RK_RUNS], fb[RK_RUNS], st[RK_RUNS]; /* run j = SMs [st[j], st[j+1]) (st[nr] := S) */
+    uint32_t nr, cur;
+    uint64_t I, M, K;
+};
+
 /* number of SMs: compile-time when FULL */
 template <int SMAX, bool FULL>
 __device__ __forceinline__ uint32_t nsm(const RkGTab& g) {
@@ -147,6 +161,15 @@ struct Rec {
 
 template <int SMAX, bool FULL>
 __device__ __forceinline__ void st_fresh(St<SMAX>& s, const RkGTab& g) {
+    if constexpr (SMAX == 0) {
+        s.nr = 1;
+        s.st[0] = 0;
+        s.fa[0] = g.freshA;
+        s.fb[0] = g.freshB;
+        s.cur = 0;
+        s.I = s.M = s.K = 0;
+        return;
+    } else {
 #pragma unroll
     for (int i = 0; i < SMAX; i++) {
         s.fa[i] = live_sm<SMAX, FULL>(i, g) ? g.freshA : 0u;
@@ -154,6 +177,7 @@ __device__ __forceinline__ void st_fresh(St<SMAX>& s, const RkGTab& g) {
     }
     s.cur = 0;
     s.I = s.M = s.K = 0;
+    }
 }
 
 /* Capacity of one SM for kernel k: min(floor(regs/dr), floor(shm/ds),
@@ -398,15 +422,138 @@ struct CapSumUpd { /* consume the new words: capacity sum for the next kernel */
     __device__ __forceinline__ void operator()(int, uint32_t a, uint32_t b) { F += cap1(a, b, k); }
 };
 
+/* ---- run-length state (SMAX == 0): the same dispatch rules (PAPER:69-81,
+ * readings L4/L5) as place_core, on runs of identical SMs ---- */
+__device__ __forceinline__ uint32_t rle_end(const St<0>& s, uint32_t j, uint32_t S) {
+    return j + 1 < s.nr ? s.st[j + 1] : S;
+}
+
+/* total capacity sum_s c_s of the state for kernel k */
+__device__ __forceinline__ uint32_t rle_capsum(const St<0>& s, const CapK& ck, uint32_t S) {
+    uint32_t F = 0;
+    for (uint32_t j = 0; j < s.nr; j++) F += (rle_end(s, j, S) - s.st[j]) * cap1(s.fa[j], s.fb[j], ck);
+    return F;
+}
+
+template <class R>
+__device__ void rle_place(const St<0>& in, St<0>& out, const RkKTab& k, uint32_t kid, const RkGTab& g, R& rec) {
+    const CapK ck = capk(k);
+    const uint32_t S = g.S;
+    uint32_t c[RK_RUNS];
+    uint32_t F = 0;
+    for (uint32_t j = 0; j < in.nr; j++) {
+        c[j] = cap1(in.fa[j], in.fb[j], ck);
+        F += (rle_end(in, j, S) - in.st[j]) * c[j];
+    }
+    uint32_t n = k.T;
+    if (n > F) { /* round closes; full rounds; fresh round from SM 0 */
+        rec.add(kid, F);
+        rec.close();
+        const uint32_t nfull = full_rounds(n - F - 1u, k);
+        rec.full(kid, nfull, k.SC);
+        const uint64_t K = in.K + round_key(in.I + (uint64_t)F * k.cA, in.M + (uint64_t)F * k.cM, g.num, g.den) +
+                           (uint64_t)nfull * k.fullkey;
+        n -= F + nfull * k.SC;
+        const uint32_t q = n / S, r = n - q * S;
+        out.st[0] = 0;
+        out.fa[0] = g.freshA - (q + (r ? 1u : 0u)) * k.dA;
+        out.fb[0] = g.freshB - (q + (r ? 1u : 0u)) * k.dB;
+        out.nr = 1;
+        if (r) {
+            out.st[1] = r;
+            out.fa[1] = g.freshA - q * k.dA;
+            out.fb[1] = g.freshB - q * k.dB;
+            out.nr = 2;
+        }
+        out.cur = r;
+        out.K = K;
+        out.I = (uint64_t)n * k.cA;
+        out.M = (uint64_t)n * k.cM;
+        rec.add(kid, n);
+        return;
+    }
+    const uint32_t cur = (g.flags & RK_FLAG_CURSOR_PER_KERNEL) ? 0u : in.cur;
+    /* tlo = max{t : f(t) < n}, f(t) = sum_runs len * min(c, t) */
+    uint32_t tlo = 0, flo = 0;
+    for (uint32_t b = g.tbits; b; b >>= 1) {
+        const uint32_t tt = tlo + b;
+        uint32_t f = 0;
+        for (uint32_t j = 0; j < in.nr; j++) f += (rle_end(in, j, S) - in.st[j]) * min(c[j], tt);
+        if (f < n) {
+            tlo = tt;
+            flo = f;
+        }
+    }
+    /* pass tlo+1: one more block to the first r eligible (c > tlo) SMs in ring
+     * order from the cursor; nc = the SM after the r-th one */
+    uint32_t need = n - flo;
+    uint32_t jc = 0;
+    for (uint32_t j = 1; j < in.nr; j++)
+        if (in.st[j] <= cur) jc = j;
+    uint32_t nc = cur;
+    for (uint32_t step = 0; step <= in.nr; step++) {
+        const uint32_t j = (jc + step) % in.nr;
+        const uint32_t lo = step == 0 ? cur : in.st[j];
+        const uint32_t hi = step == in.nr ? cur : rle_end(in, j, S);
+        if (c[j] > tlo && hi > lo) {
+            if (need <= hi - lo) {
+                nc = lo + need;
+                break;
+            }
+            need -= hi - lo;
+        }
+    }
+    if (nc >= S) nc -= S;
+    const uint32_t L = nc > cur ? nc - cur : nc + S - cur; /* ring interval [cur, cur+L) got pass tlo+1 */
+    St<0> o;
+    o.nr = 0;
+    for (uint32_t j = 0; j < in.nr; j++) {
+        const uint32_t lo = in.st[j], hi = rle_end(in, j, S);
+        uint32_t cut1 = (cur > lo && cur < hi) ? cur : hi, cut2 = (nc > lo && nc < hi) ? nc : hi;
+        if (cut2 < cut1) {
+            const uint32_t x = cut1;
+            cut1 = cut2;
+            cut2 = x;
+        }
+        const uint32_t base = min(c[j], tlo), elig = c[j] > tlo ? 1u : 0u;
+        const uint32_t ps[3] = {lo, cut1, cut2};
+        for (int q = 0; q < 3; q++) {
+            const uint32_t pstart = ps[q];
+            if (pstart >= hi || (q > 0 && pstart == ps[q - 1])) continue;
+            const uint32_t d = pstart >= cur ? pstart - cur : pstart + S - cur;
+            const uint32_t x = base + ((d < L) ? elig : 0u);
+            const uint32_t a = in.fa[j] - x * k.dA, b = in.fb[j] - x * k.dB;
+            if (o.nr && o.fa[o.nr - 1] == a && o.fb[o.nr - 1] == b) continue; /* merge equal neighbours */
+            if (o.nr < (uint32_t)RK_RUNS) {
+                o.st[o.nr] = pstart;
+                o.fa[o.nr] = a;
+                o.fb[o.nr] = b;
+                o.nr++;
+            }
+        }
+    }
+    o.cur = nc;
+    o.I = in.I + (uint64_t)n * k.cA;
+    o.M = in.M + (uint64_t)n * k.cM;
+    o.K = in.K;
+    rec.add(kid, n);
+    out = o;
+}
+
 template <int SMAX, bool FULL, class R>
 __device__ __forceinline__ void place(const St<SMAX>& in, St<SMAX>& out, const RkKTab& k, uint32_t kid,
                                       const RkGTab& g, R& rec) {
+    if constexpr (SMAX == 0) {
+        rle_place(in, out, k, kid, g, rec);
+        return;
+    } else {
     StoreUpd<SMAX> u{out};
     const Placed o = place_core<SMAX, FULL>(in, k, kid, g, rec, u);
     out.cur = o.cur;
     out.I = o.I;
     out.M = o.M;
     out.K = o.K;
+    }
 }
 
 /* The last kernel of an order: only its split into the open round and fresh
@@ -438,8 +585,12 @@ __device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, u
                                            R& rec) {
     const CapK ck = capk(k);
     uint32_t F = 0;
+    if constexpr (SMAX == 0) {
+        F = rle_capsum(s, ck, g.S);
+    } else {
 #pragma unroll
-    for (int i = 0; i < SMAX; i++) F += cap1(s.fa[i], s.fb[i], ck);
+        for (int i = 0; i < SMAX; i++) F += cap1(s.fa[i], s.fb[i], ck);
+    }
     return finish_key(F, s.I, s.M, s.K, k, kid, g, rec);
 }
 
@@ -448,9 +599,15 @@ template <int SMAX, bool FULL>
 __device__ __forceinline__ uint64_t place_finish(const St<SMAX>& in, const RkKTab& kb, uint32_t kbid,
                                                  const RkKTab& kc, uint32_t kcid, const RkGTab& g) {
     NoRec nr;
-    CapSumUpd u{capk(kc), 0u};
-    const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
-    return finish_key(u.F, o.I, o.M, o.K, kc, kcid, g, nr);
+    if constexpr (SMAX == 0) {
+        St<0> s1;
+        rle_place(in, s1, kb, kbid, g, nr);
+        return finish<0>(s1, kc, kcid, g, nr);
+    } else {
+        CapSumUpd u{capk(kc), 0u};
+        const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
+        return finish_key(u.F, o.I, o.M, o.K, kc, kcid, g, nr);
+    }
 }
 
 /* Nibble list of unused kernels, ascending: remove and return entry d. */
@@ -617,7 +774,7 @@ __device__ void commit(const rk_stats& cta, rk_stats* recs, uint32_t* counter, r
 #endif
 template <int SMAX>
 struct Depth {
-    static constexpr int value = SMAX <= 2 ? RK_DEPTH_SMALL : (SMAX <= 8 ? 4 : RK_DEPTH_LARGE);
+    static constexpr int value = SMAX == 0 ? RK_DEPTH_LARGE : (SMAX <= 2 ? RK_DEPTH_SMALL : (SMAX <= 8 ? 4 : RK_DEPTH_LARGE));
 };
 __host__ __device__ constexpr uint32_t cfact(int m) { return m <= 1 ? 1u : (uint32_t)m * cfact(m - 1); }
 
@@ -809,7 +966,7 @@ struct MinBlocks {
 #ifdef RK_EVAL_MIN_BLOCKS
     static constexpr int value = RK_EVAL_MIN_BLOCKS;
 #else
-    static constexpr int value = SMAX <= 4 ? 2 : 1;
+    static constexpr int value = (SMAX >= 1 && SMAX <= 4) ? 2 : 1;
 #endif
 };
 
@@ -1359,7 +1516,8 @@ int variant(uint32_t S) {
     if (S < 16) return 6;
     if (S == 16) return 7;
     if (S < 32) return 8;
-    return 9;
+    if (S == 32) return 9;
+    return 10; /* run-length state */
 }
 
 } /* namespace */
@@ -1377,14 +1535,16 @@ int variant(uint32_t S) {
             case 6: KERNEL<16, false><<<CFG>>>(__VA_ARGS__); break;           \
             case 7: KERNEL<16, true><<<CFG>>>(__VA_ARGS__); break;            \
             case 8: KERNEL<32, false><<<CFG>>>(__VA_ARGS__); break;           \
-            default: KERNEL<32, true><<<CFG>>>(__VA_ARGS__); break;           \
+            case 9: KERNEL<32, true><<<CFG>>>(__VA_ARGS__); break;            \
+            default: KERNEL<0, false><<<CFG>>>(__VA_ARGS__); break;           \
         }                                                                     \
     } while (0)
 /* generic (runtime-S) variant for the single-thread helpers */
 #define RK_DISPATCH_GENERIC(S, KERNEL, CFG, ...)                              \
     do {                                                                      \
         if ((S) <= 16) KERNEL<16, false><<<CFG>>>(__VA_ARGS__);               \
-        else KERNEL<32, false><<<CFG>>>(__VA_ARGS__);                         \
+        else if ((S) <= 32) KERNEL<32, false><<<CFG>>>(__VA_ARGS__);          \
+        else KERNEL<0, false><<<CFG>>>(__VA_ARGS__);                          \
     } while (0)
 #define RK_CFG(...) __VA_ARGS__
 
@@ -1400,7 +1560,8 @@ int rk_eval_max_ctas(uint32_t S, int) {
         case 6: per = eval_ctas_per_sm<16, false>(); break;
         case 7: per = eval_ctas_per_sm<16, true>(); break;
         case 8: per = eval_ctas_per_sm<32, false>(); break;
-        default: per = eval_ctas_per_sm<32, true>(); break;
+        case 9: per = eval_ctas_per_sm<32, true>(); break;
+        default: per = eval_ctas_per_sm<0, false>(); break;
     }
     return per * num_sms();
 }
@@ -1433,6 +1594,7 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
             cudaFuncSetAttribute(rk_eval_x_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             cudaFuncSetAttribute(rk_eval_x_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             cudaFuncSetAttribute(rk_eval_x_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(rk_eval_x_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         }
         RK_DISPATCH(S, rk_eval_x_kernel, RK_CFG((unsigned)ctas, kThreads, smem, st), tab_dev, first, count,
                     cand_key_dev, cand_key_imm, stats_dev, keys_dev, recs, counter, keys32_dev, key_base, ovf_dev,

@@ -19,6 +19,13 @@ MASK64 = (1 << 64) - 1
 #: N_shm_SM=48K, N_blk_SM=8").  R_B = 411/100 exactly (reading L10).
 GTX580 = (16, 32768, 49152, 48, 8, 411, 100)
 
+#: B200 preset (not a paper configuration): 148 SMs, 64K
+#: registers, 228 KB shared memory, 64 warps and 32 blocks per SM.  R_B follows
+#: the paper's GTX580 figure, which is CUDA cores x clock / DRAM bandwidth
+#: (512 x 1.544 GHz / 192.4 GB/s = 4.11): 148 x 128 x 1.965 GHz /
+#: 8.0 TB/s = 4.65 (reading L21).
+B200 = (148, 65536, 233472, 64, 32, 465, 100)
+
 SEED_BASE = 0x0151107983000000
 
 
@@ -107,6 +114,33 @@ def gen_g(rng: SplitMix64, n: int, gpu=GTX580):
             return ks
 
 
+GRID_B200 = (100, 128, 200, 256, 300, 444, 512, 600, 1000, 1024)
+RPT_B200 = (16, 24, 32, 40, 48, 64, 96, 128, 168, 255)
+SHM_B200 = (4096, 8192, 16384, 32768, 49152, 65536, 102400, 163840, 232448)
+
+
+def gen_b200(rng: SplitMix64, n: int, gpu=B200):
+    """Generator G scaled to the B200 preset: grids of 100-1024 blocks (so
+    gcd(148, grids) is small and the reduced SM count stays > 32), up to 255
+    registers/thread and 227 KB shared memory/block; classes alternate."""
+    while True:
+        ks = []
+        for i in range(n):
+            while True:
+                tpb = rng.weighted(TPB, TPB_W)
+                rpt = rng.choice(RPT_B200)
+                shm = 0 if rng.below(10) < 4 else rng.choice(SHM_B200)
+                grid = rng.choice(GRID_B200)
+                rn = rng.choice(RN_MEM if i % 2 == 0 else RN_CMP)
+                a, m = _ratio_work(rng, rn, tpb)
+                k = (grid, tpb, rpt, shm, a, m)
+                if feasible(gpu, k):
+                    break
+            ks.append(k)
+        if key_bound(gpu, ks) < (1 << 63):
+            return ks
+
+
 def gen_c3(rng: SplitMix64, n: int = 10, gpu=GTX580):
     """C3: shm- and register-limited packing (1-3 blocks/SM by regs or shm)."""
     ks = []
@@ -152,7 +186,8 @@ def gen_c2(rng: SplitMix64):
 
 
 def config(name: str):
-    """Return (gpu, kernels) for configs C1..C4 (BASELINE.json `configs`)."""
+    """Return (gpu, kernels) for configs C1..C4 (BASELINE.json `configs`) and C6
+    (the B200 preset)."""
     if name == "C1":
         return GTX580, list(W4)
     if name == "C2":
@@ -161,6 +196,8 @@ def config(name: str):
         return GTX580, gen_c3(SplitMix64(SEED_BASE + 3))
     if name == "C4":
         return GTX580, gen_g(SplitMix64(SEED_BASE + 4), 12)
+    if name == "C6":  # B200 preset (f3), same n as C4
+        return B200, gen_b200(SplitMix64(SEED_BASE + 6), 12)
     raise KeyError(name)
 
 

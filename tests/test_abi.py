@@ -109,10 +109,14 @@ def test_bad_gpu_params():
     with pytest.raises(rk.RkError) as e:
         c.rk_set_gpu_params((0, 32768, 49152, 48, 8, 411, 100))
     assert e.value.status == rk.RK_EINVAL
-    # 33 SMs: gcd(33, grids 32/16) = 1 -> 33 super-SMs > 32 on the device fast path
+    # 33 SMs: gcd(33, grids 32/16) = 1 -> 33 super-SMs: run-length state, accepted
     c.rk_set_gpu_params((33, 32768, 49152, 48, 8, 411, 100))
+    c.rk_set_kernels(W.W4)
+    # the B200 preset (148 SMs) is accepted; more than 65535 SMs is not
+    c.rk_set_gpu_params(W.B200)
+    c.rk_set_kernels(W.config("C6")[1])
     with pytest.raises(rk.RkError) as e:
-        c.rk_set_kernels(W.W4)
+        c.rk_set_gpu_params((65536, 32768, 49152, 48, 8, 411, 100))
     assert e.value.status == rk.RK_EUNSUPPORTED
     # 48 SMs with grids that are multiples of 16: reduced to 3 super-SMs, accepted
     c.rk_set_gpu_params((48, 32768, 49152, 48, 8, 411, 100))

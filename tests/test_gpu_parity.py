@@ -677,3 +677,96 @@ def test_branch_and_bound_n13_vs_full_device_sweep(ctx):
     _, _, hidx, _ = ctx.rk_heuristic_order()
     nodes = _check_best(ctx, gpu, ks, st.key_min, st.argmin, seeds=(None, hidx))
     assert nodes < 13 * N
+
+
+# ---- run-length SM state (S' > 32, e.g. the 148-SM B200 preset) ----
+BIG_GPUS = [W.B200, (33, 32768, 49152, 48, 8, 411, 100), (40, 65536, 102400, 64, 16, 7, 2),
+            (148, 65536, 233472, 64, 32, 1, 1), (1000, 32768, 49152, 48, 8, 411, 100)]
+
+
+@pytest.mark.parametrize("gi", range(len(BIG_GPUS)))
+def test_runs_state_random_sets_vs_oracle(ctx, gi):
+    gpu = BIG_GPUS[gi]
+    rng = W.SplitMix64(0x5EED + gi)
+    done = 0
+    sets = [W.gen_b200(rng, 2 + q % 6, gpu=gpu) for q in range(10)] if gpu[0] >= 148 and gpu[3] >= 64 else \
+        W.random_small_sets(0x5EED + gi, 12, 2, 7, gpu=gpu)
+    for ks in sets:
+        if not all(W.feasible(gpu, k) for k in ks):
+            continue
+        ctx.rk_set_gpu_params(gpu)
+        ctx.rk_set_kernels(ks)
+        check_full_space(ctx, gpu, ks, bins=(5,))
+        o = O.unrank(len(ks) // 2, len(ks))
+        r = O.simulate(gpu, ks, o)
+        assert ctx.rk_simulate_order(o) == (r.rounds, r.key)
+        done += 1
+    assert done >= 5
+
+
+def test_runs_state_c6_b200_preset(ctx):
+    """C6 = the B200 preset with 12 generator kernels (S' = 37 super-SMs): the full
+    device sweep's extremes and 2000 sampled keys re-simulated by the oracle, and
+    the branch-and-bound optimum agrees with the sweep."""
+    gpu, ks = W.config("C6")
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(12)
+    keys = torch.zeros(N, dtype=torch.int64, device="cuda")
+    st = ctx.rk_eval_range(0, N, 0, keys_dev=keys)
+    assert st.evaluated == N
+    assert O.simulate(gpu, ks, O.unrank(st.argmin, 12)).key == st.key_min
+    assert O.simulate(gpu, ks, O.unrank(st.argmax, 12)).key == st.key_max
+    rng = np.random.default_rng(6)
+    idx = rng.integers(0, N, 2000)
+    got = keys[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint64)
+    for i, k in zip(idx.tolist(), got.tolist()):
+        assert k == O.simulate(gpu, ks, O.unrank(i, 12)).key, i
+    _, _, hidx, _ = ctx.rk_heuristic_order()
+    _check_best(ctx, gpu, ks, st.key_min, st.argmin, seeds=(hidx,))
+
+
+def test_forced_runs_state_equals_register_state(monkeypatch):
+    """RK_FORCE_RUNS=1 routes every S through the run-length state: same keys,
+    partitions, statistics and optimum as the oracle on C2/C3 (S' = 1) and on
+    random shapes with S' in 2..32."""
+    monkeypatch.setenv("RK_FORCE_RUNS", "1")
+    c = rk.Context(0)
+    try:
+        for name in ("C2", "C3"):
+            gpu, ks = W.config(name)
+            g = _gold(f"{name.lower()}_oracle.json")
+            c.rk_set_gpu_params(gpu)
+            c.rk_set_kernels(ks)
+            st = c.rk_eval_range(0, math.factorial(len(ks)), g["cand_key"])
+            assert list(st.as_tuple()) == [g["stats"][f] for f in
+                                           ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt",
+                                            "evaluated")]
+            _check_best(c, gpu, ks, g["stats"]["key_min"], g["stats"]["argmin"])
+        for gpu in GPUS:
+            for ks in W.random_small_sets(0xF0 + gpu[0], 4, 3, 7, gpu=gpu):
+                if not all(W.feasible(gpu, k) for k in ks):
+                    continue
+                try:
+                    c.rk_set_gpu_params(gpu)
+                    c.rk_set_kernels(ks)
+                except rk.RkError as e:
+                    assert e.status == rk.RK_EUNSUPPORTED
+                    continue
+                check_full_space(c, gpu, ks, bins=(3,))
+                for q in range(3):
+                    o = O.unrank(q * 7 % math.factorial(len(ks)), len(ks))
+                    r = O.simulate(gpu, ks, o)
+                    assert c.rk_simulate_order(o) == (r.rounds, r.key)
+        # cursor-per-kernel reading through the run-length state
+        gpu, ks = W.config("C2")
+        check_full_space(c, list(gpu) + [1], ks, bins=(16,))
+        # batch path (C5 subset) through the run-length state
+        g5 = _gold("c5_oracle.json")
+        sets = W.c5_sets(64)
+        c.rk_set_gpu_params(W.GTX580)
+        res = c.rk_eval_batch(sets, [s["cand_index"] for s in g5["sets"][:64]])
+        for q in range(64):
+            assert list(res[q][0].as_tuple()) == g5["sets"][q]["stats"] and res[q][1] == g5["sets"][q]["cand_key"]
+    finally:
+        c.close()
