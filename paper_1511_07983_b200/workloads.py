@@ -23,7 +23,7 @@ GTX580 = (16, 32768, 49152, 48, 8, 411, 100)
 #: registers, 228 KB shared memory, 64 warps and 32 blocks per SM.  R_B follows
 #: the paper's GTX580 figure, which is CUDA cores x clock / DRAM bandwidth
 #: (512 x 1.544 GHz / 192.4 GB/s = 4.11): 148 x 128 x 1.965 GHz /
-#: 8.0 TB/s = 4.65 (reading L21).
+#: 8.0 TB/s = 4.65 (reading L24).
 B200 = (148, 65536, 233472, 64, 32, 465, 100)
 
 SEED_BASE = 0x0151107983000000
