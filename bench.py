@@ -7,9 +7,11 @@ Workload (BASELINE.json configs[3]): config C4 — 12 kernels fro
 Generator G (seed 0x0151107983000004) on the GTX580 model parameters, the full
 12! = 479,001,600 launch-order space.  One step = one pass of the whole hot
 path: Algorithm 1 candidate (host) + its key
-(device), unrank/pack/score/reduce over the rank's index shard with keys kept
-in HBM, [N>1: NCCL all_gather of the 64-B records + device merge], the exact
-256-bin histogram over the global [min,max], [N>1: NCCL all_reduce].  Total
+(device); pass 1 = the memo tables (deduplicated prefix states, suffix keys;
+DESIGN.md §5) rebuilt from scratch + the extremes of the rank's index shard;
+[N>1: NCCL all_gather of the 64-B records + device merge]; pass 2 = every
+exact key to HBM, the counts against the candidate and the exact 256-bin
+histogram over the global [min,max]; [N>1: NCCL all_reduce + record merge].  Total
 work per step is fixed (12!), shards are contiguous index ranges: strong
 scaling.  For N>1 launch with torchrun (one rank per GPU).
 
@@ -128,10 +130,10 @@ def oracle_rate(gpu, kernels, seconds: float, threads: int, first: int):
     return count / dt, count, dt
 
 
-def read_profile(kernel_sub: str = "rk_eval_kernel"):
+def read_profile(kernel_sub: str = "rk_eval_kernel", name: str = "r01_ncu_full_eval_hist.json"):
     """The committed `ncu --set full` summary of the same kernel (profiles/), if any:
     (dram read+write bytes per launch, issue-active %, thread instructions/launch)."""
-    fn = os.path.join(ROOT, "profiles", "r01_ncu_full_eval_hist.json")
+    fn = os.path.join(ROOT, "profiles", name)
     try:
         with open(fn) as f:
             for e in json.load(f):
@@ -141,6 +143,14 @@ def read_profile(kernel_sub: str = "rk_eval_kernel"):
     except (OSError, ValueError, KeyError, TypeError):
         pass
     return None, None, None, None
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 def run_reference(args):
@@ -249,6 +259,7 @@ def main():
     eval_ms = statistics.mean(a.elapsed_time(b) for a, b in events["eval"])
     eval_ms_max = max_over_ranks(eval_ms, sw.dev)
     hist_ms = statistics.mean(a.elapsed_time(b) for a, b in events["hist"])
+    hist_ms_max = max_over_ranks(hist_ms, sw.dev)
     assert not sw.overflowed(), "compact keys overflowed (re-run with u64 keys)"
 
     # correctness of the timed pipeline's result (global record, histogram mass)
@@ -273,13 +284,13 @@ def main():
     e2e_ms = max_over_ranks(a.elapsed_time(b), sw.dev)
     e2e_value = N * e2e_steps / (e2e_ms / 1e3)
 
-    # the same eval kernel without the SM-symmetry reduction, for reference
-    noreduce_ms = None
-    if args.no_reduce_check:
-        os.environ["RK_NO_REDUCE"] = "1"
+    # the same evaluation (stats + keys) with a switch off, for reference: without
+    # the SM-symmetry reduction, and without suffix memoisation (direct kernel)
+    def variant_ms(env):
+        os.environ[env] = "1"
         from paper_1511_07983_b200 import rk as _rk
         c2 = _rk.Context(local)
-        del os.environ["RK_NO_REDUCE"]
+        del os.environ[env]
         c2.rk_set_gpu_params(gpu)
         c2.rk_set_kernels(ks)
         rec2 = torch.zeros(8, dtype=torch.int64, device=sw.dev)
@@ -292,9 +303,16 @@ def main():
             c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, sw.keys, stream)
         b.record(stream)
         torch.cuda.synchronize()
-        noreduce_ms = max_over_ranks(a.elapsed_time(b) / 3, sw.dev)
+        r = max_over_ranks(a.elapsed_time(b) / 3, sw.dev)
         assert torch.equal(rec2, sw.glob if world > 1 else sw.rec) or world > 1
         c2.close()
+        return r
+
+    noreduce_ms = direct_ms = None
+    if args.no_reduce_check:
+        noreduce_ms = variant_ms("RK_NO_REDUCE")
+        direct_ms = variant_ms("RK_NO_MEMO")
+    memo_on, memo_levels, memo_nodes = sw.ctx.rk_memo_info()
 
     clocks = clk.summary()
     if world > 1:
@@ -304,31 +322,57 @@ def main():
         sym_g = reduce(math.gcd, [gpu[0]] + [k[0] for k in ks])
         ops = algorithmic_ops_per_order(ks)
         per_launch_orders = sw.count
-        achieved = ops * per_launch_orders / (eval_ms_max / 1e3)
-        peak = int_issue_peak_ops(1965.0)
-        traffic, issue_pct, thread_insts, kname = read_profile()
-        roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
-                    "frac": achieved / peak, "traffic": traffic,
-                    "kernel": kname or "rk_eval_kernel", "kernel_ms": eval_ms_max,
-                    "ops_per_order": ops, "orders_per_launch": per_launch_orders,
-                    "peak_basis": "148 SM x 4 SMSP x 32 lanes x 1965 MHz (integer issue, DESIGN.md §6)",
-                    "ncu_issue_active_pct": issue_pct,
-                    "executed_thread_insts_per_order": (thread_insts / N) if thread_insts else None,
-                    "note": ("achieved counts SURVEY §8(d) block-level work W per order; the kernel issues "
-                             "fewer instructions per order (closed-form water-fill, symmetry reduction, "
-                             "prefix sharing), so frac > 1; hardware utilisation = ncu_issue_active_pct")}
+        if memo_on:
+            # pass 2 (keys + counts + histogram) dominates: HBM-bound on the key stream
+            peaks = read_peaks()
+            bytes_launch = 8 * per_launch_orders
+            achieved = bytes_launch / (hist_ms_max / 1e3)
+            peak = peaks.get("hbm_gbs", 7700.0) * 1e9
+            traffic, issue_pct, _, kname = read_profile("rk_dp_keys_kernel", "r01_ncu_full_memo.json")
+            roofline = {"bound": "hbm", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": traffic,
+                        "kernel": kname or "rk_dp_keys_kernel<true>", "kernel_ms": hist_ms_max,
+                        "bytes_per_order": 8, "orders_per_launch": per_launch_orders,
+                        "peak_basis": ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if "hbm_gbs" in peaks
+                                       else "B200_PROFILING fallback 7.7 TB/s"),
+                        "ncu_issue_active_pct": issue_pct,
+                        "note": ("algorithmic bytes = the 8-B exact key of every order written to HBM; the "
+                                 "suffix rows it adds to are L2-resident (DESIGN.md §5-6)")}
+        else:
+            achieved = ops * per_launch_orders / (eval_ms_max / 1e3)
+            peak = int_issue_peak_ops(1965.0)
+            traffic, issue_pct, thread_insts, kname = read_profile()
+            roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
+                        "frac": achieved / peak, "traffic": traffic,
+                        "kernel": kname or "rk_eval_kernel", "kernel_ms": eval_ms_max,
+                        "ops_per_order": ops, "orders_per_launch": per_launch_orders,
+                        "peak_basis": "148 SM x 4 SMSP x 32 lanes x 1965 MHz (integer issue, DESIGN.md §6)",
+                        "ncu_issue_active_pct": issue_pct,
+                        "executed_thread_insts_per_order": (thread_insts / N) if thread_insts else None,
+                        "note": ("achieved counts SURVEY §8(d) block-level work W per order; the kernel issues "
+                                 "fewer instructions per order (closed-form water-fill, symmetry reduction, "
+                                 "prefix sharing), so frac > 1; hardware utilisation = ncu_issue_active_pct")}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "n": len(ks), "orders": N, "bins": args.bins,
                            "shards": world, "parallelism": f"index-space shards x{world}",
                            "keys": "u64 exact keys in HBM (8 B/order)",
-                           "l2": "keys array 8 B/order (3.83 GB at N=1) > 126 MB L2; eval phase reads no HBM input"},
+                           "l2": ("keys array 8 B/order (3.83 GB at N=1) > 126 MB L2, written once per step; "
+                                  "memo tables (suffix rows 41 MB) L2-resident")},
                 "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
-                "kernels_ms": {"rk_eval_kernel": eval_ms_max, "rk_hist_kernel": hist_ms,
-                               "step": ms_max / args.steps},
+                "kernels_ms": ({"pass1_memo_tables_and_extremes": eval_ms_max,
+                                "pass2_keys_counts_histogram": hist_ms, "step": ms_max / args.steps}
+                               if memo_on else
+                               {"rk_eval_kernel": eval_ms_max, "rk_hist_kernel": hist_ms,
+                                "step": ms_max / args.steps}),
+                "memo": {"on": memo_on, "prefix_levels": memo_levels, "nodes_per_level": memo_nodes,
+                         "suffix_depth": 5, "runs": N // 120,
+                         "direct_eval_ms": direct_ms,
+                         "note": ("keys = K(prefix) + f(state, suffix) over deduplicated prefix states; "
+                                  "exact (DESIGN.md §5); direct_eval_ms = stats+keys without memoisation")},
                 "symmetry": {"g": sym_g, "super_sms": gpu[0] // sym_g,
-                             "eval_ms_without_reduction": noreduce_ms,
+                             "eval_ms_without_reduction": noreduce_ms,  # stats + keys, memoised if planned
                              "note": "gcd(N_SM, grids) SMs act as one super-SM; exact (DESIGN.md §5)"},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sw.h2d_bytes,
                         "d2h_bytes_per_step": sw.d2h_bytes, "steps": e2e_steps},

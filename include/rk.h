@@ -232,6 +232,36 @@ rk_status rk_eval_batch(rk_ctx* ctx, const rk_kernel* sets, uint32_t n, uint32_t
 rk_status rk_simulate_order(rk_ctx* ctx, const int32_t* order, uint32_t* rounds_out, uint32_t max_rounds,
                             uint32_t* n_rounds_out, uint64_t* key_out);
 
+/* The step of the hot path in two passes, so that N ranks can agree on the
+ * histogram range in between.  When the context's
+ * suffix memoisation is on (rk_memo_info) pass 1 evaluates the
+ * extremes of [first, first+count) from the memo tables it rebuilds, and pass 2
+ * writes every key and the counts; otherwise pass 1 is rk_eval_range_async
+ * (keys written) and pass 2 only bins the stored keys.  Either way, after both:
+ * rec_dev (64 B, device) holds the range's complete rk_stats, keys_dev
+ * (u64[count], device, nullable) every key index-major, hist_dev (u64[bins],
+ * device, zeroed by the caller, accumulated) the Fig. 1 histogram over
+ * [range_dev->key_min, range_dev->key_max] (range_dev = this
+ * rec_dev for one rank, the merged record of all ranks otherwise).
+ * Pass 1: rec_dev = {key_min, key_max, argmin, argmax, n_lt, n_eq, n_gt,
+ * evaluated}, where memoised passes leave n_lt = n_eq = 0, n_gt = count.
+ * Pass 2: adds the memoised counts (n_lt, n_eq += ..., n_gt -= ...) to rec_dev.
+ * Errors: RK_EINVAL (range, missing pointers; more than 32768 bins without
+ * keys_dev), RK_ESTATE, RK_ENODEVICE, RK_ECUDA. */
+rk_status rk_sweep_pass1_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                               rk_stats* rec_dev, uint64_t* keys_dev, void* stream);
+rk_status rk_sweep_pass2_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                               const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev,
+                               rk_stats* rec_dev, void* stream);
+
+/* Suffix memoisation of the current kernel set: on_out = 1 when
+ * the device path evaluates orders as K(prefix) + f(state, suffix) from
+ * deduplicated prefix states (planned at rk_set_kernels; off for n < 6, for
+ * more than 32 super-SMs, with RK_NO_MEMO=1, or when it would not pay).
+ * levels_out = P (prefix length); nodes_out[j] (j <= P, up to max_levels) =
+ * distinct (remaining set, state) pairs after j kernels. */
+rk_status rk_memo_info(rk_ctx* ctx, uint32_t* on_out, uint32_t* levels_out, uint32_t* nodes_out, uint32_t max_levels);
+
 /* Exact optimum by branch and bound (the same (key_min,
  * argmin) as a full rk_eval_range over [0, n!) — SPEC:300, ties -> smallest
  * index — without enumerating n!).  Bound of a prefix (PAPER:79-81 round

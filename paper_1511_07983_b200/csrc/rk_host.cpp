@@ -20,6 +20,50 @@
 #include "rk_internal.h"
 
 typedef unsigned __int128 u128;
+constexpr uint32_t kSmemBinsHost = 32768; /* fused-histogram bins held in shared memory */
+
+/* Device buffer that only grows (memo arenas are reused across kernel sets). */
+struct Arena {
+    void* p = nullptr;
+    size_t cap = 0;
+    /* ensure >= bytes; keep the first `keep` bytes of the contents */
+    int reserve(size_t bytes, size_t keep = 0) {
+        if (bytes <= cap) return 0;
+        size_t want = std::max(bytes, cap + cap / 2);
+        void* q = nullptr;
+        int e = cudaMalloc(&q, want);
+        if (e) return e;
+        if (keep && p) e = cudaMemcpy(q, p, std::min(keep, cap), cudaMemcpyDeviceToDevice);
+        cudaFree(p);
+        p = q;
+        cap = want;
+        return e;
+    }
+    void release() {
+        cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+/* Suffix-memoisation plan: per-level capacities found once per
+ * kernel set (sizes only; every step rebuilds all tables).  Level j+1 holds at
+ * most cnt[j] * (n - j) nodes; the planning build measures cnt[j+1] exactly. */
+struct DpPlan {
+    bool on = false;
+    uint32_t P = 0;
+    uint32_t node_bytes = 0;
+    std::vector<uint32_t> cnt;    /* distinct nodes per level 0..P (cnt[0] = 1) */
+    std::vector<uint32_t> cap;    /* node capacity of level j (j >= 1) */
+    std::vector<size_t> noff;     /* node byte offset of level j (j >= 1) */
+    std::vector<size_t> toff;     /* hash-table slot offset of level j (j >= 1) */
+    std::vector<uint32_t> tmask;  /* slots - 1 of level j */
+    std::vector<size_t> xoff;     /* transition offset of level j (j < P): cnt[j] * n entries */
+    size_t table_slots = 0;
+    Arena nodes, tables, tid, dk, fst, counters; /* counters: P + 1 node counters, then the overflow flag */
+    Arena code, dvc, dvo, nd;                    /* suffix rows: byte codes into sorted distinct (value, count) */
+    DPView view{};
+};
 
 struct rk_ctx {
     int device = -1;
@@ -37,6 +81,9 @@ struct rk_ctx {
     uint32_t launches = 0;
     bool no_reduce = false; /* RK_NO_REDUCE=1: disable the symmetry reduction (testing) */
     bool force_runs = false; /* RK_FORCE_RUNS=1: run-length SM state for every S (testing) */
+    bool no_memo = false;    /* RK_NO_MEMO=1: direct evaluation of every order (testing) */
+    bool force_memo = false; /* RK_FORCE_MEMO=1: memoise even where it does not pay (testing) */
+    DpPlan dp;
 };
 
 /* SM count that selects the kernel variant (the table keeps the real S) */
@@ -401,6 +448,167 @@ rk_status need_kernels(rk_ctx* c) {
 
 uint64_t space(const rk_ctx* c) { return fact64((uint32_t)c->ks.size()); }
 
+void dp_free(DpPlan& d) {
+    d.nodes.release();
+    d.tables.release();
+    d.tid.release();
+    d.dk.release();
+    d.fst.release();
+    d.counters.release();
+    for (Arena* a : {&d.code, &d.dvc, &d.dvo, &d.nd}) a->release();
+    d.on = false;
+}
+
+uint32_t pow2_at_least(uint64_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+/* Enqueue levels j0..j1-1 of the plan's table build (level j reads level j's
+ * nodes and count, writes level j+1). */
+int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream) {
+    DpPlan& d = c->dp;
+    const uint32_t n = c->tab.g.n, S = c->tab.g.S;
+    char* nodes = (char*)d.nodes.p;
+    uint32_t* ctr = (uint32_t*)d.counters.p;
+    int e = 0;
+    for (uint32_t j = j0; j < j1 && !e; j++) {
+        const void* Uj = j ? nodes + d.noff[j] : nullptr;
+        e = rk_dp_level(c->tab_dev, S, Uj, j ? ctr + j : nullptr, nodes + d.noff[j + 1], ctr + j + 1, d.cap[j + 1],
+                        (uint32_t*)d.tables.p + d.toff[j + 1], d.tmask[j + 1], (uint32_t*)d.tid.p + d.xoff[j],
+                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.P + 1, (uint64_t)d.cnt[j] * n, stream, &c->launches);
+    }
+    return e;
+}
+
+/* Enqueue the table build of the current plan: clear, P levels, suffix tables. */
+int dp_build(rk_ctx* c, void* stream) {
+    DpPlan& d = c->dp;
+    cudaStream_t st = (cudaStream_t)stream;
+    int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
+    if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.P + 2) * 4, st);
+    if (!e) e = dp_levels(c, 0, d.P, stream);
+    if (!e)
+        e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
+                         (uint8_t*)d.code.p, d.dvc.p, (uint32_t*)d.dvo.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
+                         d.cnt[d.P], stream, &c->launches);
+    return e;
+}
+
+/* Find the exact per-level node counts (one synchronous level-by-level build;
+ * capacities from the previous level's exact count), keeping that layout.  Off
+ * (direct evaluation) for the run-length state, n < 6, or when it would not
+ * pay.  Buffers are grow-only arenas: no allocation once they are large enough. */
+rk_status dp_plan(rk_ctx* c) {
+    DpPlan& d = c->dp;
+    d.on = false;
+    const uint32_t n = c->tab.g.n, S = c->tab.g.S;
+    if (c->device < 0 || c->no_memo || c->force_runs || S > RK_SMAX || n < RK_DP_D + 1) return RK_OK;
+    const uint64_t kLimitEntries = 1ull << 26, kLimitBytes = 1ull << 31;
+    d.P = n - RK_DP_D;
+    d.node_bytes = rk_dp_node_bytes(S);
+    d.cnt.assign(d.P + 1, 0);
+    d.cap.assign(d.P + 1, 0);
+    d.noff.assign(d.P + 1, 0);
+    d.toff.assign(d.P + 1, 0);
+    d.tmask.assign(d.P + 1, 0);
+    d.xoff.assign(d.P + 1, 0);
+    d.cnt[0] = 1;
+    d.view = DPView{};
+    int e = d.counters.reserve(64 * 4);
+    if (!e) e = cudaMemset(d.counters.p, 0, 64 * 4);
+    size_t nb = 0, ts = 0, xs = 0;
+    for (uint32_t j = 0; j < d.P && !e; j++) {
+        const uint64_t m = d.cnt[j], work = m * n, capn = m * (n - j);
+        const uint64_t slots = pow2_at_least(2 * capn);
+        if (work > kLimitEntries || capn * d.node_bytes > kLimitBytes || slots > kLimitEntries) return RK_OK;
+        d.xoff[j] = xs;
+        xs += work;
+        d.noff[j + 1] = nb;
+        d.cap[j + 1] = (uint32_t)capn;
+        nb = (nb + capn * d.node_bytes + 255) & ~(size_t)255;
+        d.toff[j + 1] = ts;
+        d.tmask[j + 1] = (uint32_t)(slots - 1);
+        ts += slots;
+        e = d.nodes.reserve(nb, d.noff[j + 1]);
+        if (!e) e = d.tables.reserve(ts * 4);
+        if (!e) e = d.tid.reserve(xs * 4, d.xoff[j] * 4);
+        if (!e) e = d.dk.reserve(xs * 8, d.xoff[j] * 8);
+        if (!e) e = cudaMemset((uint32_t*)d.tables.p + d.toff[j + 1], 0xFF, slots * 4);
+        if (!e) e = dp_levels(c, j, j + 1, nullptr);
+        uint32_t h[2] = {0, 0}; /* level j+1 count; the overflow flag lives at P+1 */
+        if (!e) e = cudaMemcpy(&h[0], (uint32_t*)d.counters.p + j + 1, 4, cudaMemcpyDeviceToHost);
+        if (!e) e = cudaMemcpy(&h[1], (uint32_t*)d.counters.p + d.P + 1, 4, cudaMemcpyDeviceToHost);
+        if (e) break;
+        if (h[0] > capn || h[1]) return RK_OK; /* cannot happen: capacity is an upper bound */
+        d.cnt[j + 1] = h[0];
+    }
+    d.table_slots = ts;
+    if (e) {
+        cudaGetLastError();
+        return cuda_fail(c, e, "memoisation plan");
+    }
+    const uint64_t runs = fact64(n) / fact64(RK_DP_D), uP = d.cnt[d.P];
+    const uint64_t DF = fact64(RK_DP_D);
+    if (uP * DF * 8 > kLimitBytes) return RK_OK;
+    if (uP * 4 > runs && !c->force_memo) return RK_OK; /* does not pay */
+    e = d.code.reserve(uP * DF);
+    if (!e) e = d.dvc.reserve(uP * DF * 16);
+    if (!e) e = d.dvo.reserve(uP * DF * 4);
+    if (!e) e = d.nd.reserve(uP * 4);
+    if (!e) e = d.fst.reserve(uP * 4 * 8);
+    if (e) {
+        cudaGetLastError();
+        return cuda_fail(c, e, "memoisation buffers");
+    }
+    for (uint32_t j = 0; j < d.P; j++) {
+        d.view.tid[j] = (const uint32_t*)d.tid.p + d.xoff[j];
+        d.view.dk[j] = (const uint64_t*)d.dk.p + d.xoff[j];
+    }
+    d.view.code = (const uint8_t*)d.code.p;
+    d.view.dvc = d.dvc.p;
+    d.view.dvo = (const uint32_t*)d.dvo.p;
+    d.view.nd = (const uint32_t*)d.nd.p;
+    d.view.fst = (const uint64_t*)d.fst.p;
+    d.view.P = d.P;
+    d.view.D = RK_DP_D;
+    d.view.Dfact = (uint32_t)DF;
+    d.on = true;
+    return RK_OK;
+}
+
+/* the candidate key pointer, or a device zero (no candidate: every key counts as n_gt) */
+const uint64_t* cand_or_zero(rk_ctx* c, const uint64_t* cand_dev, void* stream) {
+    if (cand_dev) return cand_dev;
+    cudaMemsetAsync(c->u64_dev + 9, 0, 8, (cudaStream_t)stream);
+    return c->u64_dev + 9;
+}
+
+/* Pass 1 of the memoised path: tables + extremes of [first, first+count). */
+int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void* stream) {
+    int e = dp_build(c, stream);
+    if (!e)
+        e = rk_dp_minmax(c->tab_dev, c->dp.view, first, count, rec_dev, c->recs_dev, c->counter_dev, c->max_ctas,
+                         stream, &c->launches);
+    return e;
+}
+
+/* Pass 2: keys, counts, optional fused histogram (bins <= rk_dp_max_fused_bins()) */
+int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, const rk_stats* range_dev,
+             uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev, rk_stats* rec_dev, void* stream) {
+    return rk_dp_keys(c->tab_dev, c->dp.view, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, rec_dev,
+                      stream, &c->launches);
+}
+
+/* memoised equivalent of rk_launch_eval (stats + optional keys, optional histogram) */
+int dp_eval(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, rk_stats* stats_dev,
+            uint64_t* keys_dev, const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream) {
+    int e = dp_pass1(c, first, count, stats_dev, stream);
+    if (!e) e = dp_pass2(c, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, stats_dev, stream);
+    return e;
+}
+
 }  // namespace
 
 /* ================================ C ABI ================================== */
@@ -414,6 +622,10 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
     c->no_reduce = nr && nr[0] == '1';
     const char* fr = getenv("RK_FORCE_RUNS");
     c->force_runs = fr && fr[0] == '1';
+    const char* nm = getenv("RK_NO_MEMO");
+    c->no_memo = nm && nm[0] == '1';
+    const char* fm = getenv("RK_FORCE_MEMO");
+    c->force_memo = fm && fm[0] == '1';
     if (cuda_device >= 0) {
         int ndev = 0;
         cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -446,6 +658,7 @@ void rk_destroy(rk_ctx* c) {
     if (!c) return;
     if (c->device >= 0) {
         DeviceGuard dg(c->device);
+        dp_free(c->dp);
         cudaFree(c->tab_dev);
         cudaFree(c->recs_dev);
         cudaFree(c->counter_dev);
@@ -483,6 +696,10 @@ rk_status rk_set_kernels(rk_ctx* c, const rk_kernel* k, uint32_t n) {
     c->tab = t;
     c->ks.assign(k, k + n);
     c->has_kernels = true;
+    if (c->device >= 0) {
+        DeviceGuard dg(c->device);
+        if ((s = dp_plan(c))) return s;
+    }
     return RK_OK;
 }
 
@@ -494,6 +711,11 @@ rk_status rk_eval_range_async(rk_ctx* c, uint64_t first, uint64_t count, const u
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
+    if (c->dp.on) {
+        const int e = dp_eval(c, first, count, cand_or_zero(c, cand_key_dev, stream), stats_dev, keys_dev, nullptr, 0,
+                              nullptr, stream);
+        return e ? cuda_fail(c, e, "memoised evaluation") : RK_OK;
+    }
     int e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, stats_dev, keys_dev,
                            c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
     return e ? cuda_fail(c, e, "rk_eval_kernel launch") : RK_OK;
@@ -512,8 +734,14 @@ rk_status rk_eval_range(rk_ctx* c, uint64_t first, uint64_t count, uint64_t cand
         std::memset(out_host, 0, sizeof *out_host);
         return RK_OK;
     }
-    int e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, nullptr, candidate_key, c->stats_dev,
-                           keys_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
+    int e;
+    if (c->dp.on) {
+        e = cudaMemcpyAsync(c->u64_dev + 8, &candidate_key, 8, cudaMemcpyHostToDevice, st);
+        if (!e) e = dp_eval(c, first, count, c->u64_dev + 8, c->stats_dev, keys_dev, nullptr, 0, nullptr, stream);
+    } else {
+        e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, nullptr, candidate_key,
+                           c->stats_dev, keys_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
+    }
     if (e) return cuda_fail(c, e, "rk_eval_kernel launch");
     rk_stats h;
     e = cudaMemcpyAsync(&h, c->stats_dev, sizeof h, cudaMemcpyDeviceToHost, st);
@@ -561,10 +789,67 @@ rk_status rk_eval_range_hist_async(rk_ctx* c, uint64_t first, uint64_t count, co
     DeviceGuard dg(c->device);
     c->launches = 0;
     rk_stats* out = stats_dev ? stats_dev : c->stats_dev;
+    if (c->dp.on && bins <= rk_dp_max_fused_bins()) {
+        const int e = dp_eval(c, first, count, cand_or_zero(c, cand_key_dev, stream), out, nullptr, range_dev, bins,
+                              hist_dev, stream);
+        return e ? cuda_fail(c, e, "memoised evaluation (fused histogram)") : RK_OK;
+    }
     int e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, out, nullptr,
                            c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches, nullptr, 0, nullptr,
                            range_dev, bins, hist_dev);
     return e ? cuda_fail(c, e, "rk_eval_kernel (fused histogram) launch") : RK_OK;
+}
+
+rk_status rk_sweep_pass1_async(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                               rk_stats* rec_dev, uint64_t* keys_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!rec_dev || !cand_key_dev) return fail(c, RK_EINVAL, "rec_dev and cand_key_dev are required");
+    if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    int e;
+    if (c->dp.on) {
+        e = dp_pass1(c, first, count, rec_dev, stream);
+    } else {
+        e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, rec_dev, keys_dev,
+                           c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
+    }
+    return e ? cuda_fail(c, e, "rk_sweep_pass1_async") : RK_OK;
+}
+
+rk_status rk_sweep_pass2_async(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                               const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev,
+                               rk_stats* rec_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!rec_dev || !cand_key_dev) return fail(c, RK_EINVAL, "rec_dev and cand_key_dev are required");
+    if (hist_dev && (!range_dev || bins < 1)) return fail(c, RK_EINVAL, "histogram needs range_dev and bins >= 1");
+    if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    int e = 0;
+    if (c->dp.on) {
+        const bool fused = hist_dev && bins <= rk_dp_max_fused_bins();
+        if (hist_dev && !fused && !keys_dev) return fail(c, RK_EINVAL, "more than 4096 bins needs keys_dev");
+        e = dp_pass2(c, first, count, cand_key_dev, range_dev, fused ? bins : 0, fused ? hist_dev : nullptr, keys_dev,
+                     rec_dev, stream);
+        if (!e && hist_dev && !fused)
+            e = rk_launch_histogram(keys_dev, count, 0, 0, range_dev, bins, hist_dev, stream, &c->launches);
+    } else if (hist_dev) {
+        if (!keys_dev) return fail(c, RK_EINVAL, "keys_dev is required (direct evaluation)");
+        e = rk_launch_histogram(keys_dev, count, 0, 0, range_dev, bins, hist_dev, stream, &c->launches);
+    }
+    return e ? cuda_fail(c, e, "rk_sweep_pass2_async") : RK_OK;
+}
+
+rk_status rk_memo_info(rk_ctx* c, uint32_t* on_out, uint32_t* levels_out, uint32_t* nodes_out, uint32_t max_levels) {
+    if (!c || !on_out) return RK_EINVAL;
+    *on_out = c->dp.on ? 1u : 0u;
+    if (levels_out) *levels_out = c->dp.on ? c->dp.P : 0u;
+    if (nodes_out && c->dp.on)
+        for (uint32_t j = 0; j <= c->dp.P && j < max_levels; j++) nodes_out[j] = c->dp.cnt[j];
+    return RK_OK;
 }
 
 rk_status rk_key_lower_bound(rk_ctx* c, uint64_t* lb_out) {

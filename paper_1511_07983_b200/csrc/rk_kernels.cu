@@ -1482,6 +1482,484 @@ __global__ void __launch_bounds__(kBnbThreads) rk_bnb_kernel(const RkTables* __r
     }
 }
 
+/* ==================== Suffix memoisation ====================
+ * The key of an order is K(prefix) + f(state after the prefix, suffix): the
+ * closed rounds' key is additive and everything after depends only on the SM
+ * state, the cursor, the open round's (dI, nM) and the remaining set.  Many
+ * prefixes reach the same (remaining set, state) (C4: 3,991,680 prefixes of
+ * length 7, 42,706 distinct).  So, exactly:
+ *   levels j = 0..P-1: expand every distinct node of level j by every unused
+ *     kernel, deduplicate the results in a hash table -> level j+1 nodes, and
+ *     record the transition (node id, closed-round key increment dK);
+ *   suffix: for each distinct level-P node, the D! suffix keys f[u][sigma];
+ *   per run (D! consecutive indices sharing a P-prefix): walk the P
+ *     transitions -> (u, Kc); key(run, sigma) = Kc + f[u][sigma].
+ * Every key is the same exact integer the direct evaluation produces. */
+template <int SMAX>
+struct DNode {
+    uint32_t fa[SMAX], fb[SMAX];
+    uint32_t cur, mask;
+    uint64_t I, M;
+};
+constexpr uint32_t kDpEmpty = 0xFFFFFFFFu, kDpBusy = 0xFFFFFFFEu;
+constexpr int kDpThreads = 256;
+
+template <int SMAX>
+__device__ __forceinline__ uint64_t dnode_hash(const DNode<SMAX>& x) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&x);
+    uint64_t h = 0x243F6A8885A308D3ull;
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(DNode<SMAX>) / 4); i++) h = (h ^ w[i]) * 0x9E3779B97F4A7C15ull;
+    return h ^ (h >> 29);
+}
+
+template <int SMAX>
+__device__ __forceinline__ bool dnode_eq_ldcg(const DNode<SMAX>* stored, const DNode<SMAX>& x) {
+    const uint32_t* a = reinterpret_cast<const uint32_t*>(stored);
+    const uint32_t* b = reinterpret_cast<const uint32_t*>(&x);
+    bool eq = true;
+#pragma unroll
+    for (int i = 0; i < (int)(sizeof(DNode<SMAX>) / 4); i++) eq &= __ldcg(a + i) == b[i];
+    return eq;
+}
+
+template <int SMAX, bool FULL>
+__device__ __forceinline__ void dnode_fresh(DNode<SMAX>& d, const RkGTab& g) {
+#pragma unroll
+    for (int i = 0; i < SMAX; i++) {
+        d.fa[i] = live_sm<SMAX, FULL>(i, g) ? g.freshA : 0u;
+        d.fb[i] = live_sm<SMAX, FULL>(i, g) ? g.freshB : 0u;
+    }
+    d.cur = d.mask = 0;
+    d.I = d.M = 0;
+}
+
+/* One level: nodes of level j (count *cnt_j; nullptr = the fresh root) x unused kernels. */
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables* __restrict__ tab,
+                                                                const DNode<SMAX>* __restrict__ Uj,
+                                                                const uint32_t* __restrict__ cnt_j, DNode<SMAX>* Un,
+                                                                uint32_t* cnt_n, uint32_t cap_n, uint32_t* table,
+                                                                uint32_t tmask, uint32_t* __restrict__ tid,
+                                                                uint64_t* __restrict__ dk, uint32_t* ovf) {
+    __shared__ RkTables t;
+    load_tables(t, tab);
+    const RkGTab& g = t.g;
+    const uint32_t n = g.n;
+    const uint32_t m = Uj ? *cnt_j : 1u;
+    NoRec nr;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < m * n; c += gridDim.x * blockDim.x) {
+        const uint32_t u = c / n, k = c - u * n;
+        DNode<SMAX> nd;
+        if (Uj) nd = Uj[u];
+        else dnode_fresh<SMAX, FULL>(nd, g);
+        if ((nd.mask >> k) & 1u) {
+            tid[c] = kDpEmpty;
+            continue;
+        }
+        St<SMAX> s, s2;
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            s.fa[i] = nd.fa[i];
+            s.fb[i] = nd.fb[i];
+        }
+        s.cur = nd.cur;
+        s.I = nd.I;
+        s.M = nd.M;
+        s.K = 0;
+        place<SMAX, FULL>(s, s2, t.k[k], k, g, nr);
+        DNode<SMAX> o;
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            o.fa[i] = s2.fa[i];
+            o.fb[i] = s2.fb[i];
+        }
+        o.cur = s2.cur;
+        o.mask = nd.mask | (1u << k);
+        o.I = s2.I;
+        o.M = s2.M;
+        uint32_t pos = (uint32_t)dnode_hash(o) & tmask, id = kDpEmpty;
+        for (;;) {
+            uint32_t v = atomicCAS(&table[pos], kDpEmpty, kDpBusy);
+            if (v == kDpEmpty) { /* claimed: allocate, publish the record, then the id */
+                id = atomicAdd(cnt_n, 1u);
+                if (id < cap_n) Un[id] = o;
+                else atomicOr(ovf, 1u);
+                __threadfence();
+                atomicExch(&table[pos], id);
+                break;
+            }
+            while (v == kDpBusy) {
+                __nanosleep(32);
+                v = *(volatile uint32_t*)&table[pos];
+            }
+            if (v >= cap_n) { /* an overflowed entry: the result is discarded (plan re-sizes) */
+                atomicOr(ovf, 1u);
+                id = v;
+                break;
+            }
+            if (dnode_eq_ldcg(Un + v, o)) {
+                id = v;
+                break;
+            }
+            pos = (pos + 1u) & tmask;
+        }
+        tid[c] = id;
+        dk[c] = s2.K;
+    }
+}
+
+/* Suffix tables: for node u of level P, the D! = 120 keys (from K = 0) of its
+ * remaining kernels' orders, lexicographic in the remaining ascending ids.  A
+ * warp per node: lanes 0..19 take the 20 (first, second) suffix kernels and
+ * evaluate the 6 orders below each; the row is then encoded as its sorted
+ * distinct values dv (with multiplicities dc; ~14 per row on C4) and one byte
+ * code per order (code = rank of its key among dv), plus min/max/argmin/argmax. */
+struct SLeaf {
+    uint64_t* row;
+    __device__ __forceinline__ void operator()(uint32_t off, uint64_t K) { row[off] = K; }
+    __device__ __forceinline__ void pair(uint32_t off, uint64_t K0, uint64_t K1) {
+        row[off] = K0;
+        row[off + 1] = K1;
+    }
+};
+
+constexpr uint32_t kDF = 120; /* D! for the memo suffix depth D = 5 */
+
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables* __restrict__ tab,
+                                                                 const DNode<SMAX>* __restrict__ UP,
+                                                                 const uint32_t* __restrict__ cnt_P,
+                                                                 uint8_t* __restrict__ code, ulonglong2* __restrict__ dvc,
+                                                                 uint32_t* __restrict__ dvo, uint32_t* __restrict__ nd,
+                                                                 uint64_t* __restrict__ fst) {
+    __shared__ RkTables t;
+    __shared__ uint64_t srow[kDpThreads / 32][128];
+    load_tables(t, tab);
+    const RkGTab& g = t.g;
+    const uint32_t n = g.n, lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const uint32_t m = *cnt_P;
+    uint64_t* row = srow[w];
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < m; u += (gridDim.x * blockDim.x) >> 5) {
+        const DNode<SMAX> nd0 = UP[u];
+        uint32_t rem = 0, q0 = 0;
+        for (uint32_t k = 0; k < n; k++)
+            if (!((nd0.mask >> k) & 1u)) rem |= k << (4u * q0++);
+        if (lane < 20) {
+            St<SMAX> s;
+#pragma unroll
+            for (int i = 0; i < SMAX; i++) {
+                s.fa[i] = nd0.fa[i];
+                s.fb[i] = nd0.fb[i];
+            }
+            s.cur = nd0.cur;
+            s.I = nd0.I;
+            s.M = nd0.M;
+            s.K = 0;
+            const uint32_t a = lane >> 2, b = lane & 3u;
+            const uint32_t ka = (rem >> (4u * a)) & 15u;
+            const uint32_t r4 = (rem & ((1u << (4u * a)) - 1u)) | ((rem >> (4u * a + 4u)) << (4u * a));
+            const uint32_t kb = (r4 >> (4u * b)) & 15u;
+            const uint32_t r3 = (r4 & ((1u << (4u * b)) - 1u)) | ((r4 >> (4u * b + 4u)) << (4u * b));
+            NoRec nr;
+            St<SMAX> s1, s2;
+            place<SMAX, FULL>(s, s1, t.k[ka], ka, g, nr);
+            place<SMAX, FULL>(s1, s2, t.k[kb], kb, g, nr);
+            SLeaf leaf{row + a * 24u + b * 6u};
+            dfs<SMAX, FULL, 3>(t, s2, r3, 0u, leaf);
+        }
+        __syncwarp();
+        uint64_t v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q] = lane + 32u * q < kDF ? row[lane + 32u * q] : ~0ull;
+        /* distinct values in increasing order by repeated warp minimum (~14 rounds) */
+        uint32_t done = 0, rank = 0, cdw = 0; /* done: bit q; cdw: the lane's 4 codes, one byte each */
+#pragma unroll
+        for (int q = 0; q < 4; q++) done |= (lane + 32u * q < kDF ? 0u : 1u) << q;
+        uint64_t mn = 0, mx = 0;
+        uint32_t amn = 0, amx = 0;
+        for (;;) {
+            uint64_t lm = ~0ull;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (!((done >> q) & 1u) && v[q] < lm) lm = v[q];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const uint64_t y = __shfl_xor_sync(0xFFFFFFFFu, lm, o);
+                lm = y < lm ? y : lm;
+            }
+            if (lm == ~0ull) break; /* keys < 2^63: the sentinel means all done */
+            uint32_t cnt = 0, firstsg = 0xFFFFFFFFu;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const bool hit = !((done >> q) & 1u) && v[q] == lm;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+                cnt += __popc(bal);
+                if (bal && firstsg == 0xFFFFFFFFu) firstsg = 32u * q + (uint32_t)(__ffs(bal) - 1);
+                if (hit) {
+                    done |= 1u << q;
+                    cdw |= rank << (8 * q);
+                }
+            }
+            if (rank == 0) {
+                mn = lm;
+                amn = firstsg;
+            }
+            if (lane == 0) {
+                dvc[(uint64_t)u * kDF + rank] = make_ulonglong2(lm, cnt);
+                dvo[(uint64_t)u * kDF + rank] = (uint32_t)(lm - mn); /* exact when the row spans < 2^32 */
+            }
+            mx = lm;
+            amx = firstsg;
+            rank++;
+        }
+        /* codes: sigma = lane + 32q */
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (lane + 32u * q < kDF) code[(uint64_t)u * kDF + lane + 32u * q] = (uint8_t)(cdw >> (8 * q));
+        if (lane == 0) {
+            nd[u] = rank | ((mx - mn) >> 32 ? 0x80000000u : 0u); /* bit 31: offsets do not fit 32 bits */
+            fst[4 * (uint64_t)u] = mn;
+            fst[4 * (uint64_t)u + 1] = mx;
+            fst[4 * (uint64_t)u + 2] = amn;
+            fst[4 * (uint64_t)u + 3] = amx;
+        }
+        __syncwarp();
+    }
+}
+
+/* (node, closed key) of run `run`: the P-prefix of index run*D! through the transitions */
+__device__ __forceinline__ void dp_walk(const RkGTab& g, const DPView& v, uint64_t run, uint32_t& u, uint64_t& Kc) {
+    const uint32_t n = g.n;
+    uint64_t L = identity_list(n);
+    uint64_t rem = run * v.Dfact;
+    u = 0;
+    Kc = 0;
+    for (uint32_t j = 0; j < v.P; j++) {
+        const uint64_t f = g.fact[n - 1 - j];
+        const uint32_t d = (rem < (1ull << 32) && f < (1ull << 32)) ? (uint32_t)rem / (uint32_t)f : (uint32_t)(rem / f);
+        rem -= (uint64_t)d * f;
+        const uint32_t k = take_nibble(L, d);
+        const uint32_t c = u * n + k;
+        Kc += __ldg(v.dk[j] + c);
+        u = __ldg(v.tid[j] + c);
+    }
+}
+
+/* Pass 1: extremes (min/argmin, max/argmax; smallest index on ties) and the
+ * count of [first, first+count); n_lt = n_eq = 0, n_gt = count (pass 2 adds). */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_minmax_kernel(const RkTables* __restrict__ tab, DPView v,
+                                                                 uint64_t first, uint64_t count, rk_stats* out,
+                                                                 rk_stats* recs, uint32_t* counter) {
+    __shared__ RkTables t;
+    load_tables(t, tab);
+    const RkGTab& g = t.g;
+    TStats ts;
+    ts.init();
+    const uint64_t DF = v.Dfact, lo = first, hi = first + count;
+    const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
+    for (uint64_t run = rb + blockIdx.x * blockDim.x + threadIdx.x; run < re; run += gridDim.x * blockDim.x) {
+        uint32_t u;
+        uint64_t Kc;
+        dp_walk(g, v, run, u, Kc);
+        const uint64_t idx0 = run * DF;
+        const uint32_t olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
+        const uint32_t ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : (uint32_t)DF;
+        uint64_t mn, mx, amn, amx;
+        if (olo == 0 && ohi == DF) {
+            mn = Kc + __ldg(v.fst + 4ull * u);
+            mx = Kc + __ldg(v.fst + 4ull * u + 1);
+            amn = idx0 + __ldg(v.fst + 4ull * u + 2);
+            amx = idx0 + __ldg(v.fst + 4ull * u + 3);
+        } else {
+            mn = ~0ull;
+            mx = 0;
+            amn = amx = idx0 + olo;
+            const uint8_t* cr = v.code + (uint64_t)u * DF;
+            const ulonglong2* dr = reinterpret_cast<const ulonglong2*>(v.dvc) + (uint64_t)u * DF;
+            for (uint32_t q = olo; q < ohi; q++) {
+                const uint64_t K = Kc + __ldg(&dr[__ldg(cr + q)].x);
+                if (K < mn) { mn = K; amn = idx0 + q; }
+                if (K > mx) { mx = K; amx = idx0 + q; }
+            }
+        }
+        if (mn < ts.kmin) { ts.kmin = mn; ts.amin = amn; }
+        if (mx > ts.kmax) { ts.kmax = mx; ts.amax = amx; }
+        ts.cnt += ohi - olo;
+    }
+    const rk_stats r = block_reduce(to_rec(ts));
+    commit(r, recs, counter, out);
+}
+
+constexpr uint32_t kDpEdgeBins = 32768; /* fused histogram up to this many shared-memory bins */
+
+/* Pass 2: every key of [first, first+count) to HBM (u64, index-major), the
+ * counts against the candidate (added to rec: n_lt, n_eq; n_gt -= both) and the
+ * Fig. 1 histogram over [range.key_min, range.key_max] (HIST).  A warp takes 32
+ * consecutive runs: each lane walks one run's prefix (transition tables) and,
+ * from its node's sorted distinct suffix values (~14), counts the run's keys
+ * against the candidate and bins them (one shared atomic per distinct bin);
+ * then the warp writes the 32 runs' key blocks in index order — lane l decodes
+ * the 4 keys 4l..4l+3 (one 32-bit word of codes, 4 gathers from the node's
+ * distinct values in L1) and stores 32 B (coalesced, streaming stores).  L2
+ * reads per run: 120 B of codes + the distinct values, instead of a 960-B row. */
+template <bool HIST>
+__global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* __restrict__ tab, DPView v,
+                                                               uint64_t first, uint64_t count,
+                                                               const uint64_t* __restrict__ cand_dev,
+                                                               const rk_stats* __restrict__ range, uint32_t bins,
+                                                               uint64_t* hist, uint64_t* keys, rk_stats* rec) {
+    __shared__ RkTables t;
+    extern __shared__ uint32_t shist[]; /* HIST: u32 bins */
+    __shared__ unsigned long long cnt_lt, cnt_eq;
+    if (HIST)
+        for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) shist[i] = 0;
+    if (threadIdx.x == 0) cnt_lt = cnt_eq = 0;
+    load_tables(t, tab); /* (includes the barrier) */
+    const RkGTab& g = t.g;
+    const uint64_t cand = *cand_dev;
+    BinCalc bc;
+    if (HIST) bc.init(range->key_min, range->key_max, bins);
+    const uint32_t lane = threadIdx.x & 31u, DF = v.Dfact;
+    const ulonglong2* dvc = reinterpret_cast<const ulonglong2*>(v.dvc);
+    uint64_t nlt = 0, neq = 0; /* per lane */
+    const uint64_t lo = first, hi = first + count;
+    const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
+    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    const bool aligned = (first & 1u) == 0; /* run offsets idx0 - first even: 16-B aligned stores */
+    for (uint64_t base = rb + gw * 32; base < re; base += nw * 32) {
+        /* lane-parallel: the lane's run — prefix walk, then counts and bins from
+         * its node's sorted distinct values (one shared atomic per distinct bin) */
+        const uint64_t run = base + lane;
+        uint32_t u = 0, olo = 0, ohi = 0;
+        uint64_t Kb = 0; /* closed-round key + the row minimum: key = Kb + offset */
+        if (run < re) {
+            uint64_t Kc;
+            dp_walk(g, v, run, u, Kc);
+            const uint64_t idx0 = run * DF;
+            olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
+            ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF;
+            const uint64_t fmn = __ldg(v.fst + 4ull * u);
+            Kb = Kc + fmn;
+            if (olo == 0 && ohi == DF) {
+                const uint32_t ndv = __ldg(v.nd + u) & 0x7FFFFFFFu;
+                const ulonglong2* dr = dvc + (uint64_t)u * DF;
+                const uint64_t fmx = __ldg(v.fst + 4ull * u + 1);
+                const bool inside = cand >= Kb && cand <= Kc + fmx;
+                if (cand > Kc + fmx) nlt += DF;
+                uint32_t bp = 0xFFFFFFFFu, acc = 0;
+                for (uint32_t q0 = 0; q0 < ndv; q0 += 4) { /* 4 independent loads in flight */
+                    ulonglong2 e[4];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) e[j] = q0 + j < ndv ? __ldg(dr + q0 + j) : make_ulonglong2(0, 0);
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const uint64_t K = Kc + e[j].x;
+                        const uint32_t c = (uint32_t)e[j].y; /* 0 past the end */
+                        if (inside) {
+                            nlt += K < cand ? c : 0u;
+                            neq += K == cand ? c : 0u;
+                        }
+                        if (HIST && c) {
+                            const uint32_t b = bc(K);
+                            if (b == bp) {
+                                acc += c;
+                            } else {
+                                if (acc) atomicAdd(&shist[bp], acc);
+                                bp = b;
+                                acc = c;
+                            }
+                        }
+                    }
+                }
+                if (HIST && acc) atomicAdd(&shist[bp], acc);
+            }
+        }
+        /* warp-cooperative: decode (code bytes -> 32-bit offsets by shuffle) and
+         * store each run's 960-B key block; lane l owns keys 4l..4l+3 */
+        const uint32_t nr = (uint32_t)min((uint64_t)32, re - base);
+        const bool grp_whole = base * DF >= lo && (base + nr) * DF <= hi; /* no range-edge run */
+        const uint32_t s0 = 4u * lane;
+        uint64_t* out = keys ? keys + (base * DF - first) + s0 : nullptr;
+        /* software pipeline: run i+1's node data is in flight while run i is stored */
+        uint32_t p_nd, p_cw, p_do;
+        {
+            const uint32_t u0 = __shfl_sync(0xFFFFFFFFu, u, 0);
+            p_nd = __ldg(v.nd + u0);
+            p_cw = s0 < DF ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)u0 * DF) + lane) : 0u;
+            p_do = __ldg(v.dvo + (uint64_t)u0 * DF + lane);
+        }
+        for (uint32_t i = 0; i < nr; i++, out = out ? out + DF : nullptr) {
+            const uint32_t ui = __shfl_sync(0xFFFFFFFFu, u, i);
+            const uint64_t Ki = __shfl_sync(0xFFFFFFFFu, Kb, i);
+            const uint32_t ndv = p_nd, cw = p_cw, dlo = p_do;
+            if (i + 1 < nr) {
+                const uint32_t un = __shfl_sync(0xFFFFFFFFu, u, i + 1);
+                p_nd = __ldg(v.nd + un);
+                p_cw = s0 < DF ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)un * DF) + lane) : 0u;
+                p_do = __ldg(v.dvo + (uint64_t)un * DF + lane);
+            }
+            uint64_t k[4];
+            if (ndv <= 32u) { /* 32-bit offsets, at most 32 distinct values: one shuffle per key */
+#pragma unroll
+                for (int q = 0; q < 4; q++) k[q] = Ki + __shfl_sync(0xFFFFFFFFu, dlo, __byte_perm(cw, 0, 0x4440 + q));
+            } else {
+                const ulonglong2* dr = dvc + (uint64_t)ui * DF;
+                const uint64_t fmn = __ldg(v.fst + 4ull * ui);
+#pragma unroll
+                for (int q = 0; q < 4; q++) k[q] = Ki - fmn + __ldg(&dr[__byte_perm(cw, 0, 0x4440 + q)].x);
+            }
+            bool whole = grp_whole;
+            uint32_t oi = 0, hi_i = DF;
+            if (!grp_whole) { /* warp-uniform */
+                oi = __shfl_sync(0xFFFFFFFFu, olo, i);
+                hi_i = __shfl_sync(0xFFFFFFFFu, ohi, i);
+                whole = oi == 0 && hi_i == DF;
+            }
+            if (s0 >= DF) continue;
+            if (whole) {
+                if (out) {
+                    if (aligned) {
+                        __stcs(reinterpret_cast<ulonglong2*>(out), make_ulonglong2(k[0], k[1]));
+                        __stcs(reinterpret_cast<ulonglong2*>(out) + 1, make_ulonglong2(k[2], k[3]));
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 4; q++) __stcs(out + q, k[q]);
+                    }
+                }
+            } else { /* range-edge run: per key */
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    if (s0 + q >= oi && s0 + q < hi_i) {
+                        if (out) __stcs(out + q, k[q]);
+                        nlt += k[q] < cand;
+                        neq += k[q] == cand;
+                        if (HIST) atomicAdd(&shist[bc(k[q])], 1u);
+                    }
+                }
+            }
+        }
+    }
+    unsigned long long a = nlt, b = neq;
+    for (int o = 16; o; o >>= 1) {
+        a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+    }
+    if (lane == 0 && (a || b)) {
+        atomicAdd(&cnt_lt, a);
+        atomicAdd(&cnt_eq, b);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && (cnt_lt || cnt_eq)) {
+        atomicAdd((unsigned long long*)&rec->n_lt, cnt_lt);
+        atomicAdd((unsigned long long*)&rec->n_eq, cnt_eq);
+        atomicAdd((unsigned long long*)&rec->n_gt, 0ull - (cnt_lt + cnt_eq));
+    }
+    if (HIST)
+        for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x)
+            if (shist[i]) atomicAdd((unsigned long long*)&hist[i], (unsigned long long)shist[i]);
+}
+
 int g_num_sms = 0;
 int num_sms() {
     if (!g_num_sms) {
@@ -1767,3 +2245,106 @@ int rk_launch_bnb(const RkTables* tab_dev, uint32_t S, uint32_t P, uint64_t n_un
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
+
+/* ---- suffix memoisation launchers (register-state variants only) ---- */
+namespace {
+unsigned dp_grid(uint64_t work) {
+    const uint64_t cap = (uint64_t)num_sms() * 8;
+    uint64_t b = (work + kDpThreads - 1) / kDpThreads;
+    if (b > cap) b = cap;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+}  // namespace
+
+uint32_t rk_dp_node_bytes(uint32_t S) {
+    switch (variant(S)) {
+        case 0: return sizeof(DNode<1>);
+        case 1: return sizeof(DNode<2>);
+        case 2: case 3: return sizeof(DNode<4>);
+        case 4: case 5: return sizeof(DNode<8>);
+        case 6: case 7: return sizeof(DNode<16>);
+        case 8: case 9: return sizeof(DNode<32>);
+        default: return 0;
+    }
+}
+
+int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
+                uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
+                uint64_t work, void* stream, uint32_t* launches) {
+#define RK_DP_LEVEL_ARGS(SMAX) tab, (const DNode<SMAX>*)Uj, cnt_j, (DNode<SMAX>*)Un, cnt_n, cap_n, table, tmask, tid, dk, ovf
+    const unsigned grid = dp_grid(work);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (variant(S)) {
+        case 0: rk_dp_level_kernel<1, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(1)); break;
+        case 1: rk_dp_level_kernel<2, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(2)); break;
+        case 2: rk_dp_level_kernel<4, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(4)); break;
+        case 3: rk_dp_level_kernel<4, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(4)); break;
+        case 4: rk_dp_level_kernel<8, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(8)); break;
+        case 5: rk_dp_level_kernel<8, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(8)); break;
+        case 6: rk_dp_level_kernel<16, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(16)); break;
+        case 7: rk_dp_level_kernel<16, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(16)); break;
+        case 8: rk_dp_level_kernel<32, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(32)); break;
+        case 9: rk_dp_level_kernel<32, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(32)); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+#undef RK_DP_LEVEL_ARGS
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
+                 uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint64_t nodes, void* stream, uint32_t* launches) {
+#define RK_DP_SUF_ARGS(SMAX) tab, (const DNode<SMAX>*)UP, cnt_P, code, (ulonglong2*)dvc, dvo, nd, fst
+    const unsigned grid = dp_grid(nodes * 32);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (variant(S)) {
+        case 0: rk_dp_suffix_kernel<1, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(1)); break;
+        case 1: rk_dp_suffix_kernel<2, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(2)); break;
+        case 2: rk_dp_suffix_kernel<4, false><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(4)); break;
+        case 3: rk_dp_suffix_kernel<4, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(4)); break;
+        case 4: rk_dp_suffix_kernel<8, false><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(8)); break;
+        case 5: rk_dp_suffix_kernel<8, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(8)); break;
+        case 6: rk_dp_suffix_kernel<16, false><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(16)); break;
+        case 7: rk_dp_suffix_kernel<16, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(16)); break;
+        case 8: rk_dp_suffix_kernel<32, false><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(32)); break;
+        case 9: rk_dp_suffix_kernel<32, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(32)); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+#undef RK_DP_SUF_ARGS
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_minmax(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, rk_stats* out, rk_stats* recs,
+                 uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
+    const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
+    unsigned grid = dp_grid(runs);
+    if (grid > max_ctas) grid = max_ctas;
+    rk_dp_minmax_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, out, recs, counter);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+uint32_t rk_dp_max_fused_bins() { return kDpEdgeBins; }
+
+int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count,
+               const uint64_t* cand_dev, const rk_stats* range, uint32_t bins, uint64_t* hist, uint64_t* keys,
+               rk_stats* rec, void* stream, uint32_t* launches) {
+    const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
+    const unsigned grid = dp_grid(runs);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (hist) {
+        if (bins > kDpEdgeBins) return (int)cudaErrorInvalidValue;
+        const size_t smem = (size_t)bins * 4;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(rk_dp_keys_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        rk_dp_keys_kernel<true><<<grid, kDpThreads, smem, st>>>(tab, v, first, count, cand_dev, range, bins, hist,
+                                                                keys, rec);
+    } else {
+        rk_dp_keys_kernel<false><<<grid, kDpThreads, 0, st>>>(tab, v, first, count, cand_dev, range, 0, nullptr,
+                                                              keys, rec);
+    }
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+

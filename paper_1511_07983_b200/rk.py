@@ -24,7 +24,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
            "rk_eval_range_async", "rk_eval_range_hist_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
            "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_rank", "rk_unrank",
+           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_sweep_pass1_async", "rk_sweep_pass2_async", "rk_memo_info", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -91,6 +91,9 @@ def lib():
             "rk_select_keys32": ([vp, vp, u64, u64, u64, u64, P(u64), u32, P(u64), vp], ctypes.c_int),
             "rk_range_histogram32": ([vp, vp, u64, u64, u64, u64, u32, vp, vp], ctypes.c_int),
             "rk_heuristic_order": ([vp, P(ctypes.c_int32), P(ctypes.c_int32), P(u64), P(u64)], ctypes.c_int),
+            "rk_sweep_pass1_async": ([vp, u64, u64, vp, vp, vp, vp], ctypes.c_int),
+            "rk_sweep_pass2_async": ([vp, u64, u64, vp, vp, u32, vp, vp, vp, vp], ctypes.c_int),
+            "rk_memo_info": ([vp, P(u32), P(u32), P(u32), u32], ctypes.c_int),
             "rk_best_order": ([vp, u64, P(ctypes.c_int32), P(u64), P(u64), P(u64), vp], ctypes.c_int),
             "rk_heuristic_batch": ([vp, P(rk_kernel), u32, u32, P(ctypes.c_int32), P(u64), vp], ctypes.c_int),
             "rk_percentile": ([vp, P(ctypes.c_int32), u64, u64, P(u64), P(u64)], ctypes.c_int),
@@ -317,6 +320,23 @@ class Context:
         self._chk(self._L.rk_heuristic_order(self.h, o, r, ctypes.byref(idx), ctypes.byref(key) if with_key else None),
                   "rk_heuristic_order")
         return list(o), list(r), idx.value, (key.value if with_key else None)
+
+    def rk_sweep_pass1_async(self, first: int, count: int, cand_key_dev, rec_dev, keys_dev=None, stream=None):
+        self._chk(self._L.rk_sweep_pass1_async(self.h, first, count, _ptr(cand_key_dev), _ptr(rec_dev),
+                                               _ptr(keys_dev), _stream(stream)), "rk_sweep_pass1_async")
+
+    def rk_sweep_pass2_async(self, first: int, count: int, cand_key_dev, range_dev, bins: int, hist_dev, keys_dev,
+                             rec_dev, stream=None):
+        self._chk(self._L.rk_sweep_pass2_async(self.h, first, count, _ptr(cand_key_dev), _ptr(range_dev), bins,
+                                               _ptr(hist_dev), _ptr(keys_dev), _ptr(rec_dev), _stream(stream)),
+                  "rk_sweep_pass2_async")
+
+    def rk_memo_info(self):
+        """-> (on, P, [distinct nodes per level 0..P])"""
+        on, lv = ctypes.c_uint32(), ctypes.c_uint32()
+        nodes = (ctypes.c_uint32 * 17)()
+        self._chk(self._L.rk_memo_info(self.h, ctypes.byref(on), ctypes.byref(lv), nodes, 17), "rk_memo_info")
+        return bool(on.value), lv.value, list(nodes)[:lv.value + 1] if on.value else []
 
     def rk_best_order(self, seed_index=None, stream=None):
         """Exact optimum by branch and bound -> (order, index, key, nodes);

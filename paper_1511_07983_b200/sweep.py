@@ -100,8 +100,9 @@ class Sweeper:
 
     def step_device(self, cand_index: int, stream=None, events=None):
         """Enqueue one pass of the hot path; no host sync.  Returns #our launches.
-        events (optional dict) receives CUDA event pairs around the eval and
-        histogram kernels."""
+        events (optional dict) receives CUDA event pairs around pass 1 ("eval":
+        memo tables + extremes, or the direct evaluation) and pass 2 ("hist":
+        keys + counts + histogram, or the histogram of stored keys)."""
         c = self.ctx
         L = 0
         c.rk_eval_index_async(cand_index, self.cand, stream)                                  # a5 candidate key
@@ -111,11 +112,11 @@ class Sweeper:
         if ev:
             e0, e1 = ev(), ev()
             e0.record(st)
-        if self.compact:                                                                       # a1-a4
+        if self.compact:                                                                       # a1-a4 (u32 keys)
             c.rk_eval_range32_async(self.first, self.count, self.cand, self.rec, self.keys32, self.base, self.ovf,
                                     stream)
-        else:
-            c.rk_eval_range_async(self.first, self.count, self.cand, self.rec, self.keys, stream)
+        else:                                                                                  # a1-a4 pass 1
+            c.rk_sweep_pass1_async(self.first, self.count, self.cand, self.rec, self.keys, stream)
         L += c.launches
         if ev:
             e1.record(st)
@@ -133,14 +134,19 @@ class Sweeper:
             h0.record(st)
         if self.compact:                                                                       # a4 histogram
             c.rk_histogram32_async(self.keys32, self.count, self.base, rng, self.bins, self.hist, stream)
-        else:
-            c.rk_histogram_async(self.keys, self.count, rng, self.bins, self.hist, stream)
+        else:                                                                                  # a4 pass 2
+            c.rk_sweep_pass2_async(self.first, self.count, self.cand, rng, self.bins, self.hist, self.keys, self.rec,
+                                   stream)
         L += c.launches
         if ev:
             h1.record(st)
             events.setdefault("hist", []).append((h0, h1))
         if self.world > 1:
             all_reduce_hist(self.hist, self.group)
+            if not self.compact:  # pass 2 completed the local counts: merge the final records
+                recs = all_gather_records(self.rec, self.group)
+                c.rk_merge_stats_async(recs, self.world, self.glob, stream)
+                L += c.launches
         self.launches = L
         return L
 

@@ -770,3 +770,108 @@ def test_forced_runs_state_equals_register_state(monkeypatch):
             assert list(res[q][0].as_tuple()) == g5["sets"][q]["stats"] and res[q][1] == g5["sets"][q]["cand_key"]
     finally:
         c.close()
+
+
+# ---- suffix memoisation: memoised keys == direct keys == oracle ----
+def _direct_ctx(monkeypatch, var="RK_NO_MEMO"):
+    monkeypatch.setenv(var, "1")
+    c = rk.Context(0)
+    monkeypatch.delenv(var)
+    return c
+
+
+def test_memo_plan_info(ctx, monkeypatch):
+    gpu, ks = W.config("C4")
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    on, P, nodes = ctx.rk_memo_info()
+    assert on and P == 7 and nodes[0] == 1 and nodes[1] == 12
+    # distinct nodes never exceed the number of prefixes n!/(n-j)!
+    assert all(nodes[j] <= math.factorial(12) // math.factorial(12 - j) for j in range(P + 1))
+    ctx.rk_set_kernels(ks[:5])  # n < 6: direct
+    assert ctx.rk_memo_info()[0] is False
+    d = _direct_ctx(monkeypatch)
+    try:
+        d.rk_set_gpu_params(gpu)
+        d.rk_set_kernels(ks)
+        assert d.rk_memo_info()[0] is False
+    finally:
+        d.close()
+
+
+def test_memo_keys_equal_direct_keys(monkeypatch):
+    """Every key and statistic of the memoised path equals the direct evaluation's
+    (itself pinned to the oracle) on C2-C4 and random sets n = 6..9 over 7 GPU
+    shapes (memoisation forced on), on full spaces and on ragged ranges."""
+    d = _direct_ctx(monkeypatch)
+    ctx = _direct_ctx(monkeypatch, "RK_FORCE_MEMO")
+    try:
+        cases = [W.config(c) for c in ("C2", "C3", "C4")]
+        for gi, gpu in enumerate(GPUS):
+            for ks in W.random_small_sets(0xDEC0 + gi, 6, 6, 9, gpu=gpu):
+                if all(W.feasible(gpu, k) for k in ks):
+                    cases.append((gpu, ks))
+        checked = 0
+        for gpu, ks in cases:
+            try:
+                ctx.rk_set_gpu_params(gpu)
+                ctx.rk_set_kernels(ks)
+            except rk.RkError as e:
+                assert e.status == rk.RK_EUNSUPPORTED
+                continue
+            d.rk_set_gpu_params(gpu)
+            d.rk_set_kernels(ks)
+            N = math.factorial(len(ks))
+            cand = O.simulate(gpu, ks, O.unrank(N // 3, len(ks))).key
+            rng = np.random.default_rng(len(ks) * 7 + checked)
+            ranges = [(0, N)]
+            for _ in range(3):
+                f0 = int(rng.integers(0, N))
+                ranges.append((f0, int(rng.integers(1, min(50000, N - f0) + 1))))
+            for first, count in ranges:
+                k1 = torch.zeros(count, dtype=torch.int64, device="cuda")
+                k2 = torch.zeros(count, dtype=torch.int64, device="cuda")
+                s1 = ctx.rk_eval_range(first, count, cand, keys_dev=k1)
+                s2 = d.rk_eval_range(first, count, cand, keys_dev=k2)
+                assert s1.as_tuple() == s2.as_tuple(), (gpu, ks, first, count)
+                assert torch.equal(k1, k2)
+            if ctx.rk_memo_info()[0]:
+                checked += 1
+        assert checked >= 10
+    finally:
+        d.close()
+        ctx.close()
+
+
+def test_memo_two_pass_api_and_fused_histogram(ctx):
+    """rk_sweep_pass1/2 (the bench step): record, keys and histogram equal the
+    oracle golden for C4; pass 2 without keys gives the same histogram."""
+    gpu, ks = W.config("C4")
+    g = _gold("c4_oracle.json")
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(12)
+    cand = torch.tensor([g["cand_key"]], dtype=torch.int64, device="cuda")
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    keys = torch.zeros(N, dtype=torch.int64, device="cuda")
+    hist = torch.zeros(256, dtype=torch.int64, device="cuda")
+    ctx.rk_sweep_pass1_async(0, N, cand, rec, keys)
+    ctx.rk_sweep_pass2_async(0, N, cand, rec, 256, hist, keys, rec)
+    torch.cuda.synchronize()
+    st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
+    assert list(st.as_tuple()) == [g["stats"][f] for f in
+                                   ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt", "evaluated")]
+    assert hist.cpu().tolist() == g["hist"]
+    h2 = torch.zeros(256, dtype=torch.int64, device="cuda")
+    ctx.rk_histogram(keys, N, st.key_min, st.key_max, 256, h2)
+    assert torch.equal(hist, h2)
+    rec2 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    h3 = torch.zeros(256, dtype=torch.int64, device="cuda")
+    ctx.rk_sweep_pass1_async(0, N, cand, rec2, None)
+    ctx.rk_sweep_pass2_async(0, N, cand, rec2, 256, h3, None, rec2)
+    torch.cuda.synchronize()
+    assert torch.equal(rec2, rec) and torch.equal(h3, hist)
+    # order statistics over the memoised keys == the oracle's
+    ranks = sorted(int(r) for r in g["order_stats"])
+    got = ctx.rk_select_keys(keys, N, st.key_min, st.key_max, ranks)
+    assert got == [g["order_stats"][str(r)] for r in ranks]
