@@ -1880,23 +1880,24 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* 
         const uint32_t nr = (uint32_t)min((uint64_t)32, re - base);
         const bool grp_whole = base * DF >= lo && (base + nr) * DF <= hi; /* no range-edge run */
         const uint32_t s0 = 4u * lane;
-        uint64_t* out = keys ? keys + (base * DF - first) + s0 : nullptr;
+        const bool act = s0 < DF;                  /* lanes 30, 31 hold no keys (DF = 120) */
+        uint64_t* out = keys + (base * DF - first) + s0; /* only dereferenced when keys != nullptr */
         /* software pipeline: run i+1's node data is in flight while run i is stored */
         uint32_t p_nd, p_cw, p_do;
         {
             const uint32_t u0 = __shfl_sync(0xFFFFFFFFu, u, 0);
             p_nd = __ldg(v.nd + u0);
-            p_cw = s0 < DF ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)u0 * DF) + lane) : 0u;
+            p_cw = act ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)u0 * DF) + lane) : 0u;
             p_do = __ldg(v.dvo + (uint64_t)u0 * DF + lane);
         }
-        for (uint32_t i = 0; i < nr; i++, out = out ? out + DF : nullptr) {
+        for (uint32_t i = 0; i < nr; i++) {
             const uint32_t ui = __shfl_sync(0xFFFFFFFFu, u, i);
             const uint64_t Ki = __shfl_sync(0xFFFFFFFFu, Kb, i);
             const uint32_t ndv = p_nd, cw = p_cw, dlo = p_do;
             if (i + 1 < nr) {
                 const uint32_t un = __shfl_sync(0xFFFFFFFFu, u, i + 1);
                 p_nd = __ldg(v.nd + un);
-                p_cw = s0 < DF ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)un * DF) + lane) : 0u;
+                p_cw = act ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)un * DF) + lane) : 0u;
                 p_do = __ldg(v.dvo + (uint64_t)un * DF + lane);
             }
             uint64_t k[4];
@@ -1909,32 +1910,29 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* 
 #pragma unroll
                 for (int q = 0; q < 4; q++) k[q] = Ki - fmn + __ldg(&dr[__byte_perm(cw, 0, 0x4440 + q)].x);
             }
-            bool whole = grp_whole;
-            uint32_t oi = 0, hi_i = DF;
-            if (!grp_whole) { /* warp-uniform */
-                oi = __shfl_sync(0xFFFFFFFFu, olo, i);
-                hi_i = __shfl_sync(0xFFFFFFFFu, ohi, i);
-                whole = oi == 0 && hi_i == DF;
-            }
-            if (s0 >= DF) continue;
-            if (whole) {
-                if (out) {
+            uint64_t* o = out + (size_t)i * DF;
+            if (grp_whole) { /* warp-uniform: every run of the group lies inside the range */
+                if (keys && act) {
                     if (aligned) {
-                        __stcs(reinterpret_cast<ulonglong2*>(out), make_ulonglong2(k[0], k[1]));
-                        __stcs(reinterpret_cast<ulonglong2*>(out) + 1, make_ulonglong2(k[2], k[3]));
+                        __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(k[0], k[1]));
+                        __stcs(reinterpret_cast<ulonglong2*>(o) + 1, make_ulonglong2(k[2], k[3]));
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 4; q++) __stcs(out + q, k[q]);
+                        for (int q = 0; q < 4; q++) __stcs(o + q, k[q]);
                     }
                 }
-            } else { /* range-edge run: per key */
+            } else {
+                const uint32_t oi = __shfl_sync(0xFFFFFFFFu, olo, i), hi_i = __shfl_sync(0xFFFFFFFFu, ohi, i);
+                const bool whole = oi == 0 && hi_i == DF;
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
-                    if (s0 + q >= oi && s0 + q < hi_i) {
-                        if (out) __stcs(out + q, k[q]);
-                        nlt += k[q] < cand;
-                        neq += k[q] == cand;
-                        if (HIST) atomicAdd(&shist[bc(k[q])], 1u);
+                    if (act && s0 + q >= oi && s0 + q < hi_i) {
+                        if (keys) __stcs(o + q, k[q]);
+                        if (!whole) { /* range-edge run: per-key counts and bins */
+                            nlt += k[q] < cand;
+                            neq += k[q] == cand;
+                            if (HIST) atomicAdd(&shist[bc(k[q])], 1u);
+                        }
                     }
                 }
             }
