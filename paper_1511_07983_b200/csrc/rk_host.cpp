@@ -61,7 +61,11 @@ struct DpPlan {
     std::vector<size_t> xoff;     /* transition offset of level j (j < P): cnt[j] * n entries */
     size_t table_slots = 0;
     Arena nodes, tables, tid, dk, fst, counters; /* counters: P + 1 node counters, then the overflow flag */
-    Arena code, dvc, dvo, nd;                    /* suffix rows: byte codes into sorted distinct (value, count) */
+    Arena code, dvc, dvo, nd, offs;              /* suffix rows: byte codes into sorted distinct (value, count) */
+    Arena runsA, runsB;                          /* prefix expansion (ping-pong); the last level is the run table */
+    bool runs_ok = false;
+    uint64_t runs_first = 0, runs_count = 0;
+    const void* runs_ptr = nullptr;
     DPView view{};
 };
 
@@ -455,7 +459,8 @@ void dp_free(DpPlan& d) {
     d.dk.release();
     d.fst.release();
     d.counters.release();
-    for (Arena* a : {&d.code, &d.dvc, &d.dvo, &d.nd}) a->release();
+    for (Arena* a : {&d.code, &d.dvc, &d.dvo, &d.nd, &d.offs, &d.runsA, &d.runsB}) a->release();
+    d.runs_ok = false;
     d.on = false;
 }
 
@@ -492,7 +497,7 @@ int dp_build(rk_ctx* c, void* stream) {
     if (!e)
         e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
                          (uint8_t*)d.code.p, d.dvc.p, (uint32_t*)d.dvo.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
-                         d.cnt[d.P], stream, &c->launches);
+                         (uint32_t*)d.offs.p, d.cnt[d.P], stream, &c->launches);
     return e;
 }
 
@@ -503,6 +508,7 @@ int dp_build(rk_ctx* c, void* stream) {
 rk_status dp_plan(rk_ctx* c) {
     DpPlan& d = c->dp;
     d.on = false;
+    d.runs_ok = false;
     const uint32_t n = c->tab.g.n, S = c->tab.g.S;
     if (c->device < 0 || c->no_memo || c->force_runs || S > RK_SMAX || n < RK_DP_D + 1) return RK_OK;
     const uint64_t kLimitEntries = 1ull << 26, kLimitBytes = 1ull << 31;
@@ -556,6 +562,7 @@ rk_status dp_plan(rk_ctx* c) {
     e = d.code.reserve(uP * DF);
     if (!e) e = d.dvc.reserve(uP * DF * 16);
     if (!e) e = d.dvo.reserve(uP * DF * 4);
+    if (!e) e = d.offs.reserve(uP * DF * 4);
     if (!e) e = d.nd.reserve(uP * 4);
     if (!e) e = d.fst.reserve(uP * 4 * 8);
     if (e) {
@@ -569,6 +576,7 @@ rk_status dp_plan(rk_ctx* c) {
     d.view.code = (const uint8_t*)d.code.p;
     d.view.dvc = d.dvc.p;
     d.view.dvo = (const uint32_t*)d.dvo.p;
+    d.view.offs = (const uint32_t*)d.offs.p;
     d.view.nd = (const uint32_t*)d.nd.p;
     d.view.fst = (const uint64_t*)d.fst.p;
     d.view.P = d.P;
@@ -585,20 +593,62 @@ const uint64_t* cand_or_zero(rk_ctx* c, const uint64_t* cand_dev, void* stream) 
     return c->u64_dev + 9;
 }
 
-/* Pass 1 of the memoised path: tables + extremes of [first, first+count). */
+/* Pass 1 of the memoised path: tables, the range's run table (breadth-first
+ * prefix expansion, when <= 2^27 runs) and the extremes of [first, first+count). */
 int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void* stream) {
+    DpPlan& d = c->dp;
+    d.runs_ok = false;
+    d.view.runs = nullptr;
     int e = dp_build(c, stream);
+    const uint32_t n = c->tab.g.n, P = d.P;
+    const uint64_t DF = d.view.Dfact;
+    const uint64_t rb = first / DF, re = count ? (first + count + DF - 1) / DF : rb;
+    if (!e && re > rb && re - rb <= (1ull << 27)) {
+        e = d.runsA.reserve((re - rb) * 16);
+        if (!e) e = d.runsB.reserve((re - rb) * 16);
+        /* level j covers prefixes [a_j, b_j): span_j level-P prefixes under each */
+        std::vector<uint64_t> a(P + 1), b(P + 1);
+        uint64_t span = 1;
+        for (int j = (int)P; j >= 0; j--) {
+            a[j] = rb / span;
+            b[j] = (re - 1) / span + 1;
+            if (j > 0) span *= (n - (uint32_t)(j - 1));
+        }
+        const void* prev = nullptr;
+        for (uint32_t j = 0; j < P && !e; j++) {
+            void* dst = (j & 1u) ? d.runsB.p : d.runsA.p;
+            e = rk_dp_expand(prev, a[j], dst, a[j + 1], b[j + 1] - a[j + 1], n, j, d.view.tid[j], d.view.dk[j], stream,
+                             &c->launches);
+            prev = dst;
+        }
+        if (!e) {
+            d.runs_ok = true;
+            d.runs_first = first;
+            d.runs_count = count;
+            d.runs_ptr = prev;
+            d.view.runs = prev;
+            d.view.runs_base = rb;
+        }
+    }
     if (!e)
-        e = rk_dp_minmax(c->tab_dev, c->dp.view, first, count, rec_dev, c->recs_dev, c->counter_dev, c->max_ctas,
-                         stream, &c->launches);
+        e = rk_dp_minmax(c->tab_dev, d.view, first, count, rec_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream,
+                         &c->launches);
     return e;
 }
 
 /* Pass 2: keys, counts, optional fused histogram (bins <= rk_dp_max_fused_bins()) */
 int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, const rk_stats* range_dev,
              uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev, rk_stats* rec_dev, void* stream) {
-    return rk_dp_keys(c->tab_dev, c->dp.view, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, rec_dev,
-                      stream, &c->launches);
+    DpPlan& d = c->dp;
+    DPView v = d.view;
+    if (d.runs_ok && d.runs_first == first && d.runs_count == count) {
+        v.runs = d.runs_ptr;
+        v.runs_base = first / v.Dfact;
+    } else {
+        v.runs = nullptr; /* another range: walk the transitions */
+    }
+    return rk_dp_keys(c->tab_dev, v, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, rec_dev, stream,
+                      &c->launches);
 }
 
 /* memoised equivalent of rk_launch_eval (stats + optional keys, optional histogram) */

@@ -103,8 +103,11 @@ struct DPView {
     const uint8_t* code;           /* level-P suffix keys as D! one-byte ranks into dv, per node */
     const void* dvc;               /* per node: sorted distinct suffix keys with multiplicities, 16 B each (D! slots) */
     const uint32_t* dvo;           /* the same distinct keys minus the row minimum (32-bit, exact unless nd bit 31) */
+    const uint32_t* offs;          /* per node: the D! keys minus the row minimum, decoded (32-bit, same caveat) */
     const uint32_t* nd;            /* per node: number of distinct suffix keys */
     const uint64_t* fst;           /* per node: min, max, argmin sigma, argmax sigma */
+    const void* runs;              /* optional: expanded run table {node, mask, K lo, hi} (uint4) of runs_base.. */
+    uint64_t runs_base;
     uint32_t P, D, Dfact;
 };
 constexpr uint32_t RK_DP_D = 5; /* suffix depth: 120 keys per level-P node */
@@ -113,10 +116,13 @@ int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t*
                 uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
                 uint64_t work, void* stream, uint32_t* launches);
 int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
-                 uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint64_t nodes, void* stream, uint32_t* launches);
+                 uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
+                 uint32_t* launches);
 int rk_dp_minmax(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, rk_stats* out, rk_stats* recs,
                  uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches);
 uint32_t rk_dp_max_fused_bins();
+int rk_dp_expand(const void* Rj, uint64_t aj, void* Rn, uint64_t an, uint64_t cnt, uint32_t n, uint32_t j,
+                 const uint32_t* tid, const uint64_t* dk, void* stream, uint32_t* launches);
 int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count,
                const uint64_t* cand_dev, const rk_stats* range, uint32_t bins, uint64_t* hist, uint64_t* keys,
                rk_stats* rec, void* stream, uint32_t* launches);

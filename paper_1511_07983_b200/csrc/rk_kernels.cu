@@ -1632,7 +1632,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
                                                                  const uint32_t* __restrict__ cnt_P,
                                                                  uint8_t* __restrict__ code, ulonglong2* __restrict__ dvc,
                                                                  uint32_t* __restrict__ dvo, uint32_t* __restrict__ nd,
-                                                                 uint64_t* __restrict__ fst) {
+                                                                 uint64_t* __restrict__ fst, uint32_t* __restrict__ offs) {
     __shared__ RkTables t;
     __shared__ uint64_t srow[kDpThreads / 32][128];
     load_tables(t, tab);
@@ -1713,10 +1713,13 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
             amx = firstsg;
             rank++;
         }
-        /* codes: sigma = lane + 32q */
+        /* codes and decoded 32-bit offsets from the row minimum: sigma = lane + 32q */
 #pragma unroll
         for (int q = 0; q < 4; q++)
-            if (lane + 32u * q < kDF) code[(uint64_t)u * kDF + lane + 32u * q] = (uint8_t)(cdw >> (8 * q));
+            if (lane + 32u * q < kDF) {
+                code[(uint64_t)u * kDF + lane + 32u * q] = (uint8_t)(cdw >> (8 * q));
+                offs[(uint64_t)u * kDF + lane + 32u * q] = (uint32_t)(v[q] - mn); /* exact unless nd bit 31 */
+            }
         if (lane == 0) {
             nd[u] = rank | ((mx - mn) >> 32 ? 0x80000000u : 0u); /* bit 31: offsets do not fit 32 bits */
             fst[4 * (uint64_t)u] = mn;
@@ -1746,6 +1749,40 @@ __device__ __forceinline__ void dp_walk(const RkGTab& g, const DPView& v, uint64
     }
 }
 
+/* (node, closed key) of a run: from the expanded run table when pass 1 built
+ * one for this range (coalesced), else by walking the transitions */
+__device__ __forceinline__ void dp_run(const RkGTab& g, const DPView& v, uint64_t run, uint32_t& u, uint64_t& Kc) {
+    if (v.runs) {
+        const uint4 e = __ldg(reinterpret_cast<const uint4*>(v.runs) + (run - v.runs_base));
+        u = e.x;
+        Kc = ((uint64_t)e.w << 32) | e.z;
+    } else {
+        dp_walk(g, v, run, u, Kc);
+    }
+}
+
+/* Prefix expansion, level j -> j+1, breadth-first over the range's prefixes:
+ * entry i of level j+1 = (lexicographic prefix index) has parent i / (n-j) and
+ * takes the (i mod (n-j))-th unused kernel of the parent (ascending): the same
+ * factorial-number-system digits as the unranking (reading L11).  Entries are
+ * {node, used mask, K_closed lo, hi}; level 0 is the root. */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_expand_kernel(const uint4* __restrict__ Rj, uint64_t aj,
+                                                                 uint4* __restrict__ Rn, uint64_t an, uint64_t cnt,
+                                                                 uint32_t n, uint32_t j,
+                                                                 const uint32_t* __restrict__ tid,
+                                                                 const uint64_t* __restrict__ dk) {
+    const uint32_t full = (1u << n) - 1u;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * (uint64_t)blockDim.x) {
+        const uint64_t i = an + x, parent = i / (n - j);
+        const uint32_t d = (uint32_t)(i - parent * (n - j));
+        const uint4 e = j ? __ldg(Rj + (parent - aj)) : make_uint4(0, 0, 0, 0);
+        const uint32_t k = nth_set_bit(full & ~e.y, d);
+        const uint32_t c = e.x * n + k;
+        const uint64_t Kc = (((uint64_t)e.w << 32) | e.z) + __ldg(dk + c);
+        Rn[x] = make_uint4(__ldg(tid + c), e.y | (1u << k), (uint32_t)Kc, (uint32_t)(Kc >> 32));
+    }
+}
+
 /* Pass 1: extremes (min/argmin, max/argmax; smallest index on ties) and the
  * count of [first, first+count); n_lt = n_eq = 0, n_gt = count (pass 2 adds). */
 __global__ void __launch_bounds__(kDpThreads) rk_dp_minmax_kernel(const RkTables* __restrict__ tab, DPView v,
@@ -1761,7 +1798,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_minmax_kernel(const RkTables
     for (uint64_t run = rb + blockIdx.x * blockDim.x + threadIdx.x; run < re; run += gridDim.x * blockDim.x) {
         uint32_t u;
         uint64_t Kc;
-        dp_walk(g, v, run, u, Kc);
+        dp_run(g, v, run, u, Kc);
         const uint64_t idx0 = run * DF;
         const uint32_t olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
         const uint32_t ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : (uint32_t)DF;
@@ -1835,7 +1872,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* 
         uint64_t Kb = 0; /* closed-round key + the row minimum: key = Kb + offset */
         if (run < re) {
             uint64_t Kc;
-            dp_walk(g, v, run, u, Kc);
+            dp_run(g, v, run, u, Kc);
             const uint64_t idx0 = run * DF;
             olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
             ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF;
@@ -1882,31 +1919,35 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* 
         const uint32_t s0 = 4u * lane;
         const bool act = s0 < DF;                  /* lanes 30, 31 hold no keys (DF = 120) */
         uint64_t* out = keys + (base * DF - first) + s0; /* only dereferenced when keys != nullptr */
-        /* software pipeline: run i+1's node data is in flight while run i is stored */
-        uint32_t p_nd, p_cw, p_do;
+        /* software pipeline: run i+1's decoded offsets are in flight while run i is stored */
+        uint32_t p_nd;
+        uint4 p_of;
         {
             const uint32_t u0 = __shfl_sync(0xFFFFFFFFu, u, 0);
             p_nd = __ldg(v.nd + u0);
-            p_cw = act ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)u0 * DF) + lane) : 0u;
-            p_do = __ldg(v.dvo + (uint64_t)u0 * DF + lane);
+            p_of = act ? __ldg(reinterpret_cast<const uint4*>(v.offs + (uint64_t)u0 * DF) + lane) : make_uint4(0, 0, 0, 0);
         }
         for (uint32_t i = 0; i < nr; i++) {
             const uint32_t ui = __shfl_sync(0xFFFFFFFFu, u, i);
             const uint64_t Ki = __shfl_sync(0xFFFFFFFFu, Kb, i);
-            const uint32_t ndv = p_nd, cw = p_cw, dlo = p_do;
+            const uint32_t ndv = p_nd;
+            const uint4 of = p_of;
             if (i + 1 < nr) {
                 const uint32_t un = __shfl_sync(0xFFFFFFFFu, u, i + 1);
                 p_nd = __ldg(v.nd + un);
-                p_cw = act ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)un * DF) + lane) : 0u;
-                p_do = __ldg(v.dvo + (uint64_t)un * DF + lane);
+                p_of = act ? __ldg(reinterpret_cast<const uint4*>(v.offs + (uint64_t)un * DF) + lane)
+                           : make_uint4(0, 0, 0, 0);
             }
             uint64_t k[4];
-            if (ndv <= 32u) { /* 32-bit offsets, at most 32 distinct values: one shuffle per key */
-#pragma unroll
-                for (int q = 0; q < 4; q++) k[q] = Ki + __shfl_sync(0xFFFFFFFFu, dlo, __byte_perm(cw, 0, 0x4440 + q));
-            } else {
+            if (!(ndv >> 31)) { /* 32-bit offsets from the row minimum (the common case) */
+                k[0] = Ki + of.x;
+                k[1] = Ki + of.y;
+                k[2] = Ki + of.z;
+                k[3] = Ki + of.w;
+            } else { /* row spans >= 2^32: codes into the 64-bit distinct values */
                 const ulonglong2* dr = dvc + (uint64_t)ui * DF;
                 const uint64_t fmn = __ldg(v.fst + 4ull * ui);
+                const uint32_t cw = act ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)ui * DF) + lane) : 0u;
 #pragma unroll
                 for (int q = 0; q < 4; q++) k[q] = Ki - fmn + __ldg(&dr[__byte_perm(cw, 0, 0x4440 + q)].x);
             }
@@ -2291,8 +2332,9 @@ int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t*
 }
 
 int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
-                 uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint64_t nodes, void* stream, uint32_t* launches) {
-#define RK_DP_SUF_ARGS(SMAX) tab, (const DNode<SMAX>*)UP, cnt_P, code, (ulonglong2*)dvc, dvo, nd, fst
+                 uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
+                 uint32_t* launches) {
+#define RK_DP_SUF_ARGS(SMAX) tab, (const DNode<SMAX>*)UP, cnt_P, code, (ulonglong2*)dvc, dvo, nd, fst, offs
     const unsigned grid = dp_grid(nodes * 32);
     cudaStream_t st = (cudaStream_t)stream;
     switch (variant(S)) {
@@ -2346,3 +2388,11 @@ int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t co
     return (int)cudaGetLastError();
 }
 
+
+int rk_dp_expand(const void* Rj, uint64_t aj, void* Rn, uint64_t an, uint64_t cnt, uint32_t n, uint32_t j,
+                 const uint32_t* tid, const uint64_t* dk, void* stream, uint32_t* launches) {
+    rk_dp_expand_kernel<<<dp_grid(cnt), kDpThreads, 0, (cudaStream_t)stream>>>((const uint4*)Rj, aj, (uint4*)Rn, an,
+                                                                              cnt, n, j, tid, dk);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
