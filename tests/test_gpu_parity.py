@@ -807,6 +807,11 @@ def test_memo_keys_equal_direct_keys(monkeypatch):
     ctx = _direct_ctx(monkeypatch, "RK_FORCE_MEMO")
     try:
         cases = [W.config(c) for c in ("C2", "C3", "C4")]
+        # huge per-block work: suffix rows span >= 2^32 (the 64-bit decode path)
+        for ks in W.random_small_sets(0x91DE, 4, 7, 8):
+            wide = [(k[0], k[1], k[2], k[3], min(k[4] * 797, (1 << 32) - 1), min(k[5] * 787, (1 << 32) - 1)) for k in ks]
+            if W.key_bound(W.GTX580, wide) < (1 << 62):
+                cases.append((W.GTX580, wide))
         for gi, gpu in enumerate(GPUS):
             for ks in W.random_small_sets(0xDEC0 + gi, 6, 6, 9, gpu=gpu):
                 if all(W.feasible(gpu, k) for k in ks):
@@ -835,6 +840,19 @@ def test_memo_keys_equal_direct_keys(monkeypatch):
                 s2 = d.rk_eval_range(first, count, cand, keys_dev=k2)
                 assert s1.as_tuple() == s2.as_tuple(), (gpu, ks, first, count)
                 assert torch.equal(k1, k2)
+                # the two-pass API with the fused histogram == histogram of the direct keys
+                for B in (7, 256):
+                    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+                    cd = torch.tensor([cand], dtype=torch.int64, device="cuda")
+                    h1 = torch.zeros(B, dtype=torch.int64, device="cuda")
+                    ctx.rk_sweep_pass1_async(first, count, cd, rec, None)
+                    ctx.rk_sweep_pass2_async(first, count, cd, rec, B, h1, None, rec)
+                    h2 = torch.zeros(B, dtype=torch.int64, device="cuda")
+                    d.rk_histogram(k2, count, s2.key_min, s2.key_max, B, h2)
+                    torch.cuda.synchronize()
+                    assert torch.equal(h1, h2), (first, count, B)
+                    assert rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes())).as_tuple() \
+                        == s2.as_tuple()
             if ctx.rk_memo_info()[0]:
                 checked += 1
         assert checked >= 10
