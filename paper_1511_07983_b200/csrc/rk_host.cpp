@@ -510,7 +510,7 @@ rk_status dp_plan(rk_ctx* c) {
     d.on = false;
     d.runs_ok = false;
     const uint32_t n = c->tab.g.n, S = c->tab.g.S;
-    if (c->device < 0 || c->no_memo || c->force_runs || S > RK_SMAX || n < RK_DP_D + 1) return RK_OK;
+    if (c->device < 0 || c->no_memo || c->force_runs || n < RK_DP_D + 1) return RK_OK; /* S > 32: run-length nodes */
     const uint64_t kLimitEntries = 1ull << 26, kLimitBytes = 1ull << 31;
     d.P = n - RK_DP_D;
     d.node_bytes = rk_dp_node_bytes(S);

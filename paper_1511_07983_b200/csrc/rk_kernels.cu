@@ -1523,15 +1523,80 @@ __device__ __forceinline__ bool dnode_eq_ldcg(const DNode<SMAX>* stored, const D
     return eq;
 }
 
+/* run-length nodes (S' > 32): unused run slots are zero, so equal states have
+ * equal words (hash and compare) */
+template <>
+struct DNode<0> {
+    uint32_t fa[RK_RUNS], fb[RK_RUNS], st[RK_RUNS];
+    uint32_t nr, cur, mask, pad;
+    uint64_t I, M;
+};
+
 template <int SMAX, bool FULL>
 __device__ __forceinline__ void dnode_fresh(DNode<SMAX>& d, const RkGTab& g) {
+    if constexpr (SMAX == 0) {
+        for (int i = 0; i < RK_RUNS; i++) d.fa[i] = d.fb[i] = d.st[i] = 0;
+        d.fa[0] = g.freshA;
+        d.fb[0] = g.freshB;
+        d.nr = 1;
+        d.pad = 0;
+    } else {
 #pragma unroll
-    for (int i = 0; i < SMAX; i++) {
-        d.fa[i] = live_sm<SMAX, FULL>(i, g) ? g.freshA : 0u;
-        d.fb[i] = live_sm<SMAX, FULL>(i, g) ? g.freshB : 0u;
+        for (int i = 0; i < SMAX; i++) {
+            d.fa[i] = live_sm<SMAX, FULL>(i, g) ? g.freshA : 0u;
+            d.fb[i] = live_sm<SMAX, FULL>(i, g) ? g.freshB : 0u;
+        }
     }
     d.cur = d.mask = 0;
     d.I = d.M = 0;
+}
+
+/* node -> placement state (closed key 0) */
+template <int SMAX>
+__device__ __forceinline__ void node_to_st(const DNode<SMAX>& d, St<SMAX>& s) {
+    if constexpr (SMAX == 0) {
+        for (int i = 0; i < RK_RUNS; i++) {
+            s.fa[i] = d.fa[i];
+            s.fb[i] = d.fb[i];
+            s.st[i] = d.st[i];
+        }
+        s.nr = d.nr;
+    } else {
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            s.fa[i] = d.fa[i];
+            s.fb[i] = d.fb[i];
+        }
+    }
+    s.cur = d.cur;
+    s.I = d.I;
+    s.M = d.M;
+    s.K = 0;
+}
+
+/* placement state -> canonical node words */
+template <int SMAX>
+__device__ __forceinline__ void st_to_node(const St<SMAX>& s, uint32_t mask, DNode<SMAX>& d) {
+    if constexpr (SMAX == 0) {
+        for (int i = 0; i < RK_RUNS; i++) {
+            const bool used = (uint32_t)i < s.nr;
+            d.fa[i] = used ? s.fa[i] : 0u;
+            d.fb[i] = used ? s.fb[i] : 0u;
+            d.st[i] = used ? s.st[i] : 0u;
+        }
+        d.nr = s.nr;
+        d.pad = 0;
+    } else {
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            d.fa[i] = s.fa[i];
+            d.fb[i] = s.fb[i];
+        }
+    }
+    d.cur = s.cur;
+    d.mask = mask;
+    d.I = s.I;
+    d.M = s.M;
 }
 
 /* One level: nodes of level j (count *cnt_j; nullptr = the fresh root) x unused kernels. */
@@ -1558,26 +1623,10 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
             continue;
         }
         St<SMAX> s, s2;
-#pragma unroll
-        for (int i = 0; i < SMAX; i++) {
-            s.fa[i] = nd.fa[i];
-            s.fb[i] = nd.fb[i];
-        }
-        s.cur = nd.cur;
-        s.I = nd.I;
-        s.M = nd.M;
-        s.K = 0;
+        node_to_st<SMAX>(nd, s);
         place<SMAX, FULL>(s, s2, t.k[k], k, g, nr);
         DNode<SMAX> o;
-#pragma unroll
-        for (int i = 0; i < SMAX; i++) {
-            o.fa[i] = s2.fa[i];
-            o.fb[i] = s2.fb[i];
-        }
-        o.cur = s2.cur;
-        o.mask = nd.mask | (1u << k);
-        o.I = s2.I;
-        o.M = s2.M;
+        st_to_node<SMAX>(s2, nd.mask | (1u << k), o);
         uint32_t pos = (uint32_t)dnode_hash(o) & tmask, id = kDpEmpty;
         for (;;) {
             uint32_t v = atomicCAS(&table[pos], kDpEmpty, kDpBusy);
@@ -1647,15 +1696,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
             if (!((nd0.mask >> k) & 1u)) rem |= k << (4u * q0++);
         if (lane < 20) {
             St<SMAX> s;
-#pragma unroll
-            for (int i = 0; i < SMAX; i++) {
-                s.fa[i] = nd0.fa[i];
-                s.fb[i] = nd0.fb[i];
-            }
-            s.cur = nd0.cur;
-            s.I = nd0.I;
-            s.M = nd0.M;
-            s.K = 0;
+            node_to_st<SMAX>(nd0, s);
             const uint32_t a = lane >> 2, b = lane & 3u;
             const uint32_t ka = (rem >> (4u * a)) & 15u;
             const uint32_t r4 = (rem & ((1u << (4u * a)) - 1u)) | ((rem >> (4u * a + 4u)) << (4u * a));
@@ -2315,7 +2356,7 @@ uint32_t rk_dp_node_bytes(uint32_t S) {
         case 4: case 5: return sizeof(DNode<8>);
         case 6: case 7: return sizeof(DNode<16>);
         case 8: case 9: return sizeof(DNode<32>);
-        default: return 0;
+        default: return sizeof(DNode<0>);
     }
 }
 
@@ -2336,7 +2377,7 @@ int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t*
         case 7: rk_dp_level_kernel<16, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(16)); break;
         case 8: rk_dp_level_kernel<32, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(32)); break;
         case 9: rk_dp_level_kernel<32, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(32)); break;
-        default: return (int)cudaErrorInvalidValue;
+        default: rk_dp_level_kernel<0, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(0)); break;
     }
 #undef RK_DP_LEVEL_ARGS
     if (launches) (*launches)++;
@@ -2360,7 +2401,7 @@ int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t
         case 7: rk_dp_suffix_kernel<16, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(16)); break;
         case 8: rk_dp_suffix_kernel<32, false><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(32)); break;
         case 9: rk_dp_suffix_kernel<32, true><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(32)); break;
-        default: return (int)cudaErrorInvalidValue;
+        default: rk_dp_suffix_kernel<0, false><<<grid, kDpThreads, 0, st>>>(RK_DP_SUF_ARGS(0)); break;
     }
 #undef RK_DP_SUF_ARGS
     if (launches) (*launches)++;

@@ -893,3 +893,40 @@ def test_memo_two_pass_api_and_fused_histogram(ctx):
     ranks = sorted(int(r) for r in g["order_stats"])
     got = ctx.rk_select_keys(keys, N, st.key_min, st.key_max, ranks)
     assert got == [g["order_stats"][str(r)] for r in ranks]
+
+
+def test_memo_run_length_nodes_vs_oracle_and_direct(monkeypatch):
+    """Memoisation over run-length SM states (S' > 32, e.g. the B200 preset):
+    full spaces vs the oracle (memoisation forced on small sets) and C6's every
+    key vs the direct run-length kernel."""
+    fm = _direct_ctx(monkeypatch, "RK_FORCE_MEMO")
+    d = _direct_ctx(monkeypatch)
+    try:
+        done = 0
+        for gi, gpu in enumerate(BIG_GPUS[:3]):
+            rng = W.SplitMix64(0x7A11 + gi)
+            for q in range(3):
+                ks = W.gen_b200(rng, 6 + q % 2, gpu=gpu) if gpu[3] >= 64 else \
+                    W.random_small_sets(0x7A11 + gi * 7 + q, 1, 6, 7, gpu=gpu)[0]
+                if not all(W.feasible(gpu, k) for k in ks):
+                    continue
+                fm.rk_set_gpu_params(gpu)
+                fm.rk_set_kernels(ks)
+                assert fm.rk_memo_info()[0]
+                check_full_space(fm, gpu, ks, bins=(9,))
+                done += 1
+        assert done >= 5
+        gpu, ks = W.config("C6")
+        N = math.factorial(12)
+        for c in (fm, d):
+            c.rk_set_gpu_params(gpu)
+            c.rk_set_kernels(ks)
+        assert fm.rk_memo_info()[0] and not d.rk_memo_info()[0]
+        k1 = torch.zeros(N, dtype=torch.int64, device="cuda")
+        k2 = torch.zeros(N, dtype=torch.int64, device="cuda")
+        s1 = fm.rk_eval_range(0, N, 0, keys_dev=k1)
+        s2 = d.rk_eval_range(0, N, 0, keys_dev=k2)
+        assert s1.as_tuple() == s2.as_tuple() and torch.equal(k1, k2)
+    finally:
+        fm.close()
+        d.close()
