@@ -1881,20 +1881,8 @@ constexpr uint32_t kDpEdgeBins = 32768; /* fused histogram up to this many share
  * the 4 keys 4l..4l+3 (one 32-bit word of codes, 4 gathers from the node's
  * distinct values in L1) and stores 32 B (coalesced, streaming stores).  L2
  * reads per run: 120 B of codes + the distinct values, instead of a 960-B row. */
-#ifndef RK_DP_STORE
-#define RK_DP_STORE 0
-#endif
-/* key-stream stores: 0 = streaming (evict-first), 1 = default write-back */
-template <class T>
-__device__ __forceinline__ void rk_st(T* p, const T& x) {
-    if (RK_DP_STORE == 0) __stcs(p, x);
-    else *p = x;
-}
-#ifndef RK_DP_KEYS_MINB
-#define RK_DP_KEYS_MINB 1
-#endif
 template <bool HIST>
-__global__ void __launch_bounds__(kDpThreads, RK_DP_KEYS_MINB) rk_dp_keys_kernel(const RkTables* __restrict__ tab, DPView v,
+__global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* __restrict__ tab, DPView v,
                                                                uint64_t first, uint64_t count,
                                                                const uint64_t* __restrict__ cand_dev,
                                                                const rk_stats* __restrict__ range, uint32_t bins,
@@ -2008,11 +1996,11 @@ __global__ void __launch_bounds__(kDpThreads, RK_DP_KEYS_MINB) rk_dp_keys_kernel
             if (grp_whole) { /* warp-uniform: every run of the group lies inside the range */
                 if (keys && act) {
                     if (aligned) {
-                        rk_st(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(k[0], k[1]));
-                        rk_st(reinterpret_cast<ulonglong2*>(o) + 1, make_ulonglong2(k[2], k[3]));
+                        __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(k[0], k[1]));
+                        __stcs(reinterpret_cast<ulonglong2*>(o) + 1, make_ulonglong2(k[2], k[3]));
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 4; q++) rk_st(o + q, k[q]);
+                        for (int q = 0; q < 4; q++) __stcs(o + q, k[q]);
                     }
                 }
             } else {
@@ -2021,7 +2009,7 @@ __global__ void __launch_bounds__(kDpThreads, RK_DP_KEYS_MINB) rk_dp_keys_kernel
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
                     if (act && s0 + q >= oi && s0 + q < hi_i) {
-                        if (keys) rk_st(o + q, k[q]);
+                        if (keys) __stcs(o + q, k[q]);
                         if (!whole) { /* range-edge run: per-key counts and bins */
                             nlt += k[q] < cand;
                             neq += k[q] == cand;
