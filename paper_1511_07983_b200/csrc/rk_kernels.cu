@@ -1957,59 +1957,82 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* 
          * store each run's 960-B key block; lane l owns keys 4l..4l+3 */
         const uint32_t nr = (uint32_t)min((uint64_t)32, re - base);
         const bool grp_whole = base * DF >= lo && (base + nr) * DF <= hi; /* no range-edge run */
-        const uint32_t s0 = 4u * lane;
-        const bool act = s0 < DF;                  /* lanes 30, 31 hold no keys (DF = 120) */
-        uint64_t* out = keys + (base * DF - first) + s0; /* only dereferenced when keys != nullptr */
-        /* software pipeline: run i+1's decoded offsets are in flight while run i is stored */
+        /* two runs per step, a half-warp each: lane hl of a half owns the key pairs
+         * (2c, 2c+1), c = 15q + hl (q = 0..3), so every load (8 B of offsets) and
+         * store (16 B of keys) instruction of a half covers one contiguous span */
+        const uint32_t half = lane >> 4, hl = lane & 15u;
+        const bool act = hl < 15u; /* 15 lanes x 4 pairs = DF / 2 = 60 */
+        uint64_t* outb = keys + (base * DF - first) + 2u * hl; /* only dereferenced when keys != nullptr */
+        /* software pipeline: the next pair of runs' offsets is in flight while this pair is stored */
         uint32_t p_nd;
-        uint4 p_of;
+        uint2 p_o[4];
         {
-            const uint32_t u0 = __shfl_sync(0xFFFFFFFFu, u, 0);
+            const uint32_t src = min(half, nr - 1);
+            const uint32_t u0 = __shfl_sync(0xFFFFFFFFu, u, src);
             p_nd = __ldg(v.nd + u0);
-            p_of = act ? __ldg(reinterpret_cast<const uint4*>(v.offs + (uint64_t)u0 * DF) + lane) : make_uint4(0, 0, 0, 0);
+            const uint2* r = reinterpret_cast<const uint2*>(v.offs + (uint64_t)u0 * DF) + hl;
+#pragma unroll
+            for (int q = 0; q < 4; q++) p_o[q] = act ? __ldg(r + 15 * q) : make_uint2(0, 0);
         }
-        for (uint32_t i = 0; i < nr; i++) {
-            const uint32_t ui = __shfl_sync(0xFFFFFFFFu, u, i);
-            const uint64_t Ki = __shfl_sync(0xFFFFFFFFu, Kb, i);
+        for (uint32_t i0 = 0; i0 < nr; i0 += 2) {
+            const uint32_t i = i0 + half;
+            const bool valid = i < nr;
+            const uint32_t src = valid ? i : i0;
+            const uint32_t ui = __shfl_sync(0xFFFFFFFFu, u, src);
+            const uint64_t Ki = __shfl_sync(0xFFFFFFFFu, Kb, src);
             const uint32_t ndv = p_nd;
-            const uint4 of = p_of;
-            if (i + 1 < nr) {
-                const uint32_t un = __shfl_sync(0xFFFFFFFFu, u, i + 1);
+            uint2 of[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) of[q] = p_o[q];
+            if (i0 + 2 < nr) {
+                const uint32_t srcn = min(i0 + 2 + half, nr - 1);
+                const uint32_t un = __shfl_sync(0xFFFFFFFFu, u, srcn);
                 p_nd = __ldg(v.nd + un);
-                p_of = act ? __ldg(reinterpret_cast<const uint4*>(v.offs + (uint64_t)un * DF) + lane)
-                           : make_uint4(0, 0, 0, 0);
+                const uint2* r = reinterpret_cast<const uint2*>(v.offs + (uint64_t)un * DF) + hl;
+#pragma unroll
+                for (int q = 0; q < 4; q++) p_o[q] = act ? __ldg(r + 15 * q) : make_uint2(0, 0);
             }
-            uint64_t k[4];
+            uint64_t k[8]; /* k[2q], k[2q+1] = keys 2c, 2c+1 of c = 15q + hl */
             if (!(ndv >> 31)) { /* 32-bit offsets from the row minimum (the common case) */
-                k[0] = Ki + of.x;
-                k[1] = Ki + of.y;
-                k[2] = Ki + of.z;
-                k[3] = Ki + of.w;
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    k[2 * q] = Ki + of[q].x;
+                    k[2 * q + 1] = Ki + of[q].y;
+                }
             } else { /* row spans >= 2^32: codes into the 64-bit distinct values */
                 const ulonglong2* dr = dvc + (uint64_t)ui * DF;
                 const uint64_t fmn = __ldg(v.fst + 4ull * ui);
-                const uint32_t cw = act ? __ldg(reinterpret_cast<const uint32_t*>(v.code + (uint64_t)ui * DF) + lane) : 0u;
+                const uint8_t* cr = v.code + (uint64_t)ui * DF;
 #pragma unroll
-                for (int q = 0; q < 4; q++) k[q] = Ki - fmn + __ldg(&dr[__byte_perm(cw, 0, 0x4440 + q)].x);
+                for (int q = 0; q < 4; q++) {
+                    const uint32_t c2 = 2u * (15u * q + hl);
+                    k[2 * q] = act ? Ki - fmn + __ldg(&dr[__ldg(cr + c2)].x) : 0ull;
+                    k[2 * q + 1] = act ? Ki - fmn + __ldg(&dr[__ldg(cr + c2 + 1)].x) : 0ull;
+                }
             }
-            uint64_t* o = out + (size_t)i * DF;
+            uint64_t* o = outb + (size_t)i * DF;
             if (grp_whole) { /* warp-uniform: every run of the group lies inside the range */
-                if (keys && act) {
+                if (keys && act && valid) {
                     if (aligned) {
-                        __stcs(reinterpret_cast<ulonglong2*>(o), make_ulonglong2(k[0], k[1]));
-                        __stcs(reinterpret_cast<ulonglong2*>(o) + 1, make_ulonglong2(k[2], k[3]));
+#pragma unroll
+                        for (int q = 0; q < 4; q++)
+                            __stcs(reinterpret_cast<ulonglong2*>(o + 30 * q), make_ulonglong2(k[2 * q], k[2 * q + 1]));
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 4; q++) __stcs(o + q, k[q]);
+                        for (int q = 0; q < 4; q++) {
+                            __stcs(o + 30 * q, k[2 * q]);
+                            __stcs(o + 30 * q + 1, k[2 * q + 1]);
+                        }
                     }
                 }
             } else {
-                const uint32_t oi = __shfl_sync(0xFFFFFFFFu, olo, i), hi_i = __shfl_sync(0xFFFFFFFFu, ohi, i);
+                const uint32_t oi = __shfl_sync(0xFFFFFFFFu, olo, src), hi_i = __shfl_sync(0xFFFFFFFFu, ohi, src);
                 const bool whole = oi == 0 && hi_i == DF;
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    if (act && s0 + q >= oi && s0 + q < hi_i) {
-                        if (keys) __stcs(o + q, k[q]);
+                for (int q = 0; q < 8; q++) {
+                    const uint32_t sg = 2u * (15u * (q >> 1) + hl) + (q & 1);
+                    if (valid && act && sg >= oi && sg < hi_i) {
+                        if (keys) __stcs(o + 30 * (q >> 1) + (q & 1), k[q]);
                         if (!whole) { /* range-edge run: per-key counts and bins */
                             nlt += k[q] < cand;
                             neq += k[q] == cand;
