@@ -1719,7 +1719,57 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
         for (int q = 0; q < 4; q++) done |= (lane + 32u * q < kDF ? 0u : 1u) << q;
         uint64_t mn = 0, mx = 0;
         uint32_t amn = 0, amx = 0;
-        for (;;) {
+        /* the row's range: when it spans < 2^32 (the common case) the rounds run on
+         * 32-bit offsets with one REDUX.MIN per round */
+        uint64_t r_lo = ~0ull, r_hi = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            if (!((done >> q) & 1u)) {
+                r_lo = v[q] < r_lo ? v[q] : r_lo;
+                r_hi = v[q] > r_hi ? v[q] : r_hi;
+            }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t y = __shfl_xor_sync(0xFFFFFFFFu, r_lo, o), z = __shfl_xor_sync(0xFFFFFFFFu, r_hi, o);
+            r_lo = y < r_lo ? y : r_lo;
+            r_hi = z > r_hi ? z : r_hi;
+        }
+        const bool narrow = ((r_hi - r_lo) >> 32) == 0;
+        for (uint32_t processed = 0; narrow && processed < kDF;) {
+            uint32_t w32[4], lm = 0xFFFFFFFFu;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                w32[q] = (uint32_t)(v[q] - r_lo);
+                if (!((done >> q) & 1u) && w32[q] < lm) lm = w32[q];
+            }
+            lm = __reduce_min_sync(0xFFFFFFFFu, lm);
+            uint32_t cnt = 0, firstsg = 0xFFFFFFFFu;
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const bool hit = !((done >> q) & 1u) && w32[q] == lm;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, hit);
+                cnt += __popc(bal);
+                if (bal && firstsg == 0xFFFFFFFFu) firstsg = 32u * q + (uint32_t)(__ffs(bal) - 1);
+                if (hit) {
+                    done |= 1u << q;
+                    cdw |= rank << (8 * q);
+                }
+            }
+            const uint64_t val = r_lo + lm;
+            if (rank == 0) {
+                mn = val;
+                amn = firstsg;
+            }
+            if (lane == 0) {
+                dvc[(uint64_t)u * kDF + rank] = make_ulonglong2(val, cnt);
+                dvo[(uint64_t)u * kDF + rank] = lm;
+            }
+            mx = val;
+            amx = firstsg;
+            rank++;
+            processed += cnt;
+        }
+        for (; !narrow;) {
             uint64_t lm = ~0ull;
 #pragma unroll
             for (int q = 0; q < 4; q++)
