@@ -472,7 +472,7 @@ uint32_t pow2_at_least(uint64_t x) {
 
 /* Enqueue levels j0..j1-1 of the plan's table build (level j reads level j's
  * nodes and count, writes level j+1). */
-int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream) {
+int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vector<RkExpand>* ex = nullptr) {
     DpPlan& d = c->dp;
     const uint32_t n = c->tab.g.n, S = c->tab.g.S;
     char* nodes = (char*)d.nodes.p;
@@ -480,20 +480,26 @@ int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream) {
     int e = 0;
     for (uint32_t j = j0; j < j1 && !e; j++) {
         const void* Uj = j ? nodes + d.noff[j] : nullptr;
+        /* the launch of level j also expands the range's prefixes of level j-1 -> j */
+        const RkExpand* x = (ex && j >= 1 && j - 1 < ex->size()) ? &(*ex)[j - 1] : nullptr;
         e = rk_dp_level(c->tab_dev, S, Uj, j ? ctr + j : nullptr, nodes + d.noff[j + 1], ctr + j + 1, d.cap[j + 1],
                         (uint32_t*)d.tables.p + d.toff[j + 1], d.tmask[j + 1], (uint32_t*)d.tid.p + d.xoff[j],
-                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.P + 1, (uint64_t)d.cnt[j] * n, stream, &c->launches);
+                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.P + 1, (uint64_t)d.cnt[j] * n, stream, &c->launches,
+                        x);
     }
     return e;
 }
 
-/* Enqueue the table build of the current plan: clear, P levels, suffix tables. */
-int dp_build(rk_ctx* c, void* stream) {
+/* Enqueue the table build of the current plan: clear, P levels (+ the given
+ * prefix expansions, level j-1 -> j in level j's launch, the last one after),
+ * suffix tables. */
+int dp_build(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr) {
     DpPlan& d = c->dp;
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
     if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.P + 2) * 4, st);
-    if (!e) e = dp_levels(c, 0, d.P, stream);
+    if (!e) e = dp_levels(c, 0, d.P, stream, ex);
+    if (!e && ex && ex->size() == d.P) e = rk_dp_expand(ex->back(), c->tab.g.n, stream, &c->launches);
     if (!e)
         e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
                          (uint8_t*)d.code.p, d.dvc.p, (uint32_t*)d.dvo.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
@@ -599,11 +605,12 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
     DpPlan& d = c->dp;
     d.runs_ok = false;
     d.view.runs = nullptr;
-    int e = dp_build(c, stream);
     const uint32_t n = c->tab.g.n, P = d.P;
     const uint64_t DF = d.view.Dfact;
     const uint64_t rb = first / DF, re = count ? (first + count + DF - 1) / DF : rb;
-    if (!e && re > rb && re - rb <= (1ull << 27)) {
+    std::vector<RkExpand> ex;
+    int e = 0;
+    if (re > rb && re - rb <= (1ull << 27)) {
         e = d.runsA.reserve((re - rb) * 16);
         if (!e) e = d.runsB.reserve((re - rb) * 16);
         /* level j covers prefixes [a_j, b_j): span_j level-P prefixes under each */
@@ -617,18 +624,18 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
         const void* prev = nullptr;
         for (uint32_t j = 0; j < P && !e; j++) {
             void* dst = (j & 1u) ? d.runsB.p : d.runsA.p;
-            e = rk_dp_expand(prev, a[j], dst, a[j + 1], b[j + 1] - a[j + 1], n, j, d.view.tid[j], d.view.dk[j], stream,
-                             &c->launches);
+            ex.push_back(RkExpand{prev, a[j], dst, a[j + 1], b[j + 1] - a[j + 1], j, d.view.tid[j], d.view.dk[j]});
             prev = dst;
         }
-        if (!e) {
-            d.runs_ok = true;
-            d.runs_first = first;
-            d.runs_count = count;
-            d.runs_ptr = prev;
-            d.view.runs = prev;
-            d.view.runs_base = rb;
-        }
+    }
+    if (!e) e = dp_build(c, stream, ex.empty() ? nullptr : &ex);
+    if (!e && !ex.empty()) {
+        d.runs_ok = true;
+        d.runs_first = first;
+        d.runs_count = count;
+        d.runs_ptr = ex.back().Rn;
+        d.view.runs = ex.back().Rn;
+        d.view.runs_base = rb;
     }
     if (!e)
         e = rk_dp_minmax(c->tab_dev, d.view, first, count, rec_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream,

@@ -112,17 +112,26 @@ struct DPView {
 };
 constexpr uint32_t RK_DP_D = 5; /* suffix depth: 120 keys per level-P node */
 uint32_t rk_dp_node_bytes(uint32_t S);
+/* one prefix-expansion level (entries {node, mask, K lo, hi} as uint4) */
+struct RkExpand {
+    const void* Rj;
+    uint64_t aj;
+    void* Rn;
+    uint64_t an, cnt;
+    uint32_t j;
+    const uint32_t* tid;
+    const uint64_t* dk;
+};
 int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
                 uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
-                uint64_t work, void* stream, uint32_t* launches);
+                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex = nullptr);
 int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
                  uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
                  uint32_t* launches);
 int rk_dp_minmax(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, rk_stats* out, rk_stats* recs,
                  uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches);
 uint32_t rk_dp_max_fused_bins();
-int rk_dp_expand(const void* Rj, uint64_t aj, void* Rn, uint64_t an, uint64_t cnt, uint32_t n, uint32_t j,
-                 const uint32_t* tid, const uint64_t* dk, void* stream, uint32_t* launches);
+int rk_dp_expand(const RkExpand& ex, uint32_t n, void* stream, uint32_t* launches);
 int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count,
                const uint64_t* cand_dev, const rk_stats* range, uint32_t bins, uint64_t* hist, uint64_t* keys,
                rk_stats* rec, void* stream, uint32_t* launches);

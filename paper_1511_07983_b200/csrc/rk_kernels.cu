@@ -1599,20 +1599,49 @@ __device__ __forceinline__ void st_to_node(const St<SMAX>& s, uint32_t mask, DNo
     d.M = s.M;
 }
 
-/* One level: nodes of level j (count *cnt_j; nullptr = the fresh root) x unused kernels. */
+/* Prefix expansion, level j -> j+1, breadth-first over a range's prefixes:
+ * entry i of level j+1 (lexicographic prefix index) has parent i / (n-j) and
+ * takes the (i mod (n-j))-th unused kernel of the parent (ascending): the same
+ * factorial-number-system digits as the unranking (reading L11).  Entries are
+ * {node, used mask, K_closed lo, hi}; level 0 is the root. */
+struct ExpArgs {
+    const uint4* Rj;
+    uint64_t aj;
+    uint4* Rn;
+    uint64_t an, cnt;
+    uint32_t j;
+    const uint32_t* tid;
+    const uint64_t* dk;
+};
+__device__ __forceinline__ void expand_one(const ExpArgs& x, uint64_t i0, uint32_t n) {
+    const uint32_t full = (1u << n) - 1u;
+    const uint64_t i = x.an + i0, parent = i / (n - x.j);
+    const uint32_t d = (uint32_t)(i - parent * (n - x.j));
+    const uint4 e = x.j ? __ldg(x.Rj + (parent - x.aj)) : make_uint4(0, 0, 0, 0);
+    const uint32_t k = nth_set_bit(full & ~e.y, d);
+    const uint32_t c = e.x * n + k;
+    const uint64_t Kc = (((uint64_t)e.w << 32) | e.z) + __ldg(x.dk + c);
+    x.Rn[i0] = make_uint4(__ldg(x.tid + c), e.y | (1u << k), (uint32_t)Kc, (uint32_t)(Kc >> 32));
+}
+
+/* One level: nodes of level j (count *cnt_j; nullptr = the fresh root) x unused
+ * kernels; the same launch also runs the previous level's prefix expansion (xp). */
 template <int SMAX, bool FULL>
 __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables* __restrict__ tab,
                                                                 const DNode<SMAX>* __restrict__ Uj,
                                                                 const uint32_t* __restrict__ cnt_j, DNode<SMAX>* Un,
                                                                 uint32_t* cnt_n, uint32_t cap_n, uint32_t* table,
                                                                 uint32_t tmask, uint32_t* __restrict__ tid,
-                                                                uint64_t* __restrict__ dk, uint32_t* ovf) {
+                                                                uint64_t* __restrict__ dk, uint32_t* ovf, ExpArgs xp) {
     __shared__ RkTables t;
     load_tables(t, tab);
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
     const uint32_t m = Uj ? *cnt_j : 1u;
     NoRec nr;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < xp.cnt;
+         x += gridDim.x * (uint64_t)blockDim.x)
+        expand_one(xp, x, n);
     for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < m * n; c += gridDim.x * blockDim.x) {
         const uint32_t u = c / n, k = c - u * n;
         DNode<SMAX> nd;
@@ -1852,26 +1881,9 @@ __device__ __forceinline__ void dp_run(const RkGTab& g, const DPView& v, uint64_
     }
 }
 
-/* Prefix expansion, level j -> j+1, breadth-first over the range's prefixes:
- * entry i of level j+1 = (lexicographic prefix index) has parent i / (n-j) and
- * takes the (i mod (n-j))-th unused kernel of the parent (ascending): the same
- * factorial-number-system digits as the unranking (reading L11).  Entries are
- * {node, used mask, K_closed lo, hi}; level 0 is the root. */
-__global__ void __launch_bounds__(kDpThreads) rk_dp_expand_kernel(const uint4* __restrict__ Rj, uint64_t aj,
-                                                                 uint4* __restrict__ Rn, uint64_t an, uint64_t cnt,
-                                                                 uint32_t n, uint32_t j,
-                                                                 const uint32_t* __restrict__ tid,
-                                                                 const uint64_t* __restrict__ dk) {
-    const uint32_t full = (1u << n) - 1u;
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * (uint64_t)blockDim.x) {
-        const uint64_t i = an + x, parent = i / (n - j);
-        const uint32_t d = (uint32_t)(i - parent * (n - j));
-        const uint4 e = j ? __ldg(Rj + (parent - aj)) : make_uint4(0, 0, 0, 0);
-        const uint32_t k = nth_set_bit(full & ~e.y, d);
-        const uint32_t c = e.x * n + k;
-        const uint64_t Kc = (((uint64_t)e.w << 32) | e.z) + __ldg(dk + c);
-        Rn[x] = make_uint4(__ldg(tid + c), e.y | (1u << k), (uint32_t)Kc, (uint32_t)(Kc >> 32));
-    }
+__global__ void __launch_bounds__(kDpThreads) rk_dp_expand_kernel(ExpArgs xp, uint32_t n) {
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < xp.cnt; x += gridDim.x * (uint64_t)blockDim.x)
+        expand_one(xp, x, n);
 }
 
 /* Pass 1: extremes (min/argmin, max/argmax; smallest index on ties) and the
@@ -2423,9 +2435,11 @@ uint32_t rk_dp_node_bytes(uint32_t S) {
 
 int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
                 uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
-                uint64_t work, void* stream, uint32_t* launches) {
-#define RK_DP_LEVEL_ARGS(SMAX) tab, (const DNode<SMAX>*)Uj, cnt_j, (DNode<SMAX>*)Un, cnt_n, cap_n, table, tmask, tid, dk, ovf
-    const unsigned grid = dp_grid(work);
+                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex) {
+    ExpArgs xp{};
+    if (ex) xp = ExpArgs{(const uint4*)ex->Rj, ex->aj, (uint4*)ex->Rn, ex->an, ex->cnt, ex->j, ex->tid, ex->dk};
+#define RK_DP_LEVEL_ARGS(SMAX) tab, (const DNode<SMAX>*)Uj, cnt_j, (DNode<SMAX>*)Un, cnt_n, cap_n, table, tmask, tid, dk, ovf, xp
+    const unsigned grid = dp_grid(work > xp.cnt ? work : xp.cnt);
     cudaStream_t st = (cudaStream_t)stream;
     switch (variant(S)) {
         case 0: rk_dp_level_kernel<1, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(1)); break;
@@ -2503,10 +2517,9 @@ int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t co
 }
 
 
-int rk_dp_expand(const void* Rj, uint64_t aj, void* Rn, uint64_t an, uint64_t cnt, uint32_t n, uint32_t j,
-                 const uint32_t* tid, const uint64_t* dk, void* stream, uint32_t* launches) {
-    rk_dp_expand_kernel<<<dp_grid(cnt), kDpThreads, 0, (cudaStream_t)stream>>>((const uint4*)Rj, aj, (uint4*)Rn, an,
-                                                                              cnt, n, j, tid, dk);
+int rk_dp_expand(const RkExpand& ex, uint32_t n, void* stream, uint32_t* launches) {
+    const ExpArgs xp{(const uint4*)ex.Rj, ex.aj, (uint4*)ex.Rn, ex.an, ex.cnt, ex.j, ex.tid, ex.dk};
+    rk_dp_expand_kernel<<<dp_grid(ex.cnt), kDpThreads, 0, (cudaStream_t)stream>>>(xp, n);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
