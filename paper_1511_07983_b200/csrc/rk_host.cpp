@@ -498,8 +498,7 @@ int dp_build(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr)
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
     if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.P + 2) * 4, st);
-    if (!e) e = dp_levels(c, 0, d.P, stream, ex);
-    if (!e && ex && ex->size() == d.P) e = rk_dp_expand(ex->back(), c->tab.g.n, stream, &c->launches);
+    if (!e) e = dp_levels(c, 0, d.P, stream, ex); /* the last expansion level runs with the extremes */
     if (!e)
         e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
                          (uint8_t*)d.code.p, d.dvc.p, (uint32_t*)d.dvo.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
@@ -637,9 +636,9 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
         d.view.runs = ex.back().Rn;
         d.view.runs_base = rb;
     }
-    if (!e)
+    if (!e) /* with the run table: the last expansion level is produced by this launch */
         e = rk_dp_minmax(c->tab_dev, d.view, first, count, rec_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream,
-                         &c->launches);
+                         &c->launches, ex.empty() ? nullptr : &ex.back());
     return e;
 }
 

@@ -1613,7 +1613,7 @@ struct ExpArgs {
     const uint32_t* tid;
     const uint64_t* dk;
 };
-__device__ __forceinline__ void expand_one(const ExpArgs& x, uint64_t i0, uint32_t n) {
+__device__ __forceinline__ uint4 expand_one(const ExpArgs& x, uint64_t i0, uint32_t n) {
     const uint32_t full = (1u << n) - 1u;
     const uint64_t i = x.an + i0, parent = i / (n - x.j);
     const uint32_t d = (uint32_t)(i - parent * (n - x.j));
@@ -1621,7 +1621,9 @@ __device__ __forceinline__ void expand_one(const ExpArgs& x, uint64_t i0, uint32
     const uint32_t k = nth_set_bit(full & ~e.y, d);
     const uint32_t c = e.x * n + k;
     const uint64_t Kc = (((uint64_t)e.w << 32) | e.z) + __ldg(x.dk + c);
-    x.Rn[i0] = make_uint4(__ldg(x.tid + c), e.y | (1u << k), (uint32_t)Kc, (uint32_t)(Kc >> 32));
+    const uint4 r = make_uint4(__ldg(x.tid + c), e.y | (1u << k), (uint32_t)Kc, (uint32_t)(Kc >> 32));
+    x.Rn[i0] = r;
+    return r;
 }
 
 /* One level: nodes of level j (count *cnt_j; nullptr = the fresh root) x unused
@@ -1890,7 +1892,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_expand_kernel(ExpArgs xp, ui
  * count of [first, first+count); n_lt = n_eq = 0, n_gt = count (pass 2 adds). */
 __global__ void __launch_bounds__(kDpThreads) rk_dp_minmax_kernel(const RkTables* __restrict__ tab, DPView v,
                                                                  uint64_t first, uint64_t count, rk_stats* out,
-                                                                 rk_stats* recs, uint32_t* counter) {
+                                                                 rk_stats* recs, uint32_t* counter, ExpArgs xp) {
     __shared__ RkTables t;
     load_tables(t, tab);
     const RkGTab& g = t.g;
@@ -1901,7 +1903,13 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_minmax_kernel(const RkTables
     for (uint64_t run = rb + blockIdx.x * blockDim.x + threadIdx.x; run < re; run += gridDim.x * blockDim.x) {
         uint32_t u;
         uint64_t Kc;
-        dp_run(g, v, run, u, Kc);
+        if (xp.cnt) { /* the last prefix-expansion level is produced here (entry = run - rb) */
+            const uint4 e = expand_one(xp, run - rb, g.n);
+            u = e.x;
+            Kc = ((uint64_t)e.w << 32) | e.z;
+        } else {
+            dp_run(g, v, run, u, Kc);
+        }
         const uint64_t idx0 = run * DF;
         const uint32_t olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
         const uint32_t ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : (uint32_t)DF;
@@ -2484,11 +2492,13 @@ int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t
 }
 
 int rk_dp_minmax(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, rk_stats* out, rk_stats* recs,
-                 uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
+                 uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches, const RkExpand* ex) {
+    ExpArgs xp{};
+    if (ex) xp = ExpArgs{(const uint4*)ex->Rj, ex->aj, (uint4*)ex->Rn, ex->an, ex->cnt, ex->j, ex->tid, ex->dk};
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
     unsigned grid = dp_grid(runs);
     if (grid > max_ctas) grid = max_ctas;
-    rk_dp_minmax_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, out, recs, counter);
+    rk_dp_minmax_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, out, recs, counter, xp);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
