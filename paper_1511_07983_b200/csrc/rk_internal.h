@@ -129,7 +129,6 @@ int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t
                  uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
                  uint32_t* launches);
 uint32_t rk_dp_max_fused_bins();
-int rk_dp_expand(const RkExpand& ex, uint32_t n, void* stream, uint32_t* launches);
 /* pass-1 extremes; ex (optional): the last prefix-expansion level, produced in the same launch */
 int rk_dp_minmax(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, rk_stats* out, rk_stats* recs,
                  uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches,

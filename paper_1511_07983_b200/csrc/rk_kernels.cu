@@ -1883,11 +1883,6 @@ __device__ __forceinline__ void dp_run(const RkGTab& g, const DPView& v, uint64_
     }
 }
 
-__global__ void __launch_bounds__(kDpThreads) rk_dp_expand_kernel(ExpArgs xp, uint32_t n) {
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < xp.cnt; x += gridDim.x * (uint64_t)blockDim.x)
-        expand_one(xp, x, n);
-}
-
 /* Pass 1: extremes (min/argmin, max/argmax; smallest index on ties) and the
  * count of [first, first+count); n_lt = n_eq = 0, n_gt = count (pass 2 adds). */
 __global__ void __launch_bounds__(kDpThreads) rk_dp_minmax_kernel(const RkTables* __restrict__ tab, DPView v,
@@ -2527,9 +2522,3 @@ int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t co
 }
 
 
-int rk_dp_expand(const RkExpand& ex, uint32_t n, void* stream, uint32_t* launches) {
-    const ExpArgs xp{(const uint4*)ex.Rj, ex.aj, (uint4*)ex.Rn, ex.an, ex.cnt, ex.j, ex.tid, ex.dk};
-    rk_dp_expand_kernel<<<dp_grid(ex.cnt), kDpThreads, 0, (cudaStream_t)stream>>>(xp, n);
-    if (launches) (*launches)++;
-    return (int)cudaGetLastError();
-}
