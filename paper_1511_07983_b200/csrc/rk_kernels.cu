@@ -2028,34 +2028,18 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* 
         const uint32_t half = lane >> 4, hl = lane & 15u;
         const bool act = hl < 15u; /* 15 lanes x 4 pairs = DF / 2 = 60 */
         uint64_t* outb = keys + (base * DF - first) + 2u * hl; /* only dereferenced when keys != nullptr */
-        /* software pipeline: the next pair of runs' offsets is in flight while this pair is stored */
-        uint32_t p_nd;
-        uint2 p_o[4];
-        {
-            const uint32_t src = min(half, nr - 1);
-            const uint32_t u0 = __shfl_sync(0xFFFFFFFFu, u, src);
-            p_nd = __ldg(v.nd + u0);
-            const uint2* r = reinterpret_cast<const uint2*>(v.offs + (uint64_t)u0 * DF) + hl;
-#pragma unroll
-            for (int q = 0; q < 4; q++) p_o[q] = act ? __ldg(r + 15 * q) : make_uint2(0, 0);
-        }
         for (uint32_t i0 = 0; i0 < nr; i0 += 2) {
             const uint32_t i = i0 + half;
             const bool valid = i < nr;
             const uint32_t src = valid ? i : i0;
             const uint32_t ui = __shfl_sync(0xFFFFFFFFu, u, src);
             const uint64_t Ki = __shfl_sync(0xFFFFFFFFu, Kb, src);
-            const uint32_t ndv = p_nd;
+            const uint32_t ndv = __ldg(v.nd + ui);
             uint2 of[4];
+            {
+                const uint2* r = reinterpret_cast<const uint2*>(v.offs + (uint64_t)ui * DF) + hl;
 #pragma unroll
-            for (int q = 0; q < 4; q++) of[q] = p_o[q];
-            if (i0 + 2 < nr) {
-                const uint32_t srcn = min(i0 + 2 + half, nr - 1);
-                const uint32_t un = __shfl_sync(0xFFFFFFFFu, u, srcn);
-                p_nd = __ldg(v.nd + un);
-                const uint2* r = reinterpret_cast<const uint2*>(v.offs + (uint64_t)un * DF) + hl;
-#pragma unroll
-                for (int q = 0; q < 4; q++) p_o[q] = act ? __ldg(r + 15 * q) : make_uint2(0, 0);
+                for (int q = 0; q < 4; q++) of[q] = act ? __ldg(r + 15 * q) : make_uint2(0, 0);
             }
             uint64_t k[8]; /* k[2q], k[2q+1] = keys 2c, 2c+1 of c = 15q + hl */
             if (!(ndv >> 31)) { /* 32-bit offsets from the row minimum (the common case) */
