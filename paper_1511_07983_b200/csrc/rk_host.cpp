@@ -63,6 +63,8 @@ struct DpPlan {
     Arena nodes, tables, tid, dk, fst, counters; /* counters: P + 1 node counters, then the overflow flag */
     Arena code, dvc, dvo, nd, offs;              /* suffix rows: byte codes into sorted distinct (value, count) */
     Arena runsA, runsB;                          /* prefix expansion (ping-pong); the last level is the run table */
+    bool planned = false;                        /* sizes below belong to plan_tab (byte-identical tables) */
+    RkTables plan_tab{};
     bool runs_ok = false;
     uint64_t runs_first = 0, runs_count = 0;
     const void* runs_ptr = nullptr;
@@ -462,6 +464,7 @@ void dp_free(DpPlan& d) {
     for (Arena* a : {&d.code, &d.dvc, &d.dvo, &d.nd, &d.offs, &d.runsA, &d.runsB}) a->release();
     d.runs_ok = false;
     d.on = false;
+    d.planned = false;
 }
 
 uint32_t pow2_at_least(uint64_t x) {
@@ -512,6 +515,10 @@ int dp_build(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr)
  * pay.  Buffers are grow-only arenas: no allocation once they are large enough. */
 rk_status dp_plan(rk_ctx* c) {
     DpPlan& d = c->dp;
+    /* the plan is sizes only (per-level node counts): for byte-identical tables it
+     * is the same, so keep it; every step still rebuilds all tables */
+    if (d.planned && std::memcmp(&d.plan_tab, &c->tab, sizeof(RkTables)) == 0) return RK_OK;
+    d.planned = false;
     d.on = false;
     d.runs_ok = false;
     const uint32_t n = c->tab.g.n, S = c->tab.g.S;
@@ -588,6 +595,8 @@ rk_status dp_plan(rk_ctx* c) {
     d.view.D = RK_DP_D;
     d.view.Dfact = (uint32_t)DF;
     d.on = true;
+    d.planned = true;
+    d.plan_tab = c->tab;
     return RK_OK;
 }
 
