@@ -2490,10 +2490,19 @@ int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t co
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
     unsigned grid = dp_grid(runs);
     { /* one wave: as many CTAs as are resident (no tail wave; measured -4 %) */
-        int per = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rk_dp_keys_kernel<true>, kDpThreads,
-                                                      hist ? (size_t)bins * 4 : 0);
-        if (per > 0 && grid > (unsigned)(per * num_sms())) grid = (unsigned)(per * num_sms());
+        static int cached_per = 0;
+        static uint32_t cached_bins = 0xFFFFFFFFu;
+        const uint32_t b = hist ? bins : 0u;
+        if (b != cached_bins) {
+            cached_per = 0;
+            if (hist)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per, rk_dp_keys_kernel<true>, kDpThreads,
+                                                              (size_t)bins * 4);
+            else
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per, rk_dp_keys_kernel<false>, kDpThreads, 0);
+            cached_bins = b;
+        }
+        if (cached_per > 0 && grid > (unsigned)(cached_per * num_sms())) grid = (unsigned)(cached_per * num_sms());
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (hist) {
