@@ -930,3 +930,25 @@ def test_memo_run_length_nodes_vs_oracle_and_direct(monkeypatch):
     finally:
         fm.close()
         d.close()
+
+
+def test_memo_plan_switching_sets_in_one_context(ctx):
+    """Plans are kept only for byte-identical tables: alternating kernel sets (and
+    GPU parameters) in one context give the oracle goldens every time."""
+    c2, c3 = _gold("c2_oracle.json"), _gold("c3_oracle.json")
+    fields = ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt", "evaluated")
+    for name, gold in (("C2", c2), ("C3", c3), ("C2", c2), ("C3", c3)):
+        gpu, ks = W.config(name)
+        ctx.rk_set_gpu_params(gpu)
+        ctx.rk_set_kernels(ks)
+        st = ctx.rk_eval_range(0, math.factorial(len(ks)), gold["cand_key"])
+        assert list(st.as_tuple()) == [gold["stats"][f] for f in fields], name
+    # the same kernels under the cursor-per-kernel reading (different tables) and back
+    gpu, ks = W.config("C2")
+    ost, _ = O.sweep(list(gpu) + [1], ks, cand_key=c2["cand_key"], threads=NCPU)
+    ctx.rk_set_gpu_params(list(gpu) + [1])
+    ctx.rk_set_kernels(ks)
+    assert ctx.rk_eval_range(0, 40320, c2["cand_key"]).as_tuple() == ost.as_tuple()
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    assert list(ctx.rk_eval_range(0, 40320, c2["cand_key"]).as_tuple()) == [c2["stats"][f] for f in fields]
