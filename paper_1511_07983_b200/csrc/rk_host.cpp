@@ -702,7 +702,10 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
         c->max_ctas = 0;
         for (uint32_t S : {1u, 2u, 3u, 4u, 5u, 8u, 9u, 16u, 17u, 32u, 33u})
             c->max_ctas = std::max(c->max_ctas, (uint32_t)rk_eval_max_ctas(S, cuda_device));
-        if (c->max_ctas < 256) c->max_ctas = 256;
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+        /* per-CTA record slots: also for the memo extremes pass (8 CTAs per SM) */
+        c->max_ctas = std::max<uint32_t>(c->max_ctas, (uint32_t)std::max(256, 8 * sms));
         bool ok = cudaMalloc(&c->tab_dev, sizeof(RkTables)) == cudaSuccess &&
                   cudaMalloc(&c->recs_dev, sizeof(rk_stats) * c->max_ctas * 2) == cudaSuccess &&
                   cudaMalloc(&c->counter_dev, sizeof(uint32_t)) == cudaSuccess &&
