@@ -1660,18 +1660,27 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
         st_to_node<SMAX>(s2, nd.mask | (1u << k), o);
         uint32_t pos = (uint32_t)dnode_hash(o) & tmask, id = kDpEmpty;
         for (;;) {
-            uint32_t v = atomicCAS(&table[pos], kDpEmpty, kDpBusy);
-            if (v == kDpEmpty) { /* claimed: allocate, publish the record, then the id */
+            uint32_t v;
+            /* acquire: a published id makes its record visible (paired with the release below) */
+            asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], %2, %3;"
+                         : "=r"(v)
+                         : "l"(table + pos), "r"(kDpEmpty), "r"(kDpBusy)
+                         : "memory");
+            if (v == kDpEmpty) { /* claimed: allocate, write the record, publish the id (release) */
                 id = atomicAdd(cnt_n, 1u);
                 if (id < cap_n) Un[id] = o;
                 else atomicOr(ovf, 1u);
-                __threadfence();
-                atomicExch(&table[pos], id);
+                uint32_t old;
+                asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;"
+                             : "=r"(old)
+                             : "l"(table + pos), "r"(id)
+                             : "memory");
+                (void)old;
                 break;
             }
             while (v == kDpBusy) {
                 __nanosleep(32);
-                v = *(volatile uint32_t*)&table[pos];
+                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(table + pos) : "memory");
             }
             if (v >= cap_n) { /* an overflowed entry: the result is discarded (plan re-sizes) */
                 atomicOr(ovf, 1u);
