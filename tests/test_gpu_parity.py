@@ -952,3 +952,29 @@ def test_memo_plan_switching_sets_in_one_context(ctx):
     ctx.rk_set_gpu_params(gpu)
     ctx.rk_set_kernels(ks)
     assert list(ctx.rk_eval_range(0, 40320, c2["cand_key"]).as_tuple()) == [c2["stats"][f] for f in fields]
+
+
+def test_memo_n14_full_space_vs_branch_and_bound_and_oracle(ctx):
+    """14! = 8.7e10 orders: the memoised full-space statistics
+    agree with the branch-and-bound optimum, the oracle re-simulates the extremes,
+    and sampled orders lie within them."""
+    n = 14
+    ks = W.gen_g(W.SplitMix64(W.SEED_BASE + 1000 * n), n)
+    ctx.rk_set_gpu_params(W.GTX580)
+    ctx.rk_set_kernels(ks)
+    assert ctx.rk_memo_info()[0]
+    N = math.factorial(n)
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    cd = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ctx.rk_eval_range_async(0, N, cd, rec)
+    torch.cuda.synchronize()
+    st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
+    assert st.evaluated == N
+    _, _, hidx, _ = ctx.rk_heuristic_order()
+    _, idx, key, _ = ctx.rk_best_order(hidx)
+    assert (key, idx) == (st.key_min, st.argmin)
+    assert O.simulate(W.GTX580, ks, O.unrank(st.argmin, n)).key == st.key_min
+    assert O.simulate(W.GTX580, ks, O.unrank(st.argmax, n)).key == st.key_max
+    rng = np.random.default_rng(14)
+    for i in rng.integers(0, N, 200).tolist():
+        assert st.key_min <= O.simulate(W.GTX580, ks, O.unrank(i, n)).key <= st.key_max
