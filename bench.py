@@ -358,8 +358,9 @@ def main():
                 "config": {"workload": WORKLOAD, "n": len(ks), "orders": N, "bins": args.bins,
                            "shards": world, "parallelism": f"index-space shards x{world}",
                            "keys": "u64 exact keys in HBM (8 B/order)",
-                           "l2": ("keys array 8 B/order (3.83 GB at N=1) > 126 MB L2, written once per step; "
-                                  "memo tables (suffix rows 41 MB) L2-resident")},
+                           "l2": ("inputs larger than L2 per step: the step's only input is the 856-B kernel table; "
+                                  "every memo table (~110 MB incl. the 64-MB run table) is rebuilt inside each step "
+                                  "and the 3.83 GB key array (> 126 MB L2) is written once per step")},
                 "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
                 "kernels_ms": ({"pass1_memo_tables_and_extremes": eval_ms_max,
                                 "pass2_keys_counts_histogram": hist_ms, "step": ms_max / args.steps}
