@@ -49,7 +49,11 @@ typedef struct rk_ctx rk_ctx;
 
 /* Create a context bound to CUDA device `cuda_device` (>= 0), or a host-only
  * context (cuda_device = -1) that can validate inputs and run Algorithm 1 but
- * returns RK_ENODEVICE for every model evaluation. */
+ * returns RK_ENODEVICE for every model evaluation.  Testing switches, read once
+ * here from the environment (every path computes the same exact keys):
+ * RK_NO_REDUCE=1 (no SM-symmetry reduction), RK_FORCE_RUNS=1 (run-length SM
+ * state for every S), RK_NO_MEMO=1 (direct per-order evaluation),
+ * RK_FORCE_MEMO=1 (suffix memoisation even where it does not pay). */
 rk_status rk_create(rk_ctx** out, int cuda_device);
 void rk_destroy(rk_ctx* ctx);
 const char* rk_last_error(const rk_ctx* ctx);
