@@ -67,6 +67,14 @@ def test_host_only_ctx_refuses_compute():
     with pytest.raises(rk.RkError) as e:
         c.rk_heuristic_order(with_key=True)
     assert e.value.status == rk.RK_ENODEVICE
+    # the two-pass step, the optimum and the memo plan: no device, no evaluation
+    for call in (lambda: c.rk_sweep_pass1_async(0, 24, None, None),
+                 lambda: c.rk_sweep_pass2_async(0, 24, None, None, 4, None, None, None),
+                 lambda: c.rk_best_order()):
+        with pytest.raises(rk.RkError) as e:
+            call()
+        assert e.value.status == rk.RK_ENODEVICE
+    assert c.rk_memo_info() == (False, 0, [])
 
 
 def test_create_without_gpu_fails_loudly():
