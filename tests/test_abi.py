@@ -174,3 +174,17 @@ def test_heuristic_matches_oracle_on_configs():
     for ks in sets:
         c.rk_set_kernels(ks)
         assert c.rk_heuristic_order(with_key=False)[:2] == O.heuristic(W.GTX580, ks)
+
+
+def test_heuristic_host_unspecified_branches_hand_golden():
+    """rk_heuristic_order (host Algorithm 1) on the hand-derived branch goldens
+    (tests/golden/alg1_branches.json: SPEC:182/184/187, PAPER:130/167)."""
+    import json
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "alg1_branches.json")))
+    c = rk.Context(-1)
+    c.rk_set_gpu_params(g["gpu"])
+    for case in g["cases"]:
+        c.rk_set_kernels(case["kernels"])
+        order, round_of, idx, _ = c.rk_heuristic_order(with_key=False)
+        assert (order, round_of) == (case["order"], case["round_of"]), case["name"]
+        assert idx == rk.rk_rank(case["order"])

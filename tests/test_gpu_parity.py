@@ -978,3 +978,18 @@ def test_memo_n14_full_space_vs_branch_and_bound_and_oracle(ctx):
     rng = np.random.default_rng(14)
     for i in rng.integers(0, N, 200).tolist():
         assert st.key_min <= O.simulate(W.GTX580, ks, O.unrank(i, n)).key <= st.key_max
+
+
+def test_device_algorithm1_unspecified_branches_hand_golden(ctx):
+    """rk_heuristic_batch (device Algorithm 1) on the hand-derived branch goldens:
+    ties, no feasible pair, lone kernel,
+    equal-shm insertion, bonus clamp."""
+    g = _gold("alg1_branches.json")
+    ctx.rk_set_gpu_params(g["gpu"])
+    for case in g["cases"]:
+        orders, idx = ctx.rk_heuristic_batch([case["kernels"]])
+        assert orders[0] == case["order"], case["name"]
+        assert idx[0] == O.rank(case["order"])
+        # the same set as a whole batch of copies (one thread per set)
+        orders, _ = ctx.rk_heuristic_batch([case["kernels"]] * 37)
+        assert all(o == case["order"] for o in orders)

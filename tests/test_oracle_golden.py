@@ -187,3 +187,23 @@ def test_w2_alternative_cursor_reading():
     assert [list(t) for t in r.trace] == w["rejected_reading_trace"]
     assert r.rounds == w["rejected_reading_rounds"]
     assert r.key == w["T_rejected_reading"] * w["gpu"][6]
+
+
+ALG1 = _load("alg1_branches.json")
+
+
+@pytest.mark.parametrize("case", ALG1["cases"], ids=lambda c: c["name"])
+def test_algorithm1_unspecified_branches_hand_golden(case):
+    """Ties, no feasible pair, lone kernel,
+    equal-shm insertion (reading L17) and the bonus clamp,
+    each derived by hand in tests/golden/alg1_branches.json."""
+    gpu, ks = ALG1["gpu"], case["kernels"]
+    order, round_of = O.heuristic(gpu, ks)
+    assert order == case["order"] and round_of == case["round_of"]
+    for pair, want in case["pair_scores"].items():
+        i, j = (int(x) for x in pair.split(","))
+        feasible, score, _ = O.pair_score(gpu, ks, i, j)
+        if want is None:
+            assert not feasible
+        else:
+            assert feasible and abs(score - want) <= 1e-12
