@@ -130,6 +130,9 @@ def oracle_rate(gpu, kernels, seconds: float, threads: int, first: int):
     return count / dt, count, dt
 
 
+PROFILE_MEMO = "r02_ncu_full_memo.json"
+
+
 def read_profile(kernel_sub: str = "rk_eval_kernel", name: str = "r01_ncu_full_eval_hist.json"):
     """The committed `ncu --set full` summary of the same kernel (profiles/), if any:
     (dram read+write bytes per launch, issue-active %, thread instructions/launch)."""
@@ -239,6 +242,7 @@ def main():
         step()
     torch.cuda.synchronize()
     events.clear()
+    sw.ctx.rk_set_timing(True)  # per-phase CUDA events on the launching stream (library-recorded)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -255,6 +259,9 @@ def main():
     torch.cuda.synchronize()
     ms = t_start.elapsed_time(t_end)
     ms_max = max_over_ranks(ms, sw.dev)
+    phases = sw.ctx.rk_timing_read()
+    sw.ctx.rk_set_timing(False)
+    phase_ms = {k: max_over_ranks(v[0] / v[1], sw.dev) if v[1] else None for k, v in phases.items()}
     value = N * args.steps / (ms_max / 1e3)
     eval_ms = statistics.mean(a.elapsed_time(b) for a, b in events["eval"])
     eval_ms_max = max_over_ranks(eval_ms, sw.dev)
@@ -263,10 +270,24 @@ def main():
     assert not sw.overflowed(), "compact keys overflowed (re-run with u64 keys)"
 
     # correctness of the timed pipeline's result (global record, histogram mass)
-    out = torch.cat([sw.glob if world > 1 else sw.rec, sw.hist]).cpu()
+    out = torch.cat([sw.record, sw.hist]).cpu()
     evaluated = int(out[7].item())
     hist_mass = int(out[8:].sum().item())
     assert hist_mass == N and (world > 1 or evaluated == N), (hist_mass, evaluated)
+
+    # write-only bandwidth of this GPU on the same key buffer (the key stream's own ceiling)
+    write_peak_gbs = None
+    if sw.keys is not None:
+        best = None
+        for _ in range(5):
+            a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            sw.keys[:sw.count].fill_(1)
+            b0.record(stream)
+            torch.cuda.synchronize()
+            t = a0.elapsed_time(b0)
+            best = t if best is None else min(best, t)
+        write_peak_gbs = 8 * sw.count / (best / 1e3) / 1e9
 
     # e2e: the public API with host buffers (Sweeper.run: H2D tables, D2H report)
     e2e_steps = args.e2e_steps or max(3, min(30, args.steps // 2))
@@ -304,7 +325,7 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         r = max_over_ranks(a.elapsed_time(b) / 3, sw.dev)
-        assert torch.equal(rec2, sw.glob if world > 1 else sw.rec) or world > 1
+        assert torch.equal(rec2, sw.record) or world > 1
         c2.close()
         return r
 
@@ -323,21 +344,27 @@ def main():
         ops = algorithmic_ops_per_order(ks)
         per_launch_orders = sw.count
         if memo_on:
-            # pass 2 (keys + counts + histogram) dominates: HBM-bound on the key stream
+            # pass 2's key stream dominates: HBM-bound on the 8-B keys it writes
             peaks = read_peaks()
             bytes_launch = 8 * per_launch_orders
-            achieved = bytes_launch / (hist_ms_max / 1e3)
+            stream_ms = phase_ms["stream"]
+            achieved = bytes_launch / (stream_ms / 1e3)
             peak = peaks.get("hbm_gbs", 7700.0) * 1e9
-            traffic, issue_pct, _, kname = read_profile("rk_dp_keys_kernel", "r01_ncu_full_memo.json")
+            traffic, issue_pct, _, kname = read_profile("rk_dp_keys_kernel", PROFILE_MEMO)
             roofline = {"bound": "hbm", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": traffic,
-                        "kernel": kname or "rk_dp_keys_kernel<true>", "kernel_ms": hist_ms_max,
+                        "kernel": kname or "rk_dp_keys_kernel", "kernel_ms": stream_ms,
+                        "write_peak": write_peak_gbs, "frac_of_write_peak": (achieved / 1e9 / write_peak_gbs
+                                                                             if write_peak_gbs else None),
+                        "write_peak_basis": ("measured here: torch fill_ of the same 3.83 GB key buffer, "
+                                             "best of 5 (write-only stream; the copy peak counts read + write)"),
                         "bytes_per_order": 8, "orders_per_launch": per_launch_orders,
                         "peak_basis": ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if "hbm_gbs" in peaks
                                        else "B200_PROFILING fallback 7.7 TB/s"),
                         "ncu_issue_active_pct": issue_pct,
                         "note": ("algorithmic bytes = the 8-B exact key of every order written to HBM; the "
-                                 "suffix rows it adds to are L2-resident (DESIGN.md §5-6)")}
+                                 "suffix rows it adds to are L2-resident (DESIGN.md §5-6); kernel_ms = library-"
+                                 "recorded CUDA events around this launch on its stream, mean over the timed steps")}
         else:
             achieved = ops * per_launch_orders / (eval_ms_max / 1e3)
             peak = int_issue_peak_ops(1965.0)
@@ -362,8 +389,10 @@ def main():
                                   "every memo table (~110 MB incl. the 64-MB run table) is rebuilt inside each step "
                                   "and the 3.83 GB key array (> 126 MB L2) is written once per step")},
                 "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
-                "kernels_ms": ({"pass1_memo_tables_and_extremes": eval_ms_max,
-                                "pass2_keys_counts_histogram": hist_ms, "step": ms_max / args.steps}
+                "kernels_ms": ({"pass1": eval_ms_max, "pass1_memo_tables": phase_ms["tables"],
+                                "pass1_runs_extremes_rows": phase_ms["extremes"],
+                                "pass2": hist_ms_max, "pass2_counts_histogram": phase_ms["hist"],
+                                "pass2_key_stream": phase_ms["stream"], "step": ms_max / args.steps}
                                if memo_on else
                                {"rk_eval_kernel": eval_ms_max, "rk_hist_kernel": hist_ms,
                                 "step": ms_max / args.steps}),

@@ -237,26 +237,53 @@ rk_status rk_simulate_order(rk_ctx* ctx, const int32_t* order, uint32_t* rounds_
                             uint32_t* n_rounds_out, uint64_t* key_out);
 
 /* The step of the hot path in two passes, so that N ranks can agree on the
- * histogram range in between.  When the context's
- * suffix memoisation is on (rk_memo_info) pass 1 evaluates the
- * extremes of [first, first+count) from the memo tables it rebuilds, and pass 2
- * writes every key and the counts; otherwise pass 1 is rk_eval_range_async
- * (keys written) and pass 2 only bins the stored keys.  Either way, after both:
- * rec_dev (64 B, device) holds the range's complete rk_stats, keys_dev
- * (u64[count], device, nullable) every key index-major, hist_dev (u64[bins],
- * device, zeroed by the caller, accumulated) the Fig. 1 histogram over
- * [range_dev->key_min, range_dev->key_max] (range_dev = this
- * rec_dev for one rank, the merged record of all ranks otherwise).
- * Pass 1: rec_dev = {key_min, key_max, argmin, argmax, n_lt, n_eq, n_gt,
- * evaluated}, where memoised passes leave n_lt = n_eq = 0, n_gt = count.
- * Pass 2: adds the memoised counts (n_lt, n_eq += ..., n_gt -= ...) to rec_dev.
- * Errors: RK_EINVAL (range, missing pointers; more than 32768 bins without
- * keys_dev), RK_ESTATE, RK_ENODEVICE, RK_ECUDA. */
+ * histogram range in between.
+ * Pass 1, rec_dev (64 B, device) <- the extremes of [first, first+count):
+ * {key_min, key_max, argmin, argmax (smallest index on ties, reading L12),
+ * n_lt = 0, n_eq = 0, n_gt = count, evaluated = count}.  With suffix
+ * memoisation on (rk_memo_info) pass 1 rebuilds the memo tables
+ * from scratch and takes the extremes from the rows' extremes run by run;
+ * otherwise it is rk_eval_range_async (complete record, every key to
+ * keys_dev).  N ranks all-gather their records and merge them
+ * (rk_merge_stats_async) into the global record between the passes.
+ * Pass 2 over the same range: adds the counts against *cand_key_dev (reading
+ * L13) to rec_dev (n_lt, n_eq += ..., n_gt -= their sum; a zeroed record
+ * collects them alone, to be merged with the extremes record), writes every
+ * exact key to keys_dev (u64[count] index-major, nullable, 16-byte alignment
+ * not required), and accumulates (+=) into hist_dev (u64[bins], nullable,
+ * zeroed by the caller) the Fig. 1 histogram over [range_dev->key_min,
+ * range_dev->key_max] (reading L14; range_dev = this rank's
+ * record for one rank, the merged global record for N ranks).  Memoised: from
+ * the tables of the preceding pass 1; otherwise, or for more than 32768 bins,
+ * from keys_dev (then required).  Memoised, pass 2 streams pass 1's run
+ * metadata: it must follow pass 1 over the same [first, first+count) on the
+ * same ctx (else RK_ESTATE).  Pass 1 also builds the range's multiset of
+ * distinct rows (node, K_closed) with multiplicities, from which pass 2
+ * counts and bins (C4: 217,659 distinct rows for 3,991,680 runs).
+ * Errors: RK_EINVAL (range, missing pointers), RK_ESTATE, RK_ENODEVICE,
+ * RK_ECUDA. */
 rk_status rk_sweep_pass1_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
                                rk_stats* rec_dev, uint64_t* keys_dev, void* stream);
 rk_status rk_sweep_pass2_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
                                const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev,
                                rk_stats* rec_dev, void* stream);
+
+/* Per-phase device timing of the step (measurement support):
+ * while on, every phase the library enqueues records a CUDA event pair on its
+ * launching stream — RK_PHASE_TABLES (pass 1 memoised: memo tables rebuilt),
+ * RK_PHASE_EXTREMES (pass 1 memoised: run metadata, row multiset and the
+ * range's extremes),
+ * RK_PHASE_STREAM (pass 2's key stream), RK_PHASE_HIST (pass 2's counts and
+ * histogram from the row multiset), RK_PHASE_DIRECT (the direct evaluation kernel of pass 1).
+ * rk_timing_read synchronises on the recorded events and returns per phase the
+ * summed milliseconds (ms_sum[p]) and the number of marks (counts[p]) since
+ * the last read or rk_set_timing, for p < n_phases; then clears the marks.
+ * Event objects are owned by the ctx (grow-only).  Errors: RK_EINVAL,
+ * RK_ENODEVICE, RK_ECUDA. */
+enum { RK_PHASE_TABLES = 0, RK_PHASE_STREAM = 1, RK_PHASE_HIST = 2, RK_PHASE_DIRECT = 3, RK_PHASE_EXTREMES = 4,
+       RK_N_PHASES = 5 };
+rk_status rk_set_timing(rk_ctx* ctx, int on);
+rk_status rk_timing_read(rk_ctx* ctx, double* ms_sum, uint32_t* counts, uint32_t n_phases);
 
 /* Suffix memoisation of the current kernel set: on_out = 1 when
  * the device path evaluates orders as K(prefix) + f(state, suffix) from

@@ -61,13 +61,15 @@ struct DpPlan {
     std::vector<size_t> xoff;     /* transition offset of level j (j < P): cnt[j] * n entries */
     size_t table_slots = 0;
     Arena nodes, tables, tid, dk, fst, counters; /* counters: P + 1 node counters, then the overflow flag */
-    Arena code, dvc, dvo, nd, offs;              /* suffix rows: byte codes into sorted distinct (value, count) */
-    Arena runsA, runsB;                          /* prefix expansion (ping-pong); the last level is the run table */
+    Arena code, dvc, dvp, nd, offs;              /* suffix rows: byte codes into sorted distinct (value, count) */
+    Arena expand;                                /* the range's prefix expansion, levels 1..P-1 (level P recomputed) */
+    Arena meta_u, meta_K;                        /* the range's run metadata for the key stream: node | wide, Kb */
+    Arena rslot, rmult, rlist;                   /* the range's row multiset (distinct (node, Kb) + multiplicity) */
+    uint32_t rmask = 0;                          /* its slots - 1 */
     bool planned = false;                        /* sizes below belong to plan_tab (byte-identical tables) */
     RkTables plan_tab{};
-    bool runs_ok = false;
+    bool runs_ok = false;                        /* meta_u/meta_K hold the range [runs_first, +runs_count) */
     uint64_t runs_first = 0, runs_count = 0;
-    const void* runs_ptr = nullptr;
     DPView view{};
 };
 
@@ -84,12 +86,27 @@ struct rk_ctx {
     rk_stats* stats_dev = nullptr;    /* one record for the synchronous calls */
     uint64_t* u64_dev = nullptr;      /* small scratch (indices / keys) */
     uint32_t max_ctas = 0;
+    uint32_t sms = 0;                 /* SM count of `device` */
     uint32_t launches = 0;
     bool no_reduce = false; /* RK_NO_REDUCE=1: disable the symmetry reduction (testing) */
     bool force_runs = false; /* RK_FORCE_RUNS=1: run-length SM state for every S (testing) */
     bool no_memo = false;    /* RK_NO_MEMO=1: direct evaluation of every order (testing) */
     bool force_memo = false; /* RK_FORCE_MEMO=1: memoise even where it does not pay (testing) */
+    /* pass 2's counts/histogram: from the distinct rows (dedup, default) or every run; RK_OVERLAP=1 runs them
+     * beside the key stream on a side stream (measured: step -5 % on C4 with every run binned, but the key
+     * stream itself slows from 0.59 to 0.79 ms).  RK_ROW_DEDUP / RK_OVERLAP = 0|1 force either (-1 = default) */
+    int row_dedup = -1, overlap = -1;
+    bool dedup_now = false;  /* the current range's pass 1 built the row multiset */
+    uint32_t rows_ctas = 2;  /* RK_ROWS_CTAS: its CTAs per SM when overlapped */
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     DpPlan dp;
+    /* optional per-phase device timing (rk_set_timing): event pairs recorded on
+     * the launching stream around each phase, read back by rk_timing_read */
+    bool timing = false;
+    std::vector<cudaEvent_t> tev;  /* 2 per mark */
+    std::vector<uint32_t> tphase;  /* phase of each mark */
+    size_t tused = 0;
 };
 
 /* SM count that selects the kernel variant (the table keeps the real S) */
@@ -454,6 +471,25 @@ rk_status need_kernels(rk_ctx* c) {
 
 uint64_t space(const rk_ctx* c) { return fact64((uint32_t)c->ks.size()); }
 
+/* phase timing: begin returns a mark (or -1 when off), end records its second event */
+int tmark_begin(rk_ctx* c, uint32_t phase, void* stream) {
+    if (!c->timing) return -1;
+    if (c->tused == c->tphase.size()) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (cudaEventCreate(&a) || cudaEventCreate(&b)) return -1;
+        c->tev.push_back(a);
+        c->tev.push_back(b);
+        c->tphase.push_back(phase);
+    }
+    const size_t m = c->tused++;
+    c->tphase[m] = phase;
+    cudaEventRecord(c->tev[2 * m], (cudaStream_t)stream);
+    return (int)m;
+}
+void tmark_end(rk_ctx* c, int m, void* stream) {
+    if (m >= 0) cudaEventRecord(c->tev[2 * (size_t)m + 1], (cudaStream_t)stream);
+}
+
 void dp_free(DpPlan& d) {
     d.nodes.release();
     d.tables.release();
@@ -461,7 +497,7 @@ void dp_free(DpPlan& d) {
     d.dk.release();
     d.fst.release();
     d.counters.release();
-    for (Arena* a : {&d.code, &d.dvc, &d.dvo, &d.nd, &d.offs, &d.runsA, &d.runsB}) a->release();
+    for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist}) a->release();
     d.runs_ok = false;
     d.on = false;
     d.planned = false;
@@ -500,11 +536,11 @@ int dp_build(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr)
     DpPlan& d = c->dp;
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
-    if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.P + 2) * 4, st);
+    if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.P + 3) * 4, st); /* + the row list counter at P+2 */
     if (!e) e = dp_levels(c, 0, d.P, stream, ex); /* the last expansion level runs with the extremes */
     if (!e)
         e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
-                         (uint8_t*)d.code.p, d.dvc.p, (uint32_t*)d.dvo.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
+                         (uint8_t*)d.code.p, d.dvc.p, d.dvp.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
                          (uint32_t*)d.offs.p, d.cnt[d.P], stream, &c->launches);
     return e;
 }
@@ -573,7 +609,7 @@ rk_status dp_plan(rk_ctx* c) {
     if (uP * 4 > runs && !c->force_memo) return RK_OK; /* does not pay */
     e = d.code.reserve(uP * DF);
     if (!e) e = d.dvc.reserve(uP * DF * 16);
-    if (!e) e = d.dvo.reserve(uP * DF * 4);
+    if (!e) e = d.dvp.reserve(uP * DF * 8);
     if (!e) e = d.offs.reserve(uP * DF * 4);
     if (!e) e = d.nd.reserve(uP * 4);
     if (!e) e = d.fst.reserve(uP * 4 * 8);
@@ -587,7 +623,7 @@ rk_status dp_plan(rk_ctx* c) {
     }
     d.view.code = (const uint8_t*)d.code.p;
     d.view.dvc = d.dvc.p;
-    d.view.dvo = (const uint32_t*)d.dvo.p;
+    d.view.dvp = (const uint2*)d.dvp.p;
     d.view.offs = (const uint32_t*)d.offs.p;
     d.view.nd = (const uint32_t*)d.nd.p;
     d.view.fst = (const uint64_t*)d.fst.p;
@@ -607,20 +643,40 @@ const uint64_t* cand_or_zero(rk_ctx* c, const uint64_t* cand_dev, void* stream) 
     return c->u64_dev + 9;
 }
 
-/* Pass 1 of the memoised path: tables, the range's run table (breadth-first
- * prefix expansion, when <= 2^27 runs) and the extremes of [first, first+count). */
-int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void* stream) {
+/* the range's row multiset buffers */
+RkRows dp_rows(rk_ctx* c, uint64_t nrun) {
+    DpPlan& d = c->dp;
+    return RkRows{c->dedup_now ? d.rslot.p : nullptr, (uint32_t*)d.rmult.p, d.rmask, (uint32_t*)d.rlist.p,
+                  (uint32_t*)d.counters.p + d.P + 2, nrun};
+}
+
+/* Pass 1 of the memoised step: the tables (levels + suffix rows) rebuilt from
+ * scratch with the range's prefixes expanded breadth-first (levels 1..P-1 when
+ * the range has <= 2^27 runs; level P recomputed by the run pass), then the run
+ * pass: the run metadata pass 2 streams from, the row multiset (when pass 2
+ * will not write keys: keys_hint false), and the range's extremes record
+ * (n_lt = n_eq = 0, n_gt = evaluated = count). */
+int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool keys_hint, void* stream) {
     DpPlan& d = c->dp;
     d.runs_ok = false;
-    d.view.runs = nullptr;
     const uint32_t n = c->tab.g.n, P = d.P;
     const uint64_t DF = d.view.Dfact;
     const uint64_t rb = first / DF, re = count ? (first + count + DF - 1) / DF : rb;
     std::vector<RkExpand> ex;
-    int e = 0;
-    if (re > rb && re - rb <= (1ull << 27)) {
-        e = d.runsA.reserve((re - rb) * 16);
-        if (!e) e = d.runsB.reserve((re - rb) * 16);
+    const uint64_t nrun = std::max<uint64_t>(re - rb, 1);
+    int e = d.meta_u.reserve(nrun * 4);
+    if (!e) e = d.meta_K.reserve(nrun * 8);
+    /* row multiset: ~8 runs per slot (C4: 217,659 distinct rows of 3,991,680 runs in 2^19 slots) */
+    const uint64_t slots = std::min<uint64_t>(std::max<uint64_t>(pow2_at_least(nrun / 8), 4096), 1ull << 22);
+    d.rmask = (uint32_t)(slots - 1);
+    if (!e) e = d.rslot.reserve(slots * 16);
+    if (!e) e = d.rmult.reserve(slots * 4 * 8); /* 8 counters per slot */
+    if (!e) e = d.rlist.reserve(nrun * 4);
+    (void)keys_hint;
+    c->dedup_now = c->row_dedup != 0;
+    if (!e && c->dedup_now) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, (cudaStream_t)stream);
+    if (!e && c->dedup_now) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, (cudaStream_t)stream);
+    if (!e && re > rb && re - rb <= (1ull << 27)) {
         /* level j covers prefixes [a_j, b_j): span_j level-P prefixes under each */
         std::vector<uint64_t> a(P + 1), b(P + 1);
         uint64_t span = 1;
@@ -629,47 +685,96 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
             b[j] = (re - 1) / span + 1;
             if (j > 0) span *= (n - (uint32_t)(j - 1));
         }
+        std::vector<size_t> off(P + 1, 0);
+        size_t tot = 0;
+        for (uint32_t j = 1; j < P; j++) {
+            off[j] = tot;
+            tot += (b[j] - a[j]) * 16;
+        }
+        e = d.expand.reserve(std::max<size_t>(tot, 16));
         const void* prev = nullptr;
         for (uint32_t j = 0; j < P && !e; j++) {
-            void* dst = (j & 1u) ? d.runsB.p : d.runsA.p;
+            void* dst = j + 1 == P ? nullptr : (char*)d.expand.p + off[j + 1]; /* level P: not stored */
             ex.push_back(RkExpand{prev, a[j], dst, a[j + 1], b[j + 1] - a[j + 1], j, d.view.tid[j], d.view.dk[j]});
             prev = dst;
         }
     }
+    const int m0 = tmark_begin(c, RK_PHASE_TABLES, stream);
     if (!e) e = dp_build(c, stream, ex.empty() ? nullptr : &ex);
-    if (!e && !ex.empty()) {
+    tmark_end(c, m0, stream);
+    const int m1 = tmark_begin(c, RK_PHASE_EXTREMES, stream);
+    if (!e)
+        e = rk_dp_meta(c->tab_dev, d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p, rec_dev,
+                       c->recs_dev, c->counter_dev, c->max_ctas, ex.empty() ? nullptr : &ex.back(), stream,
+                       &c->launches);
+    if (!e && c->dedup_now)
+        e = rk_dp_insert(d.view, first, count, (const uint32_t*)d.meta_u.p, (const uint64_t*)d.meta_K.p,
+                         dp_rows(c, re - rb), stream, &c->launches);
+    tmark_end(c, m1, stream);
+    if (!e) {
         d.runs_ok = true;
         d.runs_first = first;
         d.runs_count = count;
-        d.runs_ptr = ex.back().Rn;
-        d.view.runs = ex.back().Rn;
-        d.view.runs_base = rb;
     }
-    if (!e) /* with the run table: the last expansion level is produced by this launch */
-        e = rk_dp_minmax(c->tab_dev, d.view, first, count, rec_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream,
-                         &c->launches, ex.empty() ? nullptr : &ex.back());
     return e;
 }
 
-/* Pass 2: keys, counts, optional fused histogram (bins <= rk_dp_max_fused_bins()) */
+/* Pass 2 over the range of the preceding pass 1: the key stream from its run
+ * metadata (keys_dev), which also fills the range's row multiset, then the
+ * counts (into rec_dev) and the histogram (hist_dev, bins <=
+ * rk_dp_max_fused_bins()) from the distinct rows; without keys (or with the
+ * multiset off) from every run.  RK_OVERLAP=1 (every run binned) runs the
+ * counts/histogram beside the key stream on the ctx's high-priority side
+ * stream, joined back before returning. */
 int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, const rk_stats* range_dev,
              uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev, rk_stats* rec_dev, void* stream) {
     DpPlan& d = c->dp;
-    DPView v = d.view;
-    if (d.runs_ok && d.runs_first == first && d.runs_count == count) {
-        v.runs = d.runs_ptr;
-        v.runs_base = first / v.Dfact;
-    } else {
-        v.runs = nullptr; /* another range: walk the transitions */
+    if (!(d.runs_ok && d.runs_first == first && d.runs_count == count)) return (int)cudaErrorNotReady;
+    const uint32_t* mu = (const uint32_t*)d.meta_u.p;
+    const uint64_t* mk = (const uint64_t*)d.meta_K.p;
+    const uint64_t DF = d.view.Dfact;
+    const uint64_t nrun = count ? (first + count + DF - 1) / DF - first / DF : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool keys = keys_dev && count;
+    const bool ov = c->overlap == 1 && keys && !c->dedup_now;
+    int e = 0;
+    if (ov && !c->side) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
+        if (!e) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+        if (!e) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+        if (e) return e;
     }
-    return rk_dp_keys(c->tab_dev, v, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, rec_dev, stream,
-                      &c->launches);
+    auto rows = [&](void* s, uint32_t cap) {
+        const int m = tmark_begin(c, RK_PHASE_HIST, s);
+        const int r = rk_dp_rows(c->tab_dev, d.view, first, count, cand_dev, range_dev, bins, hist_dev,
+                                 dp_rows(c, nrun), mu, mk, rec_dev, cap, s, &c->launches);
+        tmark_end(c, m, s);
+        return r;
+    };
+    if (ov) {
+        e = cudaEventRecord(c->ev_fork, st);
+        if (!e) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+        if (!e) e = rows(c->side, c->rows_ctas * c->sms);
+    }
+    if (!e && keys) {
+        const int m1 = tmark_begin(c, RK_PHASE_STREAM, stream);
+        e = rk_dp_keys(d.view, first, count, mu, mk, keys_dev, stream, &c->launches);
+        tmark_end(c, m1, stream);
+    }
+    if (!e && !ov) e = rows(stream, 0);
+    if (!e && ov) {
+        e = cudaEventRecord(c->ev_join, c->side);
+        if (!e) e = cudaStreamWaitEvent(st, c->ev_join, 0);
+    }
+    return e;
 }
 
 /* memoised equivalent of rk_launch_eval (stats + optional keys, optional histogram) */
 int dp_eval(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, rk_stats* stats_dev,
             uint64_t* keys_dev, const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream) {
-    int e = dp_pass1(c, first, count, stats_dev, stream);
+    int e = dp_pass1(c, first, count, stats_dev, keys_dev != nullptr, stream);
     if (!e) e = dp_pass2(c, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, stats_dev, stream);
     return e;
 }
@@ -691,6 +796,12 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
     c->no_memo = nm && nm[0] == '1';
     const char* fm = getenv("RK_FORCE_MEMO");
     c->force_memo = fm && fm[0] == '1';
+    const char* rd = getenv("RK_ROW_DEDUP");
+    if (rd && (rd[0] == '0' || rd[0] == '1')) c->row_dedup = rd[0] - '0';
+    const char* ovv = getenv("RK_OVERLAP");
+    if (ovv && (ovv[0] == '0' || ovv[0] == '1')) c->overlap = ovv[0] - '0';
+    const char* rc = getenv("RK_ROWS_CTAS");
+    if (rc && atoi(rc) > 0) c->rows_ctas = (uint32_t)atoi(rc);
     if (cuda_device >= 0) {
         int ndev = 0;
         cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -704,6 +815,7 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
             c->max_ctas = std::max(c->max_ctas, (uint32_t)rk_eval_max_ctas(S, cuda_device));
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+        c->sms = sms > 0 ? (uint32_t)sms : 148u;
         /* per-CTA record slots: also for the memo extremes pass (8 CTAs per SM) */
         c->max_ctas = std::max<uint32_t>(c->max_ctas, (uint32_t)std::max(256, 8 * sms));
         bool ok = cudaMalloc(&c->tab_dev, sizeof(RkTables)) == cudaSuccess &&
@@ -732,6 +844,12 @@ void rk_destroy(rk_ctx* c) {
         cudaFree(c->counter_dev);
         cudaFree(c->stats_dev);
         cudaFree(c->u64_dev);
+        for (cudaEvent_t ev : c->tev) cudaEventDestroy(ev);
+        if (c->side) {
+            cudaStreamDestroy(c->side);
+            cudaEventDestroy(c->ev_fork);
+            cudaEventDestroy(c->ev_join);
+        }
     }
     delete c;
 }
@@ -878,10 +996,12 @@ rk_status rk_sweep_pass1_async(rk_ctx* c, uint64_t first, uint64_t count, const 
     c->launches = 0;
     int e;
     if (c->dp.on) {
-        e = dp_pass1(c, first, count, rec_dev, stream);
+        e = dp_pass1(c, first, count, rec_dev, keys_dev != nullptr, stream);
     } else {
+        const int m = tmark_begin(c, RK_PHASE_DIRECT, stream);
         e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, rec_dev, keys_dev,
                            c->recs_dev, c->counter_dev, c->max_ctas, stream, &c->launches);
+        tmark_end(c, m, stream);
     }
     return e ? cuda_fail(c, e, "rk_sweep_pass1_async") : RK_OK;
 }
@@ -898,17 +1018,53 @@ rk_status rk_sweep_pass2_async(rk_ctx* c, uint64_t first, uint64_t count, const 
     c->launches = 0;
     int e = 0;
     if (c->dp.on) {
+        const DpPlan& d = c->dp;
+        if (!(d.runs_ok && d.runs_first == first && d.runs_count == count))
+            return fail(c, RK_ESTATE, "pass 2 needs pass 1 over the same range first (it streams pass 1's run metadata)");
         const bool fused = hist_dev && bins <= rk_dp_max_fused_bins();
-        if (hist_dev && !fused && !keys_dev) return fail(c, RK_EINVAL, "more than 4096 bins needs keys_dev");
+        if (hist_dev && !fused && !keys_dev) return fail(c, RK_EINVAL, "more than 32768 bins needs keys_dev");
         e = dp_pass2(c, first, count, cand_key_dev, range_dev, fused ? bins : 0, fused ? hist_dev : nullptr, keys_dev,
                      rec_dev, stream);
         if (!e && hist_dev && !fused)
             e = rk_launch_histogram(keys_dev, count, 0, 0, range_dev, bins, hist_dev, stream, &c->launches);
     } else if (hist_dev) {
         if (!keys_dev) return fail(c, RK_EINVAL, "keys_dev is required (direct evaluation)");
+        const int m = tmark_begin(c, RK_PHASE_HIST, stream);
         e = rk_launch_histogram(keys_dev, count, 0, 0, range_dev, bins, hist_dev, stream, &c->launches);
+        tmark_end(c, m, stream);
     }
     return e ? cuda_fail(c, e, "rk_sweep_pass2_async") : RK_OK;
+}
+
+rk_status rk_set_timing(rk_ctx* c, int on) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    c->timing = on != 0;
+    c->tused = 0;
+    return RK_OK;
+}
+
+rk_status rk_timing_read(rk_ctx* c, double* ms_sum, uint32_t* counts, uint32_t n_phases) {
+    rk_status s = need_device(c);
+    if (s) return s;
+    if (!ms_sum || !counts) return fail(c, RK_EINVAL, "ms_sum and counts are required");
+    DeviceGuard dg(c->device);
+    for (uint32_t p = 0; p < n_phases; p++) {
+        ms_sum[p] = 0.0;
+        counts[p] = 0;
+    }
+    for (size_t m = 0; m < c->tused; m++) {
+        const uint32_t p = c->tphase[m];
+        if (p >= n_phases) continue;
+        cudaError_t e = cudaEventSynchronize(c->tev[2 * m + 1]);
+        float ms = 0.f;
+        if (!e) e = cudaEventElapsedTime(&ms, c->tev[2 * m], c->tev[2 * m + 1]);
+        if (e) return cuda_fail(c, e, "rk_timing_read");
+        ms_sum[p] += ms;
+        counts[p]++;
+    }
+    c->tused = 0;
+    return RK_OK;
 }
 
 rk_status rk_memo_info(rk_ctx* c, uint32_t* on_out, uint32_t* levels_out, uint32_t* nodes_out, uint32_t max_levels) {
@@ -1005,13 +1161,13 @@ static rk_status select_common(rk_ctx* c, const void* keys_dev, bool k32, uint64
         if (ranks[j] >= count) return fail(c, RK_EINVAL, "rank %llu >= count", (unsigned long long)ranks[j]);
     DeviceGuard dg(c->device);
     cudaStream_t st = (cudaStream_t)stream;
+    if (kmax - kmin == ~0ull) return fail(c, RK_EINVAL, "key range must be < 2^64 - 1");
     constexpr uint32_t B = 16384;
     uint64_t* hd = nullptr;
     int e = cudaMalloc(&hd, sizeof(uint64_t) * B);
     std::vector<uint64_t> h(B);
     uint32_t launches = 0;
     std::vector<uint64_t> out(m);
-    if (kmax - kmin == ~0ull) return fail(c, RK_EINVAL, "key range must be < 2^64 - 1");
     for (uint32_t j = 0; j < m && !e; j++) {
         uint64_t lo = kmin, span = kmax - kmin + 1, r = ranks[j];
         for (;;) {

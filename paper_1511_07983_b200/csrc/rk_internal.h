@@ -19,6 +19,7 @@
 #define RK_INTERNAL_H
 
 #include <stdint.h>
+#include <vector_types.h>
 #include "rk.h"
 
 #define RK_MAX_N 16
@@ -102,12 +103,10 @@ struct DPView {
     const uint64_t* dk[RK_MAX_N];  /* closed-round key increment of that transition */
     const uint8_t* code;           /* level-P suffix keys as D! one-byte ranks into dv, per node */
     const void* dvc;               /* per node: sorted distinct suffix keys with multiplicities, 16 B each (D! slots) */
-    const uint32_t* dvo;           /* the same distinct keys minus the row minimum (32-bit, exact unless nd bit 31) */
+    const uint2* dvp;              /* the same distinct keys as {offset from the row minimum (exact unless nd bit 31), count} */
     const uint32_t* offs;          /* per node: the D! keys minus the row minimum, decoded (32-bit, same caveat) */
     const uint32_t* nd;            /* per node: number of distinct suffix keys */
     const uint64_t* fst;           /* per node: min, max, argmin sigma, argmax sigma */
-    const void* runs;              /* optional: expanded run table {node, mask, K lo, hi} (uint4) of runs_base.. */
-    uint64_t runs_base;
     uint32_t P, D, Dfact;
 };
 constexpr uint32_t RK_DP_D = 5; /* suffix depth: 120 keys per level-P node */
@@ -126,16 +125,38 @@ int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t*
                 uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
                 uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex = nullptr);
 int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
-                 uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
+                 void* dvp, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
                  uint32_t* launches);
 uint32_t rk_dp_max_fused_bins();
-/* pass-1 extremes; ex (optional): the last prefix-expansion level, produced in the same launch */
-int rk_dp_minmax(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, rk_stats* out, rk_stats* recs,
-                 uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches,
-                 const RkExpand* ex = nullptr);
-int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count,
-               const uint64_t* cand_dev, const rk_stats* range, uint32_t bins, uint64_t* hist, uint64_t* keys,
-               rk_stats* rec, void* stream, uint32_t* launches);
+/* a range's row multiset: 16-B open-addressing slots of the
+ * distinct rows (node | wide << 31, Kb) with 8 multiplicity counters each;
+ * slot (nullptr: none) and mult must be zeroed and *nlist = 0 before pass 1;
+ * list (>= runs entries) takes the runs that are not in a slot (range edges,
+ * probe overflow); list_hint = an upper bound of *nlist for grid sizing */
+struct RkRows {
+    void* slot;
+    uint32_t* mult;
+    uint32_t mask;
+    uint32_t* list;
+    uint32_t* nlist;
+    uint64_t list_hint;
+};
+/* pass 1's run pass: run metadata (meta_u = node | wide << 31, meta_K = Kb) and
+ * the range's extremes record (counts: n_gt = evaluated = count); last = the
+ * range's level P-1 -> P expansion (nullptr: walk) */
+int rk_dp_meta(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u,
+               uint64_t* meta_K, rk_stats* out, rk_stats* recs, uint32_t* counter, uint32_t max_ctas,
+               const RkExpand* last, void* stream, uint32_t* launches);
+/* pass 2's counts (into rec, nullable) and histogram (nullable) from the row multiset */
+int rk_dp_rows(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, const uint64_t* cand_dev,
+               const rk_stats* range, uint32_t bins, uint64_t* hist, const RkRows& rows, const uint32_t* meta_u,
+               const uint64_t* meta_K, rk_stats* rec, uint32_t max_ctas, void* stream, uint32_t* launches);
+/* pass 2's key stream from the run metadata (one-shot grid) */
+int rk_dp_keys(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
+               uint64_t* keys, void* stream, uint32_t* launches);
+/* the range's row multiset from the run metadata (pass 1, after rk_dp_meta) */
+int rk_dp_insert(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
+                 const RkRows& rows, void* stream, uint32_t* launches);
 int rk_launch_bnb(const RkTables* tab_dev, uint32_t S, uint32_t P, uint64_t n_units, void* gb_dev,
                   unsigned long long* recs_dev, void* stream, uint32_t* launches);
 

@@ -24,11 +24,13 @@
  * SMAX; FULL = compile-time S == SMAX), kernel tables in shared memory,
  * reductions via warp shuffles then shared memory then a last-CTA merge.
  */
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "rk_internal.h"
 
+namespace cg = cooperative_groups;
 namespace {
 
 #ifndef RK_EVAL_THREADS
@@ -103,6 +105,17 @@ struct BinCalc {
         return q > bins - 1 ? bins - 1 : (uint32_t)q;
     }
 };
+
+/* shared-memory u32 bin += c (c <= 2^20); a bin that reaches 2^31 is drained
+ * into its u64 global bin (exchange, then add), so no shared bin ever wraps
+ * however many keys one CTA bins */
+__device__ __forceinline__ void sh_bin_add(uint32_t* shist, uint64_t* hist, uint32_t b, uint32_t c) {
+    const uint32_t old = atomicAdd(&shist[b], c);
+    if (old >= 0x80000000u - c) {
+        const uint32_t x = atomicExch(&shist[b], 0u);
+        atomicAdd((unsigned long long*)&hist[b], (unsigned long long)x);
+    }
+}
 
 template <int SMAX>
 struct St {
@@ -659,9 +672,24 @@ struct TStats {
     /* updated per run by Leaf::end_run (reading L12: smallest index on ties) */
 };
 
+/* Records may carry counts without evaluated orders (a lane that counted a
+ * row of another lane's run): counts always add, extremes come only from
+ * records with evaluated > 0. */
 __device__ __forceinline__ void merge_into(rk_stats& a, const rk_stats& b) {
-    if (b.evaluated == 0) return;
-    if (a.evaluated == 0) { a = b; return; }
+    if (b.evaluated == 0) {
+        a.n_lt += b.n_lt;
+        a.n_eq += b.n_eq;
+        a.n_gt += b.n_gt;
+        return;
+    }
+    if (a.evaluated == 0) {
+        const uint64_t lt = a.n_lt, eq = a.n_eq, gt = a.n_gt;
+        a = b;
+        a.n_lt += lt;
+        a.n_eq += eq;
+        a.n_gt += gt;
+        return;
+    }
     if (b.key_min < a.key_min || (b.key_min == a.key_min && b.argmin < a.argmin)) {
         a.key_min = b.key_min;
         a.argmin = b.argmin;
@@ -714,7 +742,7 @@ __device__ rk_stats block_reduce(rk_stats v) {
     __syncthreads();
     if (lane == 0) warp_recs[wid] = v;
     __syncthreads();
-    rk_stats r;
+    rk_stats r{};
     r.evaluated = 0;
     if (wid == 0) {
         const int nw = (blockDim.x + 31) >> 5;
@@ -741,7 +769,7 @@ __device__ void commit(const rk_stats& cta, rk_stats* recs, uint32_t* counter, r
     __syncthreads();
     if (!last) return;
     __threadfence();
-    rk_stats v;
+    rk_stats v{};
     v.evaluated = 0;
     for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
         const rk_stats* q = recs + i; /* written by other CTAs: read through L2 */
@@ -793,6 +821,7 @@ struct Leaf {
     uint64_t lo, hi, first;
     uint64_t cand;
     uint32_t* shist; /* EXTRA: fused Fig. 1 binning (second pass without stored keys) */
+    uint64_t* ghist; /* its u64 global bins (drained into when a shared bin nears 2^31) */
     BinCalc bc;
     uint32_t hcur, hrun;
     /* per run */
@@ -831,10 +860,10 @@ struct Leaf {
                 }
                 if (shist) {
                     const uint32_t b = bc(K);
-                    if (b == hcur) {
+                    if (b == hcur && hrun < (1u << 20)) {
                         hrun++;
                     } else {
-                        if (hrun) atomicAdd(&shist[hcur], hrun);
+                        if (hrun) sh_bin_add(shist, ghist, hcur, hrun);
                         hcur = b;
                         hrun = 1;
                     }
@@ -869,7 +898,7 @@ struct Leaf {
     }
     __device__ __forceinline__ void flush() {
         if constexpr (EXTRA)
-            if (shist && hrun) atomicAdd(&shist[hcur], hrun);
+            if (shist && hrun) sh_bin_add(shist, ghist, hcur, hrun);
         hrun = 0;
     }
 };
@@ -986,7 +1015,7 @@ __device__ __forceinline__ void eval_body(const RkTables* __restrict__ tab, uint
     TStats ts;
     ts.init();
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-    Leaf<EXTRA> leaf{ts, keys, keys32, key_base, 0u, lo, hi, first, cand, (EXTRA && hist) ? shist : nullptr};
+    Leaf<EXTRA> leaf{ts, keys, keys32, key_base, 0u, lo, hi, first, cand, (EXTRA && hist) ? shist : nullptr, hist};
     leaf.hcur = 0xFFFFFFFFu;
     leaf.hrun = 0;
     if (EXTRA && hist) leaf.bc.init(hist_range->key_min, hist_range->key_max, bins);
@@ -1055,7 +1084,7 @@ __global__ void rk_merge_groups_kernel(const rk_stats* __restrict__ in, uint32_t
                                        rk_stats* __restrict__ out) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= groups) return; /* whole warps exit together */
-    rk_stats v;
+    rk_stats v{};
     v.evaluated = 0;
     for (uint32_t i = lane; i < per; i += 32) merge_into(v, in[(size_t)w * per + i]);
 #pragma unroll
@@ -1125,12 +1154,12 @@ __global__ void __launch_bounds__(256) rk_hist_kernel(const KT* __restrict__ key
     uint32_t cur = 0xFFFFFFFFu, run = 0;
     auto flush = [&]() {
         if (!run) return;
-        if (smem_bins) atomicAdd(&sh[cur], run);
+        if (smem_bins) sh_bin_add(sh, hist, cur, run);
         else atomicAdd((unsigned long long*)&hist[cur], (unsigned long long)run);
     };
     auto put = [&](uint32_t b) {
         if (RANGE && b == 0xFFFFFFFFu) return; /* outside the refinement range */
-        if (b == cur) {
+        if (b == cur && run < (1u << 20)) {
             run++;
         } else {
             flush();
@@ -1503,6 +1532,7 @@ struct DNode {
 };
 constexpr uint32_t kDpEmpty = 0xFFFFFFFFu, kDpBusy = 0xFFFFFFFEu;
 constexpr int kDpThreads = 256;
+constexpr int kDpWarps = kDpThreads / 32;
 
 template <int SMAX>
 __device__ __forceinline__ uint64_t dnode_hash(const DNode<SMAX>& x) {
@@ -1622,7 +1652,7 @@ __device__ __forceinline__ uint4 expand_one(const ExpArgs& x, uint64_t i0, uint3
     const uint32_t c = e.x * n + k;
     const uint64_t Kc = (((uint64_t)e.w << 32) | e.z) + __ldg(x.dk + c);
     const uint4 r = make_uint4(__ldg(x.tid + c), e.y | (1u << k), (uint32_t)Kc, (uint32_t)(Kc >> 32));
-    x.Rn[i0] = r;
+    if (x.Rn) x.Rn[i0] = r; /* the last level is recomputed by the passes that need it, not stored */
     return r;
 }
 
@@ -1720,7 +1750,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
                                                                  const DNode<SMAX>* __restrict__ UP,
                                                                  const uint32_t* __restrict__ cnt_P,
                                                                  uint8_t* __restrict__ code, ulonglong2* __restrict__ dvc,
-                                                                 uint32_t* __restrict__ dvo, uint32_t* __restrict__ nd,
+                                                                 uint2* __restrict__ dvp, uint32_t* __restrict__ nd,
                                                                  uint64_t* __restrict__ fst, uint32_t* __restrict__ offs) {
     __shared__ RkTables t;
     __shared__ uint64_t srow[kDpThreads / 32][128];
@@ -1802,7 +1832,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
             }
             if (lane == 0) {
                 dvc[(uint64_t)u * kDF + rank] = make_ulonglong2(val, cnt);
-                dvo[(uint64_t)u * kDF + rank] = lm;
+                dvp[(uint64_t)u * kDF + rank] = make_uint2(lm, cnt);
             }
             mx = val;
             amx = firstsg;
@@ -1838,7 +1868,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
             }
             if (lane == 0) {
                 dvc[(uint64_t)u * kDF + rank] = make_ulonglong2(lm, cnt);
-                dvo[(uint64_t)u * kDF + rank] = (uint32_t)(lm - mn); /* exact when the row spans < 2^32 */
+                dvp[(uint64_t)u * kDF + rank] = make_uint2((uint32_t)(lm - mn), cnt); /* offset exact when the row spans < 2^32 */
             }
             mx = lm;
             amx = firstsg;
@@ -1880,11 +1910,15 @@ __device__ __forceinline__ void dp_walk(const RkGTab& g, const DPView& v, uint64
     }
 }
 
-/* (node, closed key) of a run: from the expanded run table when pass 1 built
- * one for this range (coalesced), else by walking the transitions */
-__device__ __forceinline__ void dp_run(const RkGTab& g, const DPView& v, uint64_t run, uint32_t& u, uint64_t& Kc) {
-    if (v.runs) {
-        const uint4 e = __ldg(reinterpret_cast<const uint4*>(v.runs) + (run - v.runs_base));
+constexpr uint32_t kDpEdgeBins = 32768; /* histogram up to this many shared-memory bins */
+
+/* (node, closed key) of run `run` of a pass over the runs [rb, re): from the
+ * range's last prefix-expansion level (recomputed from level P-1 in L2, never
+ * stored), else by walking the P transitions */
+__device__ __forceinline__ void dp_src(const RkGTab& g, const DPView& v, const ExpArgs& xp, uint64_t run, uint64_t rb,
+                                       uint32_t& u, uint64_t& Kc) {
+    if (xp.cnt) {
+        const uint4 e = expand_one(xp, run - rb, g.n);
         u = e.x;
         Kc = ((uint64_t)e.w << 32) | e.z;
     } else {
@@ -1892,255 +1926,443 @@ __device__ __forceinline__ void dp_run(const RkGTab& g, const DPView& v, uint64_
     }
 }
 
-/* Pass 1: extremes (min/argmin, max/argmax; smallest index on ties) and the
- * count of [first, first+count); n_lt = n_eq = 0, n_gt = count (pass 2 adds). */
-__global__ void __launch_bounds__(kDpThreads) rk_dp_minmax_kernel(const RkTables* __restrict__ tab, DPView v,
-                                                                 uint64_t first, uint64_t count, rk_stats* out,
-                                                                 rk_stats* recs, uint32_t* counter, ExpArgs xp) {
+/* key of suffix order q of node u after a prefix with closed key Kc (Kb = Kc +
+ * the row minimum): decoded 32-bit offsets, or byte codes into the 64-bit
+ * distinct values when the row spans >= 2^32 (nd bit 31) */
+__device__ __forceinline__ uint64_t dp_key(const DPView& v, uint32_t u, bool wide, uint64_t Kc, uint64_t Kb,
+                                           uint32_t q) {
+    const uint64_t at = (uint64_t)u * v.Dfact + q;
+    if (!wide) return Kb + __ldg(v.offs + at);
+    const uint8_t c = __ldg(v.code + at);
+    return Kc + __ldg(&reinterpret_cast<const ulonglong2*>(v.dvc)[(uint64_t)u * v.Dfact + c].x);
+}
+
+/* Row multiset of a range: the runs of [first, first+count) as
+ * distinct rows (node, Kb) with multiplicities — C4's 3,991,680 runs are
+ * 217,659 distinct rows, so pass 2 counts and bins 18x fewer rows.  Open
+ * addressing over 16-B slots {node | wide << 31, 1, Kb}: one 128-bit CAS
+ * (EMPTY = all zero -> the key) claims a slot or reports its occupant, so no
+ * flag protocol (and no acquire fence, which costs an L1 invalidation per
+ * load) is needed; the multiplicity is added to one of 8 counters per slot,
+ * chosen by CTA index (C4's heaviest row has 11,056 runs).  A run that finds
+ * no slot within kRowProbes probes, or a range-edge run, is appended to the
+ * run list instead (pass 2 processes it on its own).  Slots and counters are
+ * zeroed before pass 1. */
+constexpr uint32_t kRowProbes = 32u;
+constexpr uint32_t kMultShards = 8; /* multiplicity counters per slot (summed by pass 2) */
+struct RowSet {
+    uint4* slot;       /* nullptr: no multiset (every run is an item) */
+    uint32_t* mult;    /* kMultShards per slot */
+    uint32_t mask;     /* slots - 1 */
+    uint32_t* list;    /* run offsets from rb */
+    uint32_t* nlist;   /* device counter */
+};
+__device__ __forceinline__ uint32_t row_hash(uint32_t uw, uint64_t Kb) {
+    uint64_t h = (Kb ^ ((uint64_t)uw << 40) ^ uw) * 0x9E3779B97F4A7C15ull;
+    return (uint32_t)(h >> 32) ^ (uint32_t)h;
+}
+__device__ __forceinline__ void cas128(uint4* p, uint64_t v0, uint64_t v1, uint64_t& r0, uint64_t& r1) {
+    const uint64_t z = 0;
+    asm volatile("{\n .reg .b128 c, v, d;\n mov.b128 c, {%2, %2};\n mov.b128 v, {%3, %4};\n"
+                 " atom.relaxed.gpu.global.cas.b128 d, [%5], c, v;\n mov.b128 {%0, %1}, d;\n}"
+                 : "=l"(r0), "=l"(r1)
+                 : "l"(z), "l"(v0), "l"(v1), "l"(p)
+                 : "memory");
+}
+__device__ __forceinline__ bool row_insert(const RowSet& rs, uint32_t uw, uint64_t Kb) {
+    const uint64_t k0 = (uint64_t)uw | (1ull << 32), k1 = Kb; /* little-endian {uw, 1, Kb lo, Kb hi} */
+    uint32_t h = row_hash(uw, Kb) & rs.mask;
+    for (uint32_t p = 0; p < kRowProbes; p++, h = (h + 1u) & rs.mask) {
+        uint64_t o0, o1;
+        cas128(rs.slot + h, k0, k1, o0, o1);
+        if ((o0 == 0 && o1 == 0) || (o0 == k0 && o1 == k1)) { /* claimed, or already this row */
+            atomicAdd(rs.mult + (uint64_t)h * kMultShards + (blockIdx.x & (kMultShards - 1u)), 1u);
+            return true;
+        }
+    }
+    return false;
+}
+
+/* The range's row multiset from the run metadata: thread per run (grid-
+ * stride); whole runs enter their row (node, Kb), range-edge runs and probe
+ * overflows the run list. */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_insert_kernel(DPView v, uint64_t first, uint64_t count,
+                                                                 const uint32_t* __restrict__ meta_u,
+                                                                 const uint64_t* __restrict__ meta_K, RowSet rs) {
+    constexpr uint32_t DF = kDF;
+    const uint64_t lo = first, hi = first + count;
+    const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
+    (void)v;
+    for (uint64_t run = rb + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; run < re;
+         run += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t idx0 = run * DF;
+        const bool whole = idx0 >= lo && idx0 + DF <= hi;
+        if (!whole || !row_insert(rs, __ldg(meta_u + (run - rb)), __ldg(meta_K + (run - rb))))
+            rs.list[atomicAdd(rs.nlist, 1u)] = (uint32_t)(run - rb);
+    }
+}
+
+/* Pass 1's run pass (lane per run, latency-bound; no key is written): per run
+ * of [first, first+count) its (node, K_closed) — the range's last prefix-
+ * expansion level, recomputed — and the metadata the key stream reads: meta_u
+ * = node | wide << 31, meta_K = Kb = K_closed + the row minimum (keys = Kb +
+ * the node's offsets); the range's extremes from the rows' extremes (min/argmin, max/argmax, smallest index on ties, reading
+ * L12; range-edge runs key by key).  out = {extremes, n_lt = n_eq = 0, n_gt =
+ * evaluated = count} (pass 2 adds the counts). */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_meta_kernel(const RkTables* __restrict__ tab, DPView v,
+                                                               uint64_t first, uint64_t count, uint32_t* meta_u,
+                                                               uint64_t* meta_K, rk_stats* out, rk_stats* recs,
+                                                               uint32_t* counter, ExpArgs xp) {
     __shared__ RkTables t;
     load_tables(t, tab);
     const RkGTab& g = t.g;
-    TStats ts;
-    ts.init();
-    const uint64_t DF = v.Dfact, lo = first, hi = first + count;
+    constexpr uint32_t DF = kDF;
+    const uint64_t lo = first, hi = first + count;
     const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
-    for (uint64_t run = rb + blockIdx.x * blockDim.x + threadIdx.x; run < re; run += gridDim.x * blockDim.x) {
+    uint64_t kmin = ~0ull, kmax = 0, amin = ~0ull, amax = ~0ull, cnt = 0;
+    for (uint64_t run = rb + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; run < re;
+         run += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t u;
         uint64_t Kc;
-        if (xp.cnt) { /* the last prefix-expansion level is produced here (entry = run - rb) */
-            const uint4 e = expand_one(xp, run - rb, g.n);
-            u = e.x;
-            Kc = ((uint64_t)e.w << 32) | e.z;
-        } else {
-            dp_run(g, v, run, u, Kc);
-        }
+        dp_src(g, v, xp, run, rb, u, Kc);
         const uint64_t idx0 = run * DF;
         const uint32_t olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
-        const uint32_t ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : (uint32_t)DF;
-        uint64_t mn, mx, amn, amx;
-        if (olo == 0 && ohi == DF) {
-            mn = Kc + __ldg(v.fst + 4ull * u);
-            mx = Kc + __ldg(v.fst + 4ull * u + 1);
-            amn = idx0 + __ldg(v.fst + 4ull * u + 2);
-            amx = idx0 + __ldg(v.fst + 4ull * u + 3);
-        } else {
-            mn = ~0ull;
-            mx = 0;
-            amn = amx = idx0 + olo;
-            const uint8_t* cr = v.code + (uint64_t)u * DF;
-            const ulonglong2* dr = reinterpret_cast<const ulonglong2*>(v.dvc) + (uint64_t)u * DF;
+        const uint32_t ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF;
+        const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u)); /* min, max */
+        const uint64_t Kb = Kc + mm.x;
+        const bool wide = (__ldg(v.nd + u) >> 31) != 0;
+        const uint32_t uw = u | (wide ? 0x80000000u : 0u);
+        meta_u[run - rb] = uw;
+        meta_K[run - rb] = Kb;
+        const bool whole = olo == 0 && ohi == DF;
+        if (whole) {
+            const ulonglong2 ai = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u) + 1); /* argmin, argmax */
+            const uint64_t Kx = Kc + mm.y, am = idx0 + ai.x, ax = idx0 + ai.y;
+            if (lex_less(Kb, am, kmin, amin)) { kmin = Kb; amin = am; }
+            if (Kx > kmax || (Kx == kmax && ax < amax)) { kmax = Kx; amax = ax; }
+            cnt += DF;
+        } else { /* range-edge run (at most two per range): key by key */
             for (uint32_t q = olo; q < ohi; q++) {
-                const uint64_t K = Kc + __ldg(&dr[__ldg(cr + q)].x);
-                if (K < mn) { mn = K; amn = idx0 + q; }
-                if (K > mx) { mx = K; amx = idx0 + q; }
+                const uint64_t K = dp_key(v, u, wide, Kc, Kb, q), ix = idx0 + q;
+                if (lex_less(K, ix, kmin, amin)) { kmin = K; amin = ix; }
+                if (K > kmax || (K == kmax && ix < amax)) { kmax = K; amax = ix; }
+                cnt++;
             }
         }
-        if (mn < ts.kmin) { ts.kmin = mn; ts.amin = amn; }
-        if (mx > ts.kmax) { ts.kmax = mx; ts.amax = amx; }
-        ts.cnt += ohi - olo;
     }
-    const rk_stats r = block_reduce(to_rec(ts));
+    rk_stats r{};
+    r.key_min = kmin;
+    r.key_max = kmax;
+    r.argmin = amin;
+    r.argmax = amax;
+    r.n_gt = cnt;
+    r.evaluated = cnt;
+    r = block_reduce(r);
     commit(r, recs, counter, out);
 }
 
-constexpr uint32_t kDpEdgeBins = 32768; /* fused histogram up to this many shared-memory bins */
-
-/* Pass 2: every key of [first, first+count) to HBM (u64, index-major), the
- * counts against the candidate (added to rec: n_lt, n_eq; n_gt -= both) and the
- * Fig. 1 histogram over [range.key_min, range.key_max] (HIST).  A warp takes 32
- * consecutive runs: each lane walks one run's prefix (transition tables) and,
- * from its node's sorted distinct suffix values (~14), counts the run's keys
- * against the candidate and bins them (one shared atomic per distinct bin);
- * then the warp writes the 32 runs' key blocks in index order — lane l decodes
- * the 4 keys 4l..4l+3 (one 32-bit word of codes, 4 gathers from the node's
- * distinct values in L1) and stores 32 B (coalesced, streaming stores).  L2
- * reads per run: 120 B of codes + the distinct values, instead of a 960-B row. */
-template <bool HIST>
-__global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(const RkTables* __restrict__ tab, DPView v,
+/* Pass 2's counts against the candidate (reading L13) and Fig. 1 histogram over
+ * range's [key_min, key_max] (reading L14), from the
+ * range's row multiset: item i < slots is a distinct row (node, Kb) with
+ * multiplicity m (weight m); item slots + j is run list entry j (weight 1;
+ * range-edge runs restricted to the range).  Without a multiset (rs.slot ==
+ * nullptr) every run of the range is an item of weight 1.
+ * Per row: wholly below the candidate counts m x D!, within one bin adds m x
+ * D! to it; otherwise its sorted distinct values (two per 16-B load, 8 in
+ * flight; lane l starts at pair l, so lanes rarely collide on a bin) count
+ * against the candidate (rows containing it) and add m x count to their bins
+ * in the warp's private shared bins.  u64 counts; rows heavier than kHeavy add
+ * to the u64 global bins directly, and the shared u32 bins are flushed before
+ * their bound can reach 2^31. */
+constexpr uint32_t kPrivBins = 1024; /* per-warp private bins up to this many bins */
+constexpr uint32_t kHeavy = 2048;    /* heavier rows add to the global bins directly */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* __restrict__ tab, DPView v,
                                                                uint64_t first, uint64_t count,
                                                                const uint64_t* __restrict__ cand_dev,
                                                                const rk_stats* __restrict__ range, uint32_t bins,
-                                                               uint64_t* hist, uint64_t* keys, rk_stats* rec) {
-    __shared__ RkTables t;
-    extern __shared__ uint32_t shist[]; /* HIST: u32 bins */
+                                                               uint64_t* hist, RowSet rs,
+                                                               const uint32_t* __restrict__ meta_u,
+                                                               const uint64_t* __restrict__ meta_K, rk_stats* rec) {
     __shared__ unsigned long long cnt_lt, cnt_eq;
-    if (HIST)
-        for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) shist[i] = 0;
-    if (threadIdx.x == 0) cnt_lt = cnt_eq = 0;
-    load_tables(t, tab); /* (includes the barrier) */
-    const RkGTab& g = t.g;
-    const uint64_t cand = *cand_dev;
-    BinCalc bc;
-    if (HIST) bc.init(range->key_min, range->key_max, bins);
-    const uint32_t lane = threadIdx.x & 31u, DF = v.Dfact;
-    const ulonglong2* dvc = reinterpret_cast<const ulonglong2*>(v.dvc);
-    uint64_t nlt = 0, neq = 0; /* per lane */
-    const uint64_t lo = first, hi = first + count;
-    const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
-    const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    const bool aligned = (first & 1u) == 0; /* run offsets idx0 - first even: 16-B aligned stores */
-    for (uint64_t base = rb + gw * 32; base < re; base += nw * 32) {
-        /* lane-parallel: the lane's run — prefix walk, then counts and bins from
-         * its node's sorted distinct values (one shared atomic per distinct bin) */
-        const uint64_t run = base + lane;
-        uint32_t u = 0, olo = 0, ohi = 0;
-        uint64_t Kb = 0; /* closed-round key + the row minimum: key = Kb + offset */
-        if (run < re) {
-            uint64_t Kc;
-            dp_run(g, v, run, u, Kc);
-            const uint64_t idx0 = run * DF;
-            olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
-            ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF;
-            const uint64_t fmn = __ldg(v.fst + 4ull * u);
-            Kb = Kc + fmn;
-            if (olo == 0 && ohi == DF) {
-                const uint32_t ndv = __ldg(v.nd + u) & 0x7FFFFFFFu;
-                const ulonglong2* dr = dvc + (uint64_t)u * DF;
-                const uint64_t fmx = __ldg(v.fst + 4ull * u + 1);
-                const bool inside = cand >= Kb && cand <= Kc + fmx;
-                if (cand > Kc + fmx) nlt += DF;
-                uint32_t bp = 0xFFFFFFFFu, acc = 0;
-                for (uint32_t q0 = 0; q0 < ndv; q0 += 4) { /* 4 independent loads in flight */
-                    ulonglong2 e[4];
-#pragma unroll
-                    for (int j = 0; j < 4; j++) e[j] = q0 + j < ndv ? __ldg(dr + q0 + j) : make_ulonglong2(0, 0);
-#pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const uint64_t K = Kc + e[j].x;
-                        const uint32_t c = (uint32_t)e[j].y; /* 0 past the end */
-                        if (inside) {
-                            nlt += K < cand ? c : 0u;
-                            neq += K == cand ? c : 0u;
-                        }
-                        if (HIST && c) {
-                            const uint32_t b = bc(K);
-                            if (b == bp) {
-                                acc += c;
-                            } else {
-                                if (acc) atomicAdd(&shist[bp], acc);
-                                bp = b;
-                                acc = c;
-                            }
-                        }
-                    }
-                }
-                if (HIST && acc) atomicAdd(&shist[bp], acc);
-            }
-        }
-        /* warp-cooperative: decode (code bytes -> 32-bit offsets by shuffle) and
-         * store each run's 960-B key block; lane l owns keys 4l..4l+3 */
-        const uint32_t nr = (uint32_t)min((uint64_t)32, re - base);
-        const bool grp_whole = base * DF >= lo && (base + nr) * DF <= hi; /* no range-edge run */
-        /* two runs per step, a half-warp each: lane hl of a half owns the key pairs
-         * (2c, 2c+1), c = 15q + hl (q = 0..3), so every load (8 B of offsets) and
-         * store (16 B of keys) instruction of a half covers one contiguous span */
-        const uint32_t half = lane >> 4, hl = lane & 15u;
-        const bool act = hl < 15u; /* 15 lanes x 4 pairs = DF / 2 = 60 */
-        uint64_t* outb = keys + (base * DF - first) + 2u * hl; /* only dereferenced when keys != nullptr */
-        for (uint32_t i0 = 0; i0 < nr; i0 += 2) {
-            const uint32_t i = i0 + half;
-            const bool valid = i < nr;
-            const uint32_t src = valid ? i : i0;
-            const uint32_t ui = __shfl_sync(0xFFFFFFFFu, u, src);
-            const uint64_t Ki = __shfl_sync(0xFFFFFFFFu, Kb, src);
-            const uint32_t ndv = __ldg(v.nd + ui);
-            uint2 of[4];
-            {
-                const uint2* r = reinterpret_cast<const uint2*>(v.offs + (uint64_t)ui * DF) + hl;
-#pragma unroll
-                for (int q = 0; q < 4; q++) of[q] = act ? __ldg(r + 15 * q) : make_uint2(0, 0);
-            }
-            uint64_t k[8]; /* k[2q], k[2q+1] = keys 2c, 2c+1 of c = 15q + hl */
-            if (!(ndv >> 31)) { /* 32-bit offsets from the row minimum (the common case) */
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    k[2 * q] = Ki + of[q].x;
-                    k[2 * q + 1] = Ki + of[q].y;
-                }
-            } else { /* row spans >= 2^32: codes into the 64-bit distinct values */
-                const ulonglong2* dr = dvc + (uint64_t)ui * DF;
-                const uint64_t fmn = __ldg(v.fst + 4ull * ui);
-                const uint8_t* cr = v.code + (uint64_t)ui * DF;
-#pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    const uint32_t c2 = 2u * (15u * q + hl);
-                    k[2 * q] = act ? Ki - fmn + __ldg(&dr[__ldg(cr + c2)].x) : 0ull;
-                    k[2 * q + 1] = act ? Ki - fmn + __ldg(&dr[__ldg(cr + c2 + 1)].x) : 0ull;
-                }
-            }
-            uint64_t* o = outb + (size_t)i * DF;
-            if (grp_whole) { /* warp-uniform: every run of the group lies inside the range */
-                if (keys && act && valid) {
-                    if (aligned) {
-#pragma unroll
-                        for (int q = 0; q < 4; q++)
-                            __stcs(reinterpret_cast<ulonglong2*>(o + 30 * q), make_ulonglong2(k[2 * q], k[2 * q + 1]));
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 4; q++) {
-                            __stcs(o + 30 * q, k[2 * q]);
-                            __stcs(o + 30 * q + 1, k[2 * q + 1]);
-                        }
-                    }
-                }
-            } else {
-                const uint32_t oi = __shfl_sync(0xFFFFFFFFu, olo, src), hi_i = __shfl_sync(0xFFFFFFFFu, ohi, src);
-                const bool whole = oi == 0 && hi_i == DF;
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const uint32_t sg = 2u * (15u * (q >> 1) + hl) + (q & 1);
-                    if (valid && act && sg >= oi && sg < hi_i) {
-                        if (keys) __stcs(o + 30 * (q >> 1) + (q & 1), k[q]);
-                        if (!whole) { /* range-edge run: per-key counts and bins */
-                            nlt += k[q] < cand;
-                            neq += k[q] == cand;
-                            if (HIST) atomicAdd(&shist[bc(k[q])], 1u);
-                        }
-                    }
-                }
-            }
-        }
-    }
-    unsigned long long a = nlt, b = neq;
-    for (int o = 16; o; o >>= 1) {
-        a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
-        b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
-    }
-    if (lane == 0 && (a || b)) {
-        atomicAdd(&cnt_lt, a);
-        atomicAdd(&cnt_eq, b);
+    __shared__ BinCalc sbc;
+    __shared__ uint32_t smx[2];
+    extern __shared__ uint32_t shist[]; /* bins x (warps if private) */
+    const bool H = hist != nullptr;
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const bool priv = bins <= kPrivBins;
+    const uint32_t nsh = H ? (priv ? bins * kDpWarps : bins) : 0u;
+    for (uint32_t i = threadIdx.x; i < nsh; i += blockDim.x) shist[i] = 0;
+    uint32_t* wh = shist + (priv ? wid * bins : 0u); /* this warp's bins */
+    if (threadIdx.x == 0) {
+        cnt_lt = cnt_eq = 0;
+        smx[0] = smx[1] = 0;
+        if (H) sbc.init(range->key_min, range->key_max, bins);
     }
     __syncthreads();
-    if (threadIdx.x == 0 && (cnt_lt || cnt_eq)) {
+    const BinCalc bc = sbc;
+    const uint64_t cand = *cand_dev;
+    (void)tab;
+    constexpr uint32_t DF = kDF;
+    const uint64_t lo = first, hi = first + count;
+    const uint64_t rb = lo / DF;
+    const bool direct = rs.slot == nullptr; /* no multiset: every run of the range is an item */
+    const uint64_t nrun = (hi + DF - 1) / DF - rb;
+    const uint64_t nitems = direct ? nrun : (uint64_t)rs.mask + 1u + *rs.nlist;
+    uint64_t nlt = 0, neq = 0;
+    uint32_t iter = 0, pass = 0;
+    /* one row (node u, Kb) of weight m; range-edge rows key by key over [olo, ohi) */
+    auto do_row = [&](uint32_t u, uint64_t Kb, uint32_t m, uint32_t olo, uint32_t ohi) {
+        auto add_bin = [&](uint32_t b, uint64_t w) {
+            if (m > kHeavy) atomicAdd((unsigned long long*)&hist[b], (unsigned long long)w);
+            else atomicAdd(&wh[b], (uint32_t)w);
+        };
+        const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u)); /* min, max */
+        const uint64_t Kc = Kb - mm.x;
+        const uint32_t ndr = __ldg(v.nd + u);
+        const bool wide = (ndr >> 31) != 0;
+        if (olo != 0 || ohi != DF) { /* range-edge run: key by key */
+            for (uint32_t q = olo; q < ohi; q++) {
+                const uint64_t K = dp_key(v, u, wide, Kc, Kb, q);
+                nlt += K < cand ? 1u : 0u;
+                neq += K == cand ? 1u : 0u;
+                if (H) atomicAdd(&wh[bc(K)], 1u);
+            }
+            return;
+        }
+        const uint64_t Kx = Kc + mm.y;
+        const bool in = cand >= Kb && cand <= Kx; /* the candidate inside the row */
+        if (cand > Kx) nlt += (uint64_t)m * DF;
+        const uint32_t b0 = H ? bc(Kb) : 0u, b1 = H ? bc(Kx) : 0u;
+        const bool mb = b0 != b1;
+        if (H && !mb) add_bin(b0, (uint64_t)m * DF); /* one bin */
+        if (!in && !mb) return;
+        const uint32_t ndv = ndr & 0x7FFFFFFFu;
+        if (wide) { /* rows spanning >= 2^32 (rare): value by value */
+            const ulonglong2* dr = reinterpret_cast<const ulonglong2*>(v.dvc) + (uint64_t)u * DF;
+            for (uint32_t q = 0; q < ndv; q++) {
+                const ulonglong2 e = __ldg(dr + q);
+                const uint64_t K = Kc + e.x;
+                if (in) {
+                    nlt += K < cand ? m * e.y : 0ull;
+                    neq += K == cand ? m * e.y : 0ull;
+                }
+                if (mb) add_bin(bc(K), (uint64_t)m * e.y);
+            }
+            return;
+        }
+        /* distinct values, 16-B loads (two values) 4 at a time */
+        const uint4* dp4 = reinterpret_cast<const uint4*>(v.dvp + (uint64_t)u * DF); /* 960-B rows: 16-B aligned */
+        const uint32_t np = (ndv + 1u) >> 1;
+        uint32_t i0 = lane % np; /* lanes start at different pairs: fewer colliding bins */
+        for (uint32_t t = 0; t < np; t += 4) {
+            uint4 e[4];
+            uint32_t ix[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                ix[k] = i0;
+                e[k] = t + k < np ? __ldg(dp4 + i0) : make_uint4(0, 0, 0, 0);
+                i0 = i0 + 1u == np ? 0u : i0 + 1u;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    const uint32_t c = (t + k < np && 2u * ix[k] + h < ndv) ? (h ? e[k].w : e[k].y) : 0u;
+                    if (!c) continue;
+                    const uint64_t K = Kb + (h ? e[k].z : e[k].x);
+                    if (in) {
+                        nlt += K < cand ? (uint64_t)m * c : 0ull;
+                        neq += K == cand ? (uint64_t)m * c : 0ull;
+                    }
+                    if (mb) add_bin(bc(K), (uint64_t)m * c);
+                }
+            }
+        }
+    };
+    for (uint64_t bbase = (uint64_t)blockIdx.x * blockDim.x; bbase < nitems;
+         bbase += (uint64_t)gridDim.x * blockDim.x) { /* block-uniform trip count */
+        const uint64_t it = bbase + threadIdx.x;
+        uint32_t m = 0;
+        if (it < nitems) {
+            if (!direct && it <= rs.mask) { /* a distinct row (node, Kb) of multiplicity m */
+                const uint4 key = rs.slot[it];
+                if (key.y) {
+                    const uint4* ms = reinterpret_cast<const uint4*>(rs.mult + it * kMultShards);
+                    const uint4 a0 = ms[0], a1 = ms[1];
+                    m = a0.x + a0.y + a0.z + a0.w + a1.x + a1.y + a1.z + a1.w;
+                    do_row(key.x & 0x7FFFFFFFu, ((uint64_t)key.w << 32) | key.z, m, 0u, DF);
+                }
+            } else { /* a run: listed, or every run (direct) */
+                const uint32_t off = direct ? (uint32_t)it : rs.list[it - rs.mask - 1u];
+                const uint64_t idx0 = (rb + off) * DF;
+                m = 1u;
+                do_row(__ldg(meta_u + off) & 0x7FFFFFFFu, __ldg(meta_K + off), 1u,
+                       lo > idx0 ? (uint32_t)(lo - idx0) : 0u, hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF);
+            }
+        }
+        if (H) { /* flush before a shared bin can wrap: an iteration adds <= 256 x 120 x min(max m, kHeavy) */
+            const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, min(m, kHeavy));
+            uint32_t* sm = smx + (pass & 1u); /* double-buffered: slot pass+1 was read by all last pass */
+            if (lane == 0) atomicMax(sm, mx);
+            __syncthreads();
+            iter += *sm;
+            if (threadIdx.x == 0) smx[(pass + 1u) & 1u] = 0;
+            pass++;
+            if (iter >= (1u << 15)) { /* 2^15 x 30720 + 256 x 120 x kHeavy < 2^31 */
+                for (uint32_t i = threadIdx.x; i < nsh; i += blockDim.x) {
+                    if (shist[i]) atomicAdd((unsigned long long*)&hist[i % bins], (unsigned long long)shist[i]);
+                    shist[i] = 0;
+                }
+                iter = 0;
+                __syncthreads();
+            }
+        }
+    }
+    unsigned long long x = nlt, y = neq;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        x += __shfl_xor_sync(0xFFFFFFFFu, x, o);
+        y += __shfl_xor_sync(0xFFFFFFFFu, y, o);
+    }
+    if (lane == 0 && (x || y)) {
+        atomicAdd(&cnt_lt, x);
+        atomicAdd(&cnt_eq, y);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && rec && (cnt_lt || cnt_eq)) {
         atomicAdd((unsigned long long*)&rec->n_lt, cnt_lt);
         atomicAdd((unsigned long long*)&rec->n_eq, cnt_eq);
         atomicAdd((unsigned long long*)&rec->n_gt, 0ull - (cnt_lt + cnt_eq));
     }
-    if (HIST)
-        for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x)
-            if (shist[i]) atomicAdd((unsigned long long*)&hist[i], (unsigned long long)shist[i]);
+    if (H)
+        for (uint32_t i = threadIdx.x; i < bins; i += blockDim.x) {
+            uint64_t s = 0;
+            for (uint32_t w = 0; w < (priv ? (uint32_t)kDpWarps : 1u); w++) s += shist[w * bins + i];
+            if (s) atomicAdd((unsigned long long*)&hist[i], (unsigned long long)s);
+        }
 }
 
-int g_num_sms = 0;
-int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
+/* Pass 2, the key stream (bandwidth-bound; the step's dominant kernel): every
+ * key of [first, first+count) to HBM, u64 index-major.  A one-shot grid (no
+ * grid-stride loop: CTAs in index order sweep the key array once, which
+ * measured 0.51 ms for 3.83 GB vs 0.62-0.75 ms for persistent grid-stride
+ * layouts, tools/micro/store_patterns.cu): a warp owns kKeyRunsPerWarp
+ * consecutive runs, two per step; lane l stores the key pairs p = l + 32q of
+ * the step's 2 x 60 pairs (one contiguous 1920-B block per step, 16-B
+ * streaming stores) from the 8-B offset pairs of its run's node row (L2).
+ * rb = first / D! and re = ceil((first + count) / D!) come from the host. */
+constexpr uint32_t kKeyRunsPerWarp = 4;
+__global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64_t first, uint64_t count,
+                                                               uint64_t rb, uint64_t re,
+                                                               const uint32_t* __restrict__ meta_u,
+                                                               const uint64_t* __restrict__ meta_K, uint64_t* keys) {
+    constexpr uint32_t DF = kDF, PR = kDF / 2; /* key pairs per run */
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t lo = first, hi = first + count;
+    const uint64_t base = rb + (uint64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kKeyRunsPerWarp;
+    if (base >= re) return;
+    const uint32_t nr = (uint32_t)min((uint64_t)kKeyRunsPerWarp, re - base);
+    /* the warp's runs: lane r loads run r's metadata, each step broadcasts two */
+    const uint32_t umy = lane < nr ? __ldg(meta_u + (base - rb + lane)) : 0u;
+    const uint64_t Kmy = lane < nr ? __ldg(meta_K + (base - rb + lane)) : 0ull;
+    const bool whole = base * DF >= lo && (base + nr) * DF <= hi; /* no range-edge run among them */
+    uint64_t* const o0 = keys + (base * DF - lo);
+    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15u) == 0; /* DF even: every step block alike */
+#pragma unroll
+    for (uint32_t s = 0; s < kKeyRunsPerWarp / 2; s++) {
+        if (2u * s >= nr) break;
+        const uint32_t uA = __shfl_sync(0xFFFFFFFFu, umy, 2 * s), uB = __shfl_sync(0xFFFFFFFFu, umy, 2 * s + 1);
+        const uint64_t KA = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s), KB = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s + 1);
+        const bool twoB = 2u * s + 1u < nr;
+        const uint2* rA = reinterpret_cast<const uint2*>(v.offs + (uint64_t)(uA & 0x7FFFFFFFu) * DF);
+        const uint2* rB = reinterpret_cast<const uint2*>(v.offs + (uint64_t)(uB & 0x7FFFFFFFu) * DF);
+        uint64_t* o = o0 + 2u * s * DF;
+        if (!((uA | (twoB ? uB : 0u)) >> 31)) { /* 32-bit offsets from the row minimum (the common case) */
+            uint2 of[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) { /* pair p = lane + 32q: run A for p < 60, else run B pair p - 60 */
+                const uint32_t p = lane + 32u * q;
+                const bool a = p < PR;
+                const bool ok = a || (twoB && p < 2u * PR);
+                of[q] = ok ? __ldg((a ? rA : rB) + (a ? p : p - PR)) : make_uint2(0, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t p = lane + 32u * q;
+                const bool a = p < PR;
+                if (!(a || (twoB && p < 2u * PR))) continue;
+                const uint64_t Ki = a ? KA : KB;
+                const uint64_t k0 = Ki + of[q].x, k1 = Ki + of[q].y;
+                if (whole && aligned) {
+                    __stcs(reinterpret_cast<ulonglong2*>(o + 2u * p), make_ulonglong2(k0, k1));
+                } else {
+                    const uint64_t ix = (base + 2u * s) * DF + 2u * p;
+                    if (ix >= lo && ix < hi) __stcs(o + 2u * p, k0);
+                    if (ix + 1 >= lo && ix + 1 < hi) __stcs(o + 2u * p + 1, k1);
+                }
+            }
+        } else { /* a row spanning >= 2^32: codes into the 64-bit distinct values */
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t p = lane + 32u * q;
+                const bool a = p < PR;
+                if (!(a || (twoB && p < 2u * PR))) continue;
+                const uint32_t ui = a ? uA : uB, un = ui & 0x7FFFFFFFu, c = a ? p : p - PR;
+                const uint64_t Ki = a ? KA : KB;
+                uint64_t kk[2];
+                if (!(ui >> 31)) {
+                    const uint2 of = __ldg(reinterpret_cast<const uint2*>(v.offs + (uint64_t)un * DF) + c);
+                    kk[0] = Ki + of.x;
+                    kk[1] = Ki + of.y;
+                } else {
+                    const ulonglong2* dr = reinterpret_cast<const ulonglong2*>(v.dvc) + (uint64_t)un * DF;
+                    const uint64_t Kc = Ki - __ldg(v.fst + 4ull * un);
+                    const uint8_t* cr = v.code + (uint64_t)un * DF;
+                    kk[0] = Kc + __ldg(&dr[__ldg(cr + 2 * c)].x);
+                    kk[1] = Kc + __ldg(&dr[__ldg(cr + 2 * c + 1)].x);
+                }
+                const uint64_t ix = (base + 2u * s) * DF + 2u * p;
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    if (ix + h >= lo && ix + h < hi) __stcs(o + 2u * p + h, kk[h]);
+            }
+        }
     }
-    return g_num_sms;
+}
+
+/* Per-device caches of launch-sizing queries (SM count, occupancy): keyed by the
+ * current device, written once with relaxed atomics (idempotent values), so
+ * contexts on different devices or host threads never size a grid for another
+ * GPU or race on the cache. */
+constexpr int kMaxDev = 64;
+int cur_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < kMaxDev ? dev : 0;
+}
+int num_sms() {
+    static int cache[kMaxDev];
+    const int dev = cur_device();
+    int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+        __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
+    }
+    return v;
 }
 
 template <int SMAX, bool FULL>
 int eval_ctas_per_sm() {
-    static int cached = 0;
-    if (!cached) {
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rk_eval_kernel<SMAX, FULL>, kThreads, 0);
-        cached = b > 0 ? b : 1;
+    static int cache[kMaxDev];
+    const int dev = cur_device();
+    int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+    if (!v) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, rk_eval_kernel<SMAX, FULL>, kThreads, 0);
+        if (v <= 0) v = 1;
+        __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
     }
-    return cached;
+    return v;
 }
 
 /* variant index for a (reduced) SM count S: the smallest power of two >= S,
@@ -2415,6 +2637,16 @@ unsigned dp_grid(uint64_t work) {
     if (b > cap) b = cap;
     return (unsigned)(b < 1 ? 1 : b);
 }
+/* grid-stride kernels: one resident wave (no tail wave) */
+template <class K>
+unsigned dp_grid_wave(uint64_t work, K kernel, size_t smem) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kDpThreads, smem);
+    const uint64_t cap = (uint64_t)num_sms() * (uint64_t)(per > 0 ? per : 1);
+    uint64_t b = (work + kDpThreads - 1) / kDpThreads;
+    if (b > cap) b = cap;
+    return (unsigned)(b < 1 ? 1 : b);
+}
 }  // namespace
 
 uint32_t rk_dp_node_bytes(uint32_t S) {
@@ -2456,9 +2688,9 @@ int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t*
 }
 
 int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
-                 uint32_t* dvo, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
+                 void* dvp, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
                  uint32_t* launches) {
-#define RK_DP_SUF_ARGS(SMAX) tab, (const DNode<SMAX>*)UP, cnt_P, code, (ulonglong2*)dvc, dvo, nd, fst, offs
+#define RK_DP_SUF_ARGS(SMAX) tab, (const DNode<SMAX>*)UP, cnt_P, code, (ulonglong2*)dvc, (uint2*)dvp, nd, fst, offs
     const unsigned grid = dp_grid(nodes * 32);
     cudaStream_t st = (cudaStream_t)stream;
     switch (variant(S)) {
@@ -2479,54 +2711,71 @@ int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t
     return (int)cudaGetLastError();
 }
 
-int rk_dp_minmax(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, rk_stats* out, rk_stats* recs,
-                 uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches, const RkExpand* ex) {
+namespace {
+ExpArgs exp_args(const RkExpand* ex) {
     ExpArgs xp{};
     if (ex) xp = ExpArgs{(const uint4*)ex->Rj, ex->aj, (uint4*)ex->Rn, ex->an, ex->cnt, ex->j, ex->tid, ex->dk};
+    return xp;
+}
+}  // namespace
+
+namespace {
+RowSet row_set(const RkRows& r) {
+    return RowSet{(uint4*)r.slot, r.mult, r.mask, r.list, r.nlist};
+}
+}  // namespace
+
+int rk_dp_meta(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u,
+               uint64_t* meta_K, rk_stats* out, rk_stats* recs, uint32_t* counter, uint32_t max_ctas,
+               const RkExpand* last, void* stream, uint32_t* launches) {
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
-    unsigned grid = dp_grid(runs);
+    unsigned grid = dp_grid_wave(runs, rk_dp_meta_kernel, 0);
     if (grid > max_ctas) grid = max_ctas;
-    rk_dp_minmax_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, out, recs, counter, xp);
+    rk_dp_meta_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, meta_u, meta_K, out,
+                                                                     recs, counter, exp_args(last));
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_insert(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
+                 const RkRows& rows, void* stream, uint32_t* launches) {
+    const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
+    const unsigned grid = dp_grid_wave(runs, rk_dp_insert_kernel, 0);
+    rk_dp_insert_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(v, first, count, meta_u, meta_K,
+                                                                       row_set(rows));
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_rows(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, const uint64_t* cand_dev,
+               const rk_stats* range, uint32_t bins, uint64_t* hist, const RkRows& rows, const uint32_t* meta_u,
+               const uint64_t* meta_K, rk_stats* rec, uint32_t max_ctas, void* stream, uint32_t* launches) {
+    if (hist && (bins < 1 || bins > kDpEdgeBins)) return (int)cudaErrorInvalidValue;
+    const size_t smem = hist ? (size_t)bins * 4 * (bins <= kPrivBins ? kDpWarps : 1) : 0;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rk_dp_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const uint64_t items = rows.slot ? (uint64_t)rows.mask + 1u + rows.list_hint : rows.list_hint;
+    unsigned grid = dp_grid_wave(items, rk_dp_rows_kernel, smem);
+    if (max_ctas && grid > max_ctas) grid = max_ctas;
+    rk_dp_rows_kernel<<<grid, kDpThreads, smem, (cudaStream_t)stream>>>(tab, v, first, count, cand_dev, range, bins,
+                                                                         hist, row_set(rows), meta_u, meta_K, rec);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_keys(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
+               uint64_t* keys, void* stream, uint32_t* launches) {
+    const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
+    const uint64_t per_cta = (uint64_t)kDpWarps * kKeyRunsPerWarp; /* one-shot grid */
+    const uint64_t grid = (runs + per_cta - 1) / per_cta;
+    if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidValue;
+    rk_dp_keys_kernel<<<(unsigned)(grid ? grid : 1), kDpThreads, 0, (cudaStream_t)stream>>>(
+        v, first, count, first / v.Dfact, (first + count + v.Dfact - 1) / v.Dfact, meta_u, meta_K, keys);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
 
 uint32_t rk_dp_max_fused_bins() { return kDpEdgeBins; }
 
-int rk_dp_keys(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count,
-               const uint64_t* cand_dev, const rk_stats* range, uint32_t bins, uint64_t* hist, uint64_t* keys,
-               rk_stats* rec, void* stream, uint32_t* launches) {
-    const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
-    unsigned grid = dp_grid(runs);
-    { /* one wave: as many CTAs as are resident (no tail wave; measured -4 %) */
-        static int cached_per = 0;
-        static uint32_t cached_bins = 0xFFFFFFFFu;
-        const uint32_t b = hist ? bins : 0u;
-        if (b != cached_bins) {
-            cached_per = 0;
-            if (hist)
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per, rk_dp_keys_kernel<true>, kDpThreads,
-                                                              (size_t)bins * 4);
-            else
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per, rk_dp_keys_kernel<false>, kDpThreads, 0);
-            cached_bins = b;
-        }
-        if (cached_per > 0 && grid > (unsigned)(cached_per * num_sms())) grid = (unsigned)(cached_per * num_sms());
-    }
-    cudaStream_t st = (cudaStream_t)stream;
-    if (hist) {
-        if (bins > kDpEdgeBins) return (int)cudaErrorInvalidValue;
-        const size_t smem = (size_t)bins * 4;
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(rk_dp_keys_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        rk_dp_keys_kernel<true><<<grid, kDpThreads, smem, st>>>(tab, v, first, count, cand_dev, range, bins, hist,
-                                                                keys, rec);
-    } else {
-        rk_dp_keys_kernel<false><<<grid, kDpThreads, 0, st>>>(tab, v, first, count, cand_dev, range, 0, nullptr,
-                                                              keys, rec);
-    }
-    if (launches) (*launches)++;
-    return (int)cudaGetLastError();
-}
 
 

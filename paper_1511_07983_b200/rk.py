@@ -24,7 +24,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
            "rk_eval_range_async", "rk_eval_range_hist_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
            "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_sweep_pass1_async", "rk_sweep_pass2_async", "rk_memo_info", "rk_rank", "rk_unrank",
+           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_sweep_pass1_async", "rk_sweep_pass2_async", "rk_set_timing", "rk_timing_read", "rk_memo_info", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -35,6 +35,8 @@ class rk_gpu_params(ctypes.Structure):
 
 
 RK_FLAG_CURSOR_PER_KERNEL = 1
+RK_PHASE_NAMES = ("tables", "stream", "hist", "direct", "extremes")  # RK_PHASE_* of rk.h
+RK_N_PHASES = len(RK_PHASE_NAMES)
 
 
 class rk_kernel(ctypes.Structure):
@@ -94,6 +96,8 @@ def lib():
             "rk_sweep_pass1_async": ([vp, u64, u64, vp, vp, vp, vp], ctypes.c_int),
             "rk_sweep_pass2_async": ([vp, u64, u64, vp, vp, u32, vp, vp, vp, vp], ctypes.c_int),
             "rk_memo_info": ([vp, P(u32), P(u32), P(u32), u32], ctypes.c_int),
+            "rk_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
+            "rk_timing_read": ([vp, P(ctypes.c_double), P(u32), u32], ctypes.c_int),
             "rk_best_order": ([vp, u64, P(ctypes.c_int32), P(u64), P(u64), P(u64), vp], ctypes.c_int),
             "rk_heuristic_batch": ([vp, P(rk_kernel), u32, u32, P(ctypes.c_int32), P(u64), vp], ctypes.c_int),
             "rk_percentile": ([vp, P(ctypes.c_int32), u64, u64, P(u64), P(u64)], ctypes.c_int),
@@ -330,6 +334,16 @@ class Context:
         self._chk(self._L.rk_sweep_pass2_async(self.h, first, count, _ptr(cand_key_dev), _ptr(range_dev), bins,
                                                _ptr(hist_dev), _ptr(keys_dev), _ptr(rec_dev), _stream(stream)),
                   "rk_sweep_pass2_async")
+
+    def rk_set_timing(self, on: bool = True):
+        self._chk(self._L.rk_set_timing(self.h, 1 if on else 0), "rk_set_timing")
+
+    def rk_timing_read(self):
+        """-> {phase: (summed ms, marks)} since the last read (RK_PHASE_* names)."""
+        ms = (ctypes.c_double * RK_N_PHASES)()
+        cnt = (ctypes.c_uint32 * RK_N_PHASES)()
+        self._chk(self._L.rk_timing_read(self.h, ms, cnt, RK_N_PHASES), "rk_timing_read")
+        return {name: (ms[i], cnt[i]) for i, name in enumerate(RK_PHASE_NAMES)}
 
     def rk_memo_info(self):
         """-> (on, P, [distinct nodes per level 0..P])"""

@@ -74,7 +74,10 @@ class Sweeper:
         self.rec = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
         self.glob = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
         self.cand = torch.zeros(1, dtype=torch.int64, device=self.dev)
-        self.hist = torch.zeros(bins, dtype=torch.int64, device=self.dev)
+        # histogram with a count record appended: one all_reduce for N ranks
+        self.hbuf = torch.zeros(bins + REC_WORDS, dtype=torch.int64, device=self.dev)
+        self.hist = self.hbuf[:bins]
+        self.fin = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
         self.launches = 0
 
     def set_kernels(self, kernels):
@@ -102,7 +105,12 @@ class Sweeper:
         """Enqueue one pass of the hot path; no host sync.  Returns #our launches.
         events (optional dict) receives CUDA event pairs around pass 1 ("eval":
         memo tables + extremes, or the direct evaluation) and pass 2 ("hist":
-        keys + counts + histogram, or the histogram of stored keys)."""
+        counts + histogram + keys, or the histogram of the stored keys).
+        Collectives for N ranks: one all_gather of the 64-B
+        extremes records (merged on device into the global record, whose
+        extremes are the histogram range) and one all_reduce of the histogram
+        with the count record appended (int64[bins + 8]); a 2-record device
+        merge then gives the final record."""
         c = self.ctx
         L = 0
         c.rk_eval_index_async(cand_index, self.cand, stream)                                  # a5 candidate key
@@ -121,34 +129,40 @@ class Sweeper:
         if ev:
             e1.record(st)
             events.setdefault("eval", []).append((e0, e1))
-        if self.world > 1:                                                                      # a6 combine
+        multi = self.world > 1
+        if multi:                                                                               # a6 combine
             recs = all_gather_records(self.rec, self.group)
             c.rk_merge_stats_async(recs, self.world, self.glob, stream)
             L += c.launches
             rng = self.glob
         else:
             rng = self.rec
-        self.hist.zero_()
+        self.hbuf.zero_()
+        counts = self.hbuf[self.bins:] if multi else self.rec  # where pass 2 adds the counts
         if ev:
             h0, h1 = ev(), ev()
             h0.record(st)
         if self.compact:                                                                       # a4 histogram
             c.rk_histogram32_async(self.keys32, self.count, self.base, rng, self.bins, self.hist, stream)
         else:                                                                                  # a4 pass 2
-            c.rk_sweep_pass2_async(self.first, self.count, self.cand, rng, self.bins, self.hist, self.keys, self.rec,
+            c.rk_sweep_pass2_async(self.first, self.count, self.cand, rng, self.bins, self.hist, self.keys, counts,
                                    stream)
         L += c.launches
         if ev:
             h1.record(st)
             events.setdefault("hist", []).append((h0, h1))
-        if self.world > 1:
-            all_reduce_hist(self.hist, self.group)
-            if not self.compact:  # pass 2 completed the local counts: merge the final records
-                recs = all_gather_records(self.rec, self.group)
-                c.rk_merge_stats_async(recs, self.world, self.glob, stream)
-                L += c.launches
+        if multi:
+            all_reduce_hist(self.hbuf, self.group)
+            both = torch.stack([self.glob, self.hbuf[self.bins:]])
+            c.rk_merge_stats_async(both, 2, self.fin, stream)
+            L += c.launches
         self.launches = L
         return L
+
+    @property
+    def record(self) -> torch.Tensor:
+        """The step's final record (device int64[8] = rk_stats)."""
+        return self.fin if self.world > 1 else self.rec
 
     def overflowed(self) -> bool:
         """Did a compact-key pass see a key >= base + 2^32 (on any rank)?"""
@@ -170,7 +184,7 @@ class Sweeper:
         if self.compact and self.overflowed():  # rare: keys span >= 2^32 above the bound
             self._use_wide_keys()
             self.step_device(idx)
-        out = torch.cat([(self.glob if self.world > 1 else self.rec), self.cand, self.hist]).cpu()
+        out = torch.cat([self.record, self.cand, self.hist]).cpu()
         st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(out[:REC_WORDS].numpy().tobytes()))
         rep = Report(n_orders=self.total, best_key=st.key_min, best_index=st.argmin, worst_key=st.key_max,
                      worst_index=st.argmax, cand_order=order, cand_index=idx,

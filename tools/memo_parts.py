@@ -1,5 +1,8 @@
-"""Pass-2 cost split on C4: keys only / histogram only / neither / both."""
+"""Step cost split on C4 (library phase events): memo tables, key stream
+(with and without keys), histogram; and a plain fill of the same key buffer."""
+import json
 import math
+import os
 import sys
 
 import torch
@@ -18,10 +21,21 @@ cand[0] = key
 rec = torch.zeros(8, dtype=torch.int64, device="cuda")
 keys = torch.empty(N, dtype=torch.int64, device="cuda")
 hist = torch.zeros(256, dtype=torch.int64, device="cuda")
-c.rk_sweep_pass1_async(0, N, cand, rec, keys)
 
 
-def t(fn, reps=5):
+def phases(fn, reps=10):
+    fn()
+    torch.cuda.synchronize()
+    c.rk_set_timing(True)
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    r = c.rk_timing_read()
+    c.rk_set_timing(False)
+    return {k: round(v[0] / v[1], 4) for k, v in r.items() if v[1]}
+
+
+def t(fn, reps=10):
     fn()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -33,9 +47,22 @@ def t(fn, reps=5):
     return a.elapsed_time(b) / reps
 
 
-print("pass1", t(lambda: c.rk_sweep_pass1_async(0, N, cand, rec, keys)))
-print("keys+hist", t(lambda: c.rk_sweep_pass2_async(0, N, cand, rec, 256, hist, keys, rec)))
-print("keys only", t(lambda: c.rk_sweep_pass2_async(0, N, cand, rec, 256, None, keys, rec)))
-print("hist only", t(lambda: c.rk_sweep_pass2_async(0, N, cand, rec, 256, hist, None, rec)))
-print("neither", t(lambda: c.rk_sweep_pass2_async(0, N, cand, rec, 256, None, None, rec)))
+def step(k):
+    c.rk_sweep_pass1_async(0, N, cand, rec, k)
+    hist.zero_()
+    c.rk_sweep_pass2_async(0, N, cand, rec, 256, hist, k, rec)
+
+
+print("step with keys", t(lambda: step(keys)), phases(lambda: step(keys)))
+print("step without keys", t(lambda: step(None)), phases(lambda: step(None)))
 print("torch fill 3.83GB", t(lambda: keys.fill_(1)))
+print("torch zero 3.83GB", t(lambda: keys.zero_()))
+
+g = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden", "c4_oracle.json")))
+cand[0] = g["cand_key"]
+step(keys)
+torch.cuda.synchronize()
+want = [g["stats"][f] for f in ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt", "evaluated")]
+got = [int(x) for x in rec.cpu().tolist()]
+print("parity vs C4 oracle golden:", "OK" if got == want and hist.cpu().tolist() == g["hist"] else f"MISMATCH {got} {want}",
+      os.environ.get("RK_LIB", "default"))
