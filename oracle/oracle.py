@@ -58,14 +58,20 @@ def lib():
         L.or_histogram.argtypes = [u64p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, u64p]
         L.or_heuristic.argtypes = [u32p, u32p, ctypes.c_int, i32p, i32p]
         L.or_pair_score.argtypes = [u32p, u32p, ctypes.c_int, ctypes.c_int, i32p, dp, dp]
+        L.or_keys_of.argtypes = [u32p, u32p, ctypes.c_int, u64p, ctypes.c_uint64, ctypes.c_int, u64p]
         L.or_sweep_sets.argtypes = [u32p, u32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, u64p]
         _lib = L
     return _lib
 
 
+CURSOR_PER_KERNEL = 1  # L4 alt.: the round-robin cursor restarts at SM 0 for every kernel
+STRICT_RR = 2          # L4 alt.: a block goes to the cursor's SM or nowhere (no scan)
+SKIP_AHEAD = 4         # L5 alt.: a blocked kernel waits, later kernels keep filling the round
+
+
 def _gpu_arr(gpu):
-    """7-tuple (Table 1 GPU parameters) or 8-tuple with model-reading flags (bit 0:
-    cursor restarts at SM 0 for every kernel — alternative reading of L4)."""
+    """7-tuple (Table 1 GPU parameters) or 8-tuple with model-reading flags
+    (CURSOR_PER_KERNEL | STRICT_RR | SKIP_AHEAD; rk_oracle.cpp OrGpu)."""
     assert len(gpu) in (7, 8)
     g = [int(x) for x in gpu] + ([0] if len(gpu) == 7 else [])
     return (ctypes.c_uint32 * 8)(*g)
@@ -165,6 +171,18 @@ def sweep(gpu, kernels, first: int = 0, count: int | None = None, cand_key: int 
                         ctypes.byref(err)))
     s = Stats(*[int(x) for x in st], max_rel_err=err.value)
     return s, (karr if keys else None)
+
+
+def keys_of(gpu, kernels, indices, threads: int = 1):
+    """Keys of explicit lexicographic indices (numpy uint64 array in, out)."""
+    import numpy as np
+
+    idx = np.ascontiguousarray(np.asarray(indices, dtype=np.uint64))
+    out = np.zeros(len(idx), dtype=np.uint64)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    _chk(lib().or_keys_of(_gpu_arr(gpu), _kern_arr(kernels), len(kernels), idx.ctypes.data_as(u64p), len(idx),
+                          threads, out.ctypes.data_as(u64p)))
+    return out
 
 
 def histogram(keys, kmin: int, kmax: int, bins: int):

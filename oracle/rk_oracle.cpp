@@ -46,9 +46,17 @@ typedef unsigned __int128 u128;
 /* GPU: N_SM, N_reg_SM, N_shm_SM, N_warp_SM, N_blk_SM, R_B = rb_num / rb_den    */
 struct OrGpu {
     uint32_t n_sm, regs_per_sm, shm_per_sm, warps_per_sm, blocks_per_sm, rb_num, rb_den;
-    uint32_t flags; /* bit 0: the alternative reading of L4 — the round-robin cursor
-                       restarts at SM 0 for every kernel */
+    uint32_t flags; /* model-reading variants, 0 = readings L4/L5:
+                       bit 0: the round-robin cursor restarts at SM 0 for every kernel (L4 alt.)
+                       bit 1: strict round robin — a block goes to the SM under the cursor or
+                              nowhere; no scan of the other SMs (L4 alt.)
+                       bit 2: skip-ahead — a block that fits nowhere defers the rest of its
+                              kernel to the next round and dispatch continues with the next
+                              kernel in launch order (L5 alt., the option SPEC:262 rejects) */
 };
+#define OR_CURSOR_PER_KERNEL 1u
+#define OR_STRICT_RR 2u
+#define OR_SKIP_AHEAD 4u
 /* Kernel profile.  inst_per_block A_i = N_inst_i / N_tblk_i;  mem_per_block
  * M_i = A_i / R_i = 4*mem_events_i / N_tblk_i, in
  * instruction units so that the round cost is max(I_r, R_B*M_r). */
@@ -77,6 +85,7 @@ static int check_inputs(const OrGpu& g, const OrKernel* k, int n) {
     if (g.n_sm == 0 || g.regs_per_sm == 0 || g.shm_per_sm == 0 || g.warps_per_sm == 0 ||
         g.blocks_per_sm == 0 || g.rb_num == 0 || g.rb_den == 0)
         return OR_EINVAL; /* SPEC:30-32 */
+    if (g.flags & ~(OR_CURSOR_PER_KERNEL | OR_STRICT_RR | OR_SKIP_AHEAD)) return OR_EINVAL;
     if (n < 0 || n > 20) return OR_ETOOMANY;
     for (int i = 0; i < n; i++) {
         if (k[i].grid_blocks < 1) return OR_EINVAL;                                  /* SPEC:38 */
@@ -171,9 +180,80 @@ static void close_round(const OrGpu& g, const OrKernel* k, int n, std::vector<ui
     for (int i = 0; i < n; i++) p[i] = 0;
 }
 
+/* First SM, in ring order from the cursor, that can take a block of demand d
+ * ("round-robin ... until any one of the SM resource limitations is
+ * met"), or -1.  Strict round robin (flag bit 1) looks at the cursor's SM only. */
+static int find_sm(const OrGpu& g, const std::vector<SmFree>& sm, uint32_t cursor, const Demand& d) {
+    const uint32_t S = g.n_sm;
+    const uint32_t steps = (g.flags & OR_STRICT_RR) ? 1u : S;
+    for (uint32_t step = 0; step < steps; step++) { /* scan ring-wise from the cursor */
+        uint32_t s = (cursor + step) % S;
+        if (fits(sm[s], d)) return (int)s;
+    }
+    return -1;
+}
+
+/* Skip-ahead reading of L5 (flag bit 2; SPEC:262 names and rejects it): every
+ * round offers the pending blocks kernel by kernel in launch order; a kernel
+ * whose next block fits nowhere keeps the rest of its blocks for the next
+ * round and dispatch moves on to the next kernel.  The round closes once every
+ * kernel with pending blocks has been offered; the next round starts with all
+ * SMs free and the cursor at SM 0 (as in L4/L5).  Blocks of one kernel stay in
+ * order ("all thread blocks from the earliest issued kernel are
+ * first allocated").  A fresh round always places at least the first pending
+ * block (every kernel is feasible, O1), so the loop ends. */
+static void simulate_skip_ahead(const OrGpu& g, const OrKernel* k, int n, const int* order, SimOut& out,
+                                bool keep_rounds, std::vector<int32_t>* trace) {
+    const uint32_t S = g.n_sm;
+    SmFree caps{g.regs_per_sm, g.shm_per_sm, g.warps_per_sm, g.blocks_per_sm};
+    std::vector<SmFree> sm(S, caps);
+    std::vector<uint32_t> p(n, 0), pending(n, 0);
+    uint64_t left = 0;
+    for (int j = 0; j < n; j++) {
+        pending[j] = k[order[j]].grid_blocks;
+        left += pending[j];
+    }
+    out.key = 0;
+    out.t_naive = 0.0;
+    out.rounds.clear();
+    int round = 0;
+    while (left > 0) {
+        for (uint32_t s = 0; s < S; s++) sm[s] = caps;
+        uint32_t cursor = 0;
+        for (int j = 0; j < n; j++) {
+            if (pending[j] == 0) continue;
+            int ki = order[j];
+            Demand d = demand_of(k[ki]);
+            if (g.flags & OR_CURSOR_PER_KERNEL) cursor = 0;
+            while (pending[j] > 0) {
+                int found = find_sm(g, sm, cursor, d);
+                if (found < 0) break; /* the rest of kernel ki waits for the next round */
+                sm[found].regs -= d.regs;
+                sm[found].shm -= d.shm;
+                sm[found].warps -= d.warps;
+                sm[found].slots -= d.slots;
+                p[ki]++;
+                pending[j]--;
+                left--;
+                cursor = ((uint32_t)found + 1) % S;
+                if (trace) {
+                    trace->push_back(round);
+                    trace->push_back(found);
+                }
+            }
+        }
+        close_round(g, k, n, p, out, keep_rounds);
+        round++;
+    }
+}
+
 /* trace (optional): for every block in dispatch order, (round, sm). */
 static void simulate(const OrGpu& g, const OrKernel* k, int n, const int* order, SimOut& out, bool keep_rounds,
                      std::vector<int32_t>* trace) {
+    if (g.flags & OR_SKIP_AHEAD) {
+        simulate_skip_ahead(g, k, n, order, out, keep_rounds, trace);
+        return;
+    }
     const uint32_t S = g.n_sm;
     SmFree caps{g.regs_per_sm, g.shm_per_sm, g.warps_per_sm, g.blocks_per_sm};
     std::vector<SmFree> sm(S, caps);
@@ -187,16 +267,9 @@ static void simulate(const OrGpu& g, const OrKernel* k, int n, const int* order,
     for (int j = 0; j < n; j++) {
         int ki = order[j];
         Demand d = demand_of(k[ki]);
-        if (g.flags & 1u) cursor = 0; /* alternative reading of L4 (f3) */
+        if (g.flags & OR_CURSOR_PER_KERNEL) cursor = 0; /* alternative reading of L4 (f3) */
         for (uint32_t b = 0; b < k[ki].grid_blocks; b++) {
-            int found = -1;
-            for (uint32_t step = 0; step < S; step++) { /* scan ring-wise from the cursor */
-                uint32_t s = (cursor + step) % S;
-                if (fits(sm[s], d)) {
-                    found = (int)s;
-                    break;
-                }
-            }
+            int found = find_sm(g, sm, cursor, d);
             if (found < 0) { /* fits nowhere: close the round, start the next one */
                 close_round(g, k, n, p, out, keep_rounds);
                 round++;
@@ -461,6 +534,48 @@ int or_sweep(const uint32_t* gpu8, const uint32_t* kern, int n, uint64_t first, 
     stats8[6] = m.n_gt;
     stats8[7] = m.evaluated;
     if (max_rel_err) *max_rel_err = err;
+    return OR_OK;
+}
+
+/* Keys of explicit indices (parity samples): keys_out[i] = K(unrank(idx[i])),
+ * the same O2 + O3 + O4 as or_sweep, split over `threads` contiguous chunks. */
+static void keys_chunk(const OrGpu& g, const OrKernel* k, int n, const uint64_t* idx, uint64_t count,
+                       uint64_t* keys_out, int* err) {
+    std::vector<int> order(n);
+    SimOut out;
+    for (uint64_t i = 0; i < count; i++) {
+        unrank(idx[i], n, order.data());
+        simulate(g, k, n, order.data(), out, false, nullptr);
+        if ((out.key >> 64) != 0) {
+            *err = OR_EOVERFLOW;
+            return;
+        }
+        keys_out[i] = (uint64_t)out.key;
+    }
+}
+
+int or_keys_of(const uint32_t* gpu8, const uint32_t* kern, int n, const uint64_t* idx, uint64_t count, int threads,
+               uint64_t* keys_out) {
+    const OrGpu& g = *(const OrGpu*)gpu8;
+    const OrKernel* k = (const OrKernel*)kern;
+    int e = check_inputs(g, k, n);
+    if (e) return e;
+    const uint64_t N = factorial(n);
+    for (uint64_t i = 0; i < count; i++)
+        if (idx[i] >= N) return OR_EINVAL;
+    if (threads < 1) threads = 1;
+    if ((uint64_t)threads > count) threads = count ? (int)count : 1;
+    std::vector<int> errs((size_t)threads, 0);
+    std::vector<std::thread> th;
+    uint64_t base = count / threads, extra = count % threads, off = 0;
+    for (int t = 0; t < threads; t++) {
+        uint64_t c = base + ((uint64_t)t < extra ? 1 : 0);
+        th.emplace_back(keys_chunk, std::cref(g), k, n, idx + off, c, keys_out + off, &errs[(size_t)t]);
+        off += c;
+    }
+    for (auto& t : th) t.join();
+    for (int x : errs)
+        if (x) return x;
     return OR_OK;
 }
 

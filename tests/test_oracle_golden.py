@@ -207,3 +207,32 @@ def test_algorithm1_unspecified_branches_hand_golden(case):
             assert not feasible
         else:
             assert feasible and abs(score - want) <= 1e-12
+
+
+F3 = _load("readings_f3.json")
+
+
+@pytest.mark.parametrize("case", F3["cases"], ids=lambda c: c["name"])
+def test_model_reading_variants_hand_golden(case):
+    """Strict round robin (L4 alt.) and skip-ahead (L5 alt.),
+    alone and combined: rounds, dispatch trace and T derived by hand in
+    tests/golden/readings_f3.json."""
+    for flags, want in case["readings"].items():
+        gpu = list(case["gpu"]) + [int(flags)]
+        r = O.simulate(gpu, case["kernels"], case["order"], trace=True)
+        assert r.rounds == want["rounds"], (flags, r.rounds)
+        assert [list(t) for t in r.trace] == want["trace"], (flags, r.trace)
+        assert r.key == want["T"] * case["gpu"][6] and r.t_naive == want["T"]
+
+
+@pytest.mark.parametrize("threads", [1, 3])
+def test_keys_of_explicit_indices_w4_hand_golden(threads):
+    """or_keys_of (parity samples at full size) returns the hand-derived W4
+    time of every index, in any index order and thread split."""
+    g, ks = W4["gpu"], W4["kernels"]
+    idx = [row[0] for row in W4["orders"]][::-1] + [5, 5, 23, 0]
+    want = {row[0]: 100 * row[3] for row in W4["orders"]}
+    got = O.keys_of(g, ks, idx, threads=threads)
+    assert got.tolist() == [want[i] for i in idx]
+    with pytest.raises(O.OracleError):
+        O.keys_of(g, ks, [24])

@@ -297,3 +297,56 @@ def test_trace_rules_under_cursor_per_kernel_reading(seed):
                 for q in range(4):
                     used[s][q] += d[q]
                 cursor = (s + 1) % S
+
+
+READINGS = [1, 2, 3, 4, 5, 6, 7]  # f3 variants: cursor per kernel (1), strict RR (2), skip-ahead (4), combined
+
+
+@pytest.mark.parametrize("flags", READINGS)
+def test_reading_variants_keep_the_model_invariants(flags):
+    """Properties every reading of L4/L5 must keep (the hand traces in
+    readings_f3.json pin the rules themselves): block conservation,
+    the lower bound max(sum I, R_B sum M) with the exact-rational
+    re-score of the rounds, a single round when sum T <= N_SM
+    (PAPER:70-71), order invariance of identical kernels and the
+    same-side theorem; without skip-ahead, capacity safety of the trace."""
+    gpus = [list(G) + [flags], [8, 65536, 102400, 64, 16, 7, 2, flags], [3, 16384, 16384, 32, 4, 5, 1, flags]]
+    rng = W.SplitMix64(0xF3F3 + flags)
+    for gpu in gpus:
+        for ks in W.random_small_sets(0xA11 + flags, 4, 2, 6, gpu=gpu[:7]):
+            if not all(W.feasible(gpu[:7], k) for k in ks):
+                continue
+            order = list(range(len(ks)))
+            for i in range(len(order) - 1, 0, -1):
+                j = rng.below(i + 1)
+                order[i], order[j] = order[j], order[i]
+            r = O.simulate(gpu, ks, order, trace=True)
+            for i, k in enumerate(ks):
+                assert sum(p[i] for p in r.rounds) == k[0]
+            assert all(any(p) for p in r.rounds)
+            RB = Fraction(gpu[5], gpu[6])
+            T = sum(max(Fraction(sum(p[i] * ks[i][4] for i in range(len(ks)))),
+                        RB * sum(p[i] * ks[i][5] for i in range(len(ks)))) for p in r.rounds)
+            assert T * gpu[6] == r.key >= exact_lower_bound(gpu, ks)
+            if not flags & 4:  # trace in launch order: replay the capacities per (round, SM)
+                used = {}
+                blocks = [k for k in order for _ in range(ks[k][0])]
+                for k, (rr, s) in zip(blocks, r.trace):
+                    u = used.setdefault((rr, s), [0, 0, 0, 0])
+                    for q, dq in enumerate(demand(ks[k])):
+                        u[q] += dq
+                    assert all(u[q] <= gpu[1 + q] for q in range(4))
+    # single round when the blocks do not exceed N_SM
+    ks = [(3, 128, 16, 0, 311, 100), (5, 256, 32, 8192, 2400, 100), (8, 64, 20, 0, 50, 100)]
+    for order in itertools.permutations(range(3)):
+        r = O.simulate(list(G) + [flags], ks, list(order))
+        assert len(r.rounds) == 1 and r.key == exact_lower_bound(G, ks)
+    # identical kernels that differ only in N_tblk; same-side sets
+    ks = [(g, 256, 24, 12288, 800 * 3, 100 * 3) for g in (16, 48, 24, 80, 32)]
+    s, _ = O.sweep(list(G) + [flags], ks)
+    assert s.key_min == s.key_max
+    for cl in ("mem", "cmp"):
+        for ks in W.random_small_sets(0xB3, 4, 3, 5, classes=cl):
+            s, _ = O.sweep(list(G) + [flags], ks)
+            want = G[6] * sum(k[0] * k[4] for k in ks) if cl == "cmp" else G[5] * sum(k[0] * k[5] for k in ks)
+            assert s.key_min == s.key_max == want

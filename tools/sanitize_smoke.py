@@ -34,6 +34,11 @@ for name in ("C1", "C2"):
 c.rk_set_gpu_params(W.GTX580)
 c.rk_eval_batch(W.c5_sets(8))
 c.rk_heuristic_batch(W.c5_sets(8))
+# memoised step (levels, suffix rows, run pass, row multiset CAS, key stream): C3 through the public API
+from paper_1511_07983_b200.sweep import Sweeper
+gpu, ks = W.config("C3")
+rep = Sweeper(gpu).run(ks)
+assert sum(rep.hist) == rep.n_orders
 c.rk_set_gpu_params((13, 32768, 49152, 48, 8, 411, 100))  # generic (runtime-S) variant
 c.rk_set_kernels(W.W4)
 c.rk_eval_range(0, 24, 0)
