@@ -74,6 +74,24 @@ typedef struct {
 /* flags bit: the round-robin cursor restarts at SM 0 for every kernel (the
  * alternative reading of L4; PAPER:76 only says "round-robin fashion"). */
 #define RK_FLAG_CURSOR_PER_KERNEL 1u
+/* flags bit: strict round robin — a block is offered to the SM under the
+ * cursor only; if it does not fit there the round closes (L4 read literally:
+ * PAPER:76 "mapped to SMs in a round-robin fashion, until any one of the SM
+ * resource limitations is met"). */
+#define RK_FLAG_STRICT_RR 2u
+/* flags bit: skip-ahead — a kernel whose next block fits nowhere keeps its
+ * remaining blocks for the next round while dispatch continues with the later
+ * kernels in launch order; a round closes once every kernel with pending
+ * blocks has been offered (the alternative of L5 that SPEC:262 rejects;
+ * PAPER:80 "relegated to the next execution round").
+ * STRICT_RR and SKIP_AHEAD (any combination with CURSOR_PER_KERNEL) run on the
+ * per-order policy kernels: stats, keys, round partitions, candidates, batches
+ * and the two-pass step; memoisation, branch and bound, compact keys and the
+ * fused histogram return RK_EUNSUPPORTED, and so does a reduced SM count
+ * S' > 32 (run-length state) at rk_set_kernels (DESIGN.md §5 "Model-reading
+ * policies"). */
+#define RK_FLAG_SKIP_AHEAD 4u
+#define RK_FLAGS_POLICY (RK_FLAG_STRICT_RR | RK_FLAG_SKIP_AHEAD)
 rk_status rk_set_gpu_params(rk_ctx* ctx, const rk_gpu_params* p);
 
 /* Kernel profile, Table 1 bottom half:

@@ -110,7 +110,11 @@ struct rk_ctx {
 };
 
 /* SM count that selects the kernel variant (the table keeps the real S) */
-static uint32_t vS(const rk_ctx* c, uint32_t S) { return c->force_runs ? 65535u : S; }
+static uint32_t vS(const rk_ctx* c, uint32_t S) {
+    if (c->gp.flags & RK_FLAGS_POLICY) return S | RK_S_POLICY; /* per-order policy kernels */
+    return c->force_runs ? 65535u : S;
+}
+static bool policy(const rk_ctx* c) { return (c->gp.flags & RK_FLAGS_POLICY) != 0; }
 
 namespace {
 
@@ -167,7 +171,7 @@ rk_status check_params(rk_ctx* c, const rk_gpu_params& p) {
     if (!p.n_sm || !p.regs_per_sm || !p.shm_bytes_per_sm || !p.max_warps_per_sm || !p.max_blocks_per_sm ||
         !p.rb_num || !p.rb_den)
         return fail(c, RK_EINVAL, "gpu params must all be > 0 (SPEC:30-32)");
-    if (p.flags & ~RK_FLAG_CURSOR_PER_KERNEL) return fail(c, RK_EINVAL, "unknown model flags");
+    if (p.flags & ~(RK_FLAG_CURSOR_PER_KERNEL | RK_FLAGS_POLICY)) return fail(c, RK_EINVAL, "unknown model flags");
     if (p.max_blocks_per_sm > 255) return fail(c, RK_EUNSUPPORTED, "max_blocks_per_sm > 255");
     if (p.max_warps_per_sm > 32767) return fail(c, RK_EUNSUPPORTED, "max_warps_per_sm > 32767");
     if (p.n_sm > 65535) return fail(c, RK_EUNSUPPORTED, "n_sm > 65535");
@@ -213,6 +217,9 @@ rk_status build_tables(rk_ctx* c, const rk_gpu_params& p, const rk_kernel* ks, u
     }
     if (c && c->no_reduce) gb = 1;
     const uint32_t Sred = (uint32_t)(p.n_sm / gb);
+    if ((p.flags & RK_FLAGS_POLICY) && Sred > RK_SMAX)
+        return fail(c, RK_EUNSUPPORTED, "strict round robin / skip-ahead need a reduced SM count <= %u (got %u)",
+                    (unsigned)RK_SMAX, Sred);
     /* Sred <= RK_SMAX: per-SM register state; larger: run-length state (SMAX = 0) */
     const uint64_t R = p.regs_per_sm / gr, Sh = p.shm_bytes_per_sm / gs;
     if (R > 32767 || Sh > 32767)
@@ -558,7 +565,8 @@ rk_status dp_plan(rk_ctx* c) {
     d.on = false;
     d.runs_ok = false;
     const uint32_t n = c->tab.g.n, S = c->tab.g.S;
-    if (c->device < 0 || c->no_memo || c->force_runs || n < RK_DP_D + 1) return RK_OK; /* S > 32: run-length nodes */
+    if (c->device < 0 || c->no_memo || c->force_runs || policy(c) || n < RK_DP_D + 1)
+        return RK_OK; /* S > 32: run-length nodes; policies: per-order kernels */
     const uint64_t kLimitEntries = 1ull << 26, kLimitBytes = 1ull << 31;
     d.P = n - RK_DP_D;
     d.node_bytes = rk_dp_node_bytes(S);
@@ -956,6 +964,7 @@ rk_status rk_eval_range32_async(rk_ctx* c, uint64_t first, uint64_t count, const
     rk_status s = need_device(c);
     if (s || (s = need_kernels(c))) return s;
     if (!stats_dev || !keys32_dev || !ovf_dev) return fail(c, RK_EINVAL, "stats_dev, keys32_dev, ovf_dev required");
+    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "compact keys under strict round robin / skip-ahead");
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
@@ -971,6 +980,7 @@ rk_status rk_eval_range_hist_async(rk_ctx* c, uint64_t first, uint64_t count, co
     rk_status s = need_device(c);
     if (s || (s = need_kernels(c))) return s;
     if (!range_dev || !hist_dev || bins < 1 || bins > 32768) return fail(c, RK_EINVAL, "bad fused histogram args");
+    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "fused histogram under strict round robin / skip-ahead");
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
@@ -1441,6 +1451,7 @@ rk_status rk_best_order(rk_ctx* c, uint64_t seed_index, int32_t* order_out, uint
     if (s || (s = need_kernels(c))) return s;
     const uint32_t n = c->tab.g.n;
     if (seed_index != UINT64_MAX && seed_index >= space(c)) return fail(c, RK_EINVAL, "seed_index >= n!");
+    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "branch and bound under strict round robin / skip-ahead");
     DeviceGuard dg(c->device);
     c->launches = 0;
     uint64_t seed = ~0ull;

@@ -56,6 +56,11 @@ struct RkTables {
     RkKTab k[RK_MAX_N];
 };
 
+/* Variant selector bit on the S argument of the launchers: the model-reading
+ * policy kernels (RK_FLAG_STRICT_RR / RK_FLAG_SKIP_AHEAD; per-order
+ * simulation on the register state, S' <= 32). */
+constexpr uint32_t RK_S_POLICY = 0x40000000u;
+
 /* ---- launchers (rk_kernels.cu); return cudaError_t as int -------------- */
 int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t first, uint64_t count,
                    const uint64_t* cand_key_dev, uint64_t cand_key_imm, rk_stats* stats_dev, uint64_t* keys_dev,

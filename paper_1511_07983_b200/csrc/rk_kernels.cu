@@ -1129,6 +1129,261 @@ __global__ void rk_simulate_kernel(const RkTables* __restrict__ tab, const int32
     *n_rounds = rec.r;
 }
 
+/* ---- Model-reading policies -------------
+ * RK_FLAG_STRICT_RR (L4 read literally): a block is offered to the
+ * SM under the cursor only.  RK_FLAG_SKIP_AHEAD (the L5 alternative SPEC:262
+ * rejects): a kernel whose next block fits nowhere waits for the next round
+ * while the later kernels keep filling this one.  Under skip-ahead the state
+ * after a prefix carries the pending blocks of earlier kernels, so there is no
+ * prefix sharing or memoisation: one order per thread, the whole round loop,
+ * on the register state (S' <= 32 super-SMs; the symmetry reduction holds:
+ * every placement count stays a multiple of g). */
+constexpr int kPolSmax = 32;
+
+/* Blocks of kernel k the policy can place from cursor cur before one fails:
+ * first fit (L4) takes up to F = sum c_s; strict round robin sends block b to
+ * SM (cur + b) mod S, which fails first at b = min_s ((s - cur) mod S + c_s S). */
+__device__ __forceinline__ uint32_t pol_avail(const St<kPolSmax>& s, const RkKTab& k, const RkGTab& g, bool strict,
+                                              uint32_t cur, uint32_t (&c)[kPolSmax]) {
+    const CapK ck = capk(k);
+    const uint32_t S = g.S;
+    uint32_t F = 0, m = 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 0; i < kPolSmax; i++) {
+        const bool live = (uint32_t)i < S;
+        c[i] = live ? cap1(s.fa[i], s.fb[i], ck) : 0u;
+        F += c[i];
+        const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+        if (live) m = min(m, d + c[i] * S);
+    }
+    return strict ? m : F;
+}
+
+/* Place p (1 <= p <= pol_avail) blocks of kernel k from cursor cur; returns
+ * the new cursor.  First fit is the water-fill of place_core (the SM of the
+ * p-th block + 1); strict round robin gives SM s the blocks b < p with
+ * b = (s - cur) mod S (mod S), and the cursor moves by p. */
+__device__ __forceinline__ uint32_t pol_place(St<kPolSmax>& s, uint32_t p, const uint32_t (&c)[kPolSmax],
+                                              const RkKTab& k, const RkGTab& g, bool strict, uint32_t cur) {
+    const uint32_t S = g.S;
+    if (strict) {
+#pragma unroll
+        for (int i = 0; i < kPolSmax; i++) {
+            if ((uint32_t)i >= S) continue;
+            const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+            const uint32_t x = d < p ? (p - d - 1u) / S + 1u : 0u;
+            s.fa[i] -= x * k.dA;
+            s.fb[i] -= x * k.dB;
+        }
+        return (cur + p) % S;
+    }
+    uint32_t bfa[kPolSmax], bfb[kPolSmax];
+#pragma unroll
+    for (int i = 0; i < kPolSmax; i++) {
+        bfa[i] = s.fa[i];
+        bfb[i] = s.fb[i];
+    }
+    StoreUpd<kPolSmax> u{s};
+    return water_fill<kPolSmax, false>(p, c, bfa, bfb, cur, k, g, u);
+}
+
+__device__ __forceinline__ void pol_fresh(St<kPolSmax>& s, const RkGTab& g) {
+#pragma unroll
+    for (int i = 0; i < kPolSmax; i++) {
+        s.fa[i] = (uint32_t)i < g.S ? g.freshA : 0u;
+        s.fb[i] = (uint32_t)i < g.S ? g.freshB : 0u;
+    }
+}
+
+/* The last rounds of one kernel alone, from a fresh round: both readings put
+ * SC = S*C blocks in a fresh round (strict: min_s (s + C S) = C S at SM 0), so
+ * the rounds are full ones and a remainder (as finish_key). */
+template <class R>
+__device__ __forceinline__ uint64_t pol_alone(uint32_t rem, const RkKTab& k, uint32_t kid, const RkGTab& g, R& rec) {
+    const uint32_t nfull = full_rounds(rem - 1u, k);
+    rec.full(kid, nfull, k.SC);
+    rem -= nfull * k.SC;
+    rec.add(kid, rem);
+    rec.close();
+    return (uint64_t)nfull * k.fullkey + round_key((uint64_t)rem * k.cA, (uint64_t)rem * k.cM, g.num, g.den);
+}
+
+/* Exact key of one launch order (ord[0..n-1]) under the policy flags. */
+template <class R>
+__device__ uint64_t pol_key(const RkTables& t, const uint8_t (&ord)[RK_MAX_N], R& rec) {
+    const RkGTab& g = t.g;
+    const uint32_t n = g.n;
+    const bool strict = (g.flags & RK_FLAG_STRICT_RR) != 0, perk = (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0;
+    St<kPolSmax> s;
+    uint32_t c[kPolSmax];
+    uint64_t K = 0, I = 0, M = 0;
+    uint32_t cur = 0;
+    pol_fresh(s, g);
+    if (!(g.flags & RK_FLAG_SKIP_AHEAD)) {
+        /* in-order dispatch (L5): a block that cannot be placed closes the round */
+        for (uint32_t j = 0; j < n; j++) {
+            const uint32_t kid = ord[j];
+            const RkKTab& k = t.k[kid];
+            uint32_t rem = k.T;
+            if (perk) cur = 0;
+            const uint32_t p = min(rem, pol_avail(s, k, g, strict, cur, c));
+            if (p) {
+                cur = pol_place(s, p, c, k, g, strict, cur);
+                I += (uint64_t)p * k.cA;
+                M += (uint64_t)p * k.cM;
+                rec.add(kid, p);
+                rem -= p;
+            }
+            if (rem) { /* close the round; full rounds of k alone; the rest opens a fresh round */
+                K += round_key(I, M, g.num, g.den);
+                rec.close();
+                const uint32_t nfull = full_rounds(rem - 1u, k);
+                rec.full(kid, nfull, k.SC);
+                K += (uint64_t)nfull * k.fullkey;
+                rem -= nfull * k.SC;
+                pol_fresh(s, g);
+                pol_avail(s, k, g, strict, 0u, c); /* fresh capacities: 1 <= rem <= SC */
+                cur = pol_place(s, rem, c, k, g, strict, 0u);
+                I = (uint64_t)rem * k.cA;
+                M = (uint64_t)rem * k.cM;
+                rec.add(kid, rem);
+            }
+        }
+        rec.close();
+        return K + round_key(I, M, g.num, g.den);
+    }
+    /* skip-ahead: every round offers each kernel with pending blocks, in launch order */
+    uint32_t pend[RK_MAX_N];
+    uint32_t npend = n;
+    for (uint32_t j = 0; j < n; j++) pend[j] = t.k[ord[j]].T;
+    while (npend) {
+        if (npend == 1) {
+            for (uint32_t j = 0; j < n; j++)
+                if (pend[j]) return K + pol_alone(pend[j], t.k[ord[j]], ord[j], g, rec);
+        }
+        pol_fresh(s, g);
+        cur = 0;
+        I = M = 0;
+        for (uint32_t j = 0; j < n; j++) {
+            if (!pend[j]) continue;
+            const uint32_t kid = ord[j];
+            const RkKTab& k = t.k[kid];
+            if (perk) cur = 0;
+            const uint32_t p = min(pend[j], pol_avail(s, k, g, strict, cur, c));
+            if (!p) continue; /* waits for the next round */
+            cur = pol_place(s, p, c, k, g, strict, cur);
+            I += (uint64_t)p * k.cA;
+            M += (uint64_t)p * k.cM;
+            rec.add(kid, p);
+            pend[j] -= p;
+            if (!pend[j]) npend--;
+        }
+        K += round_key(I, M, g.num, g.den);
+        rec.close();
+    }
+    return K;
+}
+
+/* lexicographic unrank into kernel ids (O2's digits) */
+__device__ __forceinline__ void pol_unrank(const RkGTab& g, uint64_t idx, uint8_t (&ord)[RK_MAX_N]) {
+    uint64_t L = identity_list(g.n);
+    for (uint32_t j = 0; j < g.n; j++) {
+        const uint64_t f = g.fact[g.n - 1 - j];
+        const uint32_t d = (uint32_t)(idx / f);
+        idx -= (uint64_t)d * f;
+        ord[j] = (uint8_t)take_nibble(L, d);
+    }
+}
+
+/* stats (+ optional keys) of [first, first+count): grid-stride over indices */
+__global__ void __launch_bounds__(kThreads) rk_policy_eval_kernel(const RkTables* __restrict__ tab, uint64_t first,
+                                                                   uint64_t count, const uint64_t* cand_dev,
+                                                                   uint64_t cand_imm, rk_stats* out, uint64_t* keys,
+                                                                   rk_stats* recs, uint32_t* counter) {
+    __shared__ RkTables t;
+    load_tables(t, tab);
+    const uint64_t cand = cand_dev ? *cand_dev : cand_imm;
+    TStats ts;
+    ts.init();
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    NoRec nr;
+    uint8_t ord[RK_MAX_N];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += nth) {
+        const uint64_t idx = first + i;
+        pol_unrank(t.g, idx, ord);
+        const uint64_t key = pol_key(t, ord, nr);
+        if (keys) keys[i] = key;
+        if (key < ts.kmin) { ts.kmin = key; ts.amin = idx; } /* increasing indices: strict keeps the smallest (L12) */
+        if (key > ts.kmax || ts.cnt == 0) { ts.kmax = key; ts.amax = idx; }
+        ts.nlt += key < cand ? 1u : 0u;
+        ts.neq += key == cand ? 1u : 0u;
+        ts.cnt++;
+    }
+    const rk_stats r = block_reduce(to_rec(ts));
+    commit(r, recs, counter, out);
+}
+
+/* C5 batch under a policy: blockIdx.y = set, blockIdx.x = chunk of its indices */
+__global__ void __launch_bounds__(kThreads) rk_policy_batch_kernel(const RkTables* __restrict__ tabs,
+                                                                    const uint64_t* __restrict__ cand_keys,
+                                                                    rk_stats* recs) {
+    __shared__ RkTables t;
+    const uint32_t set = blockIdx.y;
+    load_tables(t, tabs + set);
+    const uint64_t cand = cand_keys[set], total = t.g.fact[t.g.n];
+    const uint64_t per = (total + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = min(total, (uint64_t)blockIdx.x * per), hi = min(total, lo + per);
+    TStats ts;
+    ts.init();
+    NoRec nr;
+    uint8_t ord[RK_MAX_N];
+    for (uint64_t idx = lo + threadIdx.x; idx < hi; idx += blockDim.x) {
+        pol_unrank(t.g, idx, ord);
+        const uint64_t key = pol_key(t, ord, nr);
+        if (key < ts.kmin) { ts.kmin = key; ts.amin = idx; }
+        if (key > ts.kmax || ts.cnt == 0) { ts.kmax = key; ts.amax = idx; }
+        ts.nlt += key < cand ? 1u : 0u;
+        ts.neq += key == cand ? 1u : 0u;
+        ts.cnt++;
+    }
+    const rk_stats r = block_reduce(to_rec(ts));
+    if (threadIdx.x == 0) recs[set * gridDim.x + blockIdx.x] = r;
+}
+
+/* keys of explicit indices; per_set: item i uses tabs[i], else tabs[0] */
+__global__ void rk_policy_keys_of_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ idx,
+                                         uint32_t m, int per_set, uint64_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const RkTables& t = tabs[per_set ? i : 0];
+    NoRec nr;
+    uint8_t ord[RK_MAX_N];
+    pol_unrank(t.g, idx[i], ord);
+    out[i] = pol_key(t, ord, nr);
+}
+
+__global__ void rk_policy_key_of_index_kernel(const RkTables* __restrict__ tab, uint64_t index,
+                                              uint64_t* __restrict__ out) {
+    if (threadIdx.x) return;
+    NoRec nr;
+    uint8_t ord[RK_MAX_N];
+    pol_unrank(tab->g, index, ord);
+    *out = pol_key(*tab, ord, nr);
+}
+
+/* one order -> round partition (1 thread) */
+__global__ void rk_policy_simulate_kernel(const RkTables* __restrict__ tab, const int32_t* __restrict__ order,
+                                          uint32_t* rounds, uint32_t max_rounds, uint32_t* n_rounds, uint64_t* key) {
+    const RkTables& t = *tab;
+    const uint32_t n = t.g.n;
+    for (uint32_t i = 0; i < max_rounds * n; i++) rounds[i] = 0;
+    Rec rec{rounds, max_rounds, n, 0, t.g.blkscale};
+    uint8_t ord[RK_MAX_N];
+    for (uint32_t j = 0; j < n; j++) ord[j] = (uint8_t)order[j];
+    *key = pol_key(t, ord, rec);
+    *n_rounds = rec.r;
+}
+
 /* Fig. 1 histogram: exact integer bins over [kmin, kmax]:
  * bin = min(B-1, floor((K-kmin)*B / (kmax-kmin))).  HBM-bound pass: each
  * thread reads 8 consecutive keys (two 32-B vector loads; a warp reads 2 KB
@@ -2365,6 +2620,18 @@ int eval_ctas_per_sm() {
     return v;
 }
 
+int policy_ctas_per_sm() {
+    static int cache[kMaxDev];
+    const int dev = cur_device();
+    int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
+    if (!v) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, rk_policy_eval_kernel, kThreads, 0);
+        if (v <= 0) v = 1;
+        __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
+    }
+    return v;
+}
+
 /* variant index for a (reduced) SM count S: the smallest power of two >= S,
  * FULL when equal */
 int variant(uint32_t S) {
@@ -2433,6 +2700,18 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
                    uint32_t* keys32_dev, uint64_t key_base, uint32_t* ovf_dev, const rk_stats* hist_range,
                    uint32_t bins, uint64_t* hist_dev) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (S & RK_S_POLICY) { /* model-reading policy: one order per thread (no fused extras) */
+        if (keys32_dev || hist_dev) return (int)cudaErrorNotSupported;
+        uint64_t ctas = (count + kThreads - 1) / kThreads;
+        const uint64_t cap = (uint64_t)policy_ctas_per_sm() * num_sms();
+        if (ctas > cap) ctas = cap;
+        if (ctas > max_ctas) ctas = max_ctas;
+        if (ctas < 1) ctas = 1;
+        rk_policy_eval_kernel<<<(unsigned)ctas, kThreads, 0, st>>>(tab_dev, first, count, cand_key_dev, cand_key_imm,
+                                                                   stats_dev, keys_dev, recs, counter);
+        if (launches) (*launches)++;
+        return (int)cudaGetLastError();
+    }
     const uint32_t dm = S <= 2 ? (uint32_t)RK_DEPTH_SMALL : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t R = 1;
     for (uint32_t i = 2; i <= (n < dm ? n : dm); i++) R *= i;
@@ -2543,7 +2822,11 @@ int rk_launch_keys_of(const RkTables* tabs_dev, uint32_t n, uint32_t S, const ui
                       uint64_t* out_dev, void* stream, uint32_t* launches) {
     (void)n;
     const unsigned blocks = (m + 127) / 128;
-    RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tabs_dev, idx_dev, m, 1, out_dev);
+    if (S & RK_S_POLICY)
+        rk_policy_keys_of_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(tabs_dev, idx_dev, m, 1, out_dev);
+    else
+        RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tabs_dev, idx_dev, m, 1,
+                            out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -2551,15 +2834,21 @@ int rk_launch_keys_of(const RkTables* tabs_dev, uint32_t n, uint32_t S, const ui
 int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* idx_dev, uint32_t m,
                            uint64_t* out_dev, void* stream, uint32_t* launches) {
     const unsigned blocks = (m + 127) / 128;
-    RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tab_dev, idx_dev, m, 0, out_dev);
+    if (S & RK_S_POLICY)
+        rk_policy_keys_of_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(tab_dev, idx_dev, m, 0, out_dev);
+    else
+        RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tab_dev, idx_dev, m, 0,
+                            out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
 
 int rk_launch_key_of_index(const RkTables* tab_dev, uint32_t S, uint64_t index, uint64_t* out_dev, void* stream,
                            uint32_t* launches) {
-    RK_DISPATCH(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, index,
-                out_dev);
+    if (S & RK_S_POLICY)
+        rk_policy_key_of_index_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(tab_dev, index, out_dev);
+    else
+        RK_DISPATCH(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, index, out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
@@ -2568,13 +2857,23 @@ int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const in
                        uint32_t max_rounds, uint32_t* n_rounds_dev, uint64_t* key_dev, void* stream,
                        uint32_t* launches) {
     (void)n;
-    RK_DISPATCH_GENERIC(S, rk_simulate_kernel, RK_CFG(1, 1, 0, (cudaStream_t)stream), tab_dev, order_dev, rounds_dev,
-                max_rounds, n_rounds_dev, key_dev);
+    if (S & RK_S_POLICY)
+        rk_policy_simulate_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(tab_dev, order_dev, rounds_dev, max_rounds,
+                                                                    n_rounds_dev, key_dev);
+    else
+        RK_DISPATCH_GENERIC(S, rk_simulate_kernel, RK_CFG(1, 1, 0, (cudaStream_t)stream), tab_dev, order_dev,
+                            rounds_dev, max_rounds, n_rounds_dev, key_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
 
 int rk_batch_chunks_per_set(uint32_t n, uint32_t S) {
+    if (S & RK_S_POLICY) { /* one order per thread, ~8 per thread */
+        uint64_t f = 1;
+        for (uint32_t i = 2; i <= n; i++) f *= i;
+        const uint64_t chunks = (f + kThreads * 8 - 1) / (kThreads * 8);
+        return (int)(chunks < 1 ? 1 : (chunks > 65535 ? 65535 : chunks));
+    }
     if (n < 3) return 1;
     const uint32_t dm = S <= 2 ? (uint32_t)RK_DEPTH_SMALL : (S <= 8 ? 4u : (uint32_t)RK_DEPTH_LARGE);
     uint64_t f = 1, R = 1;
@@ -2597,7 +2896,9 @@ int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n
      * the runtime-S variant runs every set with its own count. */
     const bool uniform = (S & 0x80000000u) != 0;
     const uint32_t Sm = S & 0x7FFFFFFFu;
-    if (uniform) {
+    if (Sm & RK_S_POLICY) {
+        rk_policy_batch_kernel<<<grid, kThreads, 0, st>>>(tabs_dev, cand_keys_dev, recs);
+    } else if (uniform) {
         RK_DISPATCH(Sm, rk_batch_kernel, RK_CFG(grid, kThreads, 0, st), tabs_dev, cand_keys_dev, recs);
     } else {
         RK_DISPATCH_GENERIC(Sm, rk_batch_kernel, RK_CFG(grid, kThreads, 0, st), tabs_dev, cand_keys_dev, recs);
@@ -2623,6 +2924,7 @@ int rk_bnb_ctas() { return num_sms() * 4; }
 
 int rk_launch_bnb(const RkTables* tab_dev, uint32_t S, uint32_t P, uint64_t n_units, void* gb_dev,
                   unsigned long long* recs_dev, void* stream, uint32_t* launches) {
+    if (S & RK_S_POLICY) return (int)cudaErrorNotSupported; /* the host refuses first (RK_EUNSUPPORTED) */
     RK_DISPATCH(S, rk_bnb_kernel, RK_CFG((unsigned)rk_bnb_ctas(), kBnbThreads, 0, (cudaStream_t)stream), tab_dev,
                 P, n_units, (BnbGlobal*)gb_dev, recs_dev);
     if (launches) (*launches)++;

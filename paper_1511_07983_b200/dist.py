@@ -12,8 +12,9 @@ NVSwitch for the two real exchange steps of the path:
 
 Everything else is local: rank g evaluates the contiguous index shard
 [g*N/G, (g+1)*N/G) with its own kernels and keeps its keys in its own HBM.
-The collective helpers are device-agnostic so the same code runs over gloo on
-CPU tensors in tests.
+The collective helpers are device-agnostic: with the gloo backend (the CPU
+tests, and the multi-rank GPU tests whose ranks share one device) CUDA tensors
+are staged through host memory; with NCCL they stay on the device.
 """
 from __future__ import annotations
 
@@ -30,8 +31,25 @@ def shard_bounds(total: int, world: int, rank: int) -> tuple[int, int]:
     return lo, hi - lo
 
 
+def _staged(t: torch.Tensor, group) -> bool:
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def all_reduce(t: torch.Tensor, op=dist.ReduceOp.SUM, group=None) -> torch.Tensor:
+    """In-place all_reduce (host-staged for CUDA tensors under gloo)."""
+    if _staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
 def all_gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
     """rec: int64[8] (one rk_stats) -> int64[world, 8] on every rank."""
+    if _staged(rec, group):
+        return all_gather_records(rec.cpu(), group).to(rec.device)
     world = dist.get_world_size(group)
     out = torch.empty((world, REC_WORDS), dtype=torch.int64, device=rec.device)
     dist.all_gather_into_tensor(out, rec.view(1, REC_WORDS), group=group)
@@ -40,14 +58,13 @@ def all_gather_records(rec: torch.Tensor, group=None) -> torch.Tensor:
 
 def all_reduce_hist(hist: torch.Tensor, group=None) -> torch.Tensor:
     """Sum u64 (stored as int64) histograms over ranks, in place."""
-    dist.all_reduce(hist, op=dist.ReduceOp.SUM, group=group)
-    return hist
+    return all_reduce(hist, dist.ReduceOp.SUM, group)
 
 
 def max_over_ranks(x: float, device, group=None) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=device)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        all_reduce(t, dist.ReduceOp.MAX, group)
     return float(t.item())
 
 
@@ -69,7 +86,7 @@ def select_keys_sharded(count_fn, kmin: int, kmax: int, ranks, bins: int = 16384
             nb = span if span <= bins else bins
             h = count_fn(lo, span, nb)
             if multi:
-                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+                all_reduce(h, dist.ReduceOp.SUM, group)
             c = torch.cumsum(h.to("cpu", torch.int64), 0)
             b = int(torch.searchsorted(c, torch.tensor([r], dtype=torch.int64), right=True).item())
             if b >= nb:

@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 
 from . import rk
-from .dist import REC_WORDS, all_gather_records, all_reduce_hist, shard_bounds
+from .dist import REC_WORDS, all_gather_records, all_reduce, all_reduce_hist, shard_bounds
 
 
 @dataclass
@@ -168,7 +168,7 @@ class Sweeper:
         """Did a compact-key pass see a key >= base + 2^32 (on any rank)?"""
         f = self.ovf.clone()
         if self.world > 1:
-            dist.all_reduce(f, op=dist.ReduceOp.MAX, group=self.group)
+            all_reduce(f, dist.ReduceOp.MAX, self.group)
         return bool(f.item())
 
     def heuristic(self):

@@ -215,30 +215,76 @@ def test_errors_through_abi(ctx):
 
 
 def test_c4_full_space_bench_config_vs_oracle_golden(ctx):
-    """12! in the launch configuration bench.py times: aggregates + histogram vs
-    the full multi-core oracle run (tests/golden/c4_oracle.json), per-order keys
-    on samples the oracle computes one by one."""
+    """12! in the launch configuration bench.py times (rk_sweep_pass1/2: the
+    memoised step with keys, counts and the fused histogram): aggregates +
+    histogram vs the full multi-core oracle run (tests/golden/c4_oracle.json);
+    per-order keys by the SURVEY §8(d) protocol — 10^6 random indices plus the
+    first and last 10^5 indices of every shard of an 8-way split — each
+    computed by the oracle one by one (O.keys_of)."""
     g = _gold("c4_oracle.json")
     gpu, ks = W.config("C4")
     assert g["kernels"] == [list(k) for k in ks]
     ctx.rk_set_gpu_params(gpu)
     ctx.rk_set_kernels(ks)
+    assert ctx.rk_memo_info()[0], "the bench configuration runs the memoised step"
     order, _, idx, key = ctx.rk_heuristic_order()
     assert order == g["cand_order"] and idx == g["cand_index"] and key == g["cand_key"]
     N = math.factorial(12)
     keys = torch.empty(N, dtype=torch.int64, device="cuda")
-    st = ctx.rk_eval_range(0, N, key, keys_dev=keys)
+    cand = torch.tensor([key], dtype=torch.int64, device="cuda")
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    hist = torch.zeros(g["bins"], dtype=torch.int64, device="cuda")
+    ctx.rk_sweep_pass1_async(0, N, cand, rec, keys)
+    ctx.rk_sweep_pass2_async(0, N, cand, rec, g["bins"], hist, keys, rec)
+    torch.cuda.synchronize()
+    st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
     assert list(st.as_tuple()) == [g["stats"][f] for f in
                                    ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt", "evaluated")]
-    h = torch.zeros(g["bins"], dtype=torch.int64, device="cuda")
-    ctx.rk_histogram(keys, N, st.key_min, st.key_max, g["bins"], h)
-    assert h.cpu().tolist() == g["hist"]
+    assert hist.cpu().tolist() == g["hist"]
     rng = np.random.default_rng(12)
-    sample = np.concatenate([rng.integers(0, N, 20000), np.arange(0, 2000), np.arange(N - 2000, N)] +
-                            [np.arange(s * N // 8, s * N // 8 + 500) for s in range(1, 8)])
-    kh = keys[torch.from_numpy(sample).cuda()].cpu().numpy().view(np.uint64)
-    for i, k in zip(sample.tolist(), kh.tolist()):
-        assert O.simulate(gpu, ks, O.unrank(i, 12)).key == k, i
+    parts = [rng.integers(0, N, 10 ** 6)]
+    for s in range(8):
+        lo, hi = s * N // 8, (s + 1) * N // 8
+        parts += [np.arange(lo, lo + 10 ** 5), np.arange(hi - 10 ** 5, hi)]
+    sample = np.concatenate(parts).astype(np.uint64)
+    want = O.keys_of(gpu, ks, sample, threads=NCPU)
+    got = keys[torch.from_numpy(sample.view(np.int64)).cuda()].cpu().numpy().view(np.uint64)
+    bad = np.nonzero(got != want)[0]
+    assert len(bad) == 0, f"{len(bad)} of {len(sample)} sampled keys differ, e.g. index {sample[bad[0]]}"
+    # O5: the reported doubles K/den are within 1e-12 of the naive SPEC:210 double
+    for i, k in zip(sample[:200].tolist(), want[:200].tolist()):
+        r = O.simulate(gpu, ks, O.unrank(i, 12))
+        assert abs(r.t_naive - k / gpu[6]) <= 1e-12 * r.t_naive
+
+
+def test_memo_with_cursor_per_kernel_reading_vs_oracle(monkeypatch):
+    """Memoisation under RK_FLAG_CURSOR_PER_KERNEL (the L4 alternative; the
+    level/suffix tables and the run pass all use the flag): full spaces of C2,
+    C3 and random n = 6..8 sets over the GPU shapes, memoisation forced on,
+    every key and statistic vs the block-by-block oracle."""
+    ctx = _direct_ctx(monkeypatch, "RK_FORCE_MEMO")
+    try:
+        cases = [W.config("C2"), W.config("C3")]
+        for gi, gpu in enumerate(GPUS[:5]):
+            for ks in W.random_small_sets(0xC0C0 + gi, 3, 6, 8, gpu=gpu):
+                if all(W.feasible(gpu, k) for k in ks):
+                    cases.append((gpu, ks))
+        checked = 0
+        for gpu, ks in cases:
+            g = list(gpu) + [rk.RK_FLAG_CURSOR_PER_KERNEL]
+            try:
+                ctx.rk_set_gpu_params(g)
+                ctx.rk_set_kernels(ks)
+            except rk.RkError as e:
+                assert e.status == rk.RK_EUNSUPPORTED
+                continue
+            if not ctx.rk_memo_info()[0]:
+                continue
+            check_full_space(ctx, g, ks, bins=(64,))
+            checked += 1
+        assert checked >= 6
+    finally:
+        ctx.close()
 
 
 def test_c5_batch_vs_oracle_golden(ctx):
@@ -993,3 +1039,110 @@ def test_device_algorithm1_unspecified_branches_hand_golden(ctx):
         # the same set as a whole batch of copies (one thread per set)
         orders, _ = ctx.rk_heuristic_batch([case["kernels"]] * 37)
         assert all(o == case["order"] for o in orders)
+
+
+F3 = _gold("readings_f3.json")
+POLICY_FLAGS = [2, 3, 4, 5, 6, 7]  # strict RR (2) / skip-ahead (4), with and without cursor-per-kernel (1)
+
+
+def test_policy_readings_hand_golden_through_abi(ctx):
+    """strict round robin and skip-ahead (rk.h RK_FLAG_STRICT_RR /
+    RK_FLAG_SKIP_AHEAD) reproduce the hand traces of tests/golden/readings_f3.json:
+    round partitions and T of every case and reading, and the full space of each
+    case against the oracle."""
+    for case in F3["cases"]:
+        for flags, want in case["readings"].items():
+            gpu = list(case["gpu"]) + [int(flags)]
+            ctx.rk_set_gpu_params(gpu)
+            ctx.rk_set_kernels(case["kernels"])
+            rounds, key = ctx.rk_simulate_order(case["order"])
+            assert rounds == want["rounds"] and key == want["T"] * case["gpu"][6], (case["name"], flags)
+            check_full_space(ctx, gpu, case["kernels"], bins=(5,))
+
+
+@pytest.mark.parametrize("flags", POLICY_FLAGS)
+def test_policy_full_spaces_vs_oracle(ctx, flags):
+    """Per-order policy kernels vs the block-by-block oracle: every key, the
+    statistics and histograms on C1 (W4 + random sets), C2 and random sets
+    over the GPU shapes (symmetry reduction on, S' <= 32)."""
+    for ks in [W.W4] + W.c1_random_sets()[:16]:
+        check_full_space(ctx, list(W.GTX580) + [flags], ks, bins=(3,))
+    done = 0
+    for gi, gpu in enumerate(GPUS):
+        for ks in W.random_small_sets(0xF300 + 16 * flags + gi, 6, 2, 7, gpu=gpu):
+            if not all(W.feasible(gpu, k) for k in ks):
+                continue
+            ctx.rk_set_gpu_params(list(gpu) + [flags])
+            ctx.rk_set_kernels(ks)
+            check_full_space(ctx, list(gpu) + [flags], ks, bins=(7,))
+            done += 1
+    assert done >= 10
+    gpu, ks = W.config("C2")
+    check_full_space(ctx, list(gpu) + [flags], ks, bins=(256,))
+
+
+@pytest.mark.parametrize("flags", [2, 4, 6])
+def test_policy_c3_full_space_and_c4_samples_vs_oracle(ctx, flags):
+    """C3 (3.6M orders) element by element; C4 (12!) on 20,000 random indices
+    plus both ends (the oracle computes them one by one), under each policy."""
+    gpu, ks = W.config("C3")
+    check_full_space(ctx, list(gpu) + [flags], ks, bins=(256,))
+    gpu, ks = W.config("C4")
+    g = list(gpu) + [flags]
+    ctx.rk_set_gpu_params(g)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(12)
+    rng = np.random.default_rng(flags)
+    sample = np.concatenate([rng.integers(0, N, 20000), np.arange(0, 500), np.arange(N - 500, N)]).astype(np.uint64)
+    want = O.keys_of(g, ks, sample, threads=NCPU)
+    idx = torch.from_numpy(sample.view(np.int64)).cuda()
+    keys = torch.empty(N, dtype=torch.int64, device="cuda")
+    st = ctx.rk_eval_range(0, N, 0, keys_dev=keys)
+    assert st.evaluated == N and st.n_gt == N
+    assert np.array_equal(keys[idx].cpu().numpy().view(np.uint64), want)
+    assert st.key_min == int(keys.min().item()) and st.key_max == int(keys.max().item())
+
+
+def test_policy_batch_and_public_api_vs_oracle(ctx):
+    """C5-shaped batch under each policy (per-set stats vs the oracle's per-set
+    sweep with Algorithm 1's candidate) and the public Sweeper report."""
+    from paper_1511_07983_b200.sweep import Sweeper
+    sets = W.c5_sets(24)
+    for flags in (2, 4, 6):
+        g = list(W.GTX580) + [flags]
+        ctx.rk_set_gpu_params(g)
+        res = ctx.rk_eval_batch(sets)
+        want = O.sweep_sets(g, sets, threads=NCPU)
+        for (st, ck), (ost, oidx, ock) in zip(res, want):
+            assert st.as_tuple() == ost.as_tuple() and ck == ock
+        gpu, ks = W.config("C3")
+        rep = Sweeper(list(gpu) + [flags]).run(ks)
+        cand = O.simulate(list(gpu) + [flags], ks, O.heuristic(gpu, ks)[0]).key
+        ost, okeys = O.sweep(list(gpu) + [flags], ks, cand_key=cand, threads=NCPU, keys=True)
+        assert (rep.best_key, rep.worst_key, rep.best_index, rep.worst_index, rep.n_lt, rep.n_eq, rep.n_gt) == \
+            (ost.key_min, ost.key_max, ost.argmin, ost.argmax, ost.n_lt, ost.n_eq, ost.n_gt)
+        assert rep.cand_key == cand
+        assert rep.hist == O.histogram(okeys, ost.key_min, ost.key_max, 256)
+
+
+def test_policy_unsupported_paths_fail_loudly(ctx):
+    """Policies run on the per-order kernels only: S' > 32, branch and bound,
+    compact keys and the fused histogram return RK_EUNSUPPORTED."""
+    gpu, ks = W.config("C6")
+    ctx.rk_set_gpu_params(list(gpu) + [rk.RK_FLAG_STRICT_RR])
+    with pytest.raises(rk.RkError) as e:
+        ctx.rk_set_kernels(ks)
+    assert e.value.status == rk.RK_EUNSUPPORTED
+    gpu, ks = W.config("C2")
+    ctx.rk_set_gpu_params(list(gpu) + [rk.RK_FLAG_SKIP_AHEAD])
+    ctx.rk_set_kernels(ks)
+    assert ctx.rk_memo_info()[0] is False
+    with pytest.raises(rk.RkError) as e:
+        ctx.rk_best_order()
+    assert e.value.status == rk.RK_EUNSUPPORTED
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    k32 = torch.empty(40320, dtype=torch.int32, device="cuda")
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with pytest.raises(rk.RkError) as e:
+        ctx.rk_eval_range32_async(0, 40320, None, rec, k32, 0, ovf)
+    assert e.value.status == rk.RK_EUNSUPPORTED

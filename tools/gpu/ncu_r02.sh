@@ -1,15 +1,20 @@
 # round-2 ncu evidence: launch list of the bench step + full captures of the step's kernels
+# (.ncu-rep files are exported to CSV on the box and removed: gpurun copies back <= 64 MiB)
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 $NCU --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "launches rc=$?"
-for k in rk_dp_keys_kernel rk_dp_suffix_kernel rk_dp_meta_kernel rk_dp_rows_kernel rk_dp_insert_kernel; do
-  $NCU --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o gpurun_out/full_$k -f \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_$k.log 2>&1; echo "$k rc=$?"
-done
-$NCU --set full --clock-control none --import-source on -k regex:rk_dp_level_kernel -s 21 -c 7 -o gpurun_out/full_levels -f \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_levels.log 2>&1; echo "levels rc=$?"
-timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool memcheck python tools/sanitize_smoke.py > gpurun_out/san_memcheck.log 2>&1; echo "memcheck rc=$?"
-RK_FORCE_MEMO=1 timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool racecheck python tools/sanitize_smoke.py > gpurun_out/san_racecheck.log 2>&1; echo "racecheck rc=$?"
-RK_FORCE_MEMO=1 timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool synccheck python tools/sanitize_smoke.py > gpurun_out/san_synccheck.log 2>&1; echo "synccheck rc=$?"
-tail -3 gpurun_out/san_*.log
+cap() { # name regex skip count
+  $NCU --set full --clock-control none --import-source on -k regex:$2 -s $3 -c $4 -o /tmp/full_$1 -f \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_$1.log 2>&1; echo "$1 rc=$?"
+  $NCU -i /tmp/full_$1.ncu-rep --page raw --csv > gpurun_out/full_$1_raw.csv 2>/dev/null
+  $NCU -i /tmp/full_$1.ncu-rep --page source --csv > gpurun_out/full_$1_source.csv 2>/dev/null
+  ls -la /tmp/full_$1.ncu-rep gpurun_out/full_$1_*.csv
+}
+cap keys rk_dp_keys_kernel 3 1
+cap suffix rk_dp_suffix_kernel 3 1
+cap meta rk_dp_meta_kernel 3 1
+cap rows rk_dp_rows_kernel 3 1
+cap insert rk_dp_insert_kernel 3 1
+cap levels rk_dp_level_kernel 21 7
+du -sh gpurun_out

@@ -2,6 +2,7 @@
 
     summarize_ncu.py full <rep.ncu-rep> <out.json>        # --set full capture
     summarize_ncu.py launches <launches.csv> <out.json>    # gpu__time_duration list
+    summarize_ncu.py fullcsv <out.json> <raw.csv>...       # `ncu -i rep --page raw --csv` exports (units row)
 """
 import csv
 import io
@@ -62,6 +63,40 @@ def full(rep, out):
         print(json.dumps(e)[:400])
 
 
+UNIT = {"ns": 1e-9, "nsecond": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0,
+        "second": 1.0, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "hz": 1.0, "Khz": 1e3,
+        "Mhz": 1e6, "Ghz": 1e9}
+
+
+def fullcsv(out, *files):
+    """Same summary as full() from raw CSV exports (second row = units; values
+    converted to base units: seconds, bytes, Hz)."""
+    res = []
+    for fn in files:
+        rows = list(csv.reader(open(fn)))
+        hdr, units = rows[0], rows[1]
+        for r in rows[2:]:
+            d, u = dict(zip(hdr, r)), dict(zip(hdr, units))
+            e = {"kernel": d.get("Kernel Name", "").split("(")[0], "source": fn.split("/")[-1]}
+            for k, (m, sc) in KEYS.items():
+                v = num(d.get(m))
+                if v is not None:
+                    v *= UNIT.get(u.get(m, ""), 1.0)
+                    if k == "duration_ms":
+                        v *= 1e3
+                    elif k == "sm_mhz":
+                        v *= 1e-6
+                e[k] = v
+            stalls = {k.split("stalled_")[1]: num(v) for k, v in d.items()
+                      if "pcsamp_warps_issue_stalled" in k and not k.endswith("not_issued") and num(v)}
+            tot = sum(stalls.values()) or 1
+            e["stall_pct"] = {k: round(100 * v / tot, 1) for k, v in sorted(stalls.items(), key=lambda x: -x[1])[:8]}
+            res.append(e)
+    json.dump(res, open(out, "w"), indent=1)
+    for e in res:
+        print(json.dumps(e)[:600])
+
+
 def launches(fn, out):
     rows = list(csv.reader(open(fn)))
     h = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
@@ -87,4 +122,4 @@ def launches(fn, out):
 
 
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"full": full, "launches": launches, "fullcsv": fullcsv}[sys.argv[1]](*sys.argv[2:])
