@@ -148,6 +148,17 @@ def read_profile(kernel_sub: str = "rk_eval_kernel", name: str = "r01_ncu_full_e
     return None, None, None, None
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def read_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -190,7 +201,8 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": WORKLOAD, "n": len(ks), "orders": N, "sample_per_step": count},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -289,21 +301,35 @@ def main():
             best = t if best is None else min(best, t)
         write_peak_gbs = 8 * sw.count / (best / 1e3) / 1e9
 
-    # e2e: the public API with host buffers (Sweeper.run: H2D tables, D2H report)
+    # e2e: the public API with host buffers.  Sweeper.run = H2D of the kernel
+    # table, rk_set_kernels (validation + the memo plan: no plan is cached, every
+    # call re-plans), Algorithm 1, the step, D2H of the report
     e2e_steps = args.e2e_steps or max(3, min(30, args.steps // 2))
+
+    def e2e(sets):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        r = None
+        for kset in sets:
+            r = sw.run(kset)
+        b.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b), sw.dev), r
+
     for _ in range(2):
         sw.run(ks)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(e2e_steps):
-        rep = sw.run(ks)
-    b.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(a.elapsed_time(b), sw.dev)
+    e2e_ms, rep = e2e([ks] * e2e_steps)
     e2e_value = N * e2e_steps / (e2e_ms / 1e3)
+    # the same call on a fresh seeded 12-kernel Generator-G set each step (other
+    # sets, other memo sizes: context for the C4 number above)
+    fresh = [W.gen_g(W.SplitMix64(W.SEED_BASE + 0x4000 + i), 12) for i in range(e2e_steps + 2)]
+    for kset in fresh[:2]:
+        sw.run(kset)
+    fresh_ms, _ = e2e(fresh[2:])
+    sw.run(ks)  # back to C4: record, candidate and keys of the bench workload
 
     # the same evaluation (stats + keys) with a switch off, for reference: without
     # the SM-symmetry reduction, and without suffix memoisation (direct kernel)
@@ -405,7 +431,14 @@ def main():
                              "eval_ms_without_reduction": noreduce_ms,  # stats + keys, memoised if planned
                              "note": "gcd(N_SM, grids) SMs act as one super-SM; exact (DESIGN.md §5)"},
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sw.h2d_bytes,
-                        "d2h_bytes_per_step": sw.d2h_bytes, "steps": e2e_steps},
+                        "d2h_bytes_per_step": sw.d2h_bytes, "steps": e2e_steps,
+                        "ms_per_step": e2e_ms / e2e_steps,
+                        "note": ("Sweeper.run(C4) per step: H2D kernel table, rk_set_kernels with a fresh "
+                                 "memo plan (no plan cache), Algorithm 1, pass 1/2, D2H report"),
+                        "fresh_sets": {"value": N * e2e_steps / (fresh_ms / 1e3), "unit": UNIT,
+                                       "ms_per_step": fresh_ms / e2e_steps,
+                                       "sets": (f"{e2e_steps} other Generator-G 12-kernel sets, seeds "
+                                                f"SEED_BASE+0x4000+2..")}},
                 "result": {"best_T": rep.best_key / gpu[6], "best_index": rep.best_index,
                            "worst_T": rep.worst_key / gpu[6], "cand_index": rep.cand_index,
                            "percentile": rep.percentile, "speedup_over_worst": rep.speedup_over_worst,
@@ -413,9 +446,15 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             v, cnt, dt = oracle_rate(gpu, ks, args.cpu_seconds, threads, N // 3)
+            v1, cnt1, dt1 = oracle_rate(gpu, ks, 3.0, 1, N // 5)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                                     "sample": f"{cnt} consecutive C4 orders from index {N // 3} "
-                                              f"({dt:.1f} s on {threads} threads)"}
+                                              f"({dt:.1f} s on {threads} threads)",
+                                    "cpu_model": cpu_model(),
+                                    "one_thread": {"value": v1, "sample": f"{cnt1} consecutive C4 orders from index "
+                                                                          f"{N // 5} ({dt1:.1f} s, 1 thread)",
+                                                   "projected_full_12!_s": N / v1,
+                                                   "note": "projection: 12! / the measured 1-thread rate"}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

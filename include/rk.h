@@ -311,6 +311,17 @@ rk_status rk_timing_read(rk_ctx* ctx, double* ms_sum, uint32_t* counts, uint32_t
  * distinct (remaining set, state) pairs after j kernels. */
 rk_status rk_memo_info(rk_ctx* ctx, uint32_t* on_out, uint32_t* levels_out, uint32_t* nodes_out, uint32_t max_levels);
 
+/* Race audit of the memo tables built by the most recent pass 1 (diagnostic;
+ * DESIGN.md §5 "lock-free hash tables"): checks every level's open-addressing
+ * table and transitions on the device and returns 8 counters in out[8]:
+ * [0] levels over capacity, [1] slots left BUSY, [2] published ids >= count,
+ * [3] nodes not found first from their own hash (lost publish or duplicate
+ * state), [4] transitions neither EMPTY nor a valid id, [5] levels whose
+ * published slots != count, [6] levels whose count != the plan's count,
+ * [7] nodes audited.  [0..6] are all 0 for a race-free build.  Synchronous.
+ * Errors: RK_ESTATE (memoisation off or no pass 1 yet), RK_ENODEVICE, RK_ECUDA. */
+rk_status rk_memo_audit(rk_ctx* ctx, uint64_t* out);
+
 /* Exact optimum by branch and bound (the same (key_min,
  * argmin) as a full rk_eval_range over [0, n!) — SPEC:300, ties -> smallest
  * index — without enumerating n!).  Bound of a prefix (PAPER:79-81 round

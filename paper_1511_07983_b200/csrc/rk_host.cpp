@@ -59,6 +59,7 @@ struct DpPlan {
     std::vector<size_t> toff;     /* hash-table slot offset of level j (j >= 1) */
     std::vector<uint32_t> tmask;  /* slots - 1 of level j */
     std::vector<size_t> xoff;     /* transition offset of level j (j < P): cnt[j] * n entries */
+    std::vector<uint64_t> work;   /* launch work of level j: (nodes of level j) * n */
     size_t table_slots = 0;
     Arena nodes, tables, tid, dk, fst, counters; /* counters: P + 1 node counters, then the overflow flag */
     Arena code, dvc, dvp, nd, offs;              /* suffix rows: byte codes into sorted distinct (value, count) */
@@ -66,8 +67,6 @@ struct DpPlan {
     Arena meta_u, meta_K;                        /* the range's run metadata for the key stream: node | wide, Kb */
     Arena rslot, rmult, rlist;                   /* the range's row multiset (distinct (node, Kb) + multiplicity) */
     uint32_t rmask = 0;                          /* its slots - 1 */
-    bool planned = false;                        /* sizes below belong to plan_tab (byte-identical tables) */
-    RkTables plan_tab{};
     bool runs_ok = false;                        /* meta_u/meta_K hold the range [runs_first, +runs_count) */
     uint64_t runs_first = 0, runs_count = 0;
     DPView view{};
@@ -507,7 +506,6 @@ void dp_free(DpPlan& d) {
     for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist}) a->release();
     d.runs_ok = false;
     d.on = false;
-    d.planned = false;
 }
 
 uint32_t pow2_at_least(uint64_t x) {
@@ -530,7 +528,7 @@ int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vect
         const RkExpand* x = (ex && j >= 1 && j - 1 < ex->size()) ? &(*ex)[j - 1] : nullptr;
         e = rk_dp_level(c->tab_dev, S, Uj, j ? ctr + j : nullptr, nodes + d.noff[j + 1], ctr + j + 1, d.cap[j + 1],
                         (uint32_t*)d.tables.p + d.toff[j + 1], d.tmask[j + 1], (uint32_t*)d.tid.p + d.xoff[j],
-                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.P + 1, (uint64_t)d.cnt[j] * n, stream, &c->launches,
+                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.P + 1, d.work[j], stream, &c->launches,
                         x);
     }
     return e;
@@ -552,39 +550,23 @@ int dp_build(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr)
     return e;
 }
 
-/* Find the exact per-level node counts (one synchronous level-by-level build;
- * capacities from the previous level's exact count), keeping that layout.  Off
- * (direct evaluation) for the run-length state, n < 6, or when it would not
- * pay.  Buffers are grow-only arenas: no allocation once they are large enough. */
-rk_status dp_plan(rk_ctx* c) {
+constexpr uint64_t kLimitEntries = 1ull << 26, kLimitBytes = 1ull << 31;
+
+/* Level layout from per-level node counts (or upper bounds) m[0..P]: level j's
+ * transitions m[j]*n, level j+1's capacity cap[j+1] and a hash table of
+ * pow2(2*cap) slots.  Grow-only arenas (no copy unless keep_nodes: every
+ * build rewrites them).
+ * false = over the size limits (memoisation off). */
+bool dp_layout(rk_ctx* c, const std::vector<uint64_t>& m, const std::vector<uint64_t>& cap, int& e,
+               bool keep_nodes = false) {
     DpPlan& d = c->dp;
-    /* the plan is sizes only (per-level node counts): for byte-identical tables it
-     * is the same, so keep it; every step still rebuilds all tables */
-    if (d.planned && std::memcmp(&d.plan_tab, &c->tab, sizeof(RkTables)) == 0) return RK_OK;
-    d.planned = false;
-    d.on = false;
-    d.runs_ok = false;
-    const uint32_t n = c->tab.g.n, S = c->tab.g.S;
-    if (c->device < 0 || c->no_memo || c->force_runs || policy(c) || n < RK_DP_D + 1)
-        return RK_OK; /* S > 32: run-length nodes; policies: per-order kernels */
-    const uint64_t kLimitEntries = 1ull << 26, kLimitBytes = 1ull << 31;
-    d.P = n - RK_DP_D;
-    d.node_bytes = rk_dp_node_bytes(S);
-    d.cnt.assign(d.P + 1, 0);
-    d.cap.assign(d.P + 1, 0);
-    d.noff.assign(d.P + 1, 0);
-    d.toff.assign(d.P + 1, 0);
-    d.tmask.assign(d.P + 1, 0);
-    d.xoff.assign(d.P + 1, 0);
-    d.cnt[0] = 1;
-    d.view = DPView{};
-    int e = d.counters.reserve(64 * 4);
-    if (!e) e = cudaMemset(d.counters.p, 0, 64 * 4);
-    size_t nb = 0, ts = 0, xs = 0;
-    for (uint32_t j = 0; j < d.P && !e; j++) {
-        const uint64_t m = d.cnt[j], work = m * n, capn = m * (n - j);
+    const uint32_t n = c->tab.g.n;
+    size_t nb = 0, ts = 0, xs = 0, tb = 0;
+    for (uint32_t j = 0; j < d.P; j++) {
+        const uint64_t work = m[j] * n, capn = cap[j + 1];
         const uint64_t slots = pow2_at_least(2 * capn);
-        if (work > kLimitEntries || capn * d.node_bytes > kLimitBytes || slots > kLimitEntries) return RK_OK;
+        if (work > kLimitEntries || capn * d.node_bytes > kLimitBytes || slots > kLimitEntries) return false;
+        d.work[j] = work;
         d.xoff[j] = xs;
         xs += work;
         d.noff[j + 1] = nb;
@@ -593,23 +575,93 @@ rk_status dp_plan(rk_ctx* c) {
         d.toff[j + 1] = ts;
         d.tmask[j + 1] = (uint32_t)(slots - 1);
         ts += slots;
-        e = d.nodes.reserve(nb, d.noff[j + 1]);
-        if (!e) e = d.tables.reserve(ts * 4);
-        if (!e) e = d.tid.reserve(xs * 4, d.xoff[j] * 4);
-        if (!e) e = d.dk.reserve(xs * 8, d.xoff[j] * 8);
-        if (!e) e = cudaMemset((uint32_t*)d.tables.p + d.toff[j + 1], 0xFF, slots * 4);
-        if (!e) e = dp_levels(c, j, j + 1, nullptr);
-        uint32_t h[2] = {0, 0}; /* level j+1 count; the overflow flag lives at P+1 */
-        if (!e) e = cudaMemcpy(&h[0], (uint32_t*)d.counters.p + j + 1, 4, cudaMemcpyDeviceToHost);
-        if (!e) e = cudaMemcpy(&h[1], (uint32_t*)d.counters.p + d.P + 1, 4, cudaMemcpyDeviceToHost);
-        if (e) break;
-        if (h[0] > capn || h[1]) return RK_OK; /* cannot happen: capacity is an upper bound */
-        d.cnt[j + 1] = h[0];
     }
+    tb = nb + ts * 4 + xs * 12;
+    if (tb > 3 * kLimitBytes) return false;
     d.table_slots = ts;
+    e = d.nodes.reserve(nb, keep_nodes ? d.nodes.cap : 0); /* level-by-level: earlier levels stay */
+    if (!e) e = d.tables.reserve(ts * 4);
+    if (!e) e = d.tid.reserve(xs * 4);
+    if (!e) e = d.dk.reserve(xs * 8);
+    return true;
+}
+
+/* Find the exact per-level node counts.  Fast path: all P levels in one go with
+ * upper-bound capacities (level j+1 holds at most min(n!/(n-j-1)!, 2^22)
+ * distinct nodes) and ONE synchronous read of the counts; a capped level that
+ * overflows (flag, probe guard) falls back to the level-by-level build whose
+ * capacities come from the previous level's exact count.  Then the exact
+ * layout the steps use.  Every rk_set_kernels re-plans (no cache), so the
+ * first step on a new kernel set costs what a repeated one does plus this
+ * plan.  Off (direct evaluation) for the run-length state, n < 6, the policy
+ * readings, or when it would not pay. */
+rk_status dp_plan(rk_ctx* c) {
+    DpPlan& d = c->dp;
+    d.on = false;
+    d.runs_ok = false;
+    const uint32_t n = c->tab.g.n, S = c->tab.g.S;
+    if (c->device < 0 || c->no_memo || c->force_runs || policy(c) || n < RK_DP_D + 1)
+        return RK_OK; /* S > 32: run-length nodes; policies: per-order kernels */
+    d.P = n - RK_DP_D;
+    d.node_bytes = rk_dp_node_bytes(S);
+    d.cnt.assign(d.P + 1, 0);
+    d.cap.assign(d.P + 1, 0);
+    d.noff.assign(d.P + 1, 0);
+    d.toff.assign(d.P + 1, 0);
+    d.tmask.assign(d.P + 1, 0);
+    d.xoff.assign(d.P + 1, 0);
+    d.work.assign(d.P + 1, 0);
+    d.cnt[0] = 1;
+    d.view = DPView{};
+    int e = d.counters.reserve(64 * 4);
+    bool counted = false;
+    {   /* fast path: upper-bound capacities, one sync */
+        std::vector<uint64_t> ub(d.P + 1, 1);
+        for (uint32_t j = 0; j < d.P; j++) ub[j + 1] = std::min<uint64_t>(ub[j] * (n - j), 1ull << 22);
+        if (!e && dp_layout(c, ub, ub, e) && !e) {
+            e = cudaMemset(d.tables.p, 0xFF, d.table_slots * 4);
+            if (!e) e = cudaMemset(d.counters.p, 0, 64 * 4);
+            if (!e) e = dp_levels(c, 0, d.P, nullptr);
+            std::vector<uint32_t> h(d.P + 2, 0); /* counts of levels 0..P, the overflow flag at P+1 */
+            if (!e) e = cudaMemcpy(h.data(), d.counters.p, (d.P + 2) * 4, cudaMemcpyDeviceToHost);
+            if (!e && !h[d.P + 1]) {
+                counted = true;
+                for (uint32_t j = 1; j <= d.P; j++) {
+                    d.cnt[j] = h[j];
+                    counted = counted && h[j] <= ub[j];
+                }
+            }
+        }
+    }
+    if (!e && !counted) { /* level by level, exact capacities */
+        std::vector<uint64_t> m(d.P + 1, 0), cap(d.P + 1, 0);
+        m[0] = 1;
+        e = cudaMemset(d.counters.p, 0, 64 * 4);
+        for (uint32_t j = 0; j < d.P && !e; j++) {
+            cap[j + 1] = m[j] * (n - j);
+            for (uint32_t q = j + 1; q <= d.P; q++) m[q] = q == j + 1 ? cap[j + 1] : 1;
+            std::vector<uint64_t> cq(d.P + 1, 1);
+            for (uint32_t q = 1; q <= j + 1; q++) cq[q] = cap[q];
+            if (!dp_layout(c, m, cq, e, true) || e) return e ? cuda_fail(c, e, "memoisation plan") : RK_OK;
+            e = cudaMemset((uint32_t*)d.tables.p + d.toff[j + 1], 0xFF, (d.tmask[j + 1] + 1ull) * 4);
+            if (!e) e = dp_levels(c, j, j + 1, nullptr);
+            uint32_t h[2] = {0, 0}; /* level j+1 count; the overflow flag lives at P+1 */
+            if (!e) e = cudaMemcpy(&h[0], (uint32_t*)d.counters.p + j + 1, 4, cudaMemcpyDeviceToHost);
+            if (!e) e = cudaMemcpy(&h[1], (uint32_t*)d.counters.p + d.P + 1, 4, cudaMemcpyDeviceToHost);
+            if (e) break;
+            if (h[0] > cap[j + 1] || h[1]) return RK_OK; /* cannot happen: capacity is an upper bound */
+            m[j + 1] = d.cnt[j + 1] = h[0];
+        }
+    }
     if (e) {
         cudaGetLastError();
         return cuda_fail(c, e, "memoisation plan");
+    }
+    {   /* the exact layout of the steps: level j+1 capacity cnt[j] * (n - j) */
+        std::vector<uint64_t> m(d.P + 1), cap(d.P + 1, 0);
+        for (uint32_t j = 0; j <= d.P; j++) m[j] = d.cnt[j];
+        for (uint32_t j = 0; j < d.P; j++) cap[j + 1] = (uint64_t)d.cnt[j] * (n - j);
+        if (!dp_layout(c, m, cap, e) || e) return e ? cuda_fail(c, e, "memoisation layout") : RK_OK;
     }
     const uint64_t runs = fact64(n) / fact64(RK_DP_D), uP = d.cnt[d.P];
     const uint64_t DF = fact64(RK_DP_D);
@@ -639,8 +691,6 @@ rk_status dp_plan(rk_ctx* c) {
     d.view.D = RK_DP_D;
     d.view.Dfact = (uint32_t)DF;
     d.on = true;
-    d.planned = true;
-    d.plan_tab = c->tab;
     return RK_OK;
 }
 
@@ -1083,6 +1133,37 @@ rk_status rk_memo_info(rk_ctx* c, uint32_t* on_out, uint32_t* levels_out, uint32
     if (levels_out) *levels_out = c->dp.on ? c->dp.P : 0u;
     if (nodes_out && c->dp.on)
         for (uint32_t j = 0; j <= c->dp.P && j < max_levels; j++) nodes_out[j] = c->dp.cnt[j];
+    return RK_OK;
+}
+
+rk_status rk_memo_audit(rk_ctx* c, uint64_t* out) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!out) return fail(c, RK_EINVAL, "out is required");
+    DpPlan& d = c->dp;
+    if (!d.on || !d.runs_ok) return fail(c, RK_ESTATE, "memo audit needs memoisation on and a pass 1 first");
+    DeviceGuard dg(c->device);
+    unsigned long long* bad = nullptr;
+    std::vector<unsigned long long> h(6 * d.P, 0);
+    std::vector<uint32_t> cnt(d.P + 1, 0);
+    int e = cudaMalloc(&bad, sizeof(unsigned long long) * 6 * d.P);
+    if (!e) e = cudaMemset(bad, 0, sizeof(unsigned long long) * 6 * d.P);
+    const char* nodes = (const char*)d.nodes.p;
+    for (uint32_t j = 1; j <= d.P && !e; j++)
+        e = rk_dp_audit(c->tab.g.S, nodes + d.noff[j], (const uint32_t*)d.counters.p + j, d.cap[j],
+                        (const uint32_t*)d.tables.p + d.toff[j], d.tmask[j], d.view.tid[j - 1], d.work[j - 1],
+                        bad + 6 * (j - 1), nullptr);
+    if (!e) e = cudaMemcpy(h.data(), bad, sizeof(unsigned long long) * 6 * d.P, cudaMemcpyDeviceToHost);
+    if (!e) e = cudaMemcpy(cnt.data(), d.counters.p, 4 * (d.P + 1), cudaMemcpyDeviceToHost);
+    cudaFree(bad);
+    if (e) return cuda_fail(c, e, "rk_memo_audit");
+    for (int q = 0; q < 8; q++) out[q] = 0;
+    for (uint32_t j = 1; j <= d.P; j++) {
+        for (int q = 0; q < 5; q++) out[q] += h[6 * (j - 1) + q];
+        out[5] += h[6 * (j - 1) + 5] != cnt[j];   /* published slots != count */
+        out[6] += cnt[j] != d.cnt[j];             /* count != the plan's (deterministic) count */
+        out[7] += cnt[j];
+    }
     return RK_OK;
 }
 

@@ -133,6 +133,10 @@ int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t
                  void* dvp, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
                  uint32_t* launches);
 uint32_t rk_dp_max_fused_bins();
+/* race audit of level (U, cnt) and its hash table + the previous level's
+ * transitions; bad = 6 zeroed u64 counters (rk_dp_audit_kernel) */
+int rk_dp_audit(uint32_t S, const void* U, const uint32_t* cnt, uint32_t cap, const uint32_t* table, uint32_t tmask,
+                const uint32_t* tid_prev, uint64_t work_prev, unsigned long long* bad, void* stream);
 /* a range's row multiset: 16-B open-addressing slots of the
  * distinct rows (node | wide << 31, Kb) with 8 multiplicity counters each;
  * slot (nullptr: none) and mult must be zeroed and *nlist = 0 before pass 1;

@@ -1924,7 +1924,9 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
     load_tables(t, tab);
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
-    const uint32_t m = Uj ? *cnt_j : 1u;
+    /* an overflowed level (capped planning capacities) stops every
+     * later level: its count may exceed the nodes it stored */
+    const uint32_t m = Uj ? (*(volatile uint32_t*)ovf ? 0u : *cnt_j) : 1u;
     NoRec nr;
     for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < xp.cnt;
          x += gridDim.x * (uint64_t)blockDim.x)
@@ -1944,7 +1946,11 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
         DNode<SMAX> o;
         st_to_node<SMAX>(s2, nd.mask | (1u << k), o);
         uint32_t pos = (uint32_t)dnode_hash(o) & tmask, id = kDpEmpty;
-        for (;;) {
+        for (uint32_t probes = 0;; probes++) {
+            if (probes > tmask) { /* table full (only with capped planning capacities) */
+                atomicOr(ovf, 1u);
+                break;
+            }
             uint32_t v;
             /* acquire: a published id makes its record visible (paired with the release below) */
             asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], %2, %3;"
@@ -1980,6 +1986,47 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
         }
         tid[c] = id;
         dk[c] = s2.K;
+    }
+}
+
+/* Race audit of one level's lock-free hash table after a build (no sanitizer
+ * on this pool): bad[0] count over capacity, bad[1] slots left
+ * BUSY (a claim never published), bad[2] published ids >= count, bad[3] nodes
+ * whose probe from their own hash meets an EMPTY slot or another id with an
+ * equal record first (lost publish / duplicate state), bad[4] transitions of
+ * the previous level that are neither EMPTY (used kernel) nor < count, bad[5]
+ * published slots (must equal the count). */
+template <int SMAX>
+__global__ void rk_dp_audit_kernel(const DNode<SMAX>* __restrict__ U, const uint32_t* cnt_p, uint32_t cap,
+                                   const uint32_t* __restrict__ table, uint32_t tmask,
+                                   const uint32_t* __restrict__ tid_prev, uint64_t work_prev,
+                                   unsigned long long* bad) {
+    const uint32_t cnt = *cnt_p, c = min(cnt, cap);
+    const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = gridDim.x * (uint64_t)blockDim.x;
+    if (gt == 0 && cnt > cap) atomicAdd(bad + 0, 1ull);
+    for (uint64_t i = gt; i <= (uint64_t)tmask; i += nth) {
+        const uint32_t v = table[i];
+        if (v == kDpBusy) atomicAdd(bad + 1, 1ull);
+        else if (v != kDpEmpty) atomicAdd(bad + (v >= c ? 2 : 5), 1ull);
+    }
+    for (uint64_t id = gt; id < c; id += nth) {
+        const DNode<SMAX> x = U[id];
+        uint32_t pos = (uint32_t)dnode_hash(x) & tmask;
+        bool ok = false;
+        for (uint32_t p = 0; p <= tmask; p++) {
+            const uint32_t v = table[pos];
+            if (v == kDpEmpty) break;
+            if (v < c && dnode_eq_ldcg(U + v, x)) {
+                ok = v == (uint32_t)id;
+                break;
+            }
+            pos = (pos + 1u) & tmask;
+        }
+        if (!ok) atomicAdd(bad + 3, 1ull);
+    }
+    for (uint64_t i = gt; i < work_prev; i += nth) {
+        const uint32_t v = tid_prev[i];
+        if (v != kDpEmpty && v >= c) atomicAdd(bad + 4, 1ull);
     }
 }
 
@@ -2986,6 +3033,24 @@ int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t*
     }
 #undef RK_DP_LEVEL_ARGS
     if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_audit(uint32_t S, const void* U, const uint32_t* cnt, uint32_t cap, const uint32_t* table, uint32_t tmask,
+                const uint32_t* tid_prev, uint64_t work_prev, unsigned long long* bad, void* stream) {
+#define RK_DP_AUDIT_ARGS(SMAX) (const DNode<SMAX>*)U, cnt, cap, table, tmask, tid_prev, work_prev, bad
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned grid = 4u * (unsigned)num_sms();
+    switch (variant(S)) {
+        case 0: rk_dp_audit_kernel<1><<<grid, 256, 0, st>>>(RK_DP_AUDIT_ARGS(1)); break;
+        case 1: rk_dp_audit_kernel<2><<<grid, 256, 0, st>>>(RK_DP_AUDIT_ARGS(2)); break;
+        case 2: case 3: rk_dp_audit_kernel<4><<<grid, 256, 0, st>>>(RK_DP_AUDIT_ARGS(4)); break;
+        case 4: case 5: rk_dp_audit_kernel<8><<<grid, 256, 0, st>>>(RK_DP_AUDIT_ARGS(8)); break;
+        case 6: case 7: rk_dp_audit_kernel<16><<<grid, 256, 0, st>>>(RK_DP_AUDIT_ARGS(16)); break;
+        case 8: case 9: rk_dp_audit_kernel<32><<<grid, 256, 0, st>>>(RK_DP_AUDIT_ARGS(32)); break;
+        default: rk_dp_audit_kernel<0><<<grid, 256, 0, st>>>(RK_DP_AUDIT_ARGS(0)); break;
+    }
+#undef RK_DP_AUDIT_ARGS
     return (int)cudaGetLastError();
 }
 

@@ -24,7 +24,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
            "rk_eval_range_async", "rk_eval_range_hist_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
            "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_sweep_pass1_async", "rk_sweep_pass2_async", "rk_set_timing", "rk_timing_read", "rk_memo_info", "rk_rank", "rk_unrank",
+           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_sweep_pass1_async", "rk_sweep_pass2_async", "rk_set_timing", "rk_timing_read", "rk_memo_info", "rk_memo_audit", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -98,6 +98,7 @@ def lib():
             "rk_sweep_pass1_async": ([vp, u64, u64, vp, vp, vp, vp], ctypes.c_int),
             "rk_sweep_pass2_async": ([vp, u64, u64, vp, vp, u32, vp, vp, vp, vp], ctypes.c_int),
             "rk_memo_info": ([vp, P(u32), P(u32), P(u32), u32], ctypes.c_int),
+            "rk_memo_audit": ([vp, P(u64)], ctypes.c_int),
             "rk_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
             "rk_timing_read": ([vp, P(ctypes.c_double), P(u32), u32], ctypes.c_int),
             "rk_best_order": ([vp, u64, P(ctypes.c_int32), P(u64), P(u64), P(u64), vp], ctypes.c_int),
@@ -353,6 +354,12 @@ class Context:
         nodes = (ctypes.c_uint32 * 17)()
         self._chk(self._L.rk_memo_info(self.h, ctypes.byref(on), ctypes.byref(lv), nodes, 17), "rk_memo_info")
         return bool(on.value), lv.value, list(nodes)[:lv.value + 1] if on.value else []
+
+    def rk_memo_audit(self):
+        """-> 8 counters of the race audit of the last pass 1's memo tables (rk.h)."""
+        out = (ctypes.c_uint64 * 8)()
+        self._chk(self._L.rk_memo_audit(self.h, out), "rk_memo_audit")
+        return list(out)
 
     def rk_best_order(self, seed_index=None, stream=None):
         """Exact optimum by branch and bound -> (order, index, key, nodes);

@@ -1146,3 +1146,52 @@ def test_policy_unsupported_paths_fail_loudly(ctx):
     with pytest.raises(rk.RkError) as e:
         ctx.rk_eval_range32_async(0, 40320, None, rec, k32, 0, ovf)
     assert e.value.status == rk.RK_EUNSUPPORTED
+
+
+def test_memo_hash_tables_race_audit(monkeypatch):
+    """Race evidence for the lock-free memo hash tables (CAS claim, release
+    publish, acquire probe; compute-sanitizer is not available on this pool):
+    after every one of many rebuilds — C4 (the bench set) and random sets over
+    the GPU shapes with memoisation forced — the device audit (rk_memo_audit)
+    finds no BUSY slot, no lost publish, no duplicate state, no bad transition,
+    per-level counts equal to the plan's, and the step's record and keys are
+    bit-identical to the first build's (itself equal to the oracle: the C4
+    golden test and test_memo_keys_equal_direct_keys)."""
+    ctx = _direct_ctx(monkeypatch, "RK_FORCE_MEMO")
+    try:
+        cases = [W.config("C4"), W.config("C3"), W.config("C2")]
+        for gi, gpu in enumerate(GPUS):
+            for ks in W.random_small_sets(0xA0D1 + gi, 2, 8, 9, gpu=gpu):
+                if all(W.feasible(gpu, k) for k in ks):
+                    cases.append((gpu, ks))
+        audited = 0
+        for ci, (gpu, ks) in enumerate(cases):
+            try:
+                ctx.rk_set_gpu_params(gpu)
+                ctx.rk_set_kernels(ks)
+            except rk.RkError as e:
+                assert e.status == rk.RK_EUNSUPPORTED
+                continue
+            if not ctx.rk_memo_info()[0]:
+                continue
+            N = math.factorial(len(ks))
+            reps = 12 if ci == 0 else 4
+            keys = torch.empty(N, dtype=torch.int64, device="cuda")
+            cand = torch.zeros(1, dtype=torch.int64, device="cuda")
+            rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+            first = None
+            for r in range(reps):
+                ctx.rk_sweep_pass1_async(0, N, cand, rec, keys)
+                ctx.rk_sweep_pass2_async(0, N, cand, None, 0, None, keys, rec)
+                bad = ctx.rk_memo_audit()
+                assert bad[:7] == [0] * 7, (ci, r, bad)
+                assert bad[7] == sum(ctx.rk_memo_info()[2][1:])
+                h = (rec.cpu().clone(), torch.sum(keys * 7919 + 1).item(), keys[::9973].cpu())
+                if first is None:
+                    first = h
+                else:
+                    assert torch.equal(h[0], first[0]) and h[1] == first[1] and torch.equal(h[2], first[2])
+            audited += 1
+        assert audited >= 6
+    finally:
+        ctx.close()
