@@ -91,11 +91,14 @@ struct rk_ctx {
     bool force_runs = false; /* RK_FORCE_RUNS=1: run-length SM state for every S (testing) */
     bool no_memo = false;    /* RK_NO_MEMO=1: direct evaluation of every order (testing) */
     bool force_memo = false; /* RK_FORCE_MEMO=1: memoise even where it does not pay (testing) */
-    /* pass 2's counts/histogram: from the distinct rows (dedup, default) or every run; RK_OVERLAP=1 runs them
-     * beside the key stream on a side stream (measured: step -5 % on C4 with every run binned, but the key
-     * stream itself slows from 0.59 to 0.79 ms).  RK_ROW_DEDUP / RK_OVERLAP = 0|1 force either (-1 = default) */
+    /* pass 2's counts/histogram: from the distinct rows (dedup, default) or every run.  With keys, the row
+     * multiset (insert) and the counts/histogram (rows) run beside the key stream on a high-priority side
+     * stream (default with dedup; RK_OVERLAP=0 serialises them; with every run binned, RK_OVERLAP=1 overlaps
+     * too, measured slower: the key stream slows from 0.59 to 0.79 ms).  RK_ROW_DEDUP / RK_OVERLAP = 0|1
+     * force either (-1 = default) */
     int row_dedup = -1, overlap = -1;
-    bool dedup_now = false;  /* the current range's pass 1 built the row multiset */
+    bool dedup_now = false;  /* the current range's counts/histogram come from the row multiset */
+    bool insert_pending = false; /* pass 1 left the multiset to pass 2 (built beside the key stream) */
     uint32_t rows_ctas = 2;  /* RK_ROWS_CTAS: its CTAs per SM when overlapped */
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -730,10 +733,11 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e) e = d.rslot.reserve(slots * 16);
     if (!e) e = d.rmult.reserve(slots * 4 * 8); /* 8 counters per slot */
     if (!e) e = d.rlist.reserve(nrun * 4);
-    (void)keys_hint;
     c->dedup_now = c->row_dedup != 0;
-    if (!e && c->dedup_now) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, (cudaStream_t)stream);
-    if (!e && c->dedup_now) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, (cudaStream_t)stream);
+    /* with keys the multiset is built in pass 2, beside the key stream */
+    c->insert_pending = c->dedup_now && keys_hint && c->overlap != 0;
+    if (!e && c->dedup_now && !c->insert_pending) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, (cudaStream_t)stream);
+    if (!e && c->dedup_now && !c->insert_pending) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, (cudaStream_t)stream);
     if (!e && re > rb && re - rb <= (1ull << 27)) {
         /* level j covers prefixes [a_j, b_j): span_j level-P prefixes under each */
         std::vector<uint64_t> a(P + 1), b(P + 1);
@@ -765,7 +769,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
         e = rk_dp_meta(c->tab_dev, d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p, rec_dev,
                        c->recs_dev, c->counter_dev, c->max_ctas, ex.empty() ? nullptr : &ex.back(), stream,
                        &c->launches);
-    if (!e && c->dedup_now)
+    if (!e && c->dedup_now && !c->insert_pending)
         e = rk_dp_insert(d.view, first, count, (const uint32_t*)d.meta_u.p, (const uint64_t*)d.meta_K.p,
                          dp_rows(c, re - rb), stream, &c->launches);
     tmark_end(c, m1, stream);
@@ -778,12 +782,12 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
 }
 
 /* Pass 2 over the range of the preceding pass 1: the key stream from its run
- * metadata (keys_dev), which also fills the range's row multiset, then the
- * counts (into rec_dev) and the histogram (hist_dev, bins <=
- * rk_dp_max_fused_bins()) from the distinct rows; without keys (or with the
- * multiset off) from every run.  RK_OVERLAP=1 (every run binned) runs the
- * counts/histogram beside the key stream on the ctx's high-priority side
- * stream, joined back before returning. */
+ * metadata (keys_dev), the counts (into rec_dev) and the histogram (hist_dev,
+ * bins <= rk_dp_max_fused_bins()) from the distinct rows (or every run with
+ * the multiset off).  With keys, the multiset (insert, left pending by pass
+ * 1) and the counts/histogram run on the ctx's high-priority side stream
+ * beside the HBM-bound key stream (both latency-bound on atomics), joined back
+ * before returning; RK_OVERLAP=1 also overlaps the every-run binning. */
 int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, const rk_stats* range_dev,
              uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev, rk_stats* rec_dev, void* stream) {
     DpPlan& d = c->dp;
@@ -794,7 +798,9 @@ int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev
     const uint64_t nrun = count ? (first + count + DF - 1) / DF - first / DF : 0;
     cudaStream_t st = (cudaStream_t)stream;
     const bool keys = keys_dev && count;
-    const bool ov = c->overlap == 1 && keys && !c->dedup_now;
+    const bool pend = c->insert_pending;
+    c->insert_pending = false;
+    const bool ov = keys && (pend || (c->overlap == 1 && !c->dedup_now));
     int e = 0;
     if (ov && !c->side) {
         int lo = 0, hi = 0;
@@ -806,8 +812,15 @@ int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev
     }
     auto rows = [&](void* s, uint32_t cap) {
         const int m = tmark_begin(c, RK_PHASE_HIST, s);
-        const int r = rk_dp_rows(c->tab_dev, d.view, first, count, cand_dev, range_dev, bins, hist_dev,
-                                 dp_rows(c, nrun), mu, mk, rec_dev, cap, s, &c->launches);
+        int r = 0;
+        if (pend) { /* the multiset of this range: zero, then insert every whole run */
+            r = cudaMemsetAsync(d.rslot.p, 0, (d.rmask + 1ull) * 16, (cudaStream_t)s);
+            if (!r) r = cudaMemsetAsync(d.rmult.p, 0, (d.rmask + 1ull) * 32, (cudaStream_t)s);
+            if (!r) r = rk_dp_insert(d.view, first, count, mu, mk, dp_rows(c, nrun), s, &c->launches);
+        }
+        if (!r)
+            r = rk_dp_rows(c->tab_dev, d.view, first, count, cand_dev, range_dev, bins, hist_dev, dp_rows(c, nrun),
+                           mu, mk, rec_dev, cap, s, &c->launches);
         tmark_end(c, m, s);
         return r;
     };

@@ -1138,11 +1138,12 @@ __global__ void rk_simulate_kernel(const RkTables* __restrict__ tab, const int32
  * prefix sharing or memoisation: one order per thread, the whole round loop,
  * on the register state (S' <= 32 super-SMs; the symmetry reduction holds:
  * every placement count stays a multiple of g). */
-constexpr int kPolSmax = 32;
+/* SM-state width: the smallest of {2, 8, 32} >= S' (runtime S inside) */
 
 /* Blocks of kernel k the policy can place from cursor cur before one fails:
  * first fit (L4) takes up to F = sum c_s; strict round robin sends block b to
  * SM (cur + b) mod S, which fails first at b = min_s ((s - cur) mod S + c_s S). */
+template <int kPolSmax>
 __device__ __forceinline__ uint32_t pol_avail(const St<kPolSmax>& s, const RkKTab& k, const RkGTab& g, bool strict,
                                               uint32_t cur, uint32_t (&c)[kPolSmax]) {
     const CapK ck = capk(k);
@@ -1163,6 +1164,7 @@ __device__ __forceinline__ uint32_t pol_avail(const St<kPolSmax>& s, const RkKTa
  * the new cursor.  First fit is the water-fill of place_core (the SM of the
  * p-th block + 1); strict round robin gives SM s the blocks b < p with
  * b = (s - cur) mod S (mod S), and the cursor moves by p. */
+template <int kPolSmax>
 __device__ __forceinline__ uint32_t pol_place(St<kPolSmax>& s, uint32_t p, const uint32_t (&c)[kPolSmax],
                                               const RkKTab& k, const RkGTab& g, bool strict, uint32_t cur) {
     const uint32_t S = g.S;
@@ -1187,6 +1189,7 @@ __device__ __forceinline__ uint32_t pol_place(St<kPolSmax>& s, uint32_t p, const
     return water_fill<kPolSmax, false>(p, c, bfa, bfb, cur, k, g, u);
 }
 
+template <int kPolSmax>
 __device__ __forceinline__ void pol_fresh(St<kPolSmax>& s, const RkGTab& g) {
 #pragma unroll
     for (int i = 0; i < kPolSmax; i++) {
@@ -1209,7 +1212,7 @@ __device__ __forceinline__ uint64_t pol_alone(uint32_t rem, const RkKTab& k, uin
 }
 
 /* Exact key of one launch order (ord[0..n-1]) under the policy flags. */
-template <class R>
+template <int kPolSmax, class R>
 __device__ uint64_t pol_key(const RkTables& t, const uint8_t (&ord)[RK_MAX_N], R& rec) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
@@ -1296,6 +1299,7 @@ __device__ __forceinline__ void pol_unrank(const RkGTab& g, uint64_t idx, uint8_
 }
 
 /* stats (+ optional keys) of [first, first+count): grid-stride over indices */
+template <int kPolSmax>
 __global__ void __launch_bounds__(kThreads) rk_policy_eval_kernel(const RkTables* __restrict__ tab, uint64_t first,
                                                                    uint64_t count, const uint64_t* cand_dev,
                                                                    uint64_t cand_imm, rk_stats* out, uint64_t* keys,
@@ -1311,7 +1315,7 @@ __global__ void __launch_bounds__(kThreads) rk_policy_eval_kernel(const RkTables
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += nth) {
         const uint64_t idx = first + i;
         pol_unrank(t.g, idx, ord);
-        const uint64_t key = pol_key(t, ord, nr);
+        const uint64_t key = pol_key<kPolSmax>(t, ord, nr);
         if (keys) keys[i] = key;
         if (key < ts.kmin) { ts.kmin = key; ts.amin = idx; } /* increasing indices: strict keeps the smallest (L12) */
         if (key > ts.kmax || ts.cnt == 0) { ts.kmax = key; ts.amax = idx; }
@@ -1324,6 +1328,7 @@ __global__ void __launch_bounds__(kThreads) rk_policy_eval_kernel(const RkTables
 }
 
 /* C5 batch under a policy: blockIdx.y = set, blockIdx.x = chunk of its indices */
+template <int kPolSmax>
 __global__ void __launch_bounds__(kThreads) rk_policy_batch_kernel(const RkTables* __restrict__ tabs,
                                                                     const uint64_t* __restrict__ cand_keys,
                                                                     rk_stats* recs) {
@@ -1339,7 +1344,7 @@ __global__ void __launch_bounds__(kThreads) rk_policy_batch_kernel(const RkTable
     uint8_t ord[RK_MAX_N];
     for (uint64_t idx = lo + threadIdx.x; idx < hi; idx += blockDim.x) {
         pol_unrank(t.g, idx, ord);
-        const uint64_t key = pol_key(t, ord, nr);
+        const uint64_t key = pol_key<kPolSmax>(t, ord, nr);
         if (key < ts.kmin) { ts.kmin = key; ts.amin = idx; }
         if (key > ts.kmax || ts.cnt == 0) { ts.kmax = key; ts.amax = idx; }
         ts.nlt += key < cand ? 1u : 0u;
@@ -1351,6 +1356,7 @@ __global__ void __launch_bounds__(kThreads) rk_policy_batch_kernel(const RkTable
 }
 
 /* keys of explicit indices; per_set: item i uses tabs[i], else tabs[0] */
+template <int kPolSmax>
 __global__ void rk_policy_keys_of_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ idx,
                                          uint32_t m, int per_set, uint64_t* __restrict__ out) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1359,19 +1365,21 @@ __global__ void rk_policy_keys_of_kernel(const RkTables* __restrict__ tabs, cons
     NoRec nr;
     uint8_t ord[RK_MAX_N];
     pol_unrank(t.g, idx[i], ord);
-    out[i] = pol_key(t, ord, nr);
+    out[i] = pol_key<kPolSmax>(t, ord, nr);
 }
 
+template <int kPolSmax>
 __global__ void rk_policy_key_of_index_kernel(const RkTables* __restrict__ tab, uint64_t index,
                                               uint64_t* __restrict__ out) {
     if (threadIdx.x) return;
     NoRec nr;
     uint8_t ord[RK_MAX_N];
     pol_unrank(tab->g, index, ord);
-    *out = pol_key(*tab, ord, nr);
+    *out = pol_key<kPolSmax>(*tab, ord, nr);
 }
 
 /* one order -> round partition (1 thread) */
+template <int kPolSmax>
 __global__ void rk_policy_simulate_kernel(const RkTables* __restrict__ tab, const int32_t* __restrict__ order,
                                           uint32_t* rounds, uint32_t max_rounds, uint32_t* n_rounds, uint64_t* key) {
     const RkTables& t = *tab;
@@ -1380,7 +1388,7 @@ __global__ void rk_policy_simulate_kernel(const RkTables* __restrict__ tab, cons
     Rec rec{rounds, max_rounds, n, 0, t.g.blkscale};
     uint8_t ord[RK_MAX_N];
     for (uint32_t j = 0; j < n; j++) ord[j] = (uint8_t)order[j];
-    *key = pol_key(t, ord, rec);
+    *key = pol_key<kPolSmax>(t, ord, rec);
     *n_rounds = rec.r;
 }
 
@@ -2667,16 +2675,20 @@ int eval_ctas_per_sm() {
     return v;
 }
 
-int policy_ctas_per_sm() {
+template <int W>
+int policy_ctas_per_sm_w() {
     static int cache[kMaxDev];
     const int dev = cur_device();
     int v = __atomic_load_n(&cache[dev], __ATOMIC_RELAXED);
     if (!v) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, rk_policy_eval_kernel, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, rk_policy_eval_kernel<W>, kThreads, 0);
         if (v <= 0) v = 1;
         __atomic_store_n(&cache[dev], v, __ATOMIC_RELAXED);
     }
     return v;
+}
+int policy_ctas_per_sm(uint32_t S) {
+    return S <= 2 ? policy_ctas_per_sm_w<2>() : (S <= 8 ? policy_ctas_per_sm_w<8>() : policy_ctas_per_sm_w<32>());
 }
 
 /* variant index for a (reduced) SM count S: the smallest power of two >= S,
@@ -2722,6 +2734,14 @@ int variant(uint32_t S) {
         else KERNEL<0, false><<<CFG>>>(__VA_ARGS__);                          \
     } while (0)
 #define RK_CFG(...) __VA_ARGS__
+/* model-reading policy kernels: state width 2, 8 or 32 (S' <= 32) */
+#define RK_DISPATCH_POLICY(S, KERNEL, CFG, ...)                               \
+    do {                                                                      \
+        const uint32_t s_ = (S) & ~RK_S_POLICY;                               \
+        if (s_ <= 2) KERNEL<2><<<CFG>>>(__VA_ARGS__);                         \
+        else if (s_ <= 8) KERNEL<8><<<CFG>>>(__VA_ARGS__);                    \
+        else KERNEL<32><<<CFG>>>(__VA_ARGS__);                                \
+    } while (0)
 
 int rk_eval_max_ctas(uint32_t S, int) {
     int per;
@@ -2750,12 +2770,12 @@ int rk_launch_eval(const RkTables* tab_dev, uint32_t n, uint32_t S, uint64_t fir
     if (S & RK_S_POLICY) { /* model-reading policy: one order per thread (no fused extras) */
         if (keys32_dev || hist_dev) return (int)cudaErrorNotSupported;
         uint64_t ctas = (count + kThreads - 1) / kThreads;
-        const uint64_t cap = (uint64_t)policy_ctas_per_sm() * num_sms();
+        const uint64_t cap = (uint64_t)policy_ctas_per_sm(S & ~RK_S_POLICY) * num_sms();
         if (ctas > cap) ctas = cap;
         if (ctas > max_ctas) ctas = max_ctas;
         if (ctas < 1) ctas = 1;
-        rk_policy_eval_kernel<<<(unsigned)ctas, kThreads, 0, st>>>(tab_dev, first, count, cand_key_dev, cand_key_imm,
-                                                                   stats_dev, keys_dev, recs, counter);
+        RK_DISPATCH_POLICY(S, rk_policy_eval_kernel, RK_CFG((unsigned)ctas, kThreads, 0, st), tab_dev, first, count,
+                           cand_key_dev, cand_key_imm, stats_dev, keys_dev, recs, counter);
         if (launches) (*launches)++;
         return (int)cudaGetLastError();
     }
@@ -2870,7 +2890,8 @@ int rk_launch_keys_of(const RkTables* tabs_dev, uint32_t n, uint32_t S, const ui
     (void)n;
     const unsigned blocks = (m + 127) / 128;
     if (S & RK_S_POLICY)
-        rk_policy_keys_of_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(tabs_dev, idx_dev, m, 1, out_dev);
+        RK_DISPATCH_POLICY(S, rk_policy_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tabs_dev, idx_dev,
+                           m, 1, out_dev);
     else
         RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tabs_dev, idx_dev, m, 1,
                             out_dev);
@@ -2882,7 +2903,8 @@ int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* 
                            uint64_t* out_dev, void* stream, uint32_t* launches) {
     const unsigned blocks = (m + 127) / 128;
     if (S & RK_S_POLICY)
-        rk_policy_keys_of_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(tab_dev, idx_dev, m, 0, out_dev);
+        RK_DISPATCH_POLICY(S, rk_policy_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tab_dev, idx_dev,
+                           m, 0, out_dev);
     else
         RK_DISPATCH_GENERIC(S, rk_keys_of_kernel, RK_CFG(blocks, 128, 0, (cudaStream_t)stream), tab_dev, idx_dev, m, 0,
                             out_dev);
@@ -2893,7 +2915,8 @@ int rk_launch_keys_of_same(const RkTables* tab_dev, uint32_t S, const uint64_t* 
 int rk_launch_key_of_index(const RkTables* tab_dev, uint32_t S, uint64_t index, uint64_t* out_dev, void* stream,
                            uint32_t* launches) {
     if (S & RK_S_POLICY)
-        rk_policy_key_of_index_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(tab_dev, index, out_dev);
+        RK_DISPATCH_POLICY(S, rk_policy_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, index,
+                           out_dev);
     else
         RK_DISPATCH(S, rk_key_of_index_kernel, RK_CFG(1, 32, 0, (cudaStream_t)stream), tab_dev, index, out_dev);
     if (launches) (*launches)++;
@@ -2905,8 +2928,8 @@ int rk_launch_simulate(const RkTables* tab_dev, uint32_t n, uint32_t S, const in
                        uint32_t* launches) {
     (void)n;
     if (S & RK_S_POLICY)
-        rk_policy_simulate_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(tab_dev, order_dev, rounds_dev, max_rounds,
-                                                                    n_rounds_dev, key_dev);
+        RK_DISPATCH_POLICY(S, rk_policy_simulate_kernel, RK_CFG(1, 1, 0, (cudaStream_t)stream), tab_dev, order_dev,
+                           rounds_dev, max_rounds, n_rounds_dev, key_dev);
     else
         RK_DISPATCH_GENERIC(S, rk_simulate_kernel, RK_CFG(1, 1, 0, (cudaStream_t)stream), tab_dev, order_dev,
                             rounds_dev, max_rounds, n_rounds_dev, key_dev);
@@ -2944,7 +2967,7 @@ int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n
     const bool uniform = (S & 0x80000000u) != 0;
     const uint32_t Sm = S & 0x7FFFFFFFu;
     if (Sm & RK_S_POLICY) {
-        rk_policy_batch_kernel<<<grid, kThreads, 0, st>>>(tabs_dev, cand_keys_dev, recs);
+        RK_DISPATCH_POLICY(Sm, rk_policy_batch_kernel, RK_CFG(grid, kThreads, 0, st), tabs_dev, cand_keys_dev, recs);
     } else if (uniform) {
         RK_DISPATCH(Sm, rk_batch_kernel, RK_CFG(grid, kThreads, 0, st), tabs_dev, cand_keys_dev, recs);
     } else {
