@@ -415,8 +415,9 @@ def main():
                                   "every memo table (~110 MB incl. the 64-MB run table) is rebuilt inside each step "
                                   "and the 3.83 GB key array (> 126 MB L2) is written once per step")},
                 "gpu_launches": launches, "clocks": clocks, "roofline": roofline,
-                "kernels_ms": ({"pass1": eval_ms_max, "pass1_memo_tables": phase_ms["tables"],
-                                "pass1_runs_extremes_rows": phase_ms["extremes"],
+                "kernels_ms": ({"pass1": eval_ms_max, "pass1_levels_and_suffix_rows": phase_ms["tables"],
+                                "pass1_run_pass_and_multiset_side_stream": phase_ms["runs"],
+                                "pass1_extremes": phase_ms["extremes"],
                                 "pass2": hist_ms_max, "pass2_counts_histogram": phase_ms["hist"],
                                 "pass2_key_stream": phase_ms["stream"], "step": ms_max / args.steps}
                                if memo_on else

@@ -288,18 +288,20 @@ rk_status rk_sweep_pass2_async(rk_ctx* ctx, uint64_t first, uint64_t count, cons
 
 /* Per-phase device timing of the step (measurement support):
  * while on, every phase the library enqueues records a CUDA event pair on its
- * launching stream — RK_PHASE_TABLES (pass 1 memoised: memo tables rebuilt),
- * RK_PHASE_EXTREMES (pass 1 memoised: run metadata, row multiset and the
- * range's extremes),
- * RK_PHASE_STREAM (pass 2's key stream), RK_PHASE_HIST (pass 2's counts and
- * histogram from the row multiset), RK_PHASE_DIRECT (the direct evaluation kernel of pass 1).
+ * launching stream — RK_PHASE_TABLES (pass 1 memoised: levels + suffix rows
+ * rebuilt, main stream), RK_PHASE_RUNS (pass 1 memoised: each run's node and
+ * closed key + the row multiset, on the ctx's side stream beside the suffix
+ * rows), RK_PHASE_EXTREMES (pass 1 memoised: the key stream's run metadata and
+ * the range's extremes), RK_PHASE_STREAM (pass 2's key stream), RK_PHASE_HIST
+ * (pass 2's counts and histogram from the row multiset), RK_PHASE_DIRECT (the
+ * direct evaluation kernel of pass 1).
  * rk_timing_read synchronises on the recorded events and returns per phase the
  * summed milliseconds (ms_sum[p]) and the number of marks (counts[p]) since
  * the last read or rk_set_timing, for p < n_phases; then clears the marks.
  * Event objects are owned by the ctx (grow-only).  Errors: RK_EINVAL,
  * RK_ENODEVICE, RK_ECUDA. */
 enum { RK_PHASE_TABLES = 0, RK_PHASE_STREAM = 1, RK_PHASE_HIST = 2, RK_PHASE_DIRECT = 3, RK_PHASE_EXTREMES = 4,
-       RK_N_PHASES = 5 };
+       RK_PHASE_RUNS = 5, RK_N_PHASES = 6 };
 rk_status rk_set_timing(rk_ctx* ctx, int on);
 rk_status rk_timing_read(rk_ctx* ctx, double* ms_sum, uint32_t* counts, uint32_t n_phases);
 

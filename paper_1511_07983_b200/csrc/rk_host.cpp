@@ -91,14 +91,12 @@ struct rk_ctx {
     bool force_runs = false; /* RK_FORCE_RUNS=1: run-length SM state for every S (testing) */
     bool no_memo = false;    /* RK_NO_MEMO=1: direct evaluation of every order (testing) */
     bool force_memo = false; /* RK_FORCE_MEMO=1: memoise even where it does not pay (testing) */
-    /* pass 2's counts/histogram: from the distinct rows (dedup, default) or every run.  With keys, the row
-     * multiset (insert) and the counts/histogram (rows) run beside the key stream on a high-priority side
-     * stream (default with dedup; RK_OVERLAP=0 serialises them; with every run binned, RK_OVERLAP=1 overlaps
-     * too, measured slower: the key stream slows from 0.59 to 0.79 ms).  RK_ROW_DEDUP / RK_OVERLAP = 0|1
-     * force either (-1 = default) */
+    /* pass 2's counts/histogram: from the distinct rows (dedup, default) or every run.  Pass 1's run pass
+     * (run metadata + the row multiset) runs beside the suffix-row build, pass 2's counts/histogram beside
+     * the key stream, both on a high-priority side stream (RK_OVERLAP=0: all serial).  RK_ROW_DEDUP /
+     * RK_OVERLAP = 0|1 force either (-1 = default) */
     int row_dedup = -1, overlap = -1;
     bool dedup_now = false;  /* the current range's counts/histogram come from the row multiset */
-    bool insert_pending = false; /* pass 1 left the multiset to pass 2 (built beside the key stream) */
     uint32_t rows_ctas = 2;  /* RK_ROWS_CTAS: its CTAs per SM when overlapped */
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -537,19 +535,35 @@ int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vect
     return e;
 }
 
-/* Enqueue the table build of the current plan: clear, P levels (+ the given
- * prefix expansions, level j-1 -> j in level j's launch, the last one after),
- * suffix tables. */
-int dp_build(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr) {
+/* Enqueue the level build of the current plan: clear, P levels (+ the given
+ * prefix expansions, level j-1 -> j in level j's launch; the last one runs in
+ * the run pass). */
+int dp_build_levels(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr) {
     DpPlan& d = c->dp;
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
     if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.P + 3) * 4, st); /* + the row list counter at P+2 */
-    if (!e) e = dp_levels(c, 0, d.P, stream, ex); /* the last expansion level runs with the extremes */
-    if (!e)
-        e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
-                         (uint8_t*)d.code.p, d.dvc.p, d.dvp.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
-                         (uint32_t*)d.offs.p, d.cnt[d.P], stream, &c->launches);
+    if (!e) e = dp_levels(c, 0, d.P, stream, ex);
+    return e;
+}
+
+/* Enqueue the suffix rows of the level-P nodes (after the levels). */
+int dp_build_suffix(rk_ctx* c, void* stream) {
+    DpPlan& d = c->dp;
+    return rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
+                        (uint8_t*)d.code.p, d.dvc.p, d.dvp.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
+                        (uint32_t*)d.offs.p, d.cnt[d.P], stream, &c->launches);
+}
+
+/* the ctx's high-priority side stream and its fork/join events */
+int ensure_side(rk_ctx* c) {
+    if (c->side) return 0;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* pr = getenv("RK_SIDE_PRIO"); /* testing: 0 = the default priority */
+    int e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, (pr && pr[0] == '0') ? lo : hi);
+    if (!e) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (!e) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
     return e;
 }
 
@@ -711,12 +725,13 @@ RkRows dp_rows(rk_ctx* c, uint64_t nrun) {
                   (uint32_t*)d.counters.p + d.P + 2, nrun};
 }
 
-/* Pass 1 of the memoised step: the tables (levels + suffix rows) rebuilt from
- * scratch with the range's prefixes expanded breadth-first (levels 1..P-1 when
- * the range has <= 2^27 runs; level P recomputed by the run pass), then the run
- * pass: the run metadata pass 2 streams from, the row multiset (when pass 2
- * will not write keys: keys_hint false), and the range's extremes record
- * (n_lt = n_eq = 0, n_gt = evaluated = count). */
+/* Pass 1 of the memoised step: the levels rebuilt from scratch with the
+ * range's prefixes expanded breadth-first (levels 1..P-1 when the range has
+ * <= 2^27 runs; level P recomputed by the run pass), then — concurrently — the
+ * suffix rows (main stream) and the run pass (side stream: each run's (node,
+ * K_closed) and the row multiset), then the extremes pass (the key stream's
+ * metadata and the range's extremes record: n_lt = n_eq = 0, n_gt = evaluated
+ * = count).  RK_OVERLAP=0 runs the run pass on the main stream. */
 int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool keys_hint, void* stream) {
     DpPlan& d = c->dp;
     d.runs_ok = false;
@@ -725,6 +740,8 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     const uint64_t rb = first / DF, re = count ? (first + count + DF - 1) / DF : rb;
     std::vector<RkExpand> ex;
     const uint64_t nrun = std::max<uint64_t>(re - rb, 1);
+    (void)keys_hint;
+    cudaStream_t st = (cudaStream_t)stream;
     int e = d.meta_u.reserve(nrun * 4);
     if (!e) e = d.meta_K.reserve(nrun * 8);
     /* row multiset: ~8 runs per slot (C4: 217,659 distinct rows of 3,991,680 runs in 2^19 slots) */
@@ -734,10 +751,8 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e) e = d.rmult.reserve(slots * 4 * 8); /* 8 counters per slot */
     if (!e) e = d.rlist.reserve(nrun * 4);
     c->dedup_now = c->row_dedup != 0;
-    /* with keys the multiset is built in pass 2, beside the key stream */
-    c->insert_pending = c->dedup_now && keys_hint && c->overlap != 0;
-    if (!e && c->dedup_now && !c->insert_pending) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, (cudaStream_t)stream);
-    if (!e && c->dedup_now && !c->insert_pending) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, (cudaStream_t)stream);
+    const bool side = c->overlap != 0;
+    if (!e && side) e = ensure_side(c);
     if (!e && re > rb && re - rb <= (1ull << 27)) {
         /* level j covers prefixes [a_j, b_j): span_j level-P prefixes under each */
         std::vector<uint64_t> a(P + 1), b(P + 1);
@@ -762,16 +777,25 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
         }
     }
     const int m0 = tmark_begin(c, RK_PHASE_TABLES, stream);
-    if (!e) e = dp_build(c, stream, ex.empty() ? nullptr : &ex);
+    if (!e && c->dedup_now) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, st);
+    if (!e && c->dedup_now) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, st);
+    if (!e) e = dp_build_levels(c, stream, ex.empty() ? nullptr : &ex);
+    void* rs = side ? (void*)c->side : stream;
+    if (!e && side) e = cudaEventRecord(c->ev_fork, st);
+    if (!e && side) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    const int mr = tmark_begin(c, RK_PHASE_RUNS, rs);
+    if (!e)
+        e = rk_dp_runs(c->tab_dev, d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p,
+                       dp_rows(c, re - rb), ex.empty() ? nullptr : &ex.back(), rs, &c->launches);
+    tmark_end(c, mr, rs);
+    if (!e && side) e = cudaEventRecord(c->ev_join, c->side);
+    if (!e) e = dp_build_suffix(c, stream);
     tmark_end(c, m0, stream);
+    if (!e && side) e = cudaStreamWaitEvent(st, c->ev_join, 0);
     const int m1 = tmark_begin(c, RK_PHASE_EXTREMES, stream);
     if (!e)
-        e = rk_dp_meta(c->tab_dev, d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p, rec_dev,
-                       c->recs_dev, c->counter_dev, c->max_ctas, ex.empty() ? nullptr : &ex.back(), stream,
-                       &c->launches);
-    if (!e && c->dedup_now && !c->insert_pending)
-        e = rk_dp_insert(d.view, first, count, (const uint32_t*)d.meta_u.p, (const uint64_t*)d.meta_K.p,
-                         dp_rows(c, re - rb), stream, &c->launches);
+        e = rk_dp_meta(d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p, rec_dev, c->recs_dev,
+                       c->counter_dev, c->max_ctas, stream, &c->launches);
     tmark_end(c, m1, stream);
     if (!e) {
         d.runs_ok = true;
@@ -782,12 +806,10 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
 }
 
 /* Pass 2 over the range of the preceding pass 1: the key stream from its run
- * metadata (keys_dev), the counts (into rec_dev) and the histogram (hist_dev,
- * bins <= rk_dp_max_fused_bins()) from the distinct rows (or every run with
- * the multiset off).  With keys, the multiset (insert, left pending by pass
- * 1) and the counts/histogram run on the ctx's high-priority side stream
- * beside the HBM-bound key stream (both latency-bound on atomics), joined back
- * before returning; RK_OVERLAP=1 also overlaps the every-run binning. */
+ * metadata (keys_dev), then the counts (into rec_dev) and the histogram
+ * (hist_dev, bins <= rk_dp_max_fused_bins()) from the distinct rows (or every
+ * run with the multiset off); with keys they run beside the key stream on the
+ * ctx's high-priority side stream (RK_OVERLAP=0: after it). */
 int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, const rk_stats* range_dev,
              uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev, rk_stats* rec_dev, void* stream) {
     DpPlan& d = c->dp;
@@ -798,33 +820,16 @@ int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev
     const uint64_t nrun = count ? (first + count + DF - 1) / DF - first / DF : 0;
     cudaStream_t st = (cudaStream_t)stream;
     const bool keys = keys_dev && count;
-    const bool pend = c->insert_pending;
-    c->insert_pending = false;
-    const bool ov = keys && (pend || (c->overlap == 1 && !c->dedup_now));
-    int e = 0;
-    if (ov && !c->side) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
-        if (!e) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
-        if (!e) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-        if (e) return e;
-    }
+    const bool ov = keys && c->overlap != 0;
+    int e = ov ? ensure_side(c) : 0;
     auto rows = [&](void* s, uint32_t cap) {
         const int m = tmark_begin(c, RK_PHASE_HIST, s);
-        int r = 0;
-        if (pend) { /* the multiset of this range: zero, then insert every whole run */
-            r = cudaMemsetAsync(d.rslot.p, 0, (d.rmask + 1ull) * 16, (cudaStream_t)s);
-            if (!r) r = cudaMemsetAsync(d.rmult.p, 0, (d.rmask + 1ull) * 32, (cudaStream_t)s);
-            if (!r) r = rk_dp_insert(d.view, first, count, mu, mk, dp_rows(c, nrun), s, &c->launches);
-        }
-        if (!r)
-            r = rk_dp_rows(c->tab_dev, d.view, first, count, cand_dev, range_dev, bins, hist_dev, dp_rows(c, nrun),
-                           mu, mk, rec_dev, cap, s, &c->launches);
+        const int r = rk_dp_rows(c->tab_dev, d.view, first, count, cand_dev, range_dev, bins, hist_dev,
+                                 dp_rows(c, nrun), mu, mk, rec_dev, cap, s, &c->launches);
         tmark_end(c, m, s);
         return r;
     };
-    if (ov) {
+    if (!e && ov) {
         e = cudaEventRecord(c->ev_fork, st);
         if (!e) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
         if (!e) e = rows(c->side, c->rows_ctas * c->sms);

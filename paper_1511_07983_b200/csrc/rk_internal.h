@@ -150,12 +150,17 @@ struct RkRows {
     uint32_t* nlist;
     uint64_t list_hint;
 };
-/* pass 1's run pass: run metadata (meta_u = node | wide << 31, meta_K = Kb) and
- * the range's extremes record (counts: n_gt = evaluated = count); last = the
- * range's level P-1 -> P expansion (nullptr: walk) */
-int rk_dp_meta(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u,
-               uint64_t* meta_K, rk_stats* out, rk_stats* recs, uint32_t* counter, uint32_t max_ctas,
-               const RkExpand* last, void* stream, uint32_t* launches);
+/* pass 1's run pass: per run of the range its (node, K_closed) into meta_u /
+ * meta_K, and the row multiset (rows.slot nullable); last = the range's level
+ * P-1 -> P expansion (nullptr: walk).  Needs the levels only (runs beside the
+ * suffix rows). */
+int rk_dp_runs(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u,
+               uint64_t* meta_K, const RkRows& rows, const RkExpand* last, void* stream, uint32_t* launches);
+/* pass 1's extremes pass (after the run pass and the suffix rows): meta_u |=
+ * wide << 31, meta_K = Kb, and the range's extremes record (counts: n_gt =
+ * evaluated = count) */
+int rk_dp_meta(const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u, uint64_t* meta_K, rk_stats* out,
+               rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches);
 /* pass 2's counts (into rec, nullable) and histogram (nullable) from the row multiset */
 int rk_dp_rows(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, const uint64_t* cand_dev,
                const rk_stats* range, uint32_t bins, uint64_t* hist, const RkRows& rows, const uint32_t* meta_u,
@@ -163,9 +168,6 @@ int rk_dp_rows(const RkTables* tab, const DPView& v, uint64_t first, uint64_t co
 /* pass 2's key stream from the run metadata (one-shot grid) */
 int rk_dp_keys(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
                uint64_t* keys, void* stream, uint32_t* launches);
-/* the range's row multiset from the run metadata (pass 1, after rk_dp_meta) */
-int rk_dp_insert(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
-                 const RkRows& rows, void* stream, uint32_t* launches);
 int rk_launch_bnb(const RkTables* tab_dev, uint32_t S, uint32_t P, uint64_t n_units, void* gb_dev,
                   unsigned long long* recs_dev, void* stream, uint32_t* launches);
 

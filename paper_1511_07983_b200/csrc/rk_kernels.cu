@@ -2248,16 +2248,16 @@ __device__ __forceinline__ uint64_t dp_key(const DPView& v, uint32_t u, bool wid
 }
 
 /* Row multiset of a range: the runs of [first, first+count) as
- * distinct rows (node, Kb) with multiplicities — C4's 3,991,680 runs are
+ * distinct rows (node, K_closed) with multiplicities — C4's 3,991,680 runs are
  * 217,659 distinct rows, so pass 2 counts and bins 18x fewer rows.  Open
- * addressing over 16-B slots {node | wide << 31, 1, Kb}: one 128-bit CAS
+ * addressing over 16-B slots {node, 1, K_closed}: one 128-bit CAS
  * (EMPTY = all zero -> the key) claims a slot or reports its occupant, so no
  * flag protocol (and no acquire fence, which costs an L1 invalidation per
  * load) is needed; the multiplicity is added to one of 8 counters per slot,
  * chosen by CTA index (C4's heaviest row has 11,056 runs).  A run that finds
  * no slot within kRowProbes probes, or a range-edge run, is appended to the
  * run list instead (pass 2 processes it on its own).  Slots and counters are
- * zeroed before pass 1. */
+ * zeroed before the run pass. */
 constexpr uint32_t kRowProbes = 32u;
 constexpr uint32_t kMultShards = 8; /* multiplicity counters per slot (summed by pass 2) */
 struct RowSet {
@@ -2293,48 +2293,54 @@ __device__ __forceinline__ bool row_insert(const RowSet& rs, uint32_t uw, uint64
     return false;
 }
 
-/* The range's row multiset from the run metadata: thread per run (grid-
- * stride); whole runs enter their row (node, Kb), range-edge runs and probe
- * overflows the run list. */
-__global__ void __launch_bounds__(kDpThreads) rk_dp_insert_kernel(DPView v, uint64_t first, uint64_t count,
-                                                                 const uint32_t* __restrict__ meta_u,
-                                                                 const uint64_t* __restrict__ meta_K, RowSet rs) {
-    constexpr uint32_t DF = kDF;
-    const uint64_t lo = first, hi = first + count;
-    const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
-    (void)v;
-    for (uint64_t run = rb + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; run < re;
-         run += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t idx0 = run * DF;
-        const bool whole = idx0 >= lo && idx0 + DF <= hi;
-        if (!whole || !row_insert(rs, __ldg(meta_u + (run - rb)), __ldg(meta_K + (run - rb))))
-            rs.list[atomicAdd(rs.nlist, 1u)] = (uint32_t)(run - rb);
-    }
-}
-
-/* Pass 1's run pass (lane per run, latency-bound; no key is written): per run
- * of [first, first+count) its (node, K_closed) — the range's last prefix-
- * expansion level, recomputed — and the metadata the key stream reads: meta_u
- * = node | wide << 31, meta_K = Kb = K_closed + the row minimum (keys = Kb +
- * the node's offsets); the range's extremes from the rows' extremes (min/argmin, max/argmax, smallest index on ties, reading
- * L12; range-edge runs key by key).  out = {extremes, n_lt = n_eq = 0, n_gt =
- * evaluated = count} (pass 2 adds the counts). */
-__global__ void __launch_bounds__(kDpThreads) rk_dp_meta_kernel(const RkTables* __restrict__ tab, DPView v,
+/* Pass 1's run pass (lane per run; runs beside the suffix-row build on a side
+ * stream — it needs only the levels): per run of [first, first+count) its
+ * (node, K_closed) from the range's last prefix-expansion level (recomputed,
+ * or by walking the P transitions) into meta_u / meta_K, and, with a row
+ * multiset, whole runs enter their row (node, K_closed); range-edge runs and
+ * probe overflows go to the run list. */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_runs_kernel(const RkTables* __restrict__ tab, DPView v,
                                                                uint64_t first, uint64_t count, uint32_t* meta_u,
-                                                               uint64_t* meta_K, rk_stats* out, rk_stats* recs,
-                                                               uint32_t* counter, ExpArgs xp) {
+                                                               uint64_t* meta_K, RowSet rs, ExpArgs xp) {
     __shared__ RkTables t;
     load_tables(t, tab);
     const RkGTab& g = t.g;
     constexpr uint32_t DF = kDF;
     const uint64_t lo = first, hi = first + count;
     const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
-    uint64_t kmin = ~0ull, kmax = 0, amin = ~0ull, amax = ~0ull, cnt = 0;
     for (uint64_t run = rb + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; run < re;
          run += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t u;
         uint64_t Kc;
         dp_src(g, v, xp, run, rb, u, Kc);
+        meta_u[run - rb] = u;
+        meta_K[run - rb] = Kc;
+        if (rs.slot) {
+            const uint64_t idx0 = run * DF;
+            const bool whole = idx0 >= lo && idx0 + DF <= hi;
+            if (!whole || !row_insert(rs, u, Kc)) rs.list[atomicAdd(rs.nlist, 1u)] = (uint32_t)(run - rb);
+        }
+    }
+}
+
+/* Pass 1's extremes pass (lane per run, after the run pass and the suffix
+ * rows): turns each run's (node, K_closed) into the metadata the key stream
+ * reads — meta_u = node | wide << 31, meta_K = Kb = K_closed + the row minimum
+ * (keys = Kb + the node's offsets) — and reduces the range's extremes from the
+ * rows' extremes (min/argmin, max/argmax, smallest index on ties, reading
+ * L12; range-edge runs key by key).  out = {extremes, n_lt = n_eq = 0, n_gt =
+ * evaluated = count} (pass 2 adds the counts). */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_meta_kernel(DPView v, uint64_t first, uint64_t count,
+                                                               uint32_t* meta_u, uint64_t* meta_K, rk_stats* out,
+                                                               rk_stats* recs, uint32_t* counter) {
+    constexpr uint32_t DF = kDF;
+    const uint64_t lo = first, hi = first + count;
+    const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
+    uint64_t kmin = ~0ull, kmax = 0, amin = ~0ull, amax = ~0ull, cnt = 0;
+    for (uint64_t run = rb + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; run < re;
+         run += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = meta_u[run - rb];
+        const uint64_t Kc = meta_K[run - rb];
         const uint64_t idx0 = run * DF;
         const uint32_t olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
         const uint32_t ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF;
@@ -2500,7 +2506,8 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
                     const uint4* ms = reinterpret_cast<const uint4*>(rs.mult + it * kMultShards);
                     const uint4 a0 = ms[0], a1 = ms[1];
                     m = a0.x + a0.y + a0.z + a0.w + a1.x + a1.y + a1.z + a1.w;
-                    do_row(key.x & 0x7FFFFFFFu, ((uint64_t)key.w << 32) | key.z, m, 0u, DF);
+                    const uint32_t u = key.x; /* the slot holds (node, K_closed): Kb = K_closed + the row min */
+                    do_row(u, (((uint64_t)key.w << 32) | key.z) + __ldg(v.fst + 4ull * u), m, 0u, DF);
                 }
             } else { /* a run: listed, or every run (direct) */
                 const uint32_t off = direct ? (uint32_t)it : rs.list[it - rs.mask - 1u];
@@ -3115,24 +3122,23 @@ RowSet row_set(const RkRows& r) {
 }
 }  // namespace
 
-int rk_dp_meta(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u,
-               uint64_t* meta_K, rk_stats* out, rk_stats* recs, uint32_t* counter, uint32_t max_ctas,
-               const RkExpand* last, void* stream, uint32_t* launches) {
+int rk_dp_runs(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u,
+               uint64_t* meta_K, const RkRows& rows, const RkExpand* last, void* stream, uint32_t* launches) {
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
-    unsigned grid = dp_grid_wave(runs, rk_dp_meta_kernel, 0);
-    if (grid > max_ctas) grid = max_ctas;
-    rk_dp_meta_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, meta_u, meta_K, out,
-                                                                     recs, counter, exp_args(last));
+    const unsigned grid = dp_grid_wave(runs, rk_dp_runs_kernel, 0);
+    rk_dp_runs_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, meta_u, meta_K,
+                                                                     row_set(rows), exp_args(last));
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
 
-int rk_dp_insert(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
-                 const RkRows& rows, void* stream, uint32_t* launches) {
+int rk_dp_meta(const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u, uint64_t* meta_K, rk_stats* out,
+               rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
-    const unsigned grid = dp_grid_wave(runs, rk_dp_insert_kernel, 0);
-    rk_dp_insert_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(v, first, count, meta_u, meta_K,
-                                                                       row_set(rows));
+    unsigned grid = dp_grid_wave(runs, rk_dp_meta_kernel, 0);
+    if (grid > max_ctas) grid = max_ctas;
+    rk_dp_meta_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(v, first, count, meta_u, meta_K, out, recs,
+                                                                     counter);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

@@ -37,7 +37,7 @@ class rk_gpu_params(ctypes.Structure):
 RK_FLAG_CURSOR_PER_KERNEL = 1
 RK_FLAG_STRICT_RR = 2
 RK_FLAG_SKIP_AHEAD = 4
-RK_PHASE_NAMES = ("tables", "stream", "hist", "direct", "extremes")  # RK_PHASE_* of rk.h
+RK_PHASE_NAMES = ("tables", "stream", "hist", "direct", "extremes", "runs")  # RK_PHASE_* of rk.h
 RK_N_PHASES = len(RK_PHASE_NAMES)
 
 
