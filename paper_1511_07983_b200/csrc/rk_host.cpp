@@ -51,7 +51,8 @@ struct Arena {
  * most cnt[j] * (n - j) nodes; the planning build measures cnt[j+1] exactly. */
 struct DpPlan {
     bool on = false;
-    uint32_t P = 0;
+    uint32_t P = 0;               /* run level: prefixes of P kernels, suffix rows of D = n - P kernels */
+    uint32_t L = 0;               /* levels built: P + 1 (level P+1 feeds the 24-key rows of the suffix build) */
     uint32_t node_bytes = 0;
     std::vector<uint32_t> cnt;    /* distinct nodes per level 0..P (cnt[0] = 1) */
     std::vector<uint32_t> cap;    /* node capacity of level j (j >= 1) */
@@ -63,6 +64,7 @@ struct DpPlan {
     size_t table_slots = 0;
     Arena nodes, tables, tid, dk, fst, counters; /* counters: P + 1 node counters, then the overflow flag */
     Arena code, dvc, dvp, nd, offs;              /* suffix rows: byte codes into sorted distinct (value, count) */
+    Arena row24;                                 /* the (D-1)! = 24 suffix keys of every level-(P+1) node */
     Arena expand;                                /* the range's prefix expansion, levels 1..P-1 (level P recomputed) */
     Arena meta_u, meta_K;                        /* the range's run metadata for the key stream: node | wide, Kb */
     Arena rslot, rmult, rlist;                   /* the range's row multiset (distinct (node, Kb) + multiplicity) */
@@ -504,7 +506,7 @@ void dp_free(DpPlan& d) {
     d.dk.release();
     d.fst.release();
     d.counters.release();
-    for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist}) a->release();
+    for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.row24, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist}) a->release();
     d.runs_ok = false;
     d.on = false;
 }
@@ -526,10 +528,10 @@ int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vect
     for (uint32_t j = j0; j < j1 && !e; j++) {
         const void* Uj = j ? nodes + d.noff[j] : nullptr;
         /* the launch of level j also expands the range's prefixes of level j-1 -> j */
-        const RkExpand* x = (ex && j >= 1 && j - 1 < ex->size()) ? &(*ex)[j - 1] : nullptr;
+        const RkExpand* x = (ex && j >= 1 && j < d.P && j - 1 < ex->size()) ? &(*ex)[j - 1] : nullptr;
         e = rk_dp_level(c->tab_dev, S, Uj, j ? ctr + j : nullptr, nodes + d.noff[j + 1], ctr + j + 1, d.cap[j + 1],
                         (uint32_t*)d.tables.p + d.toff[j + 1], d.tmask[j + 1], (uint32_t*)d.tid.p + d.xoff[j],
-                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.P + 1, d.work[j], stream, &c->launches,
+                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.L + 1, d.work[j], stream, &c->launches,
                         x);
     }
     return e;
@@ -542,17 +544,24 @@ int dp_build_levels(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = n
     DpPlan& d = c->dp;
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
-    if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.P + 3) * 4, st); /* + the row list counter at P+2 */
-    if (!e) e = dp_levels(c, 0, d.P, stream, ex);
+    if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.L + 3) * 4, st); /* + the overflow flag, the row list counter */
+    if (!e) e = dp_levels(c, 0, d.L, stream, ex);
     return e;
 }
 
-/* Enqueue the suffix rows of the level-P nodes (after the levels). */
+/* Enqueue the suffix rows of the level-P nodes (after the levels): the 24-key
+ * rows of the level-(P+1) nodes, then per level-P node its 120 keys gathered
+ * through the level-P transitions and encoded. */
 int dp_build_suffix(rk_ctx* c, void* stream) {
     DpPlan& d = c->dp;
-    return rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
-                        (uint8_t*)d.code.p, d.dvc.p, d.dvp.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p,
-                        (uint32_t*)d.offs.p, d.cnt[d.P], stream, &c->launches);
+    int e = rk_dp_row24(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.L], (uint32_t*)d.counters.p + d.L,
+                        (uint64_t*)d.row24.p, d.cnt[d.L], stream, &c->launches);
+    if (!e)
+        e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
+                         d.view.tid[d.P], d.view.dk[d.P], (const uint64_t*)d.row24.p, (uint8_t*)d.code.p, d.dvc.p,
+                         d.dvp.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p, (uint32_t*)d.offs.p, d.cnt[d.P], stream,
+                         &c->launches);
+    return e;
 }
 
 /* the ctx's high-priority side stream and its fork/join events */
@@ -579,7 +588,7 @@ bool dp_layout(rk_ctx* c, const std::vector<uint64_t>& m, const std::vector<uint
     DpPlan& d = c->dp;
     const uint32_t n = c->tab.g.n;
     size_t nb = 0, ts = 0, xs = 0, tb = 0;
-    for (uint32_t j = 0; j < d.P; j++) {
+    for (uint32_t j = 0; j < d.L; j++) {
         const uint64_t work = m[j] * n, capn = cap[j + 1];
         const uint64_t slots = pow2_at_least(2 * capn);
         if (work > kLimitEntries || capn * d.node_bytes > kLimitBytes || slots > kLimitEntries) return false;
@@ -620,30 +629,31 @@ rk_status dp_plan(rk_ctx* c) {
     if (c->device < 0 || c->no_memo || c->force_runs || policy(c) || n < RK_DP_D + 1)
         return RK_OK; /* S > 32: run-length nodes; policies: per-order kernels */
     d.P = n - RK_DP_D;
+    d.L = d.P + 1;
     d.node_bytes = rk_dp_node_bytes(S);
-    d.cnt.assign(d.P + 1, 0);
-    d.cap.assign(d.P + 1, 0);
-    d.noff.assign(d.P + 1, 0);
-    d.toff.assign(d.P + 1, 0);
-    d.tmask.assign(d.P + 1, 0);
-    d.xoff.assign(d.P + 1, 0);
-    d.work.assign(d.P + 1, 0);
+    d.cnt.assign(d.L + 1, 0);
+    d.cap.assign(d.L + 1, 0);
+    d.noff.assign(d.L + 1, 0);
+    d.toff.assign(d.L + 1, 0);
+    d.tmask.assign(d.L + 1, 0);
+    d.xoff.assign(d.L + 1, 0);
+    d.work.assign(d.L + 1, 0);
     d.cnt[0] = 1;
     d.view = DPView{};
     int e = d.counters.reserve(64 * 4);
     bool counted = false;
     {   /* fast path: upper-bound capacities, one sync */
-        std::vector<uint64_t> ub(d.P + 1, 1);
-        for (uint32_t j = 0; j < d.P; j++) ub[j + 1] = std::min<uint64_t>(ub[j] * (n - j), 1ull << 22);
+        std::vector<uint64_t> ub(d.L + 1, 1);
+        for (uint32_t j = 0; j < d.L; j++) ub[j + 1] = std::min<uint64_t>(ub[j] * (n - j), 1ull << 22);
         if (!e && dp_layout(c, ub, ub, e) && !e) {
             e = cudaMemset(d.tables.p, 0xFF, d.table_slots * 4);
             if (!e) e = cudaMemset(d.counters.p, 0, 64 * 4);
-            if (!e) e = dp_levels(c, 0, d.P, nullptr);
-            std::vector<uint32_t> h(d.P + 2, 0); /* counts of levels 0..P, the overflow flag at P+1 */
-            if (!e) e = cudaMemcpy(h.data(), d.counters.p, (d.P + 2) * 4, cudaMemcpyDeviceToHost);
-            if (!e && !h[d.P + 1]) {
+            if (!e) e = dp_levels(c, 0, d.L, nullptr);
+            std::vector<uint32_t> h(d.L + 2, 0); /* counts of levels 0..L, the overflow flag at L+1 */
+            if (!e) e = cudaMemcpy(h.data(), d.counters.p, (d.L + 2) * 4, cudaMemcpyDeviceToHost);
+            if (!e && !h[d.L + 1]) {
                 counted = true;
-                for (uint32_t j = 1; j <= d.P; j++) {
+                for (uint32_t j = 1; j <= d.L; j++) {
                     d.cnt[j] = h[j];
                     counted = counted && h[j] <= ub[j];
                 }
@@ -651,20 +661,20 @@ rk_status dp_plan(rk_ctx* c) {
         }
     }
     if (!e && !counted) { /* level by level, exact capacities */
-        std::vector<uint64_t> m(d.P + 1, 0), cap(d.P + 1, 0);
+        std::vector<uint64_t> m(d.L + 1, 0), cap(d.L + 1, 0);
         m[0] = 1;
         e = cudaMemset(d.counters.p, 0, 64 * 4);
-        for (uint32_t j = 0; j < d.P && !e; j++) {
+        for (uint32_t j = 0; j < d.L && !e; j++) {
             cap[j + 1] = m[j] * (n - j);
-            for (uint32_t q = j + 1; q <= d.P; q++) m[q] = q == j + 1 ? cap[j + 1] : 1;
-            std::vector<uint64_t> cq(d.P + 1, 1);
+            for (uint32_t q = j + 1; q <= d.L; q++) m[q] = q == j + 1 ? cap[j + 1] : 1;
+            std::vector<uint64_t> cq(d.L + 1, 1);
             for (uint32_t q = 1; q <= j + 1; q++) cq[q] = cap[q];
             if (!dp_layout(c, m, cq, e, true) || e) return e ? cuda_fail(c, e, "memoisation plan") : RK_OK;
             e = cudaMemset((uint32_t*)d.tables.p + d.toff[j + 1], 0xFF, (d.tmask[j + 1] + 1ull) * 4);
             if (!e) e = dp_levels(c, j, j + 1, nullptr);
             uint32_t h[2] = {0, 0}; /* level j+1 count; the overflow flag lives at P+1 */
             if (!e) e = cudaMemcpy(&h[0], (uint32_t*)d.counters.p + j + 1, 4, cudaMemcpyDeviceToHost);
-            if (!e) e = cudaMemcpy(&h[1], (uint32_t*)d.counters.p + d.P + 1, 4, cudaMemcpyDeviceToHost);
+            if (!e) e = cudaMemcpy(&h[1], (uint32_t*)d.counters.p + d.L + 1, 4, cudaMemcpyDeviceToHost);
             if (e) break;
             if (h[0] > cap[j + 1] || h[1]) return RK_OK; /* cannot happen: capacity is an upper bound */
             m[j + 1] = d.cnt[j + 1] = h[0];
@@ -675,9 +685,9 @@ rk_status dp_plan(rk_ctx* c) {
         return cuda_fail(c, e, "memoisation plan");
     }
     {   /* the exact layout of the steps: level j+1 capacity cnt[j] * (n - j) */
-        std::vector<uint64_t> m(d.P + 1), cap(d.P + 1, 0);
-        for (uint32_t j = 0; j <= d.P; j++) m[j] = d.cnt[j];
-        for (uint32_t j = 0; j < d.P; j++) cap[j + 1] = (uint64_t)d.cnt[j] * (n - j);
+        std::vector<uint64_t> m(d.L + 1), cap(d.L + 1, 0);
+        for (uint32_t j = 0; j <= d.L; j++) m[j] = d.cnt[j];
+        for (uint32_t j = 0; j < d.L; j++) cap[j + 1] = (uint64_t)d.cnt[j] * (n - j);
         if (!dp_layout(c, m, cap, e) || e) return e ? cuda_fail(c, e, "memoisation layout") : RK_OK;
     }
     const uint64_t runs = fact64(n) / fact64(RK_DP_D), uP = d.cnt[d.P];
@@ -690,11 +700,12 @@ rk_status dp_plan(rk_ctx* c) {
     if (!e) e = d.offs.reserve(uP * DF * 4);
     if (!e) e = d.nd.reserve(uP * 4);
     if (!e) e = d.fst.reserve(uP * 4 * 8);
+    if (!e) e = d.row24.reserve((uint64_t)d.cnt[d.L] * 24 * 8 + 8);
     if (e) {
         cudaGetLastError();
         return cuda_fail(c, e, "memoisation buffers");
     }
-    for (uint32_t j = 0; j < d.P; j++) {
+    for (uint32_t j = 0; j < d.L; j++) {
         d.view.tid[j] = (const uint32_t*)d.tid.p + d.xoff[j];
         d.view.dk[j] = (const uint64_t*)d.dk.p + d.xoff[j];
     }
@@ -722,7 +733,7 @@ const uint64_t* cand_or_zero(rk_ctx* c, const uint64_t* cand_dev, void* stream) 
 RkRows dp_rows(rk_ctx* c, uint64_t nrun) {
     DpPlan& d = c->dp;
     return RkRows{c->dedup_now ? d.rslot.p : nullptr, (uint32_t*)d.rmult.p, d.rmask, (uint32_t*)d.rlist.p,
-                  (uint32_t*)d.counters.p + d.P + 2, nrun};
+                  (uint32_t*)d.counters.p + d.L + 2, nrun};
 }
 
 /* Pass 1 of the memoised step: the levels rebuilt from scratch with the
@@ -1162,21 +1173,21 @@ rk_status rk_memo_audit(rk_ctx* c, uint64_t* out) {
     if (!d.on || !d.runs_ok) return fail(c, RK_ESTATE, "memo audit needs memoisation on and a pass 1 first");
     DeviceGuard dg(c->device);
     unsigned long long* bad = nullptr;
-    std::vector<unsigned long long> h(6 * d.P, 0);
-    std::vector<uint32_t> cnt(d.P + 1, 0);
-    int e = cudaMalloc(&bad, sizeof(unsigned long long) * 6 * d.P);
-    if (!e) e = cudaMemset(bad, 0, sizeof(unsigned long long) * 6 * d.P);
+    std::vector<unsigned long long> h(6 * d.L, 0);
+    std::vector<uint32_t> cnt(d.L + 1, 0);
+    int e = cudaMalloc(&bad, sizeof(unsigned long long) * 6 * d.L);
+    if (!e) e = cudaMemset(bad, 0, sizeof(unsigned long long) * 6 * d.L);
     const char* nodes = (const char*)d.nodes.p;
-    for (uint32_t j = 1; j <= d.P && !e; j++)
+    for (uint32_t j = 1; j <= d.L && !e; j++)
         e = rk_dp_audit(c->tab.g.S, nodes + d.noff[j], (const uint32_t*)d.counters.p + j, d.cap[j],
                         (const uint32_t*)d.tables.p + d.toff[j], d.tmask[j], d.view.tid[j - 1], d.work[j - 1],
                         bad + 6 * (j - 1), nullptr);
-    if (!e) e = cudaMemcpy(h.data(), bad, sizeof(unsigned long long) * 6 * d.P, cudaMemcpyDeviceToHost);
-    if (!e) e = cudaMemcpy(cnt.data(), d.counters.p, 4 * (d.P + 1), cudaMemcpyDeviceToHost);
+    if (!e) e = cudaMemcpy(h.data(), bad, sizeof(unsigned long long) * 6 * d.L, cudaMemcpyDeviceToHost);
+    if (!e) e = cudaMemcpy(cnt.data(), d.counters.p, 4 * (d.L + 1), cudaMemcpyDeviceToHost);
     cudaFree(bad);
     if (e) return cuda_fail(c, e, "rk_memo_audit");
     for (int q = 0; q < 8; q++) out[q] = 0;
-    for (uint32_t j = 1; j <= d.P; j++) {
+    for (uint32_t j = 1; j <= d.L; j++) {
         for (int q = 0; q < 5; q++) out[q] += h[6 * (j - 1) + q];
         out[5] += h[6 * (j - 1) + 5] != cnt[j];   /* published slots != count */
         out[6] += cnt[j] != d.cnt[j];             /* count != the plan's (deterministic) count */

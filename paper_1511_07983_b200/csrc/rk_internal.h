@@ -129,9 +129,13 @@ struct RkExpand {
 int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
                 uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
                 uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex = nullptr);
-int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
-                 void* dvp, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
-                 uint32_t* launches);
+/* the 24 suffix keys of every level-(P+1) node (row24: nodes x 24 u64) */
+int rk_dp_row24(const RkTables* tab, uint32_t S, const void* U, const uint32_t* cnt, uint64_t* row24, uint64_t nodes,
+                void* stream, uint32_t* launches);
+/* the level-P suffix rows from the level-P transitions and row24 */
+int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, const uint32_t* tidP,
+                 const uint64_t* dkP, const uint64_t* row24, uint8_t* code, void* dvc, void* dvp, uint32_t* nd,
+                 uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream, uint32_t* launches);
 uint32_t rk_dp_max_fused_bins();
 /* race audit of level (U, cnt) and its hash table + the previous level's
  * transitions; bad = 6 zeroed u64 counters (rk_dp_audit_kernel) */

@@ -2044,55 +2044,81 @@ __global__ void rk_dp_audit_kernel(const DNode<SMAX>* __restrict__ U, const uint
  * evaluate the 6 orders below each; the row is then encoded as its sorted
  * distinct values dv (with multiplicities dc; ~14 per row on C4) and one byte
  * code per order (code = rank of its key among dv), plus min/max/argmin/argmax. */
-struct SLeaf {
-    uint64_t* row;
-    __device__ __forceinline__ void operator()(uint32_t off, uint64_t K) { row[off] = K; }
-    __device__ __forceinline__ void pair(uint32_t off, uint64_t K0, uint64_t K1) {
-        row[off] = K0;
-        row[off + 1] = K1;
-    }
-};
 
 constexpr uint32_t kDF = 120; /* D! for the memo suffix depth D = 5 */
 
+/* The (D-1)! = 24 suffix keys (from K = 0) of every level-(P+1) node, in the
+ * lexicographic order of its 4 remaining kernels (ascending ids): thread per
+ * (node, first, second) triple places the first two and evaluates both orders
+ * of the last two (place + finish). */
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kDpThreads) rk_dp_row24_kernel(const RkTables* __restrict__ tab,
+                                                                const DNode<SMAX>* __restrict__ U,
+                                                                const uint32_t* __restrict__ cnt,
+                                                                uint64_t* __restrict__ row24) {
+    __shared__ RkTables t;
+    load_tables(t, tab);
+    const RkGTab& g = t.g;
+    const uint32_t n = g.n, m = *cnt;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < (uint64_t)m * 12u;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t w = (uint32_t)(x / 12u), ab = (uint32_t)(x - (uint64_t)w * 12u);
+        const DNode<SMAX> nd0 = U[w];
+        uint32_t rem = 0, q0 = 0;
+        for (uint32_t k = 0; k < n; k++)
+            if (!((nd0.mask >> k) & 1u)) rem |= k << (4u * q0++);
+        const uint32_t a = ab / 3u, b = ab - 3u * a;
+        const uint32_t ka = (rem >> (4u * a)) & 15u;
+        const uint32_t r3 = (rem & ((1u << (4u * a)) - 1u)) | ((rem >> (4u * a + 4u)) << (4u * a));
+        const uint32_t kb = (r3 >> (4u * b)) & 15u;
+        const uint32_t r2 = (r3 & ((1u << (4u * b)) - 1u)) | ((r3 >> (4u * b + 4u)) << (4u * b));
+        const uint32_t kc = r2 & 15u, kd = (r2 >> 4) & 15u; /* kc < kd */
+        St<SMAX> s, s1, s2;
+        node_to_st<SMAX>(nd0, s);
+        NoRec nr;
+        place<SMAX, FULL>(s, s1, t.k[ka], ka, g, nr);
+        place<SMAX, FULL>(s1, s2, t.k[kb], kb, g, nr);
+        uint64_t* o = row24 + (uint64_t)w * 24u + 6u * a + 2u * b;
+        o[0] = place_finish<SMAX, FULL>(s2, t.k[kc], kc, t.k[kd], kd, g);
+        o[1] = place_finish<SMAX, FULL>(s2, t.k[kd], kd, t.k[kc], kc, g);
+    }
+}
+
+/* Suffix rows of the level-P nodes: the 120 keys (from K = 0) of a node's 5
+ * remaining kernels' orders, lexicographic in the remaining ascending ids —
+ * order a*24 + r is the a-th remaining kernel first: key = dK(u, k_a) +
+ * row24[child(u, k_a)][r] through the level-P transitions (the same additivity
+ * as the memo itself).  A warp per node encodes the row as its sorted
+ * distinct values dv (with multiplicities dc; ~14 per row on C4) and one byte
+ * code per order (code = rank of its key among dv), the decoded 32-bit
+ * offsets from the row minimum, plus min/max/argmin/argmax. */
 template <int SMAX, bool FULL>
 __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables* __restrict__ tab,
                                                                  const DNode<SMAX>* __restrict__ UP,
                                                                  const uint32_t* __restrict__ cnt_P,
+                                                                 const uint32_t* __restrict__ tidP,
+                                                                 const uint64_t* __restrict__ dkP,
+                                                                 const uint64_t* __restrict__ row24,
                                                                  uint8_t* __restrict__ code, ulonglong2* __restrict__ dvc,
                                                                  uint2* __restrict__ dvp, uint32_t* __restrict__ nd,
                                                                  uint64_t* __restrict__ fst, uint32_t* __restrict__ offs) {
-    __shared__ RkTables t;
-    __shared__ uint64_t srow[kDpThreads / 32][128];
-    load_tables(t, tab);
-    const RkGTab& g = t.g;
-    const uint32_t n = g.n, lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const uint32_t n = tab->g.n, lane = threadIdx.x & 31u;
     const uint32_t m = *cnt_P;
-    uint64_t* row = srow[w];
     for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < m; u += (gridDim.x * blockDim.x) >> 5) {
-        const DNode<SMAX> nd0 = UP[u];
+        const uint32_t mask = UP[u].mask;
         uint32_t rem = 0, q0 = 0;
         for (uint32_t k = 0; k < n; k++)
-            if (!((nd0.mask >> k) & 1u)) rem |= k << (4u * q0++);
-        if (lane < 20) {
-            St<SMAX> s;
-            node_to_st<SMAX>(nd0, s);
-            const uint32_t a = lane >> 2, b = lane & 3u;
-            const uint32_t ka = (rem >> (4u * a)) & 15u;
-            const uint32_t r4 = (rem & ((1u << (4u * a)) - 1u)) | ((rem >> (4u * a + 4u)) << (4u * a));
-            const uint32_t kb = (r4 >> (4u * b)) & 15u;
-            const uint32_t r3 = (r4 & ((1u << (4u * b)) - 1u)) | ((r4 >> (4u * b + 4u)) << (4u * b));
-            NoRec nr;
-            St<SMAX> s1, s2;
-            place<SMAX, FULL>(s, s1, t.k[ka], ka, g, nr);
-            place<SMAX, FULL>(s1, s2, t.k[kb], kb, g, nr);
-            SLeaf leaf{row + a * 24u + b * 6u};
-            dfs<SMAX, FULL, 3>(t, s2, r3, 0u, leaf);
-        }
-        __syncwarp();
+            if (!((mask >> k) & 1u)) rem |= k << (4u * q0++);
         uint64_t v[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) v[q] = lane + 32u * q < kDF ? row[lane + 32u * q] : ~0ull;
+        for (int q = 0; q < 4; q++) {
+            const uint32_t sg = lane + 32u * q, a = sg / 24u, r = sg - 24u * a;
+            v[q] = ~0ull;
+            if (sg < kDF) {
+                const uint32_t c = u * n + ((rem >> (4u * a)) & 15u);
+                v[q] = __ldg(dkP + c) + __ldg(row24 + (uint64_t)__ldg(tidP + c) * 24u + r);
+            }
+        }
         /* distinct values in increasing order by repeated warp minimum (~14 rounds) */
         uint32_t done = 0, rank = 0, cdw = 0; /* done: bit q; cdw: the lane's 4 codes, one byte each */
 #pragma unroll
@@ -3084,10 +3110,34 @@ int rk_dp_audit(uint32_t S, const void* U, const uint32_t* cnt, uint32_t cap, co
     return (int)cudaGetLastError();
 }
 
-int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, uint8_t* code, void* dvc,
-                 void* dvp, uint32_t* nd, uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream,
-                 uint32_t* launches) {
-#define RK_DP_SUF_ARGS(SMAX) tab, (const DNode<SMAX>*)UP, cnt_P, code, (ulonglong2*)dvc, (uint2*)dvp, nd, fst, offs
+int rk_dp_row24(const RkTables* tab, uint32_t S, const void* U, const uint32_t* cnt, uint64_t* row24, uint64_t nodes,
+                void* stream, uint32_t* launches) {
+#define RK_DP_R24_ARGS(SMAX) tab, (const DNode<SMAX>*)U, cnt, row24
+    const unsigned grid = dp_grid(nodes * 12);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (variant(S)) {
+        case 0: rk_dp_row24_kernel<1, true><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(1)); break;
+        case 1: rk_dp_row24_kernel<2, true><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(2)); break;
+        case 2: rk_dp_row24_kernel<4, false><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(4)); break;
+        case 3: rk_dp_row24_kernel<4, true><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(4)); break;
+        case 4: rk_dp_row24_kernel<8, false><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(8)); break;
+        case 5: rk_dp_row24_kernel<8, true><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(8)); break;
+        case 6: rk_dp_row24_kernel<16, false><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(16)); break;
+        case 7: rk_dp_row24_kernel<16, true><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(16)); break;
+        case 8: rk_dp_row24_kernel<32, false><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(32)); break;
+        case 9: rk_dp_row24_kernel<32, true><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(32)); break;
+        default: rk_dp_row24_kernel<0, false><<<grid, kDpThreads, 0, st>>>(RK_DP_R24_ARGS(0)); break;
+    }
+#undef RK_DP_R24_ARGS
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_suffix(const RkTables* tab, uint32_t S, const void* UP, const uint32_t* cnt_P, const uint32_t* tidP,
+                 const uint64_t* dkP, const uint64_t* row24, uint8_t* code, void* dvc, void* dvp, uint32_t* nd,
+                 uint64_t* fst, uint32_t* offs, uint64_t nodes, void* stream, uint32_t* launches) {
+#define RK_DP_SUF_ARGS(SMAX) tab, (const DNode<SMAX>*)UP, cnt_P, tidP, dkP, row24, code, (ulonglong2*)dvc, (uint2*)dvp, \
+                             nd, fst, offs
     const unsigned grid = dp_grid(nodes * 32);
     cudaStream_t st = (cudaStream_t)stream;
     switch (variant(S)) {

@@ -1185,7 +1185,7 @@ def test_memo_hash_tables_race_audit(monkeypatch):
                 ctx.rk_sweep_pass2_async(0, N, cand, None, 0, None, keys, rec)
                 bad = ctx.rk_memo_audit()
                 assert bad[:7] == [0] * 7, (ci, r, bad)
-                assert bad[7] == sum(ctx.rk_memo_info()[2][1:])
+                assert bad[7] > sum(ctx.rk_memo_info()[2][1:])  # levels 1..P + the level-(P+1) nodes
                 h = (rec.cpu().clone(), torch.sum(keys * 7919 + 1).item(), keys[::9973].cpu())
                 if first is None:
                     first = h
