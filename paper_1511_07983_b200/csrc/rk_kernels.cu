@@ -1966,7 +1966,12 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
                          : "l"(table + pos), "r"(kDpEmpty), "r"(kDpBusy)
                          : "memory");
             if (v == kDpEmpty) { /* claimed: allocate, write the record, publish the id (release) */
-                id = atomicAdd(cnt_n, 1u);
+                /* warp-aggregated id allocation: one atomic per group of claimants (every claim
+                 * of a level hits this one counter, so per-thread atomics serialise at L2) */
+                const cg::coalesced_group cl = cg::coalesced_threads();
+                uint32_t base = 0;
+                if (cl.thread_rank() == 0) base = atomicAdd(cnt_n, cl.size());
+                id = cl.shfl(base, 0) + cl.thread_rank();
                 if (id < cap_n) Un[id] = o;
                 else atomicOr(ovf, 1u);
                 uint32_t old;
