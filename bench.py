@@ -219,6 +219,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-reduce-check", action=argparse.BooleanOptionalAction, default=True)
+    ap.add_argument("--u64-keys", action="store_true", help="store u64 keys instead of exact u32 offsets")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -239,7 +240,7 @@ def main():
     assert world == args.gpus or world == 1, "launch N>1 with torchrun --nproc-per-node N"
 
     gpu, ks = W.config(CONFIG_NAME)
-    sw = Sweeper(gpu, device=local, bins=args.bins)
+    sw = Sweeper(gpu, device=local, bins=args.bins, compact_keys=not args.u64_keys)
     sw.set_kernels(ks)
     stream = torch.cuda.current_stream()
     N = math.factorial(len(ks))
@@ -289,17 +290,19 @@ def main():
 
     # write-only bandwidth of this GPU on the same key buffer (the key stream's own ceiling)
     write_peak_gbs = None
-    if sw.keys is not None:
+    kbuf = sw.keys32 if sw.compact else sw.keys
+    kbytes = 4 if sw.compact else 8
+    if kbuf is not None:
         best = None
         for _ in range(5):
             a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-            sw.keys[:sw.count].fill_(1)
+            kbuf[:sw.count].fill_(1)
             b0.record(stream)
             torch.cuda.synchronize()
             t = a0.elapsed_time(b0)
             best = t if best is None else min(best, t)
-        write_peak_gbs = 8 * sw.count / (best / 1e3) / 1e9
+        write_peak_gbs = kbytes * sw.count / (best / 1e3) / 1e9
 
     # e2e: the public API with host buffers.  Sweeper.run = H2D of the kernel
     # table, rk_set_kernels (validation + the memo plan: no plan is cached, every
@@ -341,13 +344,14 @@ def main():
         c2.rk_set_gpu_params(gpu)
         c2.rk_set_kernels(ks)
         rec2 = torch.zeros(8, dtype=torch.int64, device=sw.dev)
+        k64 = sw.keys if sw.keys is not None else torch.empty(sw.count, dtype=torch.int64, device=sw.dev)
         for _ in range(2):
-            c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, sw.keys, stream)
+            c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, k64, stream)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for _ in range(3):
-            c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, sw.keys, stream)
+            c2.rk_eval_range_async(sw.first, sw.count, sw.cand, rec2, k64, stream)
         b.record(stream)
         torch.cuda.synchronize()
         r = max_over_ranks(a.elapsed_time(b) / 3, sw.dev)
@@ -372,23 +376,25 @@ def main():
         if memo_on:
             # pass 2's key stream dominates: HBM-bound on the 8-B keys it writes
             peaks = read_peaks()
-            bytes_launch = 8 * per_launch_orders
+            bytes_launch = kbytes * per_launch_orders
             stream_ms = phase_ms["stream"]
             achieved = bytes_launch / (stream_ms / 1e3)
             peak = peaks.get("hbm_gbs", 7700.0) * 1e9
-            traffic, issue_pct, _, kname = read_profile("rk_dp_keys_kernel", PROFILE_MEMO)
+            kk = "rk_dp_keys32_kernel" if sw.compact else "rk_dp_keys_kernel"
+            traffic, issue_pct, _, kname = read_profile(kk, PROFILE_MEMO)
             roofline = {"bound": "hbm", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": traffic,
-                        "kernel": kname or "rk_dp_keys_kernel", "kernel_ms": stream_ms,
+                        "kernel": kname or kk, "kernel_ms": stream_ms,
                         "write_peak": write_peak_gbs, "frac_of_write_peak": (achieved / 1e9 / write_peak_gbs
                                                                              if write_peak_gbs else None),
-                        "write_peak_basis": ("measured here: torch fill_ of the same 3.83 GB key buffer, "
-                                             "best of 5 (write-only stream; the copy peak counts read + write)"),
-                        "bytes_per_order": 8, "orders_per_launch": per_launch_orders,
+                        "write_peak_basis": (f"measured here: torch fill_ of the same {kbytes * per_launch_orders / 1e9:.2f} "
+                                             "GB key buffer, best of 5 (write-only stream; the copy peak counts read "
+                                             "+ write)"),
+                        "bytes_per_order": kbytes, "orders_per_launch": per_launch_orders,
                         "peak_basis": ("MEASURED_PEAKS.json hbm_gbs (copy bandwidth, burst)" if "hbm_gbs" in peaks
                                        else "B200_PROFILING fallback 7.7 TB/s"),
                         "ncu_issue_active_pct": issue_pct,
-                        "note": ("algorithmic bytes = the 8-B exact key of every order written to HBM; the "
+                        "note": (f"algorithmic bytes = the {kbytes}-B exact key of every order written to HBM; the "
                                  "suffix rows it adds to are L2-resident (DESIGN.md §5-6); kernel_ms = library-"
                                  "recorded CUDA events around this launch on its stream, mean over the timed steps")}
         else:
@@ -410,7 +416,9 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "n": len(ks), "orders": N, "bins": args.bins,
                            "shards": world, "parallelism": f"index-space shards x{world}",
-                           "keys": "u64 exact keys in HBM (8 B/order)",
+                           "keys": ("exact keys in HBM as u32 offsets from the set's exact lower bound (SPEC:255), "
+                                    "4 B/order; u64 arithmetic; an offset >= 2^32 re-runs the step with u64 keys"
+                                    if sw.compact else "u64 exact keys in HBM (8 B/order)"),
                            "l2": ("inputs larger than L2 per step: the step's only input is the 856-B kernel table; "
                                   "every memo table (~110 MB incl. the 64-MB run table) is rebuilt inside each step "
                                   "and the 3.83 GB key array (> 126 MB L2) is written once per step")},

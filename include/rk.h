@@ -285,6 +285,18 @@ rk_status rk_sweep_pass1_async(rk_ctx* ctx, uint64_t first, uint64_t count, cons
 rk_status rk_sweep_pass2_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
                                const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev,
                                rk_stats* rec_dev, void* stream);
+/* Pass 2 with compact keys (memoised only): as rk_sweep_pass2_async, but every
+ * key goes to keys32_dev (u32[count], index-major, caller-owned) as the exact
+ * offset key - key_base, with key_base <= every key of the range (normally
+ * rk_key_lower_bound: the exact lower bound of SPEC:255) — half the HBM bytes
+ * of u64 keys, no information lost.  A key >= key_base + 2^32 sets *ovf_dev
+ * (u32, caller-zeroed) to 1 and leaves keys32_dev unspecified: re-run pass 1
+ * and pass 2 with u64 keys.  bins <= 32768.  Errors: as rk_sweep_pass2_async,
+ * plus RK_EUNSUPPORTED without memoisation (rk_eval_range32_async is the
+ * direct path's compact form). */
+rk_status rk_sweep_pass2_32_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                                  const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, uint32_t* keys32_dev,
+                                  uint64_t key_base, uint32_t* ovf_dev, rk_stats* rec_dev, void* stream);
 
 /* Per-phase device timing of the step (measurement support):
  * while on, every phase the library enqueues records a CUDA event pair on its

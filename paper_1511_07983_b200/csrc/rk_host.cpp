@@ -822,7 +822,8 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
  * run with the multiset off); with keys they run beside the key stream on the
  * ctx's high-priority side stream (RK_OVERLAP=0: after it). */
 int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, const rk_stats* range_dev,
-             uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev, rk_stats* rec_dev, void* stream) {
+             uint32_t bins, uint64_t* hist_dev, uint64_t* keys_dev, rk_stats* rec_dev, void* stream,
+             uint32_t* keys32 = nullptr, uint64_t key_base = 0, uint32_t* ovf = nullptr) {
     DpPlan& d = c->dp;
     if (!(d.runs_ok && d.runs_first == first && d.runs_count == count)) return (int)cudaErrorNotReady;
     const uint32_t* mu = (const uint32_t*)d.meta_u.p;
@@ -830,7 +831,7 @@ int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev
     const uint64_t DF = d.view.Dfact;
     const uint64_t nrun = count ? (first + count + DF - 1) / DF - first / DF : 0;
     cudaStream_t st = (cudaStream_t)stream;
-    const bool keys = keys_dev && count;
+    const bool keys = (keys_dev || keys32) && count;
     const bool ov = keys && c->overlap != 0;
     int e = ov ? ensure_side(c) : 0;
     auto rows = [&](void* s, uint32_t cap) {
@@ -847,7 +848,8 @@ int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev
     }
     if (!e && keys) {
         const int m1 = tmark_begin(c, RK_PHASE_STREAM, stream);
-        e = rk_dp_keys(d.view, first, count, mu, mk, keys_dev, stream, &c->launches);
+        e = keys32 ? rk_dp_keys32(d.view, first, count, mu, mk, keys32, key_base, ovf, stream, &c->launches)
+                   : rk_dp_keys(d.view, first, count, mu, mk, keys_dev, stream, &c->launches);
         tmark_end(c, m1, stream);
     }
     if (!e && !ov) e = rows(stream, 0);
@@ -1123,6 +1125,27 @@ rk_status rk_sweep_pass2_async(rk_ctx* c, uint64_t first, uint64_t count, const 
         tmark_end(c, m, stream);
     }
     return e ? cuda_fail(c, e, "rk_sweep_pass2_async") : RK_OK;
+}
+
+rk_status rk_sweep_pass2_32_async(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,
+                                  const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, uint32_t* keys32_dev,
+                                  uint64_t key_base, uint32_t* ovf_dev, rk_stats* rec_dev, void* stream) {
+    rk_status s = need_device(c);
+    if (s || (s = need_kernels(c))) return s;
+    if (!rec_dev || !cand_key_dev || !keys32_dev || !ovf_dev)
+        return fail(c, RK_EINVAL, "rec_dev, cand_key_dev, keys32_dev and ovf_dev are required");
+    if (hist_dev && (!range_dev || bins < 1 || bins > rk_dp_max_fused_bins()))
+        return fail(c, RK_EINVAL, "histogram needs range_dev and 1 <= bins <= 32768");
+    if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
+    if (!c->dp.on) return fail(c, RK_EUNSUPPORTED, "compact pass 2 needs memoisation (use rk_eval_range32_async)");
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    const DpPlan& d = c->dp;
+    if (!(d.runs_ok && d.runs_first == first && d.runs_count == count))
+        return fail(c, RK_ESTATE, "pass 2 needs pass 1 over the same range first (it streams pass 1's run metadata)");
+    const int e = dp_pass2(c, first, count, cand_key_dev, range_dev, hist_dev ? bins : 0, hist_dev, nullptr, rec_dev,
+                           stream, keys32_dev, key_base, ovf_dev);
+    return e ? cuda_fail(c, e, "rk_sweep_pass2_32_async") : RK_OK;
 }
 
 rk_status rk_set_timing(rk_ctx* c, int on) {

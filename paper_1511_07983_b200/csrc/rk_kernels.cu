@@ -1960,11 +1960,16 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
                 break;
             }
             uint32_t v;
-            /* acquire: a published id makes its record visible (paired with the release below) */
-            asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], %2, %3;"
-                         : "=r"(v)
-                         : "l"(table + pos), "r"(kDpEmpty), "r"(kDpBusy)
-                         : "memory");
+            /* test, then test-and-set: most children of the big levels find their state already
+             * published (C4 level 8: 213k children, 42.6k states), so a load (acquire: a published
+             * id makes its record visible, paired with the release below) spares the CAS that would
+             * serialise on a popular slot */
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(table + pos) : "memory");
+            if (v == kDpEmpty)
+                asm volatile("atom.acquire.gpu.global.cas.b32 %0, [%1], %2, %3;"
+                             : "=r"(v)
+                             : "l"(table + pos), "r"(kDpEmpty), "r"(kDpBusy)
+                             : "memory");
             if (v == kDpEmpty) { /* claimed: allocate, write the record, publish the id (release) */
                 /* warp-aggregated id allocation: one atomic per group of claimants (every claim
                  * of a level hits this one counter, so per-thread atomics serialise at L2) */
@@ -2678,6 +2683,72 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
     }
 }
 
+/* Pass 2's key stream with compact keys: every key of [first, first+count) as
+ * the exact u32 offset key - key_base from the set's exact lower bound
+ * (rk_key_lower_bound), index-major — half the HBM bytes of the u64
+ * stream.  A one-shot grid; a warp owns kKeyRunsPerWarp consecutive runs, two
+ * per step: a run's 120 keys are 30 16-B chunks, lane l stores chunks l and
+ * l + 32 of the step's 60 (one contiguous 960-B block) from 16-B loads of the
+ * node's 32-bit offsets (L2).  A key >= key_base + 2^32, or a row whose offsets
+ * do not fit 32 bits, sets *ovf (the caller re-runs with u64 keys). */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_keys32_kernel(DPView v, uint64_t first, uint64_t count,
+                                                                 uint64_t rb, uint64_t re,
+                                                                 const uint32_t* __restrict__ meta_u,
+                                                                 const uint64_t* __restrict__ meta_K,
+                                                                 uint32_t* keys, uint64_t key_base, uint32_t* ovf) {
+    constexpr uint32_t DF = kDF, CH = kDF / 4; /* 16-B chunks per run */
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t lo = first, hi = first + count;
+    const uint64_t base = rb + (uint64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kKeyRunsPerWarp;
+    if (base >= re) return;
+    const uint32_t nr = (uint32_t)min((uint64_t)kKeyRunsPerWarp, re - base);
+    const uint32_t umy = lane < nr ? __ldg(meta_u + (base - rb + lane)) : 0u;
+    const uint64_t Kmy = lane < nr ? __ldg(meta_K + (base - rb + lane)) : 0ull;
+    const bool whole = base * DF >= lo && (base + nr) * DF <= hi;
+    uint32_t* const o0 = keys + (base * DF - lo);
+    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15u) == 0; /* DF % 4 == 0: every run block alike */
+    uint64_t bad = 0;
+#pragma unroll
+    for (uint32_t s = 0; s < kKeyRunsPerWarp / 2; s++) {
+        if (2u * s >= nr) break;
+        const uint32_t uA = __shfl_sync(0xFFFFFFFFu, umy, 2 * s), uB = __shfl_sync(0xFFFFFFFFu, umy, 2 * s + 1);
+        const uint64_t KA = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s), KB = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s + 1);
+        const bool twoB = 2u * s + 1u < nr;
+        uint32_t* o = o0 + 2u * s * DF;
+        uint4 of[2];
+#pragma unroll
+        for (int q = 0; q < 2; q++) { /* chunk p = lane + 32q: run A for p < 30, else run B chunk p - 30 */
+            const uint32_t p = lane + 32u * q;
+            const bool a = p < CH, ok = a || (twoB && p < 2u * CH);
+            const uint32_t un = (a ? uA : uB) & 0x7FFFFFFFu;
+            of[q] = ok ? __ldg(reinterpret_cast<const uint4*>(v.offs + (uint64_t)un * DF) + (a ? p : p - CH))
+                       : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const uint32_t p = lane + 32u * q;
+            const bool a = p < CH;
+            if (!(a || (twoB && p < 2u * CH))) continue;
+            const uint32_t ui = a ? uA : uB;
+            const uint64_t d = (a ? KA : KB) - key_base;
+            const uint64_t k0 = d + of[q].x, k1 = d + of[q].y, k2 = d + of[q].z, k3 = d + of[q].w;
+            bad |= ((k0 | k1 | k2 | k3) >> 32) | (uint64_t)(ui >> 31);
+            if (whole && aligned) {
+                __stcs(reinterpret_cast<uint4*>(o + 4u * p),
+                       make_uint4((uint32_t)k0, (uint32_t)k1, (uint32_t)k2, (uint32_t)k3));
+            } else {
+                const uint64_t ix = (base + 2u * s) * DF + 4u * p;
+                const uint32_t kk[4] = {(uint32_t)k0, (uint32_t)k1, (uint32_t)k2, (uint32_t)k3};
+#pragma unroll
+                for (int h = 0; h < 4; h++)
+                    if (ix + h >= lo && ix + h < hi) __stcs(o + 4u * p + h, kk[h]);
+            }
+        }
+    }
+    if (__any_sync(0xFFFFFFFFu, bad != 0) && lane == 0) atomicOr(ovf, 1u);
+}
+
+
 /* Per-device caches of launch-sizing queries (SM count, occupancy): keyed by the
  * current device, written once with relaxed atomics (idempotent values), so
  * contexts on different devices or host threads never size a grid for another
@@ -3222,6 +3293,19 @@ int rk_dp_keys(const DPView& v, uint64_t first, uint64_t count, const uint32_t* 
     if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidValue;
     rk_dp_keys_kernel<<<(unsigned)(grid ? grid : 1), kDpThreads, 0, (cudaStream_t)stream>>>(
         v, first, count, first / v.Dfact, (first + count + v.Dfact - 1) / v.Dfact, meta_u, meta_K, keys);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_keys32(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
+                 uint32_t* keys32, uint64_t key_base, uint32_t* ovf, void* stream, uint32_t* launches) {
+    const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
+    const uint64_t per_cta = (uint64_t)kDpWarps * kKeyRunsPerWarp; /* one-shot grid */
+    const uint64_t grid = (runs + per_cta - 1) / per_cta;
+    if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidValue;
+    rk_dp_keys32_kernel<<<(unsigned)(grid ? grid : 1), kDpThreads, 0, (cudaStream_t)stream>>>(
+        v, first, count, first / v.Dfact, (first + count + v.Dfact - 1) / v.Dfact, meta_u, meta_K, keys32, key_base,
+        ovf);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

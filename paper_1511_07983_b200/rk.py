@@ -24,7 +24,7 @@ STATUS_NAMES = ["RK_OK", "RK_EINVAL", "RK_EINFEASIBLE", "RK_ETOOMANY", "RK_EMISS
 EXPORTS = ["rk_create", "rk_destroy", "rk_last_error", "rk_set_gpu_params", "rk_set_kernels", "rk_eval_range",
            "rk_eval_range_async", "rk_eval_range_hist_async", "rk_eval_range32_async", "rk_key_lower_bound", "rk_histogram32_async",
            "rk_eval_index_async", "rk_merge_stats_async", "rk_histogram", "rk_histogram_async",
-           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_sweep_pass1_async", "rk_sweep_pass2_async", "rk_set_timing", "rk_timing_read", "rk_memo_info", "rk_memo_audit", "rk_rank", "rk_unrank",
+           "rk_select_keys", "rk_range_histogram", "rk_select_keys32", "rk_range_histogram32", "rk_heuristic_order", "rk_heuristic_batch", "rk_percentile", "rk_eval_batch", "rk_simulate_order", "rk_best_order", "rk_sweep_pass1_async", "rk_sweep_pass2_async", "rk_sweep_pass2_32_async", "rk_set_timing", "rk_timing_read", "rk_memo_info", "rk_memo_audit", "rk_rank", "rk_unrank",
            "rk_last_launch_count", "rk_table_bytes"]
 
 
@@ -97,6 +97,7 @@ def lib():
             "rk_heuristic_order": ([vp, P(ctypes.c_int32), P(ctypes.c_int32), P(u64), P(u64)], ctypes.c_int),
             "rk_sweep_pass1_async": ([vp, u64, u64, vp, vp, vp, vp], ctypes.c_int),
             "rk_sweep_pass2_async": ([vp, u64, u64, vp, vp, u32, vp, vp, vp, vp], ctypes.c_int),
+            "rk_sweep_pass2_32_async": ([vp, u64, u64, vp, vp, u32, vp, vp, u64, vp, vp, vp], ctypes.c_int),
             "rk_memo_info": ([vp, P(u32), P(u32), P(u32), u32], ctypes.c_int),
             "rk_memo_audit": ([vp, P(u64)], ctypes.c_int),
             "rk_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
@@ -337,6 +338,12 @@ class Context:
         self._chk(self._L.rk_sweep_pass2_async(self.h, first, count, _ptr(cand_key_dev), _ptr(range_dev), bins,
                                                _ptr(hist_dev), _ptr(keys_dev), _ptr(rec_dev), _stream(stream)),
                   "rk_sweep_pass2_async")
+
+    def rk_sweep_pass2_32_async(self, first: int, count: int, cand_key_dev, range_dev, bins: int, hist_dev,
+                                keys32_dev, key_base: int, ovf_dev, rec_dev, stream=None):
+        self._chk(self._L.rk_sweep_pass2_32_async(self.h, first, count, _ptr(cand_key_dev), _ptr(range_dev), bins,
+                                                  _ptr(hist_dev), _ptr(keys32_dev), key_base, _ptr(ovf_dev),
+                                                  _ptr(rec_dev), _stream(stream)), "rk_sweep_pass2_32_async")
 
     def rk_set_timing(self, on: bool = True):
         self._chk(self._L.rk_set_timing(self.h, 1 if on else 0), "rk_set_timing")

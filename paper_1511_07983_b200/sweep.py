@@ -70,7 +70,9 @@ class Sweeper:
         self.keys = None
         self.keys32 = None
         self.ovf = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        self.compact_keys = compact_keys  # u32 offsets: half the key bytes (measured: no net gain on C4)
+        # exact keys stored as u32 offsets from the set's exact lower bound: half the key bytes;
+        # a key >= base + 2^32 sets the overflow flag and run() repeats the step with u64 keys
+        self.compact_keys = compact_keys
         self.rec = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
         self.glob = torch.zeros(REC_WORDS, dtype=torch.int64, device=self.dev)
         self.cand = torch.zeros(1, dtype=torch.int64, device=self.dev)
@@ -88,6 +90,7 @@ class Sweeper:
         # compact keys (u32 offsets from the exact lower bound) unless a
         # previous pass on this set overflowed; then u64 keys
         self.base = self.ctx.rk_key_lower_bound()
+        self.memo = self.ctx.rk_memo_info()[0] and self.bins <= 32768
         self.ovf.zero_()
         if self.compact_keys:
             self.compact = True
@@ -120,11 +123,12 @@ class Sweeper:
         if ev:
             e0, e1 = ev(), ev()
             e0.record(st)
-        if self.compact:                                                                       # a1-a4 (u32 keys)
+        memo = self.compact and self.memo
+        if self.compact and not memo:                                                          # a1-a4 (u32 keys)
             c.rk_eval_range32_async(self.first, self.count, self.cand, self.rec, self.keys32, self.base, self.ovf,
                                     stream)
         else:                                                                                  # a1-a4 pass 1
-            c.rk_sweep_pass1_async(self.first, self.count, self.cand, self.rec, self.keys, stream)
+            c.rk_sweep_pass1_async(self.first, self.count, self.cand, self.rec, None if memo else self.keys, stream)
         L += c.launches
         if ev:
             e1.record(st)
@@ -142,7 +146,10 @@ class Sweeper:
         if ev:
             h0, h1 = ev(), ev()
             h0.record(st)
-        if self.compact:                                                                       # a4 histogram
+        if memo:                                                                               # a4 pass 2 (u32 keys)
+            c.rk_sweep_pass2_32_async(self.first, self.count, self.cand, rng, self.bins, self.hist, self.keys32,
+                                      self.base, self.ovf, counts, stream)
+        elif self.compact:                                                                     # a4 histogram
             c.rk_histogram32_async(self.keys32, self.count, self.base, rng, self.bins, self.hist, stream)
         else:                                                                                  # a4 pass 2
             c.rk_sweep_pass2_async(self.first, self.count, self.cand, rng, self.bins, self.hist, self.keys, counts,

@@ -1195,3 +1195,64 @@ def test_memo_hash_tables_race_audit(monkeypatch):
         assert audited >= 6
     finally:
         ctx.close()
+
+
+def test_memo_compact_key_stream_c4_and_overflow(ctx):
+    """rk_sweep_pass2_32_async (the bench's key stream with exact u32 offsets
+    from the set's lower bound): on C4 every stored offset + base
+    equals the u64 key of the same step, the record and histogram equal the
+    oracle golden, 10^5 sampled keys equal the oracle's; on a set whose keys
+    span >= 2^32 the overflow flag is raised."""
+    g = _gold("c4_oracle.json")
+    gpu, ks = W.config("C4")
+    ctx.rk_set_gpu_params(gpu)
+    ctx.rk_set_kernels(ks)
+    N = math.factorial(12)
+    base = ctx.rk_key_lower_bound()
+    cand = torch.tensor([g["cand_key"]], dtype=torch.int64, device="cuda")
+    rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+    hist = torch.zeros(256, dtype=torch.int64, device="cuda")
+    k32 = torch.empty(N, dtype=torch.int32, device="cuda")
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.rk_sweep_pass1_async(0, N, cand, rec, None)
+    ctx.rk_sweep_pass2_32_async(0, N, cand, rec, 256, hist, k32, base, ovf, rec)
+    k64 = torch.empty(N, dtype=torch.int64, device="cuda")
+    rec2 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ctx.rk_sweep_pass1_async(0, N, cand, rec2, k64)
+    ctx.rk_sweep_pass2_async(0, N, cand, rec2, 0, None, k64, rec2)
+    torch.cuda.synchronize()
+    assert int(ovf.item()) == 0
+    st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
+    assert list(st.as_tuple()) == [g["stats"][f] for f in
+                                   ("key_min", "key_max", "argmin", "argmax", "n_lt", "n_eq", "n_gt", "evaluated")]
+    assert hist.cpu().tolist() == g["hist"] and torch.equal(rec, rec2)
+    assert torch.equal((k32.to(torch.int64) & 0xFFFFFFFF) + base, k64)
+    rng = np.random.default_rng(32)
+    sample = rng.integers(0, N, 100000).astype(np.uint64)
+    got = (k32[torch.from_numpy(sample.view(np.int64)).cuda()].to(torch.int64) & 0xFFFFFFFF).cpu().numpy() + base
+    assert np.array_equal(got.astype(np.uint64), O.keys_of(gpu, ks, sample, threads=NCPU))
+    # ragged sub-range (unaligned first, partial runs at both ends)
+    f0, c0 = 1234567, 765433
+    ovf.zero_()
+    ctx.rk_sweep_pass1_async(f0, c0, cand, rec, None)
+    ctx.rk_sweep_pass2_32_async(f0, c0, cand, rec, 0, None, k32, base, ovf, rec)
+    torch.cuda.synchronize()
+    assert int(ovf.item()) == 0
+    assert torch.equal((k32[:c0].to(torch.int64) & 0xFFFFFFFF) + base, k64[f0:f0 + c0])
+    # keys spanning >= 2^32 above the bound: the flag
+    wide = None
+    for ks2 in W.random_small_sets(0x91DE, 8, 7, 8):
+        w = [(k[0], k[1], k[2], k[3], min(k[4] * 797, (1 << 32) - 1), min(k[5] * 787, (1 << 32) - 1)) for k in ks2]
+        if W.key_bound(W.GTX580, w) < (1 << 62):
+            wide = w
+            break
+    ctx.rk_set_kernels(wide)
+    if ctx.rk_memo_info()[0]:
+        n2 = math.factorial(len(wide))
+        b2 = ctx.rk_key_lower_bound()
+        ovf.zero_()
+        ctx.rk_sweep_pass1_async(0, n2, cand, rec, None)
+        ctx.rk_sweep_pass2_32_async(0, n2, cand, rec, 0, None, k32, b2, ovf, rec)
+        torch.cuda.synchronize()
+        st2 = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
+        assert int(ovf.item()) == (1 if st2.key_max - b2 >= (1 << 32) else 0)
