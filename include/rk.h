@@ -289,9 +289,10 @@ rk_status rk_sweep_pass2_async(rk_ctx* ctx, uint64_t first, uint64_t count, cons
  * key goes to keys32_dev (u32[count], index-major, caller-owned) as the exact
  * offset key - key_base, with key_base <= every key of the range (normally
  * rk_key_lower_bound: the exact lower bound of SPEC:255) — half the HBM bytes
- * of u64 keys, no information lost.  A key >= key_base + 2^32 sets *ovf_dev
- * (u32, caller-zeroed) to 1 and leaves keys32_dev unspecified: re-run pass 1
- * and pass 2 with u64 keys.  bins <= 32768.  Errors: as rk_sweep_pass2_async,
+ * of u64 keys, no information lost.  range_dev is required: when
+ * range_dev->key_max >= key_base + 2^32 (some key would not fit), *ovf_dev (u32,
+ * caller-zeroed) is set to 1 and no key is written: re-run pass 1 and pass 2
+ * with u64 keys.  bins <= 32768.  Errors: as rk_sweep_pass2_async,
  * plus RK_EUNSUPPORTED without memoisation (rk_eval_range32_async is the
  * direct path's compact form). */
 rk_status rk_sweep_pass2_32_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,

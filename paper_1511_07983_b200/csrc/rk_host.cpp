@@ -848,7 +848,7 @@ int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev
     }
     if (!e && keys) {
         const int m1 = tmark_begin(c, RK_PHASE_STREAM, stream);
-        e = keys32 ? rk_dp_keys32(d.view, first, count, mu, mk, keys32, key_base, ovf, stream, &c->launches)
+        e = keys32 ? rk_dp_keys32(d.view, first, count, mu, mk, keys32, key_base, ovf, range_dev, stream, &c->launches)
                    : rk_dp_keys(d.view, first, count, mu, mk, keys_dev, stream, &c->launches);
         tmark_end(c, m1, stream);
     }
@@ -1132,8 +1132,8 @@ rk_status rk_sweep_pass2_32_async(rk_ctx* c, uint64_t first, uint64_t count, con
                                   uint64_t key_base, uint32_t* ovf_dev, rk_stats* rec_dev, void* stream) {
     rk_status s = need_device(c);
     if (s || (s = need_kernels(c))) return s;
-    if (!rec_dev || !cand_key_dev || !keys32_dev || !ovf_dev)
-        return fail(c, RK_EINVAL, "rec_dev, cand_key_dev, keys32_dev and ovf_dev are required");
+    if (!rec_dev || !cand_key_dev || !keys32_dev || !ovf_dev || !range_dev)
+        return fail(c, RK_EINVAL, "rec_dev, cand_key_dev, range_dev, keys32_dev and ovf_dev are required");
     if (hist_dev && (!range_dev || bins < 1 || bins > rk_dp_max_fused_bins()))
         return fail(c, RK_EINVAL, "histogram needs range_dev and 1 <= bins <= 32768");
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");

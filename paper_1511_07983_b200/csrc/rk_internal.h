@@ -169,9 +169,11 @@ int rk_dp_meta(const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u
 int rk_dp_rows(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, const uint64_t* cand_dev,
                const rk_stats* range, uint32_t bins, uint64_t* hist, const RkRows& rows, const uint32_t* meta_u,
                const uint64_t* meta_K, rk_stats* rec, uint32_t max_ctas, void* stream, uint32_t* launches);
-/* pass 2's compact key stream: u32 offsets from key_base, *ovf |= 1 when one does not fit */
+/* pass 2's compact key stream: u32 offsets from key_base; *ovf |= 1 (and no key written) when
+ * range->key_max - key_base >= 2^32 */
 int rk_dp_keys32(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
-                 uint32_t* keys32, uint64_t key_base, uint32_t* ovf, void* stream, uint32_t* launches);
+                 uint32_t* keys32, uint64_t key_base, uint32_t* ovf, const rk_stats* range, void* stream,
+                 uint32_t* launches);
 /* pass 2's key stream from the run metadata (one-shot grid) */
 int rk_dp_keys(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
                uint64_t* keys, void* stream, uint32_t* launches);

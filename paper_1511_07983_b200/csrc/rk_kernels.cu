@@ -2683,33 +2683,44 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
     }
 }
 
+/* runs per warp of the compact stream: twice the u64 stream's, so a CTA moves
+ * as many bytes (the one-shot grid would otherwise be CTA-launch bound) */
+constexpr uint32_t kKey32RunsPerWarp = 8;
 /* Pass 2's key stream with compact keys: every key of [first, first+count) as
  * the exact u32 offset key - key_base from the set's exact lower bound
  * (rk_key_lower_bound), index-major — half the HBM bytes of the u64
  * stream.  A one-shot grid; a warp owns kKeyRunsPerWarp consecutive runs, two
  * per step: a run's 120 keys are 30 16-B chunks, lane l stores chunks l and
  * l + 32 of the step's 60 (one contiguous 960-B block) from 16-B loads of the
- * node's 32-bit offsets (L2).  A key >= key_base + 2^32, or a row whose offsets
- * do not fit 32 bits, sets *ovf (the caller re-runs with u64 keys). */
+ * node's 32-bit offsets (L2).  Overflow is decided once, from the range's
+ * record: if range->key_max >= key_base + 2^32 (which also covers every row
+ * whose offsets do not fit 32 bits) *ovf is set and nothing is written (the
+ * caller re-runs with u64 keys); otherwise every key fits and the stream is
+ * plain 32-bit adds. */
+template <uint32_t RPW>
 __global__ void __launch_bounds__(kDpThreads) rk_dp_keys32_kernel(DPView v, uint64_t first, uint64_t count,
                                                                  uint64_t rb, uint64_t re,
                                                                  const uint32_t* __restrict__ meta_u,
                                                                  const uint64_t* __restrict__ meta_K,
-                                                                 uint32_t* keys, uint64_t key_base, uint32_t* ovf) {
+                                                                 uint32_t* keys, uint64_t key_base, uint32_t* ovf,
+                                                                 const rk_stats* __restrict__ range) {
     constexpr uint32_t DF = kDF, CH = kDF / 4; /* 16-B chunks per run */
+    if ((range->key_max - key_base) >> 32) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(ovf, 1u);
+        return;
+    }
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t lo = first, hi = first + count;
-    const uint64_t base = rb + (uint64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kKeyRunsPerWarp;
+    const uint64_t base = rb + (uint64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW;
     if (base >= re) return;
-    const uint32_t nr = (uint32_t)min((uint64_t)kKeyRunsPerWarp, re - base);
+    const uint32_t nr = (uint32_t)min((uint64_t)RPW, re - base);
     const uint32_t umy = lane < nr ? __ldg(meta_u + (base - rb + lane)) : 0u;
     const uint64_t Kmy = lane < nr ? __ldg(meta_K + (base - rb + lane)) : 0ull;
     const bool whole = base * DF >= lo && (base + nr) * DF <= hi;
     uint32_t* const o0 = keys + (base * DF - lo);
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15u) == 0; /* DF % 4 == 0: every run block alike */
-    uint64_t bad = 0;
 #pragma unroll
-    for (uint32_t s = 0; s < kKeyRunsPerWarp / 2; s++) {
+    for (uint32_t s = 0; s < RPW / 2; s++) {
         if (2u * s >= nr) break;
         const uint32_t uA = __shfl_sync(0xFFFFFFFFu, umy, 2 * s), uB = __shfl_sync(0xFFFFFFFFu, umy, 2 * s + 1);
         const uint64_t KA = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s), KB = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s + 1);
@@ -2729,23 +2740,19 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys32_kernel(DPView v, uint
             const uint32_t p = lane + 32u * q;
             const bool a = p < CH;
             if (!(a || (twoB && p < 2u * CH))) continue;
-            const uint32_t ui = a ? uA : uB;
-            const uint64_t d = (a ? KA : KB) - key_base;
-            const uint64_t k0 = d + of[q].x, k1 = d + of[q].y, k2 = d + of[q].z, k3 = d + of[q].w;
-            bad |= ((k0 | k1 | k2 | k3) >> 32) | (uint64_t)(ui >> 31);
+            const uint32_t d32 = (uint32_t)((a ? KA : KB) - key_base); /* every key - key_base < 2^32 */
+            const uint32_t k0 = d32 + of[q].x, k1 = d32 + of[q].y, k2 = d32 + of[q].z, k3 = d32 + of[q].w;
             if (whole && aligned) {
-                __stcs(reinterpret_cast<uint4*>(o + 4u * p),
-                       make_uint4((uint32_t)k0, (uint32_t)k1, (uint32_t)k2, (uint32_t)k3));
+                __stcs(reinterpret_cast<uint4*>(o + 4u * p), make_uint4(k0, k1, k2, k3));
             } else {
                 const uint64_t ix = (base + 2u * s) * DF + 4u * p;
-                const uint32_t kk[4] = {(uint32_t)k0, (uint32_t)k1, (uint32_t)k2, (uint32_t)k3};
+                const uint32_t kk[4] = {k0, k1, k2, k3};
 #pragma unroll
                 for (int h = 0; h < 4; h++)
                     if (ix + h >= lo && ix + h < hi) __stcs(o + 4u * p + h, kk[h]);
             }
         }
     }
-    if (__any_sync(0xFFFFFFFFu, bad != 0) && lane == 0) atomicOr(ovf, 1u);
 }
 
 
@@ -3298,14 +3305,20 @@ int rk_dp_keys(const DPView& v, uint64_t first, uint64_t count, const uint32_t* 
 }
 
 int rk_dp_keys32(const DPView& v, uint64_t first, uint64_t count, const uint32_t* meta_u, const uint64_t* meta_K,
-                 uint32_t* keys32, uint64_t key_base, uint32_t* ovf, void* stream, uint32_t* launches) {
+                 uint32_t* keys32, uint64_t key_base, uint32_t* ovf, const rk_stats* range, void* stream,
+                 uint32_t* launches) {
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
-    const uint64_t per_cta = (uint64_t)kDpWarps * kKeyRunsPerWarp; /* one-shot grid */
+    static const int rpw_env = [] { const char* e = getenv("RK_K32_RPW"); return e ? atoi(e) : 0; }();
+    const uint32_t rpw = rpw_env == 4 || rpw_env == 16 ? (uint32_t)rpw_env : kKey32RunsPerWarp;
+    const uint64_t per_cta = (uint64_t)kDpWarps * rpw; /* one-shot grid */
     const uint64_t grid = (runs + per_cta - 1) / per_cta;
     if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidValue;
-    rk_dp_keys32_kernel<<<(unsigned)(grid ? grid : 1), kDpThreads, 0, (cudaStream_t)stream>>>(
-        v, first, count, first / v.Dfact, (first + count + v.Dfact - 1) / v.Dfact, meta_u, meta_K, keys32, key_base,
-        ovf);
+    const uint64_t rb = first / v.Dfact, re = (first + count + v.Dfact - 1) / v.Dfact;
+    const unsigned g = (unsigned)(grid ? grid : 1);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (rpw == 4) rk_dp_keys32_kernel<4><<<g, kDpThreads, 0, st>>>(v, first, count, rb, re, meta_u, meta_K, keys32, key_base, ovf, range);
+    else if (rpw == 16) rk_dp_keys32_kernel<16><<<g, kDpThreads, 0, st>>>(v, first, count, rb, re, meta_u, meta_K, keys32, key_base, ovf, range);
+    else rk_dp_keys32_kernel<8><<<g, kDpThreads, 0, st>>>(v, first, count, rb, re, meta_u, meta_K, keys32, key_base, ovf, range);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
