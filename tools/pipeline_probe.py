@@ -17,7 +17,7 @@ N = math.factorial(12)
 out = {}
 for mode in ("one", "two", "two_prio"):
     nsw = 1 if mode == "one" else 2
-    sws = [Sweeper(gpu, device=0) for _ in range(nsw)]
+    sws = [Sweeper(gpu, device=0, compact_keys=True) for _ in range(nsw)]
     lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
     streams = [torch.cuda.Stream(priority=(-1 if (mode == "two_prio") else 0)) for _ in range(nsw)]
     for s in sws:

@@ -25,7 +25,7 @@ ap.add_argument("--coll-us", type=float, default=15.0)
 args = ap.parse_args()
 gpu, ks = W.config(args.config)
 N = math.factorial(len(ks))
-sw = Sweeper(gpu, device=0)
+sw = Sweeper(gpu, device=0, compact_keys=True)
 sw.set_kernels(ks)
 _, idx = sw.heuristic()
 stream = torch.cuda.current_stream()
