@@ -67,7 +67,7 @@ struct DpPlan {
     Arena row24;                                 /* the (D-1)! = 24 suffix keys of every level-(P+1) node */
     Arena expand;                                /* the range's prefix expansion, levels 1..P-1 (level P recomputed) */
     Arena meta_u, meta_K;                        /* the range's run metadata for the key stream: node | wide, Kb */
-    Arena rslot, rmult, rlist;                   /* the range's row multiset (distinct (node, Kb) + multiplicity) */
+    Arena rslot, rmult, rlist, rminrun;          /* the range's row multiset (distinct (node, K_closed), multiplicity, first run) */
     uint32_t rmask = 0;                          /* its slots - 1 */
     bool runs_ok = false;                        /* meta_u/meta_K hold the range [runs_first, +runs_count) */
     uint64_t runs_first = 0, runs_count = 0;
@@ -506,7 +506,7 @@ void dp_free(DpPlan& d) {
     d.dk.release();
     d.fst.release();
     d.counters.release();
-    for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.row24, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist}) a->release();
+    for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.row24, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist, &d.rminrun}) a->release();
     d.runs_ok = false;
     d.on = false;
 }
@@ -733,7 +733,7 @@ const uint64_t* cand_or_zero(rk_ctx* c, const uint64_t* cand_dev, void* stream) 
 RkRows dp_rows(rk_ctx* c, uint64_t nrun) {
     DpPlan& d = c->dp;
     return RkRows{c->dedup_now ? d.rslot.p : nullptr, (uint32_t*)d.rmult.p, d.rmask, (uint32_t*)d.rlist.p,
-                  (uint32_t*)d.counters.p + d.L + 2, nrun};
+                  (uint32_t*)d.counters.p + d.L + 2, nrun, (uint32_t*)d.rminrun.p};
 }
 
 /* Pass 1 of the memoised step: the levels rebuilt from scratch with the
@@ -761,6 +761,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e) e = d.rslot.reserve(slots * 16);
     if (!e) e = d.rmult.reserve(slots * 4 * 8); /* 8 counters per slot */
     if (!e) e = d.rlist.reserve(nrun * 4);
+    if (!e) e = d.rminrun.reserve(slots * 4);
     c->dedup_now = c->row_dedup != 0;
     const bool side = c->overlap != 0;
     if (!e && side) e = ensure_side(c);
@@ -790,6 +791,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     const int m0 = tmark_begin(c, RK_PHASE_TABLES, stream);
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, st);
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, st);
+    if (!e && c->dedup_now) e = cudaMemsetAsync(d.rminrun.p, 0xFF, slots * 4, st);
     if (!e) e = dp_build_levels(c, stream, ex.empty() ? nullptr : &ex);
     void* rs = side ? (void*)c->side : stream;
     if (!e && side) e = cudaEventRecord(c->ev_fork, st);
@@ -805,8 +807,9 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e && side) e = cudaStreamWaitEvent(st, c->ev_join, 0);
     const int m1 = tmark_begin(c, RK_PHASE_EXTREMES, stream);
     if (!e)
-        e = rk_dp_meta(d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p, rec_dev, c->recs_dev,
-                       c->counter_dev, c->max_ctas, stream, &c->launches);
+        e = rk_dp_ext(d.view, first, count, dp_rows(c, re - rb), (const uint32_t*)d.meta_u.p,
+                      (const uint64_t*)d.meta_K.p, rec_dev, c->recs_dev, c->counter_dev, c->max_ctas, stream,
+                      &c->launches);
     tmark_end(c, m1, stream);
     if (!e) {
         d.runs_ok = true;

@@ -153,6 +153,7 @@ struct RkRows {
     uint32_t* list;
     uint32_t* nlist;
     uint64_t list_hint;
+    uint32_t* minrun; /* per slot: smallest run offset of the row (0xFFFFFFFF before pass 1) */
 };
 /* pass 1's run pass: per run of the range its (node, K_closed) into meta_u /
  * meta_K, and the row multiset (rows.slot nullable); last = the range's level
@@ -160,11 +161,12 @@ struct RkRows {
  * suffix rows). */
 int rk_dp_runs(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u,
                uint64_t* meta_K, const RkRows& rows, const RkExpand* last, void* stream, uint32_t* launches);
-/* pass 1's extremes pass (after the run pass and the suffix rows): meta_u |=
- * wide << 31, meta_K = Kb, and the range's extremes record (counts: n_gt =
- * evaluated = count) */
-int rk_dp_meta(const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u, uint64_t* meta_K, rk_stats* out,
-               rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches);
+/* pass 1's extremes (after the run pass and the suffix rows) from the row
+ * multiset + run list (or every run without a multiset): the range's record
+ * (counts: n_gt = evaluated = count) */
+int rk_dp_ext(const DPView& v, uint64_t first, uint64_t count, const RkRows& rows, const uint32_t* meta_u,
+              const uint64_t* meta_K, rk_stats* out, rk_stats* recs, uint32_t* counter, uint32_t max_ctas,
+              void* stream, uint32_t* launches);
 /* pass 2's counts (into rec, nullable) and histogram (nullable) from the row multiset */
 int rk_dp_rows(const RkTables* tab, const DPView& v, uint64_t first, uint64_t count, const uint64_t* cand_dev,
                const rk_stats* range, uint32_t bins, uint64_t* hist, const RkRows& rows, const uint32_t* meta_u,

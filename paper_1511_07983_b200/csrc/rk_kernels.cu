@@ -2302,6 +2302,7 @@ struct RowSet {
     uint32_t mask;     /* slots - 1 */
     uint32_t* list;    /* run offsets from rb */
     uint32_t* nlist;   /* device counter */
+    uint32_t* minrun;  /* per slot: the smallest run offset (from rb) in the row (argmin/argmax) */
 };
 __device__ __forceinline__ uint32_t row_hash(uint32_t uw, uint64_t Kb) {
     uint64_t h = (Kb ^ ((uint64_t)uw << 40) ^ uw) * 0x9E3779B97F4A7C15ull;
@@ -2315,7 +2316,7 @@ __device__ __forceinline__ void cas128(uint4* p, uint64_t v0, uint64_t v1, uint6
                  : "l"(z), "l"(v0), "l"(v1), "l"(p)
                  : "memory");
 }
-__device__ __forceinline__ bool row_insert(const RowSet& rs, uint32_t uw, uint64_t Kb) {
+__device__ __forceinline__ bool row_insert(const RowSet& rs, uint32_t uw, uint64_t Kb, uint32_t off) {
     const uint64_t k0 = (uint64_t)uw | (1ull << 32), k1 = Kb; /* little-endian {uw, 1, Kb lo, Kb hi} */
     uint32_t h = row_hash(uw, Kb) & rs.mask;
     for (uint32_t p = 0; p < kRowProbes; p++, h = (h + 1u) & rs.mask) {
@@ -2323,6 +2324,9 @@ __device__ __forceinline__ bool row_insert(const RowSet& rs, uint32_t uw, uint64
         cas128(rs.slot + h, k0, k1, o0, o1);
         if ((o0 == 0 && o1 == 0) || (o0 == k0 && o1 == k1)) { /* claimed, or already this row */
             atomicAdd(rs.mult + (uint64_t)h * kMultShards + (blockIdx.x & (kMultShards - 1u)), 1u);
+            /* runs arrive roughly in index order: test first, so a heavy row's later runs
+             * (C4: up to 11,056 per row) do not serialise on one address */
+            if (off < __ldcg(rs.minrun + h)) atomicMin(rs.minrun + h, off);
             return true;
         }
     }
@@ -2354,46 +2358,59 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_runs_kernel(const RkTables* 
         if (rs.slot) {
             const uint64_t idx0 = run * DF;
             const bool whole = idx0 >= lo && idx0 + DF <= hi;
-            if (!whole || !row_insert(rs, u, Kc)) rs.list[atomicAdd(rs.nlist, 1u)] = (uint32_t)(run - rb);
+            if (!whole || !row_insert(rs, u, Kc, (uint32_t)(run - rb)))
+                rs.list[atomicAdd(rs.nlist, 1u)] = (uint32_t)(run - rb);
         }
     }
 }
 
-/* Pass 1's extremes pass (lane per run, after the run pass and the suffix
- * rows): turns each run's (node, K_closed) into the metadata the key stream
- * reads — meta_u = node | wide << 31, meta_K = Kb = K_closed + the row minimum
- * (keys = Kb + the node's offsets) — and reduces the range's extremes from the
- * rows' extremes (min/argmin, max/argmax, smallest index on ties, reading
- * L12; range-edge runs key by key).  out = {extremes, n_lt = n_eq = 0, n_gt =
- * evaluated = count} (pass 2 adds the counts). */
-__global__ void __launch_bounds__(kDpThreads) rk_dp_meta_kernel(DPView v, uint64_t first, uint64_t count,
-                                                               uint32_t* meta_u, uint64_t* meta_K, rk_stats* out,
-                                                               rk_stats* recs, uint32_t* counter) {
+/* Pass 1's extremes (after the run pass and the suffix rows): the range's
+ * min/argmin and max/argmax (smallest index on ties, reading L12) from the
+ * row multiset — a distinct row (node, K_closed) of multiplicity m whose
+ * smallest run is r has its minimum K_closed + row min at index
+ * (rb + r) * D! + row argmin, likewise the maximum — plus the run list (range
+ * edges key by key, probe overflows whole), or every run without a multiset.
+ * out = {extremes, n_lt = n_eq = 0, n_gt = evaluated = count} (pass 2 adds the
+ * counts). */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_ext_kernel(DPView v, uint64_t first, uint64_t count, RowSet rs,
+                                                              const uint32_t* __restrict__ meta_u,
+                                                              const uint64_t* __restrict__ meta_K, rk_stats* out,
+                                                              rk_stats* recs, uint32_t* counter) {
     constexpr uint32_t DF = kDF;
     const uint64_t lo = first, hi = first + count;
     const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
+    const bool direct = rs.slot == nullptr;
+    const uint64_t nitems = direct ? re - rb : (uint64_t)rs.mask + 1u + *rs.nlist;
     uint64_t kmin = ~0ull, kmax = 0, amin = ~0ull, amax = ~0ull, cnt = 0;
-    for (uint64_t run = rb + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; run < re;
-         run += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = meta_u[run - rb];
-        const uint64_t Kc = meta_K[run - rb];
-        const uint64_t idx0 = run * DF;
+    auto whole_row = [&](uint32_t u, uint64_t Kc, uint64_t r, uint64_t orders) {
+        const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u));     /* min, max */
+        const ulonglong2 ai = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u) + 1); /* argmin, argmax */
+        const uint64_t idx0 = (rb + r) * DF, K0 = Kc + mm.x, K1 = Kc + mm.y, am = idx0 + ai.x, ax = idx0 + ai.y;
+        if (lex_less(K0, am, kmin, amin)) { kmin = K0; amin = am; }
+        if (K1 > kmax || (K1 == kmax && ax < amax)) { kmax = K1; amax = ax; }
+        cnt += orders;
+    };
+    for (uint64_t it = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; it < nitems;
+         it += (uint64_t)gridDim.x * blockDim.x) {
+        if (!direct && it <= rs.mask) { /* a distinct row */
+            const uint4 key = rs.slot[it];
+            if (!key.y) continue;
+            const uint4* ms = reinterpret_cast<const uint4*>(rs.mult + it * kMultShards);
+            const uint4 a0 = ms[0], a1 = ms[1];
+            const uint32_t m = a0.x + a0.y + a0.z + a0.w + a1.x + a1.y + a1.z + a1.w;
+            whole_row(key.x, ((uint64_t)key.w << 32) | key.z, rs.minrun[it], (uint64_t)m * DF);
+            continue;
+        }
+        const uint32_t off = direct ? (uint32_t)it : rs.list[it - rs.mask - 1u];
+        const uint32_t u = __ldg(meta_u + off);
+        const uint64_t Kc = __ldg(meta_K + off), idx0 = (rb + off) * DF;
         const uint32_t olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
         const uint32_t ohi = hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF;
-        const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u)); /* min, max */
-        const uint64_t Kb = Kc + mm.x;
-        const bool wide = (__ldg(v.nd + u) >> 31) != 0;
-        const uint32_t uw = u | (wide ? 0x80000000u : 0u);
-        meta_u[run - rb] = uw;
-        meta_K[run - rb] = Kb;
-        const bool whole = olo == 0 && ohi == DF;
-        if (whole) {
-            const ulonglong2 ai = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u) + 1); /* argmin, argmax */
-            const uint64_t Kx = Kc + mm.y, am = idx0 + ai.x, ax = idx0 + ai.y;
-            if (lex_less(Kb, am, kmin, amin)) { kmin = Kb; amin = am; }
-            if (Kx > kmax || (Kx == kmax && ax < amax)) { kmax = Kx; amax = ax; }
-            cnt += DF;
+        if (olo == 0 && ohi == DF) {
+            whole_row(u, Kc, off, DF);
         } else { /* range-edge run (at most two per range): key by key */
+            const uint64_t Kb = Kc + __ldg(v.fst + 4ull * u);
+            const bool wide = (__ldg(v.nd + u) >> 31) != 0;
             for (uint32_t q = olo; q < ohi; q++) {
                 const uint64_t K = dp_key(v, u, wide, Kc, Kb, q), ix = idx0 + q;
                 if (lex_less(K, ix, kmin, amin)) { kmin = K; amin = ix; }
@@ -2549,7 +2566,8 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
                 const uint32_t off = direct ? (uint32_t)it : rs.list[it - rs.mask - 1u];
                 const uint64_t idx0 = (rb + off) * DF;
                 m = 1u;
-                do_row(__ldg(meta_u + off) & 0x7FFFFFFFu, __ldg(meta_K + off), 1u,
+                const uint32_t u = __ldg(meta_u + off); /* the run pass's (node, K_closed) */
+                do_row(u, __ldg(meta_K + off) + __ldg(v.fst + 4ull * u), 1u,
                        lo > idx0 ? (uint32_t)(lo - idx0) : 0u, hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF);
             }
         }
@@ -2616,8 +2634,14 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
     if (base >= re) return;
     const uint32_t nr = (uint32_t)min((uint64_t)kKeyRunsPerWarp, re - base);
     /* the warp's runs: lane r loads run r's metadata, each step broadcasts two */
-    const uint32_t umy = lane < nr ? __ldg(meta_u + (base - rb + lane)) : 0u;
-    const uint64_t Kmy = lane < nr ? __ldg(meta_K + (base - rb + lane)) : 0ull;
+    /* lane r < nr: run r's (node, K_closed) -> node | wide << 31 and Kb = K_closed + row min */
+    uint32_t umy = 0u;
+    uint64_t Kmy = 0ull;
+    if (lane < nr) {
+        const uint32_t u = __ldg(meta_u + (base - rb + lane));
+        Kmy = __ldg(meta_K + (base - rb + lane)) + __ldg(v.fst + 4ull * u);
+        umy = u | (__ldg(v.nd + u) & 0x80000000u);
+    }
     const bool whole = base * DF >= lo && (base + nr) * DF <= hi; /* no range-edge run among them */
     uint64_t* const o0 = keys + (base * DF - lo);
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15u) == 0; /* DF even: every step block alike */
@@ -2714,8 +2738,13 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys32_kernel(DPView v, uint
     const uint64_t base = rb + (uint64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW;
     if (base >= re) return;
     const uint32_t nr = (uint32_t)min((uint64_t)RPW, re - base);
-    const uint32_t umy = lane < nr ? __ldg(meta_u + (base - rb + lane)) : 0u;
-    const uint64_t Kmy = lane < nr ? __ldg(meta_K + (base - rb + lane)) : 0ull;
+    uint32_t umy = 0u; /* lane r < nr: run r's node | wide << 31 and Kb = K_closed + row min */
+    uint64_t Kmy = 0ull;
+    if (lane < nr) {
+        const uint32_t u = __ldg(meta_u + (base - rb + lane));
+        Kmy = __ldg(meta_K + (base - rb + lane)) + __ldg(v.fst + 4ull * u);
+        umy = u | (__ldg(v.nd + u) & 0x80000000u);
+    }
     const bool whole = base * DF >= lo && (base + nr) * DF <= hi;
     uint32_t* const o0 = keys + (base * DF - lo);
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15u) == 0; /* DF % 4 == 0: every run block alike */
@@ -3251,7 +3280,7 @@ ExpArgs exp_args(const RkExpand* ex) {
 
 namespace {
 RowSet row_set(const RkRows& r) {
-    return RowSet{(uint4*)r.slot, r.mult, r.mask, r.list, r.nlist};
+    return RowSet{(uint4*)r.slot, r.mult, r.mask, r.list, r.nlist, r.minrun};
 }
 }  // namespace
 
@@ -3265,13 +3294,15 @@ int rk_dp_runs(const RkTables* tab, const DPView& v, uint64_t first, uint64_t co
     return (int)cudaGetLastError();
 }
 
-int rk_dp_meta(const DPView& v, uint64_t first, uint64_t count, uint32_t* meta_u, uint64_t* meta_K, rk_stats* out,
-               rk_stats* recs, uint32_t* counter, uint32_t max_ctas, void* stream, uint32_t* launches) {
+int rk_dp_ext(const DPView& v, uint64_t first, uint64_t count, const RkRows& rows, const uint32_t* meta_u,
+              const uint64_t* meta_K, rk_stats* out, rk_stats* recs, uint32_t* counter, uint32_t max_ctas,
+              void* stream, uint32_t* launches) {
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
-    unsigned grid = dp_grid_wave(runs, rk_dp_meta_kernel, 0);
+    const uint64_t items = rows.slot ? (uint64_t)rows.mask + 1u + rows.list_hint / 64u : runs;
+    unsigned grid = dp_grid_wave(items, rk_dp_ext_kernel, 0);
     if (grid > max_ctas) grid = max_ctas;
-    rk_dp_meta_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(v, first, count, meta_u, meta_K, out, recs,
-                                                                     counter);
+    rk_dp_ext_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(v, first, count, row_set(rows), meta_u, meta_K, out,
+                                                                    recs, counter);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
