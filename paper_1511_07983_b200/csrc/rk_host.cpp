@@ -68,6 +68,9 @@ struct DpPlan {
     Arena expand;                                /* the range's prefix expansion, levels 1..P-1 (level P recomputed) */
     Arena meta_u, meta_K;                        /* the range's run metadata for the key stream: node | wide, Kb */
     Arena rslot, rmult, rlist, rminrun;          /* the range's row multiset (distinct (node, K_closed), multiplicity, first run) */
+    Arena rwlist, rwminrun;                      /* its weighted rows without a slot */
+    Arena pslot, pmult, pminrun;                 /* the parent multiset (level P-1 prefixes) */
+    uint32_t pmask = 0;
     uint32_t rmask = 0;                          /* its slots - 1 */
     bool runs_ok = false;                        /* meta_u/meta_K hold the range [runs_first, +runs_count) */
     uint64_t runs_first = 0, runs_count = 0;
@@ -506,7 +509,7 @@ void dp_free(DpPlan& d) {
     d.dk.release();
     d.fst.release();
     d.counters.release();
-    for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.row24, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist, &d.rminrun}) a->release();
+    for (Arena* a : {&d.code, &d.dvc, &d.dvp, &d.nd, &d.offs, &d.row24, &d.expand, &d.meta_u, &d.meta_K, &d.rslot, &d.rmult, &d.rlist, &d.rminrun, &d.rwlist, &d.rwminrun, &d.pslot, &d.pmult, &d.pminrun}) a->release();
     d.runs_ok = false;
     d.on = false;
 }
@@ -544,7 +547,7 @@ int dp_build_levels(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = n
     DpPlan& d = c->dp;
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
-    if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.L + 3) * 4, st); /* + the overflow flag, the row list counter */
+    if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.L + 4) * 4, st); /* + the overflow flag, the row list counters */
     if (!e) e = dp_levels(c, 0, d.L, stream, ex);
     return e;
 }
@@ -733,7 +736,8 @@ const uint64_t* cand_or_zero(rk_ctx* c, const uint64_t* cand_dev, void* stream) 
 RkRows dp_rows(rk_ctx* c, uint64_t nrun) {
     DpPlan& d = c->dp;
     return RkRows{c->dedup_now ? d.rslot.p : nullptr, (uint32_t*)d.rmult.p, d.rmask, (uint32_t*)d.rlist.p,
-                  (uint32_t*)d.counters.p + d.L + 2, nrun, (uint32_t*)d.rminrun.p};
+                  (uint32_t*)d.counters.p + d.L + 2, nrun, (uint32_t*)d.rminrun.p, d.rwlist.p, (uint32_t*)d.rwminrun.p,
+                  (uint32_t*)d.counters.p + d.L + 3};
 }
 
 /* Pass 1 of the memoised step: the levels rebuilt from scratch with the
@@ -762,6 +766,8 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e) e = d.rmult.reserve(slots * 4 * 8); /* 8 counters per slot */
     if (!e) e = d.rlist.reserve(nrun * 4);
     if (!e) e = d.rminrun.reserve(slots * 4);
+    if (!e) e = d.rwlist.reserve(nrun * 16);
+    if (!e) e = d.rwminrun.reserve(nrun * 4);
     c->dedup_now = c->row_dedup != 0;
     const bool side = c->overlap != 0;
     if (!e && side) e = ensure_side(c);
@@ -788,7 +794,22 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
             prev = dst;
         }
     }
+    /* the multiset from the stored level-(P-1) prefixes (parents, then children) when the range was expanded,
+     * else run by run in the run pass */
+    const bool hier = c->dedup_now && !ex.empty() && P >= 2;
+    uint64_t pslots = 0;
+    if (hier) {
+        const uint64_t npar = ex.back().cnt ? (re - 1) / (n - P + 1) - ex.back().aj + 1 : 1;
+        pslots = std::min<uint64_t>(std::max<uint64_t>(pow2_at_least(npar / 4), 4096), 1ull << 22);
+        d.pmask = (uint32_t)(pslots - 1);
+        if (!e) e = d.pslot.reserve(pslots * 16);
+        if (!e) e = d.pmult.reserve(pslots * 32);
+        if (!e) e = d.pminrun.reserve(pslots * 4);
+    }
     const int m0 = tmark_begin(c, RK_PHASE_TABLES, stream);
+    if (!e && hier) e = cudaMemsetAsync(d.pslot.p, 0, pslots * 16, st);
+    if (!e && hier) e = cudaMemsetAsync(d.pmult.p, 0, pslots * 32, st);
+    if (!e && hier) e = cudaMemsetAsync(d.pminrun.p, 0xFF, pslots * 4, st);
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, st);
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, st);
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rminrun.p, 0xFF, slots * 4, st);
@@ -797,9 +818,19 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e && side) e = cudaEventRecord(c->ev_fork, st);
     if (!e && side) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
     const int mr = tmark_begin(c, RK_PHASE_RUNS, rs);
+    RkRows runrows = dp_rows(c, re - rb);
+    if (hier) runrows.slot = nullptr; /* the run pass writes the run metadata only */
     if (!e)
-        e = rk_dp_runs(c->tab_dev, d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p,
-                       dp_rows(c, re - rb), ex.empty() ? nullptr : &ex.back(), rs, &c->launches);
+        e = rk_dp_runs(c->tab_dev, d.view, first, count, (uint32_t*)d.meta_u.p, (uint64_t*)d.meta_K.p, runrows,
+                       ex.empty() ? nullptr : &ex.back(), rs, &c->launches);
+    if (!e && hier) {
+        const RkExpand& lx = ex.back();
+        RkExpand parent_level = lx;
+        parent_level.Rj = ex[P - 1].Rj; /* the stored level-(P-1) prefixes */
+        const RkRows parents{d.pslot.p, (uint32_t*)d.pmult.p, d.pmask, nullptr, nullptr, 0, (uint32_t*)d.pminrun.p,
+                             nullptr, nullptr, nullptr};
+        e = rk_dp_multiset(n, first, count, &parent_level, parents, dp_rows(c, re - rb), rs, &c->launches);
+    }
     tmark_end(c, mr, rs);
     if (!e && side) e = cudaEventRecord(c->ev_join, c->side);
     if (!e) e = dp_build_suffix(c, stream);

@@ -154,7 +154,14 @@ struct RkRows {
     uint32_t* nlist;
     uint64_t list_hint;
     uint32_t* minrun; /* per slot: smallest run offset of the row (0xFFFFFFFF before pass 1) */
+    void* wlist;       /* weighted rows that found no slot: uint4 {node, m, K_closed lo, hi} */
+    uint32_t* wminrun; /* their smallest run offsets */
+    uint32_t* nwlist;  /* device counter (zeroed before pass 1) */
 };
+/* the row multiset from the range's last stored expansion level (lastexp: level P-1 -> P, its Rj = the level-(P-1)
+ * prefixes): parents multiset, then the children into rows (both zeroed before; minrun 0xFF) */
+int rk_dp_multiset(uint32_t n, uint64_t first, uint64_t count, const RkExpand* lastexp, const RkRows& parents,
+                   const RkRows& rows, void* stream, uint32_t* launches);
 /* pass 1's run pass: per run of the range its (node, K_closed) into meta_u /
  * meta_K, and the row multiset (rows.slot nullable); last = the range's level
  * P-1 -> P expansion (nullptr: walk).  Needs the levels only (runs beside the

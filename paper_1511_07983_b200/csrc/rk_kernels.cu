@@ -2303,6 +2303,9 @@ struct RowSet {
     uint32_t* list;    /* run offsets from rb */
     uint32_t* nlist;   /* device counter */
     uint32_t* minrun;  /* per slot: the smallest run offset (from rb) in the row (argmin/argmax) */
+    uint4* wlist;      /* weighted rows that found no slot: {node, m, K_closed lo, hi} */
+    uint32_t* wminrun; /* their smallest run offsets */
+    uint32_t* nwlist;  /* device counter */
 };
 __device__ __forceinline__ uint32_t row_hash(uint32_t uw, uint64_t Kb) {
     uint64_t h = (Kb ^ ((uint64_t)uw << 40) ^ uw) * 0x9E3779B97F4A7C15ull;
@@ -2316,14 +2319,15 @@ __device__ __forceinline__ void cas128(uint4* p, uint64_t v0, uint64_t v1, uint6
                  : "l"(z), "l"(v0), "l"(v1), "l"(p)
                  : "memory");
 }
-__device__ __forceinline__ bool row_insert(const RowSet& rs, uint32_t uw, uint64_t Kb, uint32_t off) {
-    const uint64_t k0 = (uint64_t)uw | (1ull << 32), k1 = Kb; /* little-endian {uw, 1, Kb lo, Kb hi} */
+__device__ __forceinline__ bool row_insert(const RowSet& rs, uint32_t uw, uint64_t Kb, uint32_t off,
+                                           uint32_t w = 1u, uint32_t tag = 1u) {
+    const uint64_t k0 = (uint64_t)uw | ((uint64_t)tag << 32), k1 = Kb; /* little-endian {uw, tag != 0, Kb lo, hi} */
     uint32_t h = row_hash(uw, Kb) & rs.mask;
     for (uint32_t p = 0; p < kRowProbes; p++, h = (h + 1u) & rs.mask) {
         uint64_t o0, o1;
         cas128(rs.slot + h, k0, k1, o0, o1);
         if ((o0 == 0 && o1 == 0) || (o0 == k0 && o1 == k1)) { /* claimed, or already this row */
-            atomicAdd(rs.mult + (uint64_t)h * kMultShards + (blockIdx.x & (kMultShards - 1u)), 1u);
+            atomicAdd(rs.mult + (uint64_t)h * kMultShards + (blockIdx.x & (kMultShards - 1u)), w);
             /* runs arrive roughly in index order: test first, so a heavy row's later runs
              * (C4: up to 11,056 per row) do not serialise on one address */
             if (off < __ldcg(rs.minrun + h)) atomicMin(rs.minrun + h, off);
@@ -2364,6 +2368,62 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_runs_kernel(const RkTables* 
     }
 }
 
+/* The row multiset without a pass over every run (the range's prefixes are
+ * expanded breadth-first, level P-1 stored): (1) rk_dp_parents_kernel
+ * collapses the level-(P-1) prefixes whose D' = n - P + 1 child runs are all
+ * whole runs of the range into a parent multiset of distinct (node, K_closed)
+ * (C4: 665,280 prefixes -> ~10^5 distinct pairs; the node's used mask rides in
+ * the slot's tag word); their other runs go to the run list.  (2)
+ * rk_dp_children_kernel expands every distinct parent by its D' unused kernels
+ * through the level-(P-1) transitions into the row multiset with the parent's
+ * multiplicity, and the child run of its smallest parent (offset
+ * (parent * D' + d) - rb) as the row's smallest run; a row that finds no slot
+ * goes to the weighted list. */
+__global__ void __launch_bounds__(kDpThreads) rk_dp_parents_kernel(ExpArgs xp, uint32_t n, uint64_t first,
+                                                                  uint64_t count, RowSet ps, RowSet rs) {
+    constexpr uint32_t DF = kDF;
+    const uint64_t lo = first, hi = first + count;
+    const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
+    const uint32_t D1 = n - xp.j;
+    const uint64_t npar = (re - 1) / D1 - xp.aj + 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < npar;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = xp.aj + i, r0 = p * D1, r1 = r0 + D1;
+        const bool whole = r0 * DF >= lo && r1 * DF <= hi;
+        if (whole) {
+            const uint4 e = __ldg(xp.Rj + i);
+            if (row_insert(ps, e.x, ((uint64_t)e.w << 32) | e.z, (uint32_t)i, 1u, e.y | 0x80000000u)) continue;
+        }
+        for (uint64_t r = max(r0, rb); r < min(r1, re); r++) rs.list[atomicAdd(rs.nlist, 1u)] = (uint32_t)(r - rb);
+    }
+}
+
+__global__ void __launch_bounds__(kDpThreads) rk_dp_children_kernel(ExpArgs xp, uint32_t n, uint64_t rb, RowSet ps,
+                                                                   RowSet rs) {
+    const uint32_t D1 = n - xp.j, full = (1u << n) - 1u;
+    const uint64_t items = ((uint64_t)ps.mask + 1u) * D1;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < items;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = x / D1;
+        const uint32_t d = (uint32_t)(x - i * D1);
+        const uint4 key = ps.slot[i];
+        if (!key.y) continue;
+        const uint4* ms = reinterpret_cast<const uint4*>(ps.mult + i * kMultShards);
+        const uint4 a0 = ms[0], a1 = ms[1];
+        const uint32_t m = a0.x + a0.y + a0.z + a0.w + a1.x + a1.y + a1.z + a1.w;
+        const uint32_t k = nth_set_bit(full & ~(key.y & 0xFFFFu), d);
+        const uint32_t c = key.x * n + k;
+        const uint32_t u = __ldg(xp.tid + c);
+        const uint64_t Kc = (((uint64_t)key.w << 32) | key.z) + __ldg(xp.dk + c);
+        const uint32_t off = (uint32_t)((xp.aj + ps.minrun[i]) * D1 + d - rb);
+        if (!row_insert(rs, u, Kc, off, m)) {
+            const uint32_t q = atomicAdd(rs.nwlist, 1u);
+            rs.wlist[q] = make_uint4(u, m, (uint32_t)Kc, (uint32_t)(Kc >> 32));
+            rs.wminrun[q] = off;
+        }
+    }
+}
+
 /* Pass 1's extremes (after the run pass and the suffix rows): the range's
  * min/argmin and max/argmax (smallest index on ties, reading L12) from the
  * row multiset — a distinct row (node, K_closed) of multiplicity m whose
@@ -2380,7 +2440,8 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_ext_kernel(DPView v, uint64_
     const uint64_t lo = first, hi = first + count;
     const uint64_t rb = lo / DF, re = (hi + DF - 1) / DF;
     const bool direct = rs.slot == nullptr;
-    const uint64_t nitems = direct ? re - rb : (uint64_t)rs.mask + 1u + *rs.nlist;
+    const uint64_t nslot = direct ? 0u : (uint64_t)rs.mask + 1u, nl = direct ? re - rb : *rs.nlist;
+    const uint64_t nitems = nslot + nl + (direct ? 0u : *rs.nwlist);
     uint64_t kmin = ~0ull, kmax = 0, amin = ~0ull, amax = ~0ull, cnt = 0;
     auto whole_row = [&](uint32_t u, uint64_t Kc, uint64_t r, uint64_t orders) {
         const ulonglong2 mm = __ldg(reinterpret_cast<const ulonglong2*>(v.fst + 4ull * u));     /* min, max */
@@ -2392,7 +2453,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_ext_kernel(DPView v, uint64_
     };
     for (uint64_t it = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; it < nitems;
          it += (uint64_t)gridDim.x * blockDim.x) {
-        if (!direct && it <= rs.mask) { /* a distinct row */
+        if (it < nslot) { /* a distinct row */
             const uint4 key = rs.slot[it];
             if (!key.y) continue;
             const uint4* ms = reinterpret_cast<const uint4*>(rs.mult + it * kMultShards);
@@ -2401,7 +2462,12 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_ext_kernel(DPView v, uint64_
             whole_row(key.x, ((uint64_t)key.w << 32) | key.z, rs.minrun[it], (uint64_t)m * DF);
             continue;
         }
-        const uint32_t off = direct ? (uint32_t)it : rs.list[it - rs.mask - 1u];
+        if (it >= nslot + nl) { /* a weighted row without a slot */
+            const uint4 e = rs.wlist[it - nslot - nl];
+            whole_row(e.x, ((uint64_t)e.w << 32) | e.z, rs.wminrun[it - nslot - nl], (uint64_t)e.y * DF);
+            continue;
+        }
+        const uint32_t off = direct ? (uint32_t)it : rs.list[it - nslot];
         const uint32_t u = __ldg(meta_u + off);
         const uint64_t Kc = __ldg(meta_K + off), idx0 = (rb + off) * DF;
         const uint32_t olo = lo > idx0 ? (uint32_t)(lo - idx0) : 0u;
@@ -2476,7 +2542,8 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
     const uint64_t rb = lo / DF;
     const bool direct = rs.slot == nullptr; /* no multiset: every run of the range is an item */
     const uint64_t nrun = (hi + DF - 1) / DF - rb;
-    const uint64_t nitems = direct ? nrun : (uint64_t)rs.mask + 1u + *rs.nlist;
+    const uint64_t nslot = direct ? 0u : (uint64_t)rs.mask + 1u, nl = direct ? nrun : *rs.nlist;
+    const uint64_t nitems = nslot + nl + (direct ? 0u : *rs.nwlist);
     uint64_t nlt = 0, neq = 0;
     uint32_t iter = 0, pass = 0;
     /* one row (node u, Kb) of weight m; range-edge rows key by key over [olo, ohi) */
@@ -2553,7 +2620,11 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
         const uint64_t it = bbase + threadIdx.x;
         uint32_t m = 0;
         if (it < nitems) {
-            if (!direct && it <= rs.mask) { /* a distinct row (node, Kb) of multiplicity m */
+            if (it >= nslot + nl) { /* a weighted row without a slot */
+                const uint4 e = rs.wlist[it - nslot - nl];
+                m = e.y;
+                do_row(e.x, (((uint64_t)e.w << 32) | e.z) + __ldg(v.fst + 4ull * e.x), m, 0u, DF);
+            } else if (it < nslot) { /* a distinct row (node, K_closed) of multiplicity m */
                 const uint4 key = rs.slot[it];
                 if (key.y) {
                     const uint4* ms = reinterpret_cast<const uint4*>(rs.mult + it * kMultShards);
@@ -2563,7 +2634,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
                     do_row(u, (((uint64_t)key.w << 32) | key.z) + __ldg(v.fst + 4ull * u), m, 0u, DF);
                 }
             } else { /* a run: listed, or every run (direct) */
-                const uint32_t off = direct ? (uint32_t)it : rs.list[it - rs.mask - 1u];
+                const uint32_t off = direct ? (uint32_t)it : rs.list[it - nslot];
                 const uint64_t idx0 = (rb + off) * DF;
                 m = 1u;
                 const uint32_t u = __ldg(meta_u + off); /* the run pass's (node, K_closed) */
@@ -3280,7 +3351,7 @@ ExpArgs exp_args(const RkExpand* ex) {
 
 namespace {
 RowSet row_set(const RkRows& r) {
-    return RowSet{(uint4*)r.slot, r.mult, r.mask, r.list, r.nlist, r.minrun};
+    return RowSet{(uint4*)r.slot, r.mult, r.mask, r.list, r.nlist, r.minrun, (uint4*)r.wlist, r.wminrun, r.nwlist};
 }
 }  // namespace
 
@@ -3290,6 +3361,24 @@ int rk_dp_runs(const RkTables* tab, const DPView& v, uint64_t first, uint64_t co
     const unsigned grid = dp_grid_wave(runs, rk_dp_runs_kernel, 0);
     rk_dp_runs_kernel<<<grid, kDpThreads, 0, (cudaStream_t)stream>>>(tab, v, first, count, meta_u, meta_K,
                                                                      row_set(rows), exp_args(last));
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+int rk_dp_multiset(uint32_t n, uint64_t first, uint64_t count, const RkExpand* lastexp, const RkRows& parents,
+                   const RkRows& rows, void* stream, uint32_t* launches) {
+    const ExpArgs xp = exp_args(lastexp);
+    const uint32_t D1 = n - xp.j;
+    const uint64_t rb = first / kDF, re = (first + count + kDF - 1) / kDF;
+    const uint64_t npar = (re - 1) / D1 - xp.aj + 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    rk_dp_parents_kernel<<<dp_grid_wave(npar, rk_dp_parents_kernel, 0), kDpThreads, 0, st>>>(
+        xp, n, first, count, row_set(parents), row_set(rows));
+    if (launches) (*launches)++;
+    int e = (int)cudaGetLastError();
+    if (e) return e;
+    rk_dp_children_kernel<<<dp_grid_wave(((uint64_t)parents.mask + 1u) * D1, rk_dp_children_kernel, 0), kDpThreads, 0,
+                            st>>>(xp, n, rb, row_set(parents), row_set(rows));
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
