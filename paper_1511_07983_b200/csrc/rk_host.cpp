@@ -543,12 +543,12 @@ int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vect
 /* Enqueue the level build of the current plan: clear, P levels (+ the given
  * prefix expansions, level j-1 -> j in level j's launch; the last one runs in
  * the run pass). */
-int dp_build_levels(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr) {
+int dp_build_levels(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = nullptr, uint32_t upto = ~0u) {
     DpPlan& d = c->dp;
     cudaStream_t st = (cudaStream_t)stream;
     int e = cudaMemsetAsync(d.tables.p, 0xFF, d.table_slots * 4, st);
     if (!e) e = cudaMemsetAsync(d.counters.p, 0, (d.L + 4) * 4, st); /* + the overflow flag, the row list counters */
-    if (!e) e = dp_levels(c, 0, d.L, stream, ex);
+    if (!e) e = dp_levels(c, 0, std::min(upto, d.L), stream, ex);
     return e;
 }
 
@@ -813,10 +813,13 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rslot.p, 0, slots * 16, st);
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rmult.p, 0, slots * 32, st);
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rminrun.p, 0xFF, slots * 4, st);
-    if (!e) e = dp_build_levels(c, stream, ex.empty() ? nullptr : &ex);
+    /* levels 0..P-1 (the run level's transitions and the range's expansions), then the run pass and the
+     * multiset fork off beside the last level (P+1, for the suffix rows), row24 and the suffix rows */
+    if (!e) e = dp_build_levels(c, stream, ex.empty() ? nullptr : &ex, P);
     void* rs = side ? (void*)c->side : stream;
     if (!e && side) e = cudaEventRecord(c->ev_fork, st);
     if (!e && side) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    if (!e && !side) e = dp_levels(c, P, d.L, stream, nullptr);
     const int mr = tmark_begin(c, RK_PHASE_RUNS, rs);
     RkRows runrows = dp_rows(c, re - rb);
     if (hier) runrows.slot = nullptr; /* the run pass writes the run metadata only */
@@ -833,6 +836,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     }
     tmark_end(c, mr, rs);
     if (!e && side) e = cudaEventRecord(c->ev_join, c->side);
+    if (!e && side) e = dp_levels(c, P, d.L, stream, nullptr);
     if (!e) e = dp_build_suffix(c, stream);
     tmark_end(c, m0, stream);
     if (!e && side) e = cudaStreamWaitEvent(st, c->ev_join, 0);
