@@ -96,6 +96,9 @@ class Sweeper:
             self.compact = True
             if self.keys32 is None or self.keys32.numel() < self.count:
                 self.keys32 = torch.empty(max(1, self.count), dtype=torch.int32, device=self.dev)
+            # the u64 buffer a set whose keys overflow the offsets falls back to, allocated up front
+            if self.keys is None or self.keys.numel() < self.count:
+                self.keys = torch.empty(max(1, self.count), dtype=torch.int64, device=self.dev)
         else:
             self._use_wide_keys()
 
@@ -188,10 +191,14 @@ class Sweeper:
         self.set_kernels(kernels)
         order, idx = self.heuristic()
         self.step_device(idx)
-        if self.compact and self.overflowed():  # rare: keys span >= 2^32 above the bound
-            self._use_wide_keys()
+        # one D2H: record, candidate key, histogram and the compact-key overflow flag (with one rank the flag
+        # is final; with N ranks the memoised pass decides it from the global range, the direct one per rank)
+        out = torch.cat([self.record, self.cand, self.hist, self.ovf.to(torch.int64)]).cpu()
+        if self.compact and (self.overflowed() if self.world > 1 else bool(out[-1].item())):
+            self._use_wide_keys()  # rare: keys span >= 2^32 above the bound
             self.step_device(idx)
-        out = torch.cat([self.record, self.cand, self.hist]).cpu()
+            out = torch.cat([self.record, self.cand, self.hist, self.ovf.to(torch.int64)]).cpu()
+        out = out[:-1]
         st = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(out[:REC_WORDS].numpy().tobytes()))
         rep = Report(n_orders=self.total, best_key=st.key_min, best_index=st.argmin, worst_key=st.key_max,
                      worst_index=st.argmax, cand_order=order, cand_index=idx,
@@ -226,4 +233,4 @@ class Sweeper:
 
     @property
     def d2h_bytes(self) -> int:
-        return 8 * (REC_WORDS + 1 + self.bins)
+        return 8 * (REC_WORDS + 1 + self.bins + 1)  # record, candidate key, histogram, overflow flag
