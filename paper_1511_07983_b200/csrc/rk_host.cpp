@@ -534,8 +534,8 @@ int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vect
         const RkExpand* x = (ex && j >= 1 && j < d.P && j - 1 < ex->size()) ? &(*ex)[j - 1] : nullptr;
         e = rk_dp_level(c->tab_dev, S, Uj, j ? ctr + j : nullptr, nodes + d.noff[j + 1], ctr + j + 1, d.cap[j + 1],
                         (uint32_t*)d.tables.p + d.toff[j + 1], d.tmask[j + 1], (uint32_t*)d.tid.p + d.xoff[j],
-                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.L + 1, d.work[j], stream, &c->launches,
-                        x);
+                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.L + 1, d.work[j] / n * (n - j), stream,
+                        &c->launches, x, n - j);
     }
     return e;
 }
@@ -1241,7 +1241,8 @@ rk_status rk_memo_audit(rk_ctx* c, uint64_t* out) {
     const char* nodes = (const char*)d.nodes.p;
     for (uint32_t j = 1; j <= d.L && !e; j++)
         e = rk_dp_audit(c->tab.g.S, nodes + d.noff[j], (const uint32_t*)d.counters.p + j, d.cap[j],
-                        (const uint32_t*)d.tables.p + d.toff[j], d.tmask[j], d.view.tid[j - 1], d.work[j - 1],
+                        (const uint32_t*)d.tables.p + d.toff[j], d.tmask[j], d.view.tid[j - 1],
+                        (uint64_t)d.cnt[j - 1] * c->tab.g.n, j > 1 ? nodes + d.noff[j - 1] : nullptr, c->tab.g.n,
                         bad + 6 * (j - 1), nullptr);
     if (!e) e = cudaMemcpy(h.data(), bad, sizeof(unsigned long long) * 6 * d.L, cudaMemcpyDeviceToHost);
     if (!e) e = cudaMemcpy(cnt.data(), d.counters.p, 4 * (d.L + 1), cudaMemcpyDeviceToHost);

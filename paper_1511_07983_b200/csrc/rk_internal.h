@@ -128,7 +128,7 @@ struct RkExpand {
 };
 int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
                 uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
-                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex = nullptr);
+                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex = nullptr, uint32_t nrem = 0);
 /* the 24 suffix keys of every level-(P+1) node (row24: nodes x 24 u64) */
 int rk_dp_row24(const RkTables* tab, uint32_t S, const void* U, const uint32_t* cnt, uint64_t* row24, uint64_t nodes,
                 void* stream, uint32_t* launches);
@@ -140,7 +140,8 @@ uint32_t rk_dp_max_fused_bins();
 /* race audit of level (U, cnt) and its hash table + the previous level's
  * transitions; bad = 6 zeroed u64 counters (rk_dp_audit_kernel) */
 int rk_dp_audit(uint32_t S, const void* U, const uint32_t* cnt, uint32_t cap, const uint32_t* table, uint32_t tmask,
-                const uint32_t* tid_prev, uint64_t work_prev, unsigned long long* bad, void* stream);
+                const uint32_t* tid_prev, uint64_t work_prev, const void* Uprev, uint32_t n, unsigned long long* bad,
+                void* stream);
 /* a range's row multiset: 16-B open-addressing slots of the
  * distinct rows (node | wide << 31, Kb) with 8 multiplicity counters each;
  * slot (nullptr: none) and mult must be zeroed and *nlist = 0 before pass 1;

@@ -1927,11 +1927,12 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
                                                                 const uint32_t* __restrict__ cnt_j, DNode<SMAX>* Un,
                                                                 uint32_t* cnt_n, uint32_t cap_n, uint32_t* table,
                                                                 uint32_t tmask, uint32_t* __restrict__ tid,
-                                                                uint64_t* __restrict__ dk, uint32_t* ovf, ExpArgs xp) {
+                                                                uint64_t* __restrict__ dk, uint32_t* ovf, ExpArgs xp,
+                                                                uint32_t nrem) {
     __shared__ RkTables t;
     load_tables(t, tab);
     const RkGTab& g = t.g;
-    const uint32_t n = g.n;
+    const uint32_t n = g.n, full = (1u << n) - 1u;
     /* an overflowed level (capped planning capacities) stops every
      * later level: its count may exceed the nodes it stored */
     const uint32_t m = Uj ? (*(volatile uint32_t*)ovf ? 0u : *cnt_j) : 1u;
@@ -1939,15 +1940,15 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
     for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < xp.cnt;
          x += gridDim.x * (uint64_t)blockDim.x)
         expand_one(xp, x, n);
-    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < m * n; c += gridDim.x * blockDim.x) {
-        const uint32_t u = c / n, k = c - u * n;
+    /* one item per live child: node u of level j by its d-th unused kernel (every node of a level
+     * has nrem = n - j unused kernels); transitions stay at u * n + k, entries of used kernels are
+     * never read (nor written) */
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < m * nrem; w += gridDim.x * blockDim.x) {
+        const uint32_t u = w / nrem, d = w - u * nrem;
         DNode<SMAX> nd;
         if (Uj) nd = Uj[u];
         else dnode_fresh<SMAX, FULL>(nd, g);
-        if ((nd.mask >> k) & 1u) {
-            tid[c] = kDpEmpty;
-            continue;
-        }
+        const uint32_t k = nth_set_bit(full & ~nd.mask, d), c = u * n + k;
         St<SMAX> s, s2;
         node_to_st<SMAX>(nd, s);
         place<SMAX, FULL>(s, s2, t.k[k], k, g, nr);
@@ -2011,14 +2012,14 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
  * on this pool): bad[0] count over capacity, bad[1] slots left
  * BUSY (a claim never published), bad[2] published ids >= count, bad[3] nodes
  * whose probe from their own hash meets an EMPTY slot or another id with an
- * equal record first (lost publish / duplicate state), bad[4] transitions of
- * the previous level that are neither EMPTY (used kernel) nor < count, bad[5]
+ * equal record first (lost publish / duplicate state), bad[4] live
+ * transitions of the previous level (unused kernels) that are not < count, bad[5]
  * published slots (must equal the count). */
 template <int SMAX>
 __global__ void rk_dp_audit_kernel(const DNode<SMAX>* __restrict__ U, const uint32_t* cnt_p, uint32_t cap,
                                    const uint32_t* __restrict__ table, uint32_t tmask,
                                    const uint32_t* __restrict__ tid_prev, uint64_t work_prev,
-                                   unsigned long long* bad) {
+                                   const DNode<SMAX>* __restrict__ Uprev, uint32_t n, unsigned long long* bad) {
     const uint32_t cnt = *cnt_p, c = min(cnt, cap);
     const uint64_t gt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = gridDim.x * (uint64_t)blockDim.x;
     if (gt == 0 && cnt > cap) atomicAdd(bad + 0, 1ull);
@@ -2042,9 +2043,12 @@ __global__ void rk_dp_audit_kernel(const DNode<SMAX>* __restrict__ U, const uint
         }
         if (!ok) atomicAdd(bad + 3, 1ull);
     }
-    for (uint64_t i = gt; i < work_prev; i += nth) {
+    for (uint64_t i = gt; i < work_prev; i += nth) { /* live transitions (unused kernels) only */
+        const uint64_t u = i / n;
+        const uint32_t k = (uint32_t)(i - u * n);
+        if (Uprev && ((Uprev[u].mask >> k) & 1u)) continue;
         const uint32_t v = tid_prev[i];
-        if (v != kDpEmpty && v >= c) atomicAdd(bad + 4, 1ull);
+        if (v >= c) atomicAdd(bad + 4, 1ull);
     }
 }
 
@@ -3251,10 +3255,10 @@ uint32_t rk_dp_node_bytes(uint32_t S) {
 
 int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
                 uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
-                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex) {
+                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex, uint32_t nrem) {
     ExpArgs xp{};
     if (ex) xp = ExpArgs{(const uint4*)ex->Rj, ex->aj, (uint4*)ex->Rn, ex->an, ex->cnt, ex->j, ex->tid, ex->dk};
-#define RK_DP_LEVEL_ARGS(SMAX) tab, (const DNode<SMAX>*)Uj, cnt_j, (DNode<SMAX>*)Un, cnt_n, cap_n, table, tmask, tid, dk, ovf, xp
+#define RK_DP_LEVEL_ARGS(SMAX) tab, (const DNode<SMAX>*)Uj, cnt_j, (DNode<SMAX>*)Un, cnt_n, cap_n, table, tmask, tid, dk, ovf, xp, nrem
     const unsigned grid = dp_grid(work > xp.cnt ? work : xp.cnt);
     cudaStream_t st = (cudaStream_t)stream;
     switch (variant(S)) {
@@ -3276,8 +3280,10 @@ int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t*
 }
 
 int rk_dp_audit(uint32_t S, const void* U, const uint32_t* cnt, uint32_t cap, const uint32_t* table, uint32_t tmask,
-                const uint32_t* tid_prev, uint64_t work_prev, unsigned long long* bad, void* stream) {
-#define RK_DP_AUDIT_ARGS(SMAX) (const DNode<SMAX>*)U, cnt, cap, table, tmask, tid_prev, work_prev, bad
+                const uint32_t* tid_prev, uint64_t work_prev, const void* Uprev, uint32_t n, unsigned long long* bad,
+                void* stream) {
+#define RK_DP_AUDIT_ARGS(SMAX) (const DNode<SMAX>*)U, cnt, cap, table, tmask, tid_prev, work_prev, \
+                               (const DNode<SMAX>*)Uprev, n, bad
     cudaStream_t st = (cudaStream_t)stream;
     const unsigned grid = 4u * (unsigned)num_sms();
     switch (variant(S)) {
