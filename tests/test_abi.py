@@ -70,6 +70,8 @@ def test_host_only_ctx_refuses_compute():
     # the two-pass step, the optimum and the memo plan: no device, no evaluation
     for call in (lambda: c.rk_sweep_pass1_async(0, 24, None, None),
                  lambda: c.rk_sweep_pass2_async(0, 24, None, None, 4, None, None, None),
+                 lambda: c.rk_sweep_pass2_32_async(0, 24, None, None, 4, None, None, 0, None, None),
+                 lambda: c.rk_memo_audit(),
                  lambda: c.rk_best_order()):
         with pytest.raises(rk.RkError) as e:
             call()
@@ -188,3 +190,25 @@ def test_heuristic_host_unspecified_branches_hand_golden():
         order, round_of, idx, _ = c.rk_heuristic_order(with_key=False)
         assert (order, round_of) == (case["order"], case["round_of"]), case["name"]
         assert idx == rk.rk_rank(case["order"])
+
+
+def test_model_reading_flags_validation_and_policy_limits():
+    """rk_gpu_params.flags: the three f3 bits are accepted, any other bit is
+    RK_EINVAL; strict RR / skip-ahead with more than 32 super-SMs is refused at
+    rk_set_kernels (RK_EUNSUPPORTED) on host-only contexts too; Algorithm 1
+    (host) is independent of the reading."""
+    c = rk.Context(-1)
+    for f in (1, 2, 3, 4, 5, 6, 7):
+        c.rk_set_gpu_params(list(W.GTX580) + [f])
+        c.rk_set_kernels(W.W4)
+        assert c.rk_heuristic_order(with_key=False)[0] == [2, 1, 0, 3]
+    with pytest.raises(rk.RkError) as e:
+        c.rk_set_gpu_params(list(W.GTX580) + [8])
+    assert e.value.status == rk.RK_EINVAL
+    gpu, ks = W.config("C6")
+    c.rk_set_gpu_params(list(gpu) + [rk.RK_FLAG_SKIP_AHEAD])
+    with pytest.raises(rk.RkError) as e:
+        c.rk_set_kernels(ks)
+    assert e.value.status == rk.RK_EUNSUPPORTED
+    c.rk_set_gpu_params(list(gpu) + [rk.RK_FLAG_CURSOR_PER_KERNEL])
+    c.rk_set_kernels(ks)  # the cursor reading runs on every state (run-length included)
