@@ -332,7 +332,9 @@ def main():
     for kset in fresh[:2]:
         sw.run(kset)
     fresh_ms, _ = e2e(fresh[2:])
-    sw.run(ks)  # back to C4: record, candidate and keys of the bench workload
+    # back to C4 (record, candidate and keys of the bench workload), with the Fig. 1 ranking deciles and the
+    # median order from exact order statistics over the keys (outside the timed regions)
+    fig1 = sw.run(ks, median=True, curve_points=11)
 
     # the same evaluation (stats + keys) with a switch off, for reference: without
     # the SM-symmetry reduction, and without suffix memoisation (direct kernel)
@@ -451,7 +453,10 @@ def main():
                 "result": {"best_T": rep.best_key / gpu[6], "best_index": rep.best_index,
                            "worst_T": rep.worst_key / gpu[6], "cand_index": rep.cand_index,
                            "percentile": rep.percentile, "speedup_over_worst": rep.speedup_over_worst,
-                           "deviation_pct": rep.deviation_pct}}
+                           "deviation_pct": rep.deviation_pct,
+                           "median_T": fig1.median_key / gpu[6],
+                           "gain_over_median_pct": fig1.gain_over_median_pct,
+                           "fig1_ranking_deciles_T": [k / gpu[6] for _, k in fig1.ranking_curve]}}
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             v, cnt, dt = oracle_rate(gpu, ks, args.cpu_seconds, threads, N // 3)

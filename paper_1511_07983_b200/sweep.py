@@ -35,6 +35,8 @@ class Report:
     hist: list
     rb_den: int
     median_key: int | None = None  # lower-middle of the sorted keys
+    # Fig. 1 ranking curve: [(rank, key)] at ranks k*N//(p-1), k < p-1, and N-1
+    ranking_curve: list | None = None
 
     @property
     def percentile(self) -> float:  # ties count for the candidate
@@ -47,6 +49,15 @@ class Report:
     @property
     def deviation_pct(self) -> float:  # Table 3: (algorithm - optimal) / optimal
         return 100.0 * (self.cand_key - self.best_key) / self.best_key
+
+    @property
+    def gain_over_median_pct(self) -> float | None:
+        """PAPER:257 "median sequence" comparison: the heuristic order's gain over
+        the median order, 100 * (T_median - T_cand) / T_cand (half of the random
+        orders are at least this much slower)."""
+        if self.median_key is None:
+            return None
+        return 100.0 * (self.median_key - self.cand_key) / self.cand_key
 
     def time(self, key: int) -> float:
         return key / self.rb_den
@@ -185,9 +196,12 @@ class Sweeper:
         order, _, idx, _ = self.ctx.rk_heuristic_order(with_key=False)  # Algorithm 1 on the host
         return order, idx
 
-    def run(self, kernels, median: bool = False) -> Report:
+    def run(self, kernels, median: bool = False, curve_points: int = 0) -> Report:
         """End to end: host profiles in (H2D), report out (D2H).  median=True adds
-        the exact median key (a few extra passes over the keys)."""
+        the exact median key and the gain over the median order
+        (PAPER:257); curve_points = p >= 2 adds the Fig. 1 ranking curve at ranks
+        k*N//(p-1) (k < p-1) and N-1 (exact order statistics: a few extra passes
+        over the keys)."""
         self.set_kernels(kernels)
         order, idx = self.heuristic()
         self.step_device(idx)
@@ -204,8 +218,19 @@ class Sweeper:
                      worst_index=st.argmax, cand_order=order, cand_index=idx,
                      cand_key=int(out[REC_WORDS].item()) & ((1 << 64) - 1), n_lt=st.n_lt, n_eq=st.n_eq,
                      n_gt=st.n_gt, hist=[int(x) for x in out[REC_WORDS + 1:].tolist()], rb_den=self.gpu[6])
+        N = self.total
+        ranks = []
         if median:
-            rep.median_key = self.select([(self.total - 1) // 2], st.key_min, st.key_max)[0]
+            ranks.append((N - 1) // 2)
+        curve = []
+        if curve_points >= 2:
+            curve = sorted(set([k * N // (curve_points - 1) for k in range(curve_points - 1)] + [N - 1]))
+        if ranks or curve:
+            got = self.select(ranks + curve, st.key_min, st.key_max)
+            if median:
+                rep.median_key = got[0]
+            if curve:
+                rep.ranking_curve = [[r, k] for r, k in zip(curve, got[len(ranks):])]
         return rep
 
     def select(self, ranks, kmin: int, kmax: int):

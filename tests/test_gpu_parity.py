@@ -1256,3 +1256,20 @@ def test_memo_compact_key_stream_c4_and_overflow(ctx):
         torch.cuda.synchronize()
         st2 = rk.Stats.from_c(rk.rk_stats.from_buffer_copy(rec.cpu().numpy().tobytes()))
         assert int(ovf.item()) == (1 if st2.key_max - b2 >= (1 << 32) else 0)
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_fig1_ranking_curve_and_median_gain_vs_oracle_golden(cfg):
+    """Fig. 1's ranking curve as deciles of the sorted keys and
+    the §6 median-sequence comparison: the public report's exact
+    order statistics equal the oracle golden's (sorted full oracle run)."""
+    from paper_1511_07983_b200.sweep import Sweeper
+    g = _gold(f"{cfg.lower()}_oracle.json")
+    gpu, ks = W.config(cfg)
+    for compact in (False, True):
+        rep = Sweeper(gpu, compact_keys=compact).run(ks, median=True, curve_points=11)
+        assert rep.median_key == g["order_stats"][str(g["median_rank"])]
+        assert [str(r) for r, _ in rep.ranking_curve] == [r for r in sorted(g["order_stats"], key=int)
+                                                          if int(r) != g["median_rank"]]
+        assert all(k == g["order_stats"][str(r)] for r, k in rep.ranking_curve)
+        assert rep.gain_over_median_pct == 100.0 * (rep.median_key - g["cand_key"]) / g["cand_key"]
