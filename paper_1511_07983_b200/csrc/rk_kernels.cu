@@ -2550,6 +2550,11 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
     const uint64_t nitems = nslot + nl + (direct ? 0u : *rs.nwlist);
     uint64_t nlt = 0, neq = 0;
     uint32_t iter = 0, pass = 0;
+    /* a narrow row whose distinct values must be visited one by one is deferred to the
+     * warp-cooperative loop below (lanes over its values): {node, Kb, m, ndv | in << 30 | mb << 31} */
+    bool defer;
+    uint32_t d_u, d_m, d_nf;
+    uint64_t d_Kb;
     /* one row (node u, Kb) of weight m; range-edge rows key by key over [olo, ohi) */
     auto do_row = [&](uint32_t u, uint64_t Kb, uint32_t m, uint32_t olo, uint32_t ohi) {
         auto add_bin = [&](uint32_t b, uint64_t w) {
@@ -2590,39 +2595,17 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
             }
             return;
         }
-        /* distinct values, 16-B loads (two values) 4 at a time */
-        const uint4* dp4 = reinterpret_cast<const uint4*>(v.dvp + (uint64_t)u * DF); /* 960-B rows: 16-B aligned */
-        const uint32_t np = (ndv + 1u) >> 1;
-        uint32_t i0 = lane % np; /* lanes start at different pairs: fewer colliding bins */
-        for (uint32_t t = 0; t < np; t += 4) {
-            uint4 e[4];
-            uint32_t ix[4];
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                ix[k] = i0;
-                e[k] = t + k < np ? __ldg(dp4 + i0) : make_uint4(0, 0, 0, 0);
-                i0 = i0 + 1u == np ? 0u : i0 + 1u;
-            }
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    const uint32_t c = (t + k < np && 2u * ix[k] + h < ndv) ? (h ? e[k].w : e[k].y) : 0u;
-                    if (!c) continue;
-                    const uint64_t K = Kb + (h ? e[k].z : e[k].x);
-                    if (in) {
-                        nlt += K < cand ? (uint64_t)m * c : 0ull;
-                        neq += K == cand ? (uint64_t)m * c : 0ull;
-                    }
-                    if (mb) add_bin(bc(K), (uint64_t)m * c);
-                }
-            }
-        }
+        defer = true; /* the distinct values: warp-cooperative, below */
+        d_u = u;
+        d_Kb = Kb;
+        d_m = m;
+        d_nf = ndv | (in ? 0x40000000u : 0u) | (mb ? 0x80000000u : 0u);
     };
     for (uint64_t bbase = (uint64_t)blockIdx.x * blockDim.x; bbase < nitems;
          bbase += (uint64_t)gridDim.x * blockDim.x) { /* block-uniform trip count */
         const uint64_t it = bbase + threadIdx.x;
         uint32_t m = 0;
+        defer = false;
         if (it < nitems) {
             if (it >= nslot + nl) { /* a weighted row without a slot */
                 const uint4 e = rs.wlist[it - nslot - nl];
@@ -2644,6 +2627,29 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_rows_kernel(const RkTables* 
                 const uint32_t u = __ldg(meta_u + off); /* the run pass's (node, K_closed) */
                 do_row(u, __ldg(meta_K + off) + __ldg(v.fst + 4ull * u), 1u,
                        lo > idx0 ? (uint32_t)(lo - idx0) : 0u, hi < idx0 + DF ? (uint32_t)(hi - idx0) : DF);
+            }
+        }
+        /* the deferred rows, one at a time per warp, lanes over their distinct values (8-B {offset,
+         * count} loads; converged, unlike a lane-per-row loop over ~14 values) */
+        for (uint32_t todo = __ballot_sync(0xFFFFFFFFu, defer); todo; todo &= todo - 1u) {
+            const int src = __ffs(todo) - 1;
+            const uint32_t u = __shfl_sync(0xFFFFFFFFu, d_u, src), wm = __shfl_sync(0xFFFFFFFFu, d_m, src);
+            const uint32_t nf = __shfl_sync(0xFFFFFFFFu, d_nf, src);
+            const uint64_t Kb = __shfl_sync(0xFFFFFFFFu, d_Kb, src);
+            const bool in = (nf >> 30) & 1u, mb = nf >> 31;
+            const uint32_t ndv = nf & 0x3FFFFFFFu;
+            for (uint32_t i = lane; i < ndv; i += 32u) {
+                const uint2 e = __ldg(v.dvp + (uint64_t)u * DF + i);
+                const uint64_t K = Kb + e.x;
+                if (in) {
+                    nlt += K < cand ? (uint64_t)wm * e.y : 0ull;
+                    neq += K == cand ? (uint64_t)wm * e.y : 0ull;
+                }
+                if (mb) {
+                    const uint32_t bn = bc(K);
+                    if (wm > kHeavy) atomicAdd((unsigned long long*)&hist[bn], (unsigned long long)wm * e.y);
+                    else atomicAdd(&wh[bn], wm * e.y);
+                }
             }
         }
         if (H) { /* flush before a shared bin can wrap: an iteration adds <= 256 x 120 x min(max m, kHeavy) */
