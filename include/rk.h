@@ -53,7 +53,11 @@ typedef struct rk_ctx rk_ctx;
  * here from the environment (every path computes the same exact keys):
  * RK_NO_REDUCE=1 (no SM-symmetry reduction), RK_FORCE_RUNS=1 (run-length SM
  * state for every S), RK_NO_MEMO=1 (direct per-order evaluation),
- * RK_FORCE_MEMO=1 (suffix memoisation even where it does not pay). */
+ * RK_FORCE_MEMO=1 (suffix memoisation even where it does not pay),
+ * RK_ROW_DEDUP=0 (pass 2 counts every run instead of the distinct rows),
+ * RK_OVERLAP=0 (the memoised step's side-stream work runs on the caller's
+ * stream), RK_ROWS_CTAS=k (CTAs per SM of the side-stream counts/histogram),
+ * RK_SIDE_PRIO=0 (the side stream at the default priority). */
 rk_status rk_create(rk_ctx** out, int cuda_device);
 void rk_destroy(rk_ctx* ctx);
 const char* rk_last_error(const rk_ctx* ctx);

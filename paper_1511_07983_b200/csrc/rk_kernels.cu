@@ -2790,7 +2790,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
 
 /* runs per warp of the compact stream: twice the u64 stream's, so a CTA moves
  * as many bytes (the one-shot grid would otherwise be CTA-launch bound) */
-constexpr uint32_t kKey32RunsPerWarp = 8;
+constexpr uint32_t kKey32RunsPerWarp = 8; /* measured: 4 / 8 / 16 within 1 % */
 /* Pass 2's key stream with compact keys: every key of [first, first+count) as
  * the exact u32 offset key - key_base from the set's exact lower bound
  * (rk_key_lower_bound), index-major — half the HBM bytes of the u64
@@ -3440,17 +3440,15 @@ int rk_dp_keys32(const DPView& v, uint64_t first, uint64_t count, const uint32_t
                  uint32_t* keys32, uint64_t key_base, uint32_t* ovf, const rk_stats* range, void* stream,
                  uint32_t* launches) {
     const uint64_t runs = (first + count + v.Dfact - 1) / v.Dfact - first / v.Dfact;
-    static const int rpw_env = [] { const char* e = getenv("RK_K32_RPW"); return e ? atoi(e) : 0; }();
-    const uint32_t rpw = rpw_env == 4 || rpw_env == 16 ? (uint32_t)rpw_env : kKey32RunsPerWarp;
+    const uint32_t rpw = kKey32RunsPerWarp;
     const uint64_t per_cta = (uint64_t)kDpWarps * rpw; /* one-shot grid */
     const uint64_t grid = (runs + per_cta - 1) / per_cta;
     if (grid > 0x7FFFFFFFull) return (int)cudaErrorInvalidValue;
     const uint64_t rb = first / v.Dfact, re = (first + count + v.Dfact - 1) / v.Dfact;
     const unsigned g = (unsigned)(grid ? grid : 1);
     cudaStream_t st = (cudaStream_t)stream;
-    if (rpw == 4) rk_dp_keys32_kernel<4><<<g, kDpThreads, 0, st>>>(v, first, count, rb, re, meta_u, meta_K, keys32, key_base, ovf, range);
-    else if (rpw == 16) rk_dp_keys32_kernel<16><<<g, kDpThreads, 0, st>>>(v, first, count, rb, re, meta_u, meta_K, keys32, key_base, ovf, range);
-    else rk_dp_keys32_kernel<8><<<g, kDpThreads, 0, st>>>(v, first, count, rb, re, meta_u, meta_K, keys32, key_base, ovf, range);
+    rk_dp_keys32_kernel<kKey32RunsPerWarp><<<g, kDpThreads, 0, st>>>(v, first, count, rb, re, meta_u, meta_K, keys32,
+                                                                      key_base, ovf, range);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }
