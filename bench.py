@@ -148,6 +148,27 @@ def read_profile(kernel_sub: str = "rk_eval_kernel", name: str = "r01_ncu_full_e
     return None, None, None, None
 
 
+def int32_issue():
+    """BASELINE.json's "% INT32 issue peak", from the committed ncu captures (profiles/): the
+    ALU-bound kernels of the memoised step (suffix rows, row24) and the direct per-order
+    kernel (rk_eval_kernel, the path for sets that do not memoise)."""
+    out = {}
+    for name, sub in (("r02_ncu_full_memo.json", "rk_dp_suffix_kernel"), ("r02_ncu_full_memo.json", "rk_dp_row24_kernel"),
+                      ("r01_ncu_full_eval_hist.json", "rk_eval_kernel")):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                for e in json.load(f):
+                    if sub in e["kernel"]:
+                        out[sub] = {"issue_active_pct": e["issue_active_pct"], "pipe_alu_pct": e["pipe_alu_pct"],
+                                    "pipe_fma_pct": e["pipe_fma_pct"], "profile": name}
+                        break
+        except (OSError, ValueError, KeyError):
+            pass
+    out["note"] = ("ncu --set full, issue-slot and INT32-pipe utilisation of the integer-bound kernels; the step's "
+                   "dominant kernel is the HBM-bound key stream (roofline)")
+    return out
+
+
 def cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as f:
@@ -433,6 +454,7 @@ def main():
                                if memo_on else
                                {"rk_eval_kernel": eval_ms_max, "rk_hist_kernel": hist_ms,
                                 "step": ms_max / args.steps}),
+                "int32_issue": int32_issue(),
                 "memo": {"on": memo_on, "prefix_levels": memo_levels, "nodes_per_level": memo_nodes,
                          "suffix_depth": 5, "runs": N // 120,
                          "direct_eval_ms": direct_ms,
