@@ -109,7 +109,8 @@ struct DPView {
     const uint8_t* code;           /* level-P suffix keys as D! one-byte ranks into dv, per node */
     const void* dvc;               /* per node: sorted distinct suffix keys with multiplicities, 16 B each (D! slots) */
     const uint2* dvp;              /* the same distinct keys as {offset from the row minimum (exact unless nd bit 31), count} */
-    const uint32_t* offs;          /* per node: the D! keys minus the row minimum, decoded (32-bit, same caveat) */
+    const uint32_t* offs;          /* per node: the low 32 bits of the D! suffix keys (offset from the row minimum =
+                                      offs - low32(min) mod 2^32, exact unless nd bit 31) */
     const uint32_t* nd;            /* per node: number of distinct suffix keys */
     const uint64_t* fst;           /* per node: min, max, argmin sigma, argmax sigma */
     uint32_t P, D, Dfact;

@@ -2229,7 +2229,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_suffix_kernel(const RkTables
         for (int q = 0; q < 4; q++)
             if (lane + 32u * q < kDF) {
                 code[(uint64_t)u * kDF + lane + 32u * q] = (uint8_t)(cdw >> (8 * q));
-                offs[(uint64_t)u * kDF + lane + 32u * q] = (uint32_t)(v[q] - mn); /* exact unless nd bit 31 */
+                offs[(uint64_t)u * kDF + lane + 32u * q] = (uint32_t)v[q]; /* low 32 bits of the suffix key */
             }
         if (lane == 0) {
             nd[u] = rank | ((mx - mn) >> 32 ? 0x80000000u : 0u); /* bit 31: offsets do not fit 32 bits */
@@ -2282,7 +2282,7 @@ __device__ __forceinline__ void dp_src(const RkGTab& g, const DPView& v, const E
 __device__ __forceinline__ uint64_t dp_key(const DPView& v, uint32_t u, bool wide, uint64_t Kc, uint64_t Kb,
                                            uint32_t q) {
     const uint64_t at = (uint64_t)u * v.Dfact + q;
-    if (!wide) return Kb + __ldg(v.offs + at);
+    if (!wide) return Kb + (uint32_t)(__ldg(v.offs + at) - (uint32_t)(Kb - Kc)); /* offset from the row min */
     const uint8_t c = __ldg(v.code + at);
     return Kc + __ldg(&reinterpret_cast<const ulonglong2*>(v.dvc)[(uint64_t)u * v.Dfact + c].x);
 }
@@ -2716,11 +2716,13 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
     const uint32_t nr = (uint32_t)min((uint64_t)kKeyRunsPerWarp, re - base);
     /* the warp's runs: lane r loads run r's metadata, each step broadcasts two */
     /* lane r < nr: run r's (node, K_closed) -> node | wide << 31 and Kb = K_closed + row min */
-    uint32_t umy = 0u;
+    uint32_t umy = 0u, mmy = 0u; /* mmy: low 32 bits of the row minimum (offsets = raw32 - mmy) */
     uint64_t Kmy = 0ull;
     if (lane < nr) {
         const uint32_t u = __ldg(meta_u + (base - rb + lane));
-        Kmy = __ldg(meta_K + (base - rb + lane)) + __ldg(v.fst + 4ull * u);
+        const uint64_t mn = __ldg(v.fst + 4ull * u);
+        Kmy = __ldg(meta_K + (base - rb + lane)) + mn;
+        mmy = (uint32_t)mn;
         umy = u | (__ldg(v.nd + u) & 0x80000000u);
     }
     const bool whole = base * DF >= lo && (base + nr) * DF <= hi; /* no range-edge run among them */
@@ -2731,6 +2733,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
         if (2u * s >= nr) break;
         const uint32_t uA = __shfl_sync(0xFFFFFFFFu, umy, 2 * s), uB = __shfl_sync(0xFFFFFFFFu, umy, 2 * s + 1);
         const uint64_t KA = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s), KB = __shfl_sync(0xFFFFFFFFu, Kmy, 2 * s + 1);
+        const uint32_t mA = __shfl_sync(0xFFFFFFFFu, mmy, 2 * s), mB = __shfl_sync(0xFFFFFFFFu, mmy, 2 * s + 1);
         const bool twoB = 2u * s + 1u < nr;
         const uint2* rA = reinterpret_cast<const uint2*>(v.offs + (uint64_t)(uA & 0x7FFFFFFFu) * DF);
         const uint2* rB = reinterpret_cast<const uint2*>(v.offs + (uint64_t)(uB & 0x7FFFFFFFu) * DF);
@@ -2750,7 +2753,8 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
                 const bool a = p < PR;
                 if (!(a || (twoB && p < 2u * PR))) continue;
                 const uint64_t Ki = a ? KA : KB;
-                const uint64_t k0 = Ki + of[q].x, k1 = Ki + of[q].y;
+                const uint32_t mi = a ? mA : mB;
+                const uint64_t k0 = Ki + (uint32_t)(of[q].x - mi), k1 = Ki + (uint32_t)(of[q].y - mi);
                 if (whole && aligned) {
                     __stcs(reinterpret_cast<ulonglong2*>(o + 2u * p), make_ulonglong2(k0, k1));
                 } else {
@@ -2770,8 +2774,9 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys_kernel(DPView v, uint64
                 uint64_t kk[2];
                 if (!(ui >> 31)) {
                     const uint2 of = __ldg(reinterpret_cast<const uint2*>(v.offs + (uint64_t)un * DF) + c);
-                    kk[0] = Ki + of.x;
-                    kk[1] = Ki + of.y;
+                    const uint32_t mi = a ? mA : mB;
+                    kk[0] = Ki + (uint32_t)(of.x - mi);
+                    kk[1] = Ki + (uint32_t)(of.y - mi);
                 } else {
                     const ulonglong2* dr = reinterpret_cast<const ulonglong2*>(v.dvc) + (uint64_t)un * DF;
                     const uint64_t Kc = Ki - __ldg(v.fst + 4ull * un);
@@ -2819,16 +2824,43 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_keys32_kernel(DPView v, uint
     const uint64_t base = rb + (uint64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW;
     if (base >= re) return;
     const uint32_t nr = (uint32_t)min((uint64_t)RPW, re - base);
-    uint32_t umy = 0u; /* lane r < nr: run r's node | wide << 31 and Kb = K_closed + row min */
+    /* lane r < nr: run r's node and K_closed.  key - key_base = (K_closed - key_base) + suffix key, and
+     * both it and every key's offset are < 2^32 (the range check above; no row is wide then), so the
+     * low 32 bits add exactly: offset = low32(K_closed - key_base) + the row's raw32 entry (mod 2^32) */
+    uint32_t umy = 0u;
     uint64_t Kmy = 0ull;
     if (lane < nr) {
-        const uint32_t u = __ldg(meta_u + (base - rb + lane));
-        Kmy = __ldg(meta_K + (base - rb + lane)) + __ldg(v.fst + 4ull * u);
-        umy = u | (__ldg(v.nd + u) & 0x80000000u);
+        umy = __ldg(meta_u + (base - rb + lane));
+        Kmy = __ldg(meta_K + (base - rb + lane));
     }
     const bool whole = base * DF >= lo && (base + nr) * DF <= hi;
     uint32_t* const o0 = keys + (base * DF - lo);
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15u) == 0; /* DF % 4 == 0: every run block alike */
+    if (whole && aligned && nr == RPW) { /* the common case: every load of the warp's runs issued up front */
+        const uint32_t dmy = (uint32_t)(Kmy - key_base); /* every key - key_base < 2^32 */
+        uint4 of[RPW / 2][2];
+#pragma unroll
+        for (uint32_t s = 0; s < RPW / 2; s++)
+#pragma unroll
+            for (int q = 0; q < 2; q++) { /* chunk p = lane + 32q: run 2s for p < 30, run 2s+1 for 30 <= p < 60 */
+                const uint32_t p = lane + 32u * q, r = 2u * s + (p < CH ? 0u : 1u);
+                const uint32_t un = __shfl_sync(0xFFFFFFFFu, umy, r) & 0x7FFFFFFFu;
+                of[s][q] = p < 2u * CH
+                               ? __ldg(reinterpret_cast<const uint4*>(v.offs + (uint64_t)un * DF) + (p < CH ? p : p - CH))
+                               : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+        for (uint32_t s = 0; s < RPW / 2; s++)
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                const uint32_t p = lane + 32u * q, r = 2u * s + (p < CH ? 0u : 1u);
+                const uint32_t d32 = __shfl_sync(0xFFFFFFFFu, dmy, r);
+                if (p < 2u * CH)
+                    __stcs(reinterpret_cast<uint4*>(o0 + 2u * s * DF + 4u * p),
+                           make_uint4(d32 + of[s][q].x, d32 + of[s][q].y, d32 + of[s][q].z, d32 + of[s][q].w));
+            }
+        return;
+    }
 #pragma unroll
     for (uint32_t s = 0; s < RPW / 2; s++) {
         if (2u * s >= nr) break;
