@@ -467,7 +467,8 @@ def main():
                         "d2h_bytes_per_step": sw.d2h_bytes, "steps": e2e_steps,
                         "ms_per_step": e2e_ms / e2e_steps,
                         "note": ("Sweeper.run(C4) per step: H2D kernel table, rk_set_kernels with a fresh "
-                                 "memo plan (no plan cache), Algorithm 1, pass 1/2, D2H report"),
+                                 "memo plan (no plan cache; the step runs over the plan's level build), "
+                                 "Algorithm 1, pass 1/2, D2H report"),
                         "fresh_sets": {"value": N * e2e_steps / (fresh_ms / 1e3), "unit": UNIT,
                                        "ms_per_step": fresh_ms / e2e_steps,
                                        "sets": (f"{e2e_steps} other Generator-G 12-kernel sets, seeds "

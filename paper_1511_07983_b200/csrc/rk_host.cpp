@@ -61,6 +61,11 @@ struct DpPlan {
     std::vector<uint32_t> tmask;  /* slots - 1 of level j */
     std::vector<size_t> xoff;     /* transition offset of level j (j < P): cnt[j] * n entries */
     std::vector<uint64_t> work;   /* launch work of level j: (nodes of level j) * n */
+    /* the plan's own build (upper-bound layout) serves the first step after rk_set_kernels: that step
+     * expands the range's prefixes over it instead of rebuilding the levels (then every step rebuilds) */
+    bool reuse_ub = false, last_ub = false;
+    std::vector<size_t> ub_noff, ub_xoff, ub_toff;
+    std::vector<uint32_t> ub_cap, ub_tmask;
     size_t table_slots = 0;
     Arena nodes, tables, tid, dk, fst, counters; /* counters: P + 1 node counters, then the overflow flag */
     Arena code, dvc, dvp, nd, offs;              /* suffix rows: byte codes into sorted distinct (value, count) */
@@ -557,10 +562,11 @@ int dp_build_levels(rk_ctx* c, void* stream, const std::vector<RkExpand>* ex = n
  * through the level-P transitions and encoded. */
 int dp_build_suffix(rk_ctx* c, void* stream) {
     DpPlan& d = c->dp;
-    int e = rk_dp_row24(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.L], (uint32_t*)d.counters.p + d.L,
+    const std::vector<size_t>& noff = d.last_ub ? d.ub_noff : d.noff;
+    int e = rk_dp_row24(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + noff[d.L], (uint32_t*)d.counters.p + d.L,
                         (uint64_t*)d.row24.p, d.cnt[d.L], stream, &c->launches);
     if (!e)
-        e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + d.noff[d.P], (uint32_t*)d.counters.p + d.P,
+        e = rk_dp_suffix(c->tab_dev, c->tab.g.S, (char*)d.nodes.p + noff[d.P], (uint32_t*)d.counters.p + d.P,
                          d.view.tid[d.P], d.view.dk[d.P], (const uint64_t*)d.row24.p, (uint8_t*)d.code.p, d.dvc.p,
                          d.dvp.p, (uint32_t*)d.nd.p, (uint64_t*)d.fst.p, (uint32_t*)d.offs.p, d.cnt[d.P], stream,
                          &c->launches);
@@ -660,6 +666,11 @@ rk_status dp_plan(rk_ctx* c) {
                     d.cnt[j] = h[j];
                     counted = counted && h[j] <= ub[j];
                 }
+                d.ub_noff = d.noff;
+                d.ub_xoff = d.xoff;
+                d.ub_toff = d.toff;
+                d.ub_cap = d.cap;
+                d.ub_tmask = d.tmask;
             }
         }
     }
@@ -691,7 +702,10 @@ rk_status dp_plan(rk_ctx* c) {
         std::vector<uint64_t> m(d.L + 1), cap(d.L + 1, 0);
         for (uint32_t j = 0; j <= d.L; j++) m[j] = d.cnt[j];
         for (uint32_t j = 0; j < d.L; j++) cap[j + 1] = (uint64_t)d.cnt[j] * (n - j);
+        const void *np = d.nodes.p, *tp = d.tid.p, *kp = d.dk.p;
         if (!dp_layout(c, m, cap, e) || e) return e ? cuda_fail(c, e, "memoisation layout") : RK_OK;
+        /* the upper-bound build is still intact unless an arena moved */
+        d.reuse_ub = counted && np == d.nodes.p && tp == d.tid.p && kp == d.dk.p;
     }
     const uint64_t runs = fact64(n) / fact64(RK_DP_D), uP = d.cnt[d.P];
     const uint64_t DF = fact64(RK_DP_D);
@@ -750,6 +764,14 @@ RkRows dp_rows(rk_ctx* c, uint64_t nrun) {
 int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool keys_hint, void* stream) {
     DpPlan& d = c->dp;
     d.runs_ok = false;
+    /* the first step after the plan runs over the plan's build (upper-bound layout); later ones rebuild */
+    const bool ub = d.reuse_ub;
+    d.reuse_ub = false;
+    d.last_ub = ub;
+    for (uint32_t j = 0; j < d.L; j++) {
+        d.view.tid[j] = (const uint32_t*)d.tid.p + (ub ? d.ub_xoff[j] : d.xoff[j]);
+        d.view.dk[j] = (const uint64_t*)d.dk.p + (ub ? d.ub_xoff[j] : d.xoff[j]);
+    }
     const uint32_t n = c->tab.g.n, P = d.P;
     const uint64_t DF = d.view.Dfact;
     const uint64_t rb = first / DF, re = count ? (first + count + DF - 1) / DF : rb;
@@ -815,11 +837,17 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e && c->dedup_now) e = cudaMemsetAsync(d.rminrun.p, 0xFF, slots * 4, st);
     /* levels 0..P-1 (the run level's transitions and the range's expansions), then the run pass and the
      * multiset fork off beside the last level (P+1, for the suffix rows), row24 and the suffix rows */
-    if (!e) e = dp_build_levels(c, stream, ex.empty() ? nullptr : &ex, P);
+    if (!e && !ub) e = dp_build_levels(c, stream, ex.empty() ? nullptr : &ex, P);
+    if (!e && ub) { /* over the plan's levels: zero the list counters, expand the range's prefixes */
+        e = cudaMemsetAsync((uint32_t*)d.counters.p + d.L + 2, 0, 8, st);
+        for (uint32_t j = 1; j < P && j - 1 < ex.size() && !e; j++)
+            e = rk_dp_level(c->tab_dev, c->tab.g.S, nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr, nullptr,
+                            (uint32_t*)d.counters.p + d.L + 1, 0, stream, &c->launches, &ex[j - 1], 0);
+    }
     void* rs = side ? (void*)c->side : stream;
     if (!e && side) e = cudaEventRecord(c->ev_fork, st);
     if (!e && side) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
-    if (!e && !side) e = dp_levels(c, P, d.L, stream, nullptr);
+    if (!e && !side && !ub) e = dp_levels(c, P, d.L, stream, nullptr);
     const int mr = tmark_begin(c, RK_PHASE_RUNS, rs);
     RkRows runrows = dp_rows(c, re - rb);
     if (hier) runrows.slot = nullptr; /* the run pass writes the run metadata only */
@@ -836,7 +864,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     }
     tmark_end(c, mr, rs);
     if (!e && side) e = cudaEventRecord(c->ev_join, c->side);
-    if (!e && side) e = dp_levels(c, P, d.L, stream, nullptr);
+    if (!e && side && !ub) e = dp_levels(c, P, d.L, stream, nullptr);
     if (!e) e = dp_build_suffix(c, stream);
     tmark_end(c, m0, stream);
     if (!e && side) e = cudaStreamWaitEvent(st, c->ev_join, 0);
@@ -1239,10 +1267,15 @@ rk_status rk_memo_audit(rk_ctx* c, uint64_t* out) {
     int e = cudaMalloc(&bad, sizeof(unsigned long long) * 6 * d.L);
     if (!e) e = cudaMemset(bad, 0, sizeof(unsigned long long) * 6 * d.L);
     const char* nodes = (const char*)d.nodes.p;
+    const bool ub = d.last_ub; /* the tables of the last pass 1: the plan's build, or the step's rebuild */
+    const std::vector<size_t>& noff = ub ? d.ub_noff : d.noff;
+    const std::vector<size_t>& toff = ub ? d.ub_toff : d.toff;
+    const std::vector<uint32_t>& cap = ub ? d.ub_cap : d.cap;
+    const std::vector<uint32_t>& tmask = ub ? d.ub_tmask : d.tmask;
     for (uint32_t j = 1; j <= d.L && !e; j++)
-        e = rk_dp_audit(c->tab.g.S, nodes + d.noff[j], (const uint32_t*)d.counters.p + j, d.cap[j],
-                        (const uint32_t*)d.tables.p + d.toff[j], d.tmask[j], d.view.tid[j - 1],
-                        (uint64_t)d.cnt[j - 1] * c->tab.g.n, j > 1 ? nodes + d.noff[j - 1] : nullptr, c->tab.g.n,
+        e = rk_dp_audit(c->tab.g.S, nodes + noff[j], (const uint32_t*)d.counters.p + j, cap[j],
+                        (const uint32_t*)d.tables.p + toff[j], tmask[j], d.view.tid[j - 1],
+                        (uint64_t)d.cnt[j - 1] * c->tab.g.n, j > 1 ? nodes + noff[j - 1] : nullptr, c->tab.g.n,
                         bad + 6 * (j - 1), nullptr);
     if (!e) e = cudaMemcpy(h.data(), bad, sizeof(unsigned long long) * 6 * d.L, cudaMemcpyDeviceToHost);
     if (!e) e = cudaMemcpy(cnt.data(), d.counters.p, 4 * (d.L + 1), cudaMemcpyDeviceToHost);
