@@ -281,7 +281,10 @@ rk_status rk_simulate_order(rk_ctx* ctx, const int32_t* order, uint32_t* rounds_
  * metadata: it must follow pass 1 over the same [first, first+count) on the
  * same ctx (else RK_ESTATE).  Pass 1 also builds the range's multiset of
  * distinct rows (node, K_closed) with multiplicities, from which pass 2
- * counts and bins (C4: 217,659 distinct rows for 3,991,680 runs).
+ * counts and bins (C4: 217,659 distinct rows for 3,991,680 runs).  Scratch:
+ * ~36 B per run of D! = 120 indices (run metadata, multiset, lists), ctx-owned
+ * and grow-only; rk_eval_range splits ranges of more than 2^26 runs itself,
+ * callers of the two-pass API split theirs.
  * Errors: RK_EINVAL (range, missing pointers), RK_ESTATE, RK_ENODEVICE,
  * RK_ECUDA. */
 rk_status rk_sweep_pass1_async(rk_ctx* ctx, uint64_t first, uint64_t count, const uint64_t* cand_key_dev,

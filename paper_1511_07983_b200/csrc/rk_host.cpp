@@ -788,8 +788,6 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e) e = d.rmult.reserve(slots * 4 * 8); /* 8 counters per slot */
     if (!e) e = d.rlist.reserve(nrun * 4);
     if (!e) e = d.rminrun.reserve(slots * 4);
-    if (!e) e = d.rwlist.reserve(nrun * 16);
-    if (!e) e = d.rwminrun.reserve(nrun * 4);
     c->dedup_now = c->row_dedup != 0;
     const bool side = c->overlap != 0;
     if (!e && side) e = ensure_side(c);
@@ -827,6 +825,9 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
         if (!e) e = d.pslot.reserve(pslots * 16);
         if (!e) e = d.pmult.reserve(pslots * 32);
         if (!e) e = d.pminrun.reserve(pslots * 4);
+        /* weighted rows without a slot: at most one per (parent slot, unused kernel) */
+        if (!e) e = d.rwlist.reserve(pslots * (n - P + 1) * 16);
+        if (!e) e = d.rwminrun.reserve(pslots * (n - P + 1) * 4);
     }
     const int m0 = tmark_begin(c, RK_PHASE_TABLES, stream);
     if (!e && hier) e = cudaMemsetAsync(d.pslot.p, 0, pslots * 16, st);
@@ -927,10 +928,35 @@ int dp_pass2(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev
 }
 
 /* memoised equivalent of rk_launch_eval (stats + optional keys, optional histogram) */
+/* memoised stats (+ optional keys, optional histogram over a given range) of [first, first+count); ranges of
+ * more than kChunkRuns runs go in chunks of whole runs (pass 1 + pass 2 each, records merged on the device),
+ * so the per-run scratch (run metadata, multiset lists: ~36 B per run) stays bounded */
+constexpr uint64_t kChunkRuns = 1ull << 26;
 int dp_eval(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev, rk_stats* stats_dev,
             uint64_t* keys_dev, const rk_stats* range_dev, uint32_t bins, uint64_t* hist_dev, void* stream) {
-    int e = dp_pass1(c, first, count, stats_dev, keys_dev != nullptr, stream);
-    if (!e) e = dp_pass2(c, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, stats_dev, stream);
+    const uint64_t DF = c->dp.view.Dfact;
+    const uint64_t nrun = count ? (first + count + DF - 1) / DF - first / DF : 0;
+    if (nrun <= kChunkRuns) {
+        int e = dp_pass1(c, first, count, stats_dev, keys_dev != nullptr, stream);
+        if (!e) e = dp_pass2(c, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, stats_dev, stream);
+        return e;
+    }
+    /* chunk records at u64_dev[16..], the running merge at stats_dev (2-record merges) */
+    rk_stats* part = reinterpret_cast<rk_stats*>(c->u64_dev + 16);
+    int e = 0;
+    for (uint64_t lo = first, end = first + count; lo < end && !e;) {
+        const uint64_t hi = std::min(end, (lo / DF + kChunkRuns) * DF);
+        rk_stats* out = lo == first ? stats_dev : part + 1;
+        e = dp_pass1(c, lo, hi - lo, out, keys_dev != nullptr, stream);
+        if (!e)
+            e = dp_pass2(c, lo, hi - lo, cand_dev, range_dev, bins, hist_dev, keys_dev ? keys_dev + (lo - first) : nullptr,
+                         out, stream);
+        if (!e && lo != first) { /* stats_dev <- merge(stats_dev, chunk) */
+            e = cudaMemcpyAsync(part, stats_dev, sizeof(rk_stats), cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+            if (!e) e = rk_launch_merge(part, 2, stats_dev, stream, &c->launches);
+        }
+        lo = hi;
+    }
     return e;
 }
 
