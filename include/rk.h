@@ -88,12 +88,14 @@ typedef struct {
  * kernels in launch order; a round closes once every kernel with pending
  * blocks has been offered (the alternative of L5 that SPEC:262 rejects;
  * PAPER:80 "relegated to the next execution round").
- * STRICT_RR and SKIP_AHEAD (any combination with CURSOR_PER_KERNEL) run on the
- * per-order policy kernels: stats, keys, round partitions, candidates, batches
- * and the two-pass step; memoisation, branch and bound, compact keys and the
- * fused histogram return RK_EUNSUPPORTED, and so does a reduced SM count
- * S' > 32 (run-length state) at rk_set_kernels (DESIGN.md §5 "Model-reading
- * policies"). */
+ * STRICT_RR keeps the prefix state of L4 (only the placement rule differs) and
+ * runs on every path of the register state (memoised step, direct kernel,
+ * branch and bound, batch).  SKIP_AHEAD (with or without the other two) runs
+ * on the per-order policy kernels: stats, keys, round partitions, candidates,
+ * batches and the two-pass step; memoisation, branch and bound, compact keys
+ * and the fused histogram return RK_EUNSUPPORTED.  STRICT_RR or SKIP_AHEAD
+ * with a reduced SM count S' > 32 (run-length state) returns RK_EUNSUPPORTED
+ * at rk_set_kernels (DESIGN.md §5 "Model-reading policies"). */
 #define RK_FLAG_SKIP_AHEAD 4u
 #define RK_FLAGS_POLICY (RK_FLAG_STRICT_RR | RK_FLAG_SKIP_AHEAD)
 rk_status rk_set_gpu_params(rk_ctx* ctx, const rk_gpu_params* p);

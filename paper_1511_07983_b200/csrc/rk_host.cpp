@@ -121,10 +121,12 @@ struct rk_ctx {
 
 /* SM count that selects the kernel variant (the table keeps the real S) */
 static uint32_t vS(const rk_ctx* c, uint32_t S) {
-    if (c->gp.flags & RK_FLAGS_POLICY) return S | RK_S_POLICY; /* per-order policy kernels */
+    if (c->gp.flags & RK_FLAG_SKIP_AHEAD) return S | RK_S_POLICY; /* per-order policy kernels */
     return c->force_runs ? 65535u : S;
 }
-static bool policy(const rk_ctx* c) { return (c->gp.flags & RK_FLAGS_POLICY) != 0; }
+/* skip-ahead: the state after a prefix carries pending blocks, so only the per-order policy kernels apply
+ * (strict round robin keeps L4's prefix state and runs on every path, register state only) */
+static bool policy(const rk_ctx* c) { return (c->gp.flags & RK_FLAG_SKIP_AHEAD) != 0; }
 
 namespace {
 
@@ -1137,7 +1139,7 @@ rk_status rk_eval_range32_async(rk_ctx* c, uint64_t first, uint64_t count, const
     rk_status s = need_device(c);
     if (s || (s = need_kernels(c))) return s;
     if (!stats_dev || !keys32_dev || !ovf_dev) return fail(c, RK_EINVAL, "stats_dev, keys32_dev, ovf_dev required");
-    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "compact keys under strict round robin / skip-ahead");
+    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "compact keys under skip-ahead");
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
@@ -1153,7 +1155,7 @@ rk_status rk_eval_range_hist_async(rk_ctx* c, uint64_t first, uint64_t count, co
     rk_status s = need_device(c);
     if (s || (s = need_kernels(c))) return s;
     if (!range_dev || !hist_dev || bins < 1 || bins > 32768) return fail(c, RK_EINVAL, "bad fused histogram args");
-    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "fused histogram under strict round robin / skip-ahead");
+    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "fused histogram under skip-ahead");
     if (first > space(c) || count > space(c) - first) return fail(c, RK_EINVAL, "range exceeds n!");
     DeviceGuard dg(c->device);
     c->launches = 0;
@@ -1682,7 +1684,7 @@ rk_status rk_best_order(rk_ctx* c, uint64_t seed_index, int32_t* order_out, uint
     if (s || (s = need_kernels(c))) return s;
     const uint32_t n = c->tab.g.n;
     if (seed_index != UINT64_MAX && seed_index >= space(c)) return fail(c, RK_EINVAL, "seed_index >= n!");
-    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "branch and bound under strict round robin / skip-ahead");
+    if (policy(c)) return fail(c, RK_EUNSUPPORTED, "branch and bound under skip-ahead");
     DeviceGuard dg(c->device);
     c->launches = 0;
     uint64_t seed = ~0ull;

@@ -357,6 +357,50 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
     }
     uint32_t n = k.T;
     Placed o;
+    if (g.flags & RK_FLAG_STRICT_RR) { /* L4 read literally: block b of the kernel goes to SM (cur + b) mod S */
+        const uint32_t S = nsm<SMAX, FULL>(g);
+        const uint32_t cur = (g.flags & RK_FLAG_CURSOR_PER_KERNEL) ? 0u : in.cur;
+        uint32_t m = 0xFFFFFFFFu; /* the first block that does not fit on its SM */
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+            if (live_sm<SMAX, FULL>(i, g)) m = min(m, d + c[i] * S);
+        }
+        if (n <= m) {
+            o.cur = (cur + n) % S;
+            upd.set_cursor(o.cur);
+#pragma unroll
+            for (int i = 0; i < SMAX; i++) {
+                const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+                const uint32_t x = d < n ? (n - d - 1u) / S + 1u : 0u;
+                upd(i, in.fa[i] - x * k.dA, in.fb[i] - x * k.dB);
+            }
+            o.I = in.I + (uint64_t)n * k.cA;
+            o.M = in.M + (uint64_t)n * k.cM;
+            o.K = in.K;
+        } else { /* m blocks close the round; full rounds of S*C; the rest from SM 0 of a fresh round */
+            rec.add(kid, m);
+            rec.close();
+            const uint32_t nfull = full_rounds(n - m - 1u, k);
+            rec.full(kid, nfull, k.SC);
+            o.K = in.K + round_key(in.I + (uint64_t)m * k.cA, in.M + (uint64_t)m * k.cM, g.num, g.den) +
+                  (uint64_t)nfull * k.fullkey;
+            n -= m + nfull * k.SC;
+            const uint32_t q = n / S, r = n - q * S;
+            o.cur = r;
+            upd.set_cursor(r);
+#pragma unroll
+            for (int i = 0; i < SMAX; i++) {
+                const uint32_t x = q + ((uint32_t)i < r ? 1u : 0u);
+                if (live_sm<SMAX, FULL>(i, g)) upd(i, g.freshA - x * k.dA, g.freshB - x * k.dB);
+                else upd(i, 0u, 0u);
+            }
+            o.I = (uint64_t)n * k.cA;
+            o.M = (uint64_t)n * k.cM;
+        }
+        rec.add(kid, n);
+        return o;
+    }
     const bool ovf = n > F;
     /* n > F: every SM takes its c_s and the next block fits nowhere, so the round
      * closes; complete single-kernel rounds follow; the rest opens a
@@ -423,6 +467,7 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
 template <int SMAX>
 struct StoreUpd {
     St<SMAX>& out;
+    __device__ __forceinline__ void set_cursor(uint32_t) {}
     __device__ __forceinline__ void operator()(int i, uint32_t a, uint32_t b) {
         out.fa[i] = a;
         out.fb[i] = b;
@@ -432,7 +477,23 @@ struct StoreUpd {
 struct CapSumUpd { /* consume the new words: capacity sum for the next kernel */
     CapK k;
     uint32_t F;
+    __device__ __forceinline__ void set_cursor(uint32_t) {}
     __device__ __forceinline__ void operator()(int, uint32_t a, uint32_t b) { F += cap1(a, b, k); }
+};
+
+/* strict round robin (RK_FLAG_STRICT_RR): the next kernel's blocks go to SM (cur + b) mod S, so the
+ * first that cannot be placed is b = min_s ((s - cur) mod S + c_s S); consumes the new words once the
+ * placing kernel has set the new cursor (0 for the cursor-per-kernel reading) */
+struct StrictCapUpd {
+    CapK k;
+    uint32_t S, cur, m;
+    bool perk;
+    __device__ __forceinline__ void set_cursor(uint32_t c) { cur = perk ? 0u : c; }
+    __device__ __forceinline__ void operator()(int i, uint32_t a, uint32_t b) {
+        if ((uint32_t)i >= S) return;
+        const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+        m = min(m, d + cap1(a, b, k) * S);
+    }
 };
 
 /* ---- run-length state (SMAX == 0): the same dispatch rules (PAPER:69-81,
@@ -600,6 +661,12 @@ __device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, u
     uint32_t F = 0;
     if constexpr (SMAX == 0) {
         F = rle_capsum(s, ck, g.S);
+    } else if (g.flags & RK_FLAG_STRICT_RR) { /* the first block that does not fit on its SM */
+        StrictCapUpd u{ck, g.S, 0u, 0xFFFFFFFFu, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0};
+        u.set_cursor(s.cur);
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) u(i, s.fa[i], s.fb[i]);
+        F = u.m;
     } else {
 #pragma unroll
         for (int i = 0; i < SMAX; i++) F += cap1(s.fa[i], s.fb[i], ck);
@@ -617,6 +684,11 @@ __device__ __forceinline__ uint64_t place_finish(const St<SMAX>& in, const RkKTa
         rle_place(in, s1, kb, kbid, g, nr);
         return finish<0>(s1, kc, kcid, g, nr);
     } else {
+        if (g.flags & RK_FLAG_STRICT_RR) {
+            StrictCapUpd u{capk(kc), nsm<SMAX, FULL>(g), 0u, 0xFFFFFFFFu, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0};
+            const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
+            return finish_key(u.m, o.I, o.M, o.K, kc, kcid, g, nr);
+        }
         CapSumUpd u{capk(kc), 0u};
         const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
         return finish_key(u.F, o.I, o.M, o.K, kc, kcid, g, nr);

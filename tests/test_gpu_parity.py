@@ -1273,3 +1273,35 @@ def test_fig1_ranking_curve_and_median_gain_vs_oracle_golden(cfg):
                                                           if int(r) != g["median_rank"]]
         assert all(k == g["order_stats"][str(r)] for r, k in rep.ranking_curve)
         assert rep.gain_over_median_pct == 100.0 * (rep.median_key - g["cand_key"]) / g["cand_key"]
+
+
+def test_strict_round_robin_on_the_memoised_and_bnb_paths(monkeypatch):
+    """RK_FLAG_STRICT_RR keeps L4's prefix state, so it runs on the memoised
+    step (forced on), the direct kernel and branch and bound: every key and
+    statistic vs the oracle on C2, C3 and random sets over the GPU shapes,
+    with and without the cursor-per-kernel reading; the optimum by branch and
+    bound equals the full sweep's."""
+    ctx = _direct_ctx(monkeypatch, "RK_FORCE_MEMO")
+    try:
+        cases = [W.config("C2"), W.config("C3")]
+        for gi, gpu in enumerate(GPUS[:5]):
+            for ks in W.random_small_sets(0x5A5A + gi, 3, 6, 8, gpu=gpu):
+                if all(W.feasible(gpu, k) for k in ks):
+                    cases.append((gpu, ks))
+        memo_checked = 0
+        for flags in (rk.RK_FLAG_STRICT_RR, rk.RK_FLAG_STRICT_RR | rk.RK_FLAG_CURSOR_PER_KERNEL):
+            for gpu, ks in cases:
+                g = list(gpu) + [flags]
+                try:
+                    ctx.rk_set_gpu_params(g)
+                    ctx.rk_set_kernels(ks)
+                except rk.RkError as e:
+                    assert e.status == rk.RK_EUNSUPPORTED
+                    continue
+                memo_checked += ctx.rk_memo_info()[0]
+                st = check_full_space(ctx, g, ks, bins=(32,))
+                _, idx, key, _ = ctx.rk_best_order()
+                assert (key, idx) == (st.key_min, st.argmin)
+        assert memo_checked >= 8
+    finally:
+        ctx.close()
