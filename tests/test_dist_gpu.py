@@ -32,14 +32,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cfg, q):
+def _worker(rank, world, port, cfg, q, compact=False):
     from paper_1511_07983_b200.sweep import Sweeper
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     gpu, ks = W.config(cfg)
-    sw = Sweeper(gpu, device=0)
+    sw = Sweeper(gpu, device=0, compact_keys=compact)
     rep = sw.run(ks, median=True)
     launches = sw.launches
     rep2 = sw.run(ks)  # a second step on the same Sweeper (buffers reused)
@@ -51,11 +51,11 @@ def _worker(rank, world, port, cfg, q):
     dist.destroy_process_group()
 
 
-def _run(world, cfg):
+def _run(world, cfg, compact=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q, compact)) for r in range(world)]
     for p in procs:
         p.start()
     got, shards, t0 = None, {}, time.time()
@@ -76,11 +76,14 @@ def _run(world, cfg):
     return got, shards
 
 
-@pytest.mark.parametrize("world,cfg", [(2, "C3"), (3, "C3"), (2, "C4"), (3, "C4")])
-def test_multi_rank_cuda_step_equals_oracle_golden(world, cfg):
+@pytest.mark.parametrize("world,cfg,compact", [(2, "C3", False), (3, "C3", False), (2, "C4", False), (3, "C4", False),
+                                               (2, "C4", True), (3, "C3", True)])
+def test_multi_rank_cuda_step_equals_oracle_golden(world, cfg, compact):
+    """compact=True: the bench's form (exact u32 key offsets; the overflow test on
+    the merged global range, so every rank decides alike)."""
     with open(os.path.join(GOLD, f"{cfg.lower()}_oracle.json")) as f:
         g = json.load(f)
-    (rep, rep2, launches, first, count), shards = _run(world, cfg)
+    (rep, rep2, launches, first, count), shards = _run(world, cfg, compact)
     N = math.factorial(len(W.config(cfg)[1]))
     assert first == 0 and count == N // world
     assert sorted(shards) == list(range(1, world)) and sum(c for _, c, _ in shards.values()) + count == N
