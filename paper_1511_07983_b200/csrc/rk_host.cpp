@@ -101,6 +101,7 @@ struct rk_ctx {
     bool force_runs = false; /* RK_FORCE_RUNS=1: run-length SM state for every S (testing) */
     bool no_memo = false;    /* RK_NO_MEMO=1: direct evaluation of every order (testing) */
     bool force_memo = false; /* RK_FORCE_MEMO=1: memoise even where it does not pay (testing) */
+    bool no_coop = false;    /* RK_NO_COOP=1: one launch per level (no cooperative multi-level launch) */
     /* pass 2's counts/histogram: from the distinct rows (dedup, default) or every run.  Pass 1's run pass
      * (run metadata + the row multiset) runs beside the suffix-row build, pass 2's counts/histogram beside
      * the key stream, both on a high-priority side stream (RK_OVERLAP=0: all serial).  RK_ROW_DEDUP /
@@ -529,22 +530,37 @@ uint32_t pow2_at_least(uint64_t x) {
 
 /* Enqueue levels j0..j1-1 of the plan's table build (level j reads level j's
  * nodes and count, writes level j+1). */
-int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vector<RkExpand>* ex = nullptr) {
-    DpPlan& d = c->dp;
-    const uint32_t n = c->tab.g.n, S = c->tab.g.S;
-    char* nodes = (char*)d.nodes.p;
-    uint32_t* ctr = (uint32_t*)d.counters.p;
+/* levels whose items (and expansion entries) stay under this go several to one cooperative launch */
+constexpr uint64_t kCoopItems = 1u << 16;
+int launch_level_run(rk_ctx* c, std::vector<RkLevel>& lv, void* stream) {
+    /* consecutive small levels share one cooperative launch (<= 8), the others get one launch each */
     int e = 0;
-    for (uint32_t j = j0; j < j1 && !e; j++) {
-        const void* Uj = j ? nodes + d.noff[j] : nullptr;
-        /* the launch of level j also expands the range's prefixes of level j-1 -> j */
-        const RkExpand* x = (ex && j >= 1 && j < d.P && j - 1 < ex->size()) ? &(*ex)[j - 1] : nullptr;
-        e = rk_dp_level(c->tab_dev, S, Uj, j ? ctr + j : nullptr, nodes + d.noff[j + 1], ctr + j + 1, d.cap[j + 1],
-                        (uint32_t*)d.tables.p + d.toff[j + 1], d.tmask[j + 1], (uint32_t*)d.tid.p + d.xoff[j],
-                        (uint64_t*)d.dk.p + d.xoff[j], ctr + d.L + 1, d.work[j] / n * (n - j), stream,
-                        &c->launches, x, n - j);
+    for (size_t i = 0; i < lv.size() && !e;) {
+        size_t j = i + 1;
+        auto small = [&](const RkLevel& l) { return l.work <= kCoopItems && (!l.ex || l.ex->cnt <= kCoopItems); };
+        if (!c->no_coop && small(lv[i]))
+            while (j < lv.size() && j - i < 8 && small(lv[j])) j++;
+        e = rk_dp_levels(c->tab_dev, c->tab.g.S, lv.data() + i, (uint32_t)(j - i), stream, &c->launches);
+        i = j;
     }
     return e;
+}
+
+int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vector<RkExpand>* ex = nullptr) {
+    DpPlan& d = c->dp;
+    const uint32_t n = c->tab.g.n;
+    char* nodes = (char*)d.nodes.p;
+    uint32_t* ctr = (uint32_t*)d.counters.p;
+    std::vector<RkLevel> lv;
+    for (uint32_t j = j0; j < j1; j++) {
+        /* the launch of level j also expands the range's prefixes of level j-1 -> j */
+        const RkExpand* x = (ex && j >= 1 && j < d.P && j - 1 < ex->size()) ? &(*ex)[j - 1] : nullptr;
+        lv.push_back(RkLevel{j ? nodes + d.noff[j] : nullptr, j ? ctr + j : nullptr, nodes + d.noff[j + 1],
+                             ctr + j + 1, d.cap[j + 1], (uint32_t*)d.tables.p + d.toff[j + 1], d.tmask[j + 1],
+                             (uint32_t*)d.tid.p + d.xoff[j], (uint64_t*)d.dk.p + d.xoff[j], ctr + d.L + 1, x, n - j,
+                             d.work[j] / n * (n - j)});
+    }
+    return launch_level_run(c, lv, stream);
 }
 
 /* Enqueue the level build of the current plan: clear, P levels (+ the given
@@ -843,9 +859,11 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     if (!e && !ub) e = dp_build_levels(c, stream, ex.empty() ? nullptr : &ex, P);
     if (!e && ub) { /* over the plan's levels: zero the list counters, expand the range's prefixes */
         e = cudaMemsetAsync((uint32_t*)d.counters.p + d.L + 2, 0, 8, st);
-        for (uint32_t j = 1; j < P && j - 1 < ex.size() && !e; j++)
-            e = rk_dp_level(c->tab_dev, c->tab.g.S, nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr, nullptr,
-                            (uint32_t*)d.counters.p + d.L + 1, 0, stream, &c->launches, &ex[j - 1], 0);
+        std::vector<RkLevel> lv;
+        for (uint32_t j = 1; j < P && j - 1 < ex.size(); j++)
+            lv.push_back(RkLevel{nullptr, nullptr, nullptr, nullptr, 0, nullptr, 0, nullptr, nullptr,
+                                 (uint32_t*)d.counters.p + d.L + 1, &ex[j - 1], 0, 0});
+        if (!e) e = launch_level_run(c, lv, stream);
     }
     void* rs = side ? (void*)c->side : stream;
     if (!e && side) e = cudaEventRecord(c->ev_fork, st);
@@ -977,6 +995,8 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
     c->force_runs = fr && fr[0] == '1';
     const char* nm = getenv("RK_NO_MEMO");
     c->no_memo = nm && nm[0] == '1';
+    const char* nc = getenv("RK_NO_COOP");
+    c->no_coop = nc && nc[0] == '1';
     const char* fm = getenv("RK_FORCE_MEMO");
     c->force_memo = fm && fm[0] == '1';
     const char* rd = getenv("RK_ROW_DEDUP");

@@ -127,9 +127,27 @@ struct RkExpand {
     const uint32_t* tid;
     const uint64_t* dk;
 };
-int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
-                uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
-                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex = nullptr, uint32_t nrem = 0);
+/* one level of the table build: level j's nodes (Uj, *cnt_j; nullptr = the fresh root) x their nrem
+ * unused kernels into level j+1 (Un, *cnt_n, capacity cap_n, hash table table/tmask, transitions tid/dk,
+ * overflow flag ovf); work = items for grid sizing; ex = the range's level j-1 -> j expansion (nullable) */
+struct RkLevel {
+    const void* Uj;
+    const uint32_t* cnt_j;
+    void* Un;
+    uint32_t* cnt_n;
+    uint32_t cap_n;
+    uint32_t* table;
+    uint32_t tmask;
+    uint32_t* tid;
+    uint64_t* dk;
+    uint32_t* ovf;
+    const RkExpand* ex;
+    uint32_t nrem;
+    uint64_t work;
+};
+/* nl consecutive levels: one launch for nl == 1, one cooperative launch (grid barriers between levels)
+ * for 1 < nl <= 8 */
+int rk_dp_levels(const RkTables* tab, uint32_t S, const RkLevel* lv, uint32_t nl, void* stream, uint32_t* launches);
 /* the 24 suffix keys of every level-(P+1) node (row24: nodes x 24 u64) */
 int rk_dp_row24(const RkTables* tab, uint32_t S, const void* U, const uint32_t* cnt, uint64_t* row24, uint64_t nodes,
                 void* stream, uint32_t* launches);

@@ -1978,48 +1978,72 @@ struct ExpArgs {
     const uint32_t* tid;
     const uint64_t* dk;
 };
+/* COH: coherent (L2) loads, for tables written earlier in the same (cooperative) launch; else the
+ * read-only path */
+template <bool COH = false>
 __device__ __forceinline__ uint4 expand_one(const ExpArgs& x, uint64_t i0, uint32_t n) {
     const uint32_t full = (1u << n) - 1u;
     const uint64_t i = x.an + i0, parent = i / (n - x.j);
     const uint32_t d = (uint32_t)(i - parent * (n - x.j));
-    const uint4 e = x.j ? __ldg(x.Rj + (parent - x.aj)) : make_uint4(0, 0, 0, 0);
+    const uint4 e = x.j ? (COH ? __ldcg(x.Rj + (parent - x.aj)) : __ldg(x.Rj + (parent - x.aj))) : make_uint4(0, 0, 0, 0);
     const uint32_t k = nth_set_bit(full & ~e.y, d);
     const uint32_t c = e.x * n + k;
-    const uint64_t Kc = (((uint64_t)e.w << 32) | e.z) + __ldg(x.dk + c);
-    const uint4 r = make_uint4(__ldg(x.tid + c), e.y | (1u << k), (uint32_t)Kc, (uint32_t)(Kc >> 32));
+    const uint64_t Kc = (((uint64_t)e.w << 32) | e.z) + (COH ? __ldcg(x.dk + c) : __ldg(x.dk + c));
+    const uint4 r = make_uint4(COH ? __ldcg(x.tid + c) : __ldg(x.tid + c), e.y | (1u << k), (uint32_t)Kc,
+                               (uint32_t)(Kc >> 32));
     if (x.Rn) x.Rn[i0] = r; /* the last level is recomputed by the passes that need it, not stored */
     return r;
 }
 
-/* One level: nodes of level j (count *cnt_j; nullptr = the fresh root) x unused
- * kernels; the same launch also runs the previous level's prefix expansion (xp). */
-template <int SMAX, bool FULL>
-__global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables* __restrict__ tab,
-                                                                const DNode<SMAX>* __restrict__ Uj,
-                                                                const uint32_t* __restrict__ cnt_j, DNode<SMAX>* Un,
-                                                                uint32_t* cnt_n, uint32_t cap_n, uint32_t* table,
-                                                                uint32_t tmask, uint32_t* __restrict__ tid,
-                                                                uint64_t* __restrict__ dk, uint32_t* ovf, ExpArgs xp,
-                                                                uint32_t nrem) {
-    __shared__ RkTables t;
-    load_tables(t, tab);
+/* One level's arguments (rk_dp_level / the cooperative multi-level launch). */
+template <int SMAX>
+struct LevelArgs {
+    const DNode<SMAX>* Uj;
+    const uint32_t* cnt_j;
+    DNode<SMAX>* Un;
+    uint32_t* cnt_n;
+    uint32_t cap_n;
+    uint32_t* table;
+    uint32_t tmask;
+    uint32_t* tid;
+    uint64_t* dk;
+    uint32_t* ovf;
+    ExpArgs xp;
+    uint32_t nrem;
+};
+
+template <int SMAX, bool FULL, bool COH>
+__device__ __forceinline__ void level_body(const RkTables& t, const LevelArgs<SMAX>& a, uint64_t gtid, uint64_t nth) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n, full = (1u << n) - 1u;
+    const DNode<SMAX>* __restrict__ Uj = a.Uj;
+    DNode<SMAX>* Un = a.Un;
+    uint32_t* table = a.table;
+    const uint32_t tmask = a.tmask, cap_n = a.cap_n, nrem = a.nrem;
+    uint32_t* ovf = a.ovf;
     /* an overflowed level (capped planning capacities) stops every
      * later level: its count may exceed the nodes it stored */
-    const uint32_t m = Uj ? (*(volatile uint32_t*)ovf ? 0u : *cnt_j) : 1u;
+    const uint32_t m = Uj ? (*(volatile uint32_t*)ovf ? 0u : *(volatile const uint32_t*)a.cnt_j) : 1u;
     NoRec nr;
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < xp.cnt;
-         x += gridDim.x * (uint64_t)blockDim.x)
-        expand_one(xp, x, n);
+    for (uint64_t x = gtid; x < a.xp.cnt; x += nth) expand_one<COH>(a.xp, x, n);
     /* one item per live child: node u of level j by its d-th unused kernel (every node of a level
      * has nrem = n - j unused kernels); transitions stay at u * n + k, entries of used kernels are
      * never read (nor written) */
-    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < m * nrem; w += gridDim.x * blockDim.x) {
-        const uint32_t u = w / nrem, d = w - u * nrem;
+    for (uint64_t w = gtid; w < (uint64_t)m * nrem; w += nth) {
+        const uint32_t u = (uint32_t)(w / nrem), d = (uint32_t)(w - (uint64_t)u * nrem);
         DNode<SMAX> nd;
-        if (Uj) nd = Uj[u];
-        else dnode_fresh<SMAX, FULL>(nd, g);
+        if (Uj) {
+            if constexpr (COH) { /* written by the previous level of this launch: through L2 */
+                uint32_t* w32 = reinterpret_cast<uint32_t*>(&nd);
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(Uj + u);
+#pragma unroll
+                for (int q = 0; q < (int)(sizeof(DNode<SMAX>) / 4); q++) w32[q] = __ldcg(src + q);
+            } else {
+                nd = Uj[u];
+            }
+        } else {
+            dnode_fresh<SMAX, FULL>(nd, g);
+        }
         const uint32_t k = nth_set_bit(full & ~nd.mask, d), c = u * n + k;
         St<SMAX> s, s2;
         node_to_st<SMAX>(nd, s);
@@ -2048,7 +2072,7 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
                  * of a level hits this one counter, so per-thread atomics serialise at L2) */
                 const cg::coalesced_group cl = cg::coalesced_threads();
                 uint32_t base = 0;
-                if (cl.thread_rank() == 0) base = atomicAdd(cnt_n, cl.size());
+                if (cl.thread_rank() == 0) base = atomicAdd(a.cnt_n, cl.size());
                 id = cl.shfl(base, 0) + cl.thread_rank();
                 if (id < cap_n) Un[id] = o;
                 else atomicOr(ovf, 1u);
@@ -2075,8 +2099,45 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables*
             }
             pos = (pos + 1u) & tmask;
         }
-        tid[c] = id;
-        dk[c] = s2.K;
+        a.tid[c] = id;
+        a.dk[c] = s2.K;
+    }
+}
+
+/* One level: nodes of level j (count *cnt_j; nullptr = the fresh root) x unused
+ * kernels; the same launch also runs the previous level's prefix expansion (xp). */
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kDpThreads) rk_dp_level_kernel(const RkTables* __restrict__ tab,
+                                                                const LevelArgs<SMAX> a) {
+    __shared__ RkTables t;
+    load_tables(t, tab);
+    level_body<SMAX, FULL, false>(t, a, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x,
+                                  gridDim.x * (uint64_t)blockDim.x);
+}
+
+/* Several small levels in one cooperative launch (grid-wide barrier between
+ * levels instead of launch boundaries; the levels of a few hundred to a few
+ * ten thousand items are each one dependent chain per item, so a launch per
+ * level mostly pays its own start-up). */
+constexpr int kCoopMaxLevels = 8;
+template <int SMAX>
+struct LevelBatch {
+    LevelArgs<SMAX> a[kCoopMaxLevels];
+    uint32_t nl;
+};
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kDpThreads) rk_dp_levels_coop_kernel(const RkTables* __restrict__ tab,
+                                                                      const LevelBatch<SMAX> b) {
+    __shared__ RkTables t;
+    load_tables(t, tab);
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = gridDim.x * (uint64_t)blockDim.x;
+    for (uint32_t l = 0; l < b.nl; l++) {
+        if (l) {
+            __threadfence();
+            grid.sync();
+        }
+        level_body<SMAX, FULL, true>(t, b.a[l], gtid, nth);
     }
 }
 
@@ -3363,30 +3424,62 @@ uint32_t rk_dp_node_bytes(uint32_t S) {
     }
 }
 
-int rk_dp_level(const RkTables* tab, uint32_t S, const void* Uj, const uint32_t* cnt_j, void* Un, uint32_t* cnt_n,
-                uint32_t cap_n, uint32_t* table, uint32_t tmask, uint32_t* tid, uint64_t* dk, uint32_t* ovf,
-                uint64_t work, void* stream, uint32_t* launches, const RkExpand* ex, uint32_t nrem) {
+namespace {
+template <int SMAX>
+LevelArgs<SMAX> level_args(const RkLevel& l) {
     ExpArgs xp{};
-    if (ex) xp = ExpArgs{(const uint4*)ex->Rj, ex->aj, (uint4*)ex->Rn, ex->an, ex->cnt, ex->j, ex->tid, ex->dk};
-#define RK_DP_LEVEL_ARGS(SMAX) tab, (const DNode<SMAX>*)Uj, cnt_j, (DNode<SMAX>*)Un, cnt_n, cap_n, table, tmask, tid, dk, ovf, xp, nrem
-    const unsigned grid = dp_grid(work > xp.cnt ? work : xp.cnt);
-    cudaStream_t st = (cudaStream_t)stream;
-    switch (variant(S)) {
-        case 0: rk_dp_level_kernel<1, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(1)); break;
-        case 1: rk_dp_level_kernel<2, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(2)); break;
-        case 2: rk_dp_level_kernel<4, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(4)); break;
-        case 3: rk_dp_level_kernel<4, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(4)); break;
-        case 4: rk_dp_level_kernel<8, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(8)); break;
-        case 5: rk_dp_level_kernel<8, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(8)); break;
-        case 6: rk_dp_level_kernel<16, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(16)); break;
-        case 7: rk_dp_level_kernel<16, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(16)); break;
-        case 8: rk_dp_level_kernel<32, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(32)); break;
-        case 9: rk_dp_level_kernel<32, true><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(32)); break;
-        default: rk_dp_level_kernel<0, false><<<grid, kDpThreads, 0, st>>>(RK_DP_LEVEL_ARGS(0)); break;
+    if (l.ex) xp = ExpArgs{(const uint4*)l.ex->Rj, l.ex->aj, (uint4*)l.ex->Rn, l.ex->an, l.ex->cnt, l.ex->j, l.ex->tid,
+                           l.ex->dk};
+    return LevelArgs<SMAX>{(const DNode<SMAX>*)l.Uj, l.cnt_j, (DNode<SMAX>*)l.Un, l.cnt_n, l.cap_n, l.table, l.tmask,
+                           l.tid, l.dk, l.ovf, xp, l.nrem};
+}
+template <int SMAX, bool FULL>
+int launch_levels(const RkTables* tab, const RkLevel* lv, uint32_t nl, cudaStream_t st) {
+    if (nl == 1) {
+        const RkLevel& l = lv[0];
+        const uint64_t xc = l.ex ? l.ex->cnt : 0;
+        rk_dp_level_kernel<SMAX, FULL><<<dp_grid(l.work > xc ? l.work : xc), kDpThreads, 0, st>>>(tab,
+                                                                                               level_args<SMAX>(l));
+        return (int)cudaGetLastError();
     }
-#undef RK_DP_LEVEL_ARGS
+    LevelBatch<SMAX> b{};
+    b.nl = nl;
+    for (uint32_t i = 0; i < nl; i++) b.a[i] = level_args<SMAX>(lv[i]);
+    static int cached[64];
+    const int dev = cur_device();
+    int per = __atomic_load_n(&cached[dev], __ATOMIC_RELAXED);
+    if (!per) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, rk_dp_levels_coop_kernel<SMAX, FULL>, kDpThreads, 0);
+        if (per <= 0) per = 1;
+        __atomic_store_n(&cached[dev], per, __ATOMIC_RELAXED);
+    }
+    const unsigned grid = (unsigned)num_sms() * (unsigned)std::min(per, 2);
+    void* args[] = {(void*)&tab, (void*)&b};
+    return (int)cudaLaunchCooperativeKernel((const void*)rk_dp_levels_coop_kernel<SMAX, FULL>, grid, kDpThreads, args,
+                                            0, st);
+}
+}  // namespace
+
+int rk_dp_levels(const RkTables* tab, uint32_t S, const RkLevel* lv, uint32_t nl, void* stream, uint32_t* launches) {
+    if (nl == 0) return 0;
+    if (nl > (uint32_t)kCoopMaxLevels) return (int)cudaErrorInvalidValue;
+    cudaStream_t st = (cudaStream_t)stream;
+    int e;
+    switch (variant(S)) {
+        case 0: e = launch_levels<1, true>(tab, lv, nl, st); break;
+        case 1: e = launch_levels<2, true>(tab, lv, nl, st); break;
+        case 2: e = launch_levels<4, false>(tab, lv, nl, st); break;
+        case 3: e = launch_levels<4, true>(tab, lv, nl, st); break;
+        case 4: e = launch_levels<8, false>(tab, lv, nl, st); break;
+        case 5: e = launch_levels<8, true>(tab, lv, nl, st); break;
+        case 6: e = launch_levels<16, false>(tab, lv, nl, st); break;
+        case 7: e = launch_levels<16, true>(tab, lv, nl, st); break;
+        case 8: e = launch_levels<32, false>(tab, lv, nl, st); break;
+        case 9: e = launch_levels<32, true>(tab, lv, nl, st); break;
+        default: e = launch_levels<0, false>(tab, lv, nl, st); break;
+    }
     if (launches) (*launches)++;
-    return (int)cudaGetLastError();
+    return e;
 }
 
 int rk_dp_audit(uint32_t S, const void* U, const uint32_t* cnt, uint32_t cap, const uint32_t* table, uint32_t tmask,
