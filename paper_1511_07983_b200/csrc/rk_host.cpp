@@ -560,7 +560,17 @@ int dp_levels(rk_ctx* c, uint32_t j0, uint32_t j1, void* stream, const std::vect
                              (uint32_t*)d.tid.p + d.xoff[j], (uint64_t*)d.dk.p + d.xoff[j], ctr + d.L + 1, x, n - j,
                              d.work[j] / n * (n - j)});
     }
-    return launch_level_run(c, lv, stream);
+    /* the leading levels small enough for one CTA (shared-memory dedup) go to one launch */
+    size_t J = 0;
+    const uint32_t im = (j0 == 0 && !c->no_coop) ? rk_dp_small_items_max(c->tab.g.S) : 0u;
+    while (im && J < lv.size() && J < 4 && lv[J].work <= im) J++;
+    int e = 0;
+    if (J >= 2) {
+        e = rk_dp_small_levels(c->tab_dev, c->tab.g.S, lv.data(), (uint32_t)J, im, stream, &c->launches);
+        lv.erase(lv.begin(), lv.begin() + J);
+    }
+    if (!e) e = launch_level_run(c, lv, stream);
+    return e;
 }
 
 /* Enqueue the level build of the current plan: clear, P levels (+ the given

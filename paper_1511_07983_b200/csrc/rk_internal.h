@@ -148,6 +148,11 @@ struct RkLevel {
 /* nl consecutive levels: one launch for nl == 1, one cooperative launch (grid barriers between levels)
  * for 1 < nl <= 8 */
 int rk_dp_levels(const RkTables* tab, uint32_t S, const RkLevel* lv, uint32_t nl, void* stream, uint32_t* launches);
+/* the first nl (<= 4) levels in one CTA (shared-memory dedup, deterministic ids); each level's live children
+ * must number <= items_max = rk_dp_small_items_max(S) (0: not available for S) */
+uint32_t rk_dp_small_items_max(uint32_t S);
+int rk_dp_small_levels(const RkTables* tab, uint32_t S, const RkLevel* lv, uint32_t nl, uint32_t items_max,
+                       void* stream, uint32_t* launches);
 /* the 24 suffix keys of every level-(P+1) node (row24: nodes x 24 u64) */
 int rk_dp_row24(const RkTables* tab, uint32_t S, const void* U, const uint32_t* cnt, uint64_t* row24, uint64_t nodes,
                 void* stream, uint32_t* launches);

@@ -2141,6 +2141,143 @@ __global__ void __launch_bounds__(kDpThreads) rk_dp_levels_coop_kernel(const RkT
     }
 }
 
+/* The first levels in ONE CTA (shared memory; no global atomics, no fences).
+ * Per level: every live child's state is staged in shared memory; after a
+ * barrier each child inserts its staging index into a shared hash table and,
+ * since every record is already visible, compares records directly (no
+ * claim/publish protocol); the children that own their slot are the level's
+ * distinct states and take ids in item order (a block scan: deterministic
+ * ids); nodes, transitions and the count go to the level arrays in global
+ * memory, and the range's level-(j-1) prefix expansion runs as in the level
+ * kernel.  C4: levels 0-2 (12 + 132 + 1140 children). */
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallMaxLevels = 4;
+template <int SMAX>
+struct SmallLevels {
+    LevelArgs<SMAX> a[kSmallMaxLevels];
+    uint32_t nl, items_max, hmask; /* hash slots = hmask + 1 >= 2 * items_max */
+};
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kSmallThreads) rk_dp_small_levels_kernel(const RkTables* __restrict__ tab,
+                                                                          const SmallLevels<SMAX> b) {
+    __shared__ RkTables t;
+    __shared__ uint32_t s_warp[kSmallThreads / 32];
+    __shared__ uint32_t s_m;
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    load_tables(t, tab);
+    const RkGTab& g = t.g;
+    const uint32_t n = g.n, full = (1u << n) - 1u, IM = b.items_max;
+    DNode<SMAX>* cur = reinterpret_cast<DNode<SMAX>*>(sm_raw);            /* level j nodes (<= IM) */
+    DNode<SMAX>* stg = cur + IM;                                           /* staged children */
+    uint64_t* sdk = reinterpret_cast<uint64_t*>(stg + IM);                 /* their closed-key increments */
+    uint32_t* sc = reinterpret_cast<uint32_t*>(sdk + IM);                  /* their transition index u*n+k */
+    uint32_t* sown = sc + IM;                                              /* their slot owner (staging index) */
+    uint32_t* sid = sown + IM;                                             /* owner -> id (exclusive scan) */
+    uint32_t* ht = sid + IM;                                               /* hash slots */
+    const uint32_t tidx = threadIdx.x, lane = tidx & 31u, wid = tidx >> 5;
+    if (tidx == 0) {
+        dnode_fresh<SMAX, FULL>(cur[0], g);
+        s_m = 1;
+    }
+    __syncthreads();
+    for (uint32_t l = 0; l < b.nl; l++) {
+        const LevelArgs<SMAX>& a = b.a[l];
+        const uint32_t m = s_m, nrem = a.nrem, items = m * nrem;
+        if (items > IM) { /* more children than the staging holds (planning capacities): flag, stop */
+            if (tidx == 0) atomicOr(a.ovf, 1u);
+            return;
+        }
+        /* the range's level j-1 -> j prefix expansion (tables written earlier in this launch) */
+        for (uint64_t x = tidx; x < a.xp.cnt; x += kSmallThreads) expand_one<true>(a.xp, x, n);
+        for (uint32_t i = tidx; i <= b.hmask; i += kSmallThreads) ht[i] = kDpEmpty;
+        NoRec nr;
+        for (uint32_t w = tidx; w < items; w += kSmallThreads) { /* stage every live child */
+            const uint32_t u = w / nrem, d = w - u * nrem;
+            const DNode<SMAX> nd = cur[u];
+            const uint32_t k = nth_set_bit(full & ~nd.mask, d);
+            St<SMAX> s0, s2;
+            node_to_st<SMAX>(nd, s0);
+            place<SMAX, FULL>(s0, s2, t.k[k], k, g, nr);
+            st_to_node<SMAX>(s2, nd.mask | (1u << k), stg[w]);
+            sdk[w] = s2.K;
+            sc[w] = u * n + k;
+        }
+        __syncthreads();
+        for (uint32_t w = tidx; w < items; w += kSmallThreads) { /* insert by staging index, compare records */
+            const DNode<SMAX>& o = stg[w];
+            uint32_t pos = (uint32_t)dnode_hash(o) & b.hmask, own = w;
+            for (;;) {
+                const uint32_t v = atomicCAS(ht + pos, kDpEmpty, w);
+                if (v == kDpEmpty) break;
+                const uint32_t* x = reinterpret_cast<const uint32_t*>(stg + v);
+                const uint32_t* y = reinterpret_cast<const uint32_t*>(&o);
+                bool eq = true;
+#pragma unroll
+                for (int q = 0; q < (int)(sizeof(DNode<SMAX>) / 4); q++) eq &= x[q] == y[q];
+                if (eq) {
+                    own = v;
+                    break;
+                }
+                pos = (pos + 1u) & b.hmask;
+            }
+            sown[w] = own;
+        }
+        __syncthreads();
+        /* ids: owners in item order (block-wide exclusive scan of the owner flags) */
+        uint32_t cnt = 0, flags = 0;
+        const uint32_t per = (items + kSmallThreads - 1) / kSmallThreads, w0 = tidx * per;
+        for (uint32_t q = 0; q < per; q++) {
+            const uint32_t w = w0 + q;
+            const bool f = w < items && sown[w] == w;
+            flags |= (f ? 1u : 0u) << q;
+            cnt += f ? 1u : 0u;
+        }
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t v = lane < kSmallThreads / 32 ? s_warp[lane] : 0u, vi = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, vi, o);
+                if (lane >= (uint32_t)o) vi += y;
+            }
+            if (lane < kSmallThreads / 32) s_warp[lane] = vi - v; /* exclusive warp offsets */
+            if (lane == 31) s_m = vi;                             /* the level's distinct states */
+        }
+        __syncthreads();
+        uint32_t id = s_warp[wid] + incl - cnt;
+        for (uint32_t q = 0; q < per; q++)
+            if ((flags >> q) & 1u) sid[w0 + q] = id++;
+        __syncthreads();
+        const uint32_t mn = s_m;
+        if (tidx == 0) *a.cnt_n = min(mn, a.cap_n);
+        if (mn > a.cap_n || mn > IM) { /* does not fit (planning capacities): flag, stop */
+            if (tidx == 0) atomicOr(a.ovf, 1u);
+            return;
+        }
+        for (uint32_t w = tidx; w < items; w += kSmallThreads) {
+            const uint32_t own = sown[w], nid = sid[own];
+            a.tid[sc[w]] = nid;
+            a.dk[sc[w]] = sdk[w];
+            if (own == w) { /* the node, and its id in the level's global table (distinct states: no compare) */
+                a.Un[nid] = stg[w];
+                uint32_t pos = (uint32_t)dnode_hash(stg[w]) & a.tmask;
+                while (atomicCAS(a.table + pos, kDpEmpty, nid) != kDpEmpty) pos = (pos + 1u) & a.tmask;
+            }
+        }
+        __syncthreads();
+        for (uint32_t w = tidx; w < items; w += kSmallThreads) /* the next level's nodes */
+            if (sown[w] == w) cur[sid[w]] = stg[w];
+        __syncthreads();
+    }
+}
+
 /* Race audit of one level's lock-free hash table after a build (no sanitizer
  * on this pool): bad[0] count over capacity, bad[1] slots left
  * BUSY (a claim never published), bad[2] published ids >= count, bad[3] nodes
@@ -3459,6 +3596,63 @@ int launch_levels(const RkTables* tab, const RkLevel* lv, uint32_t nl, cudaStrea
                                             0, st);
 }
 }  // namespace
+
+namespace {
+template <int SMAX, bool FULL>
+int launch_small(const RkTables* tab, const RkLevel* lv, uint32_t nl, uint32_t items_max, cudaStream_t st) {
+    SmallLevels<SMAX> b{};
+    b.nl = nl;
+    b.items_max = items_max;
+    uint32_t h = 1;
+    while (h < 2 * items_max) h <<= 1;
+    b.hmask = h - 1;
+    for (uint32_t i = 0; i < nl; i++) b.a[i] = level_args<SMAX>(lv[i]);
+    const size_t smem = (size_t)items_max * (2 * sizeof(DNode<SMAX>) + 8 + 4 * 3) + (size_t)h * 4;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rk_dp_small_levels_kernel<SMAX, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    rk_dp_small_levels_kernel<SMAX, FULL><<<1, kSmallThreads, smem, st>>>(tab, b);
+    return (int)cudaGetLastError();
+}
+}  // namespace
+
+uint32_t rk_dp_small_items_max(uint32_t S) {
+    const size_t budget = 190 * 1024; /* dynamic shared memory of the small-levels kernel */
+    size_t node;
+    switch (variant(S)) {
+        case 0: node = sizeof(DNode<1>); break;
+        case 1: node = sizeof(DNode<2>); break;
+        case 2: case 3: node = sizeof(DNode<4>); break;
+        case 4: case 5: node = sizeof(DNode<8>); break;
+        case 6: case 7: node = sizeof(DNode<16>); break;
+        case 8: case 9: node = sizeof(DNode<32>); break;
+        default: return 0; /* run-length nodes: no small-levels kernel */
+    }
+    return (uint32_t)(budget / (2 * node + 8 + 12 + 8)) & ~31u;
+}
+
+int rk_dp_small_levels(const RkTables* tab, uint32_t S, const RkLevel* lv, uint32_t nl, uint32_t items_max,
+                       void* stream, uint32_t* launches) {
+    if (nl == 0) return 0;
+    if (nl > (uint32_t)kSmallMaxLevels) return (int)cudaErrorInvalidValue;
+    cudaStream_t st = (cudaStream_t)stream;
+    int e;
+    switch (variant(S)) {
+        case 0: e = launch_small<1, true>(tab, lv, nl, items_max, st); break;
+        case 1: e = launch_small<2, true>(tab, lv, nl, items_max, st); break;
+        case 2: e = launch_small<4, false>(tab, lv, nl, items_max, st); break;
+        case 3: e = launch_small<4, true>(tab, lv, nl, items_max, st); break;
+        case 4: e = launch_small<8, false>(tab, lv, nl, items_max, st); break;
+        case 5: e = launch_small<8, true>(tab, lv, nl, items_max, st); break;
+        case 6: e = launch_small<16, false>(tab, lv, nl, items_max, st); break;
+        case 7: e = launch_small<16, true>(tab, lv, nl, items_max, st); break;
+        case 8: e = launch_small<32, false>(tab, lv, nl, items_max, st); break;
+        case 9: e = launch_small<32, true>(tab, lv, nl, items_max, st); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+    if (launches) (*launches)++;
+    return e;
+}
 
 int rk_dp_levels(const RkTables* tab, uint32_t S, const RkLevel* lv, uint32_t nl, void* stream, uint32_t* launches) {
     if (nl == 0) return 0;
