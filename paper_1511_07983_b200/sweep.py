@@ -107,8 +107,9 @@ class Sweeper:
             self.compact = True
             if self.keys32 is None or self.keys32.numel() < self.count:
                 self.keys32 = torch.empty(max(1, self.count), dtype=torch.int32, device=self.dev)
-            # the u64 buffer a set whose keys overflow the offsets falls back to, allocated up front
-            if self.keys is None or self.keys.numel() < self.count:
+            # the u64 buffer a set whose keys overflow the offsets falls back to: allocated up front
+            # when modest (<= 8 GB), else on the first overflow
+            if (self.keys is None or self.keys.numel() < self.count) and self.count * 8 <= (8 << 30):
                 self.keys = torch.empty(max(1, self.count), dtype=torch.int64, device=self.dev)
         else:
             self._use_wide_keys()

@@ -20,17 +20,23 @@ from paper_1511_07983_b200.sweep import Sweeper  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
+ap.add_argument("--n", type=int, default=0, help="a Generator-G set of n kernels (seed SEED_BASE + 1000 n) instead")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--gs", default="1,2,4,8")
 ap.add_argument("--coll-us", type=float, default=15.0)
 args = ap.parse_args()
-gpu, ks = W.config(args.config)
+if args.n:
+    gpu, ks = W.GTX580, W.gen_g(W.SplitMix64(W.SEED_BASE + 1000 * args.n), args.n)
+    args.config = f"G{args.n}"
+else:
+    gpu, ks = W.config(args.config)
 N = math.factorial(len(ks))
 sw = Sweeper(gpu, device=0, compact_keys=True)
 sw.set_kernels(ks)
 _, idx = sw.heuristic()
 stream = torch.cuda.current_stream()
 res = {}
-for G in (1, 2, 4, 8):
+for G in [int(x) for x in args.gs.split(",")]:
     per = []
     for g in range(G):
         sw.first, sw.count = shard_bounds(N, G, g)
