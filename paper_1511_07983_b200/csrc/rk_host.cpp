@@ -782,14 +782,16 @@ RkRows dp_rows(rk_ctx* c, uint64_t nrun) {
                   (uint32_t*)d.counters.p + d.L + 3};
 }
 
-/* Pass 1 of the memoised step: the levels rebuilt from scratch with the
- * range's prefixes expanded breadth-first (levels 1..P-1 when the range has
- * <= 2^27 runs; level P recomputed by the run pass), then — concurrently — the
- * suffix rows (main stream) and the run pass (side stream: each run's (node,
- * K_closed) and the row multiset), then the extremes pass (the key stream's
- * metadata and the range's extremes record: n_lt = n_eq = 0, n_gt = evaluated
- * = count).  RK_OVERLAP=0 runs the run pass on the main stream. */
-int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool keys_hint, void* stream) {
+/* Pass 1 of the memoised step: the levels rebuilt from scratch (the first
+ * step after a plan runs over the plan's build) with the range's prefixes
+ * expanded breadth-first (levels 1..P-1 when the range has <= 2^27 runs;
+ * level P recomputed by the run pass); then, concurrently, level P+1, row24
+ * and the suffix rows (main stream) and the run pass with the row multiset
+ * (side stream: each run's (node, K_closed); parents and children multisets);
+ * then the extremes from the distinct rows (the range's record: n_lt = n_eq =
+ * 0, n_gt = evaluated = count).  RK_OVERLAP=0 keeps everything on the main
+ * stream. */
+int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void* stream) {
     DpPlan& d = c->dp;
     d.runs_ok = false;
     /* the first step after the plan runs over the plan's build (upper-bound layout); later ones rebuild */
@@ -805,7 +807,6 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, bool 
     const uint64_t rb = first / DF, re = count ? (first + count + DF - 1) / DF : rb;
     std::vector<RkExpand> ex;
     const uint64_t nrun = std::max<uint64_t>(re - rb, 1);
-    (void)keys_hint;
     cudaStream_t st = (cudaStream_t)stream;
     int e = d.meta_u.reserve(nrun * 4);
     if (!e) e = d.meta_K.reserve(nrun * 8);
@@ -967,7 +968,7 @@ int dp_eval(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev,
     const uint64_t DF = c->dp.view.Dfact;
     const uint64_t nrun = count ? (first + count + DF - 1) / DF - first / DF : 0;
     if (nrun <= kChunkRuns) {
-        int e = dp_pass1(c, first, count, stats_dev, keys_dev != nullptr, stream);
+        int e = dp_pass1(c, first, count, stats_dev, stream);
         if (!e) e = dp_pass2(c, first, count, cand_dev, range_dev, bins, hist_dev, keys_dev, stats_dev, stream);
         return e;
     }
@@ -977,7 +978,7 @@ int dp_eval(rk_ctx* c, uint64_t first, uint64_t count, const uint64_t* cand_dev,
     for (uint64_t lo = first, end = first + count; lo < end && !e;) {
         const uint64_t hi = std::min(end, (lo / DF + kChunkRuns) * DF);
         rk_stats* out = lo == first ? stats_dev : part + 1;
-        e = dp_pass1(c, lo, hi - lo, out, keys_dev != nullptr, stream);
+        e = dp_pass1(c, lo, hi - lo, out, stream);
         if (!e)
             e = dp_pass2(c, lo, hi - lo, cand_dev, range_dev, bins, hist_dev, keys_dev ? keys_dev + (lo - first) : nullptr,
                          out, stream);
@@ -1211,7 +1212,7 @@ rk_status rk_sweep_pass1_async(rk_ctx* c, uint64_t first, uint64_t count, const 
     c->launches = 0;
     int e;
     if (c->dp.on) {
-        e = dp_pass1(c, first, count, rec_dev, keys_dev != nullptr, stream);
+        e = dp_pass1(c, first, count, rec_dev, stream);
     } else {
         const int m = tmark_begin(c, RK_PHASE_DIRECT, stream);
         e = rk_launch_eval(c->tab_dev, c->tab.g.n, vS(c, c->tab.g.S), first, count, cand_key_dev, 0, rec_dev, keys_dev,
