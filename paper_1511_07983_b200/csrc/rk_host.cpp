@@ -811,7 +811,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
     int e = d.meta_u.reserve(nrun * 4);
     if (!e) e = d.meta_K.reserve(nrun * 8);
     /* row multiset: ~8 runs per slot (C4: 217,659 distinct rows of 3,991,680 runs in 2^19 slots) */
-    const uint64_t slots = std::min<uint64_t>(std::max<uint64_t>(pow2_at_least(nrun / 8), 4096), 1ull << 22);
+    const uint64_t slots = std::min<uint64_t>(std::max<uint64_t>(pow2_at_least(nrun / 8), 4096), 1ull << 24); /* 16M slots: 13! has millions of distinct rows */
     d.rmask = (uint32_t)(slots - 1);
     if (!e) e = d.rslot.reserve(slots * 16);
     if (!e) e = d.rmult.reserve(slots * 4 * 8); /* 8 counters per slot */
@@ -849,7 +849,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
     uint64_t pslots = 0;
     if (hier) {
         const uint64_t npar = ex.back().cnt ? (re - 1) / (n - P + 1) - ex.back().aj + 1 : 1;
-        pslots = std::min<uint64_t>(std::max<uint64_t>(pow2_at_least(npar / 4), 4096), 1ull << 22);
+        pslots = std::min<uint64_t>(std::max<uint64_t>(pow2_at_least(npar / 4), 4096), 1ull << 23);
         d.pmask = (uint32_t)(pslots - 1);
         if (!e) e = d.pslot.reserve(pslots * 16);
         if (!e) e = d.pmult.reserve(pslots * 32);
