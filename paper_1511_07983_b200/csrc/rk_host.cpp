@@ -109,7 +109,8 @@ struct rk_ctx {
     int row_dedup = -1, overlap = -1;
     bool dedup_now = false;  /* the current range's counts/histogram come from the row multiset */
     uint32_t rows_ctas = 2;  /* RK_ROWS_CTAS: its CTAs per SM when overlapped */
-    cudaStream_t side = nullptr;
+    cudaStream_t side = nullptr;    /* pass 2's side stream (high priority) */
+    cudaStream_t side1 = nullptr;   /* pass 1's side stream (the default priority: the suffix rows go first) */
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     DpPlan dp;
     /* optional per-phase device timing (rk_set_timing): event pairs recorded on
@@ -601,13 +602,17 @@ int dp_build_suffix(rk_ctx* c, void* stream) {
     return e;
 }
 
-/* the ctx's high-priority side stream and its fork/join events */
+/* the ctx's side streams and their fork/join events: pass 2's counts/histogram at high priority (they
+ * should slip in beside the HBM-bound key stream), pass 1's run pass at the default priority (the suffix
+ * rows on the main stream are the longer chain); RK_SIDE_PRIO=0|1 puts both at default|high (testing) */
 int ensure_side(rk_ctx* c) {
     if (c->side) return 0;
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    const char* pr = getenv("RK_SIDE_PRIO"); /* testing: 0 = the default priority */
-    int e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, (pr && pr[0] == '0') ? lo : hi);
+    const char* pr = getenv("RK_SIDE_PRIO");
+    const int p2 = (pr && pr[0] == '0') ? lo : hi, p1 = (pr && pr[0] == '1') ? hi : lo;
+    int e = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, p2);
+    if (!e) e = cudaStreamCreateWithPriority(&c->side1, cudaStreamNonBlocking, p1);
     if (!e) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
     if (!e) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
     return e;
@@ -876,9 +881,9 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
                                  (uint32_t*)d.counters.p + d.L + 1, &ex[j - 1], 0, 0});
         if (!e) e = launch_level_run(c, lv, stream);
     }
-    void* rs = side ? (void*)c->side : stream;
+    void* rs = side ? (void*)c->side1 : stream;
     if (!e && side) e = cudaEventRecord(c->ev_fork, st);
-    if (!e && side) e = cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    if (!e && side) e = cudaStreamWaitEvent(c->side1, c->ev_fork, 0);
     if (!e && !side && !ub) e = dp_levels(c, P, d.L, stream, nullptr);
     const int mr = tmark_begin(c, RK_PHASE_RUNS, rs);
     RkRows runrows = dp_rows(c, re - rb);
@@ -895,7 +900,7 @@ int dp_pass1(rk_ctx* c, uint64_t first, uint64_t count, rk_stats* rec_dev, void*
         e = rk_dp_multiset(n, first, count, &parent_level, parents, dp_rows(c, re - rb), rs, &c->launches);
     }
     tmark_end(c, mr, rs);
-    if (!e && side) e = cudaEventRecord(c->ev_join, c->side);
+    if (!e && side) e = cudaEventRecord(c->ev_join, c->side1);
     if (!e && side && !ub) e = dp_levels(c, P, d.L, stream, nullptr);
     if (!e) e = dp_build_suffix(c, stream);
     tmark_end(c, m0, stream);
@@ -1061,6 +1066,7 @@ void rk_destroy(rk_ctx* c) {
         for (cudaEvent_t ev : c->tev) cudaEventDestroy(ev);
         if (c->side) {
             cudaStreamDestroy(c->side);
+            cudaStreamDestroy(c->side1);
             cudaEventDestroy(c->ev_fork);
             cudaEventDestroy(c->ev_join);
         }
