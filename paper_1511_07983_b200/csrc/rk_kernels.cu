@@ -341,6 +341,58 @@ __device__ __forceinline__ uint32_t water_fill(uint32_t n, const uint32_t (&c)[S
     return nc >= S ? nc - S : nc; /* cursor = SM of the last block + 1 */
 }
 
+/* Strict round robin (RK_FLAG_STRICT_RR, L4 read literally): block b of the
+ * kernel goes to SM (cur + b) mod S; out of line, so the default path keeps
+ * its register allocation. */
+template <int SMAX, bool FULL, class R, class U>
+__device__ __noinline__ Placed place_strict(const St<SMAX>& in, const uint32_t (&c)[SMAX], const RkKTab& k,
+                                            uint32_t kid, const RkGTab& g, R& rec, U& upd) {
+    uint32_t n = k.T;
+    Placed o;
+    const uint32_t S = nsm<SMAX, FULL>(g);
+    const uint32_t cur = (g.flags & RK_FLAG_CURSOR_PER_KERNEL) ? 0u : in.cur;
+    uint32_t m = 0xFFFFFFFFu; /* the first block that does not fit on its SM */
+#pragma unroll
+    for (int i = 0; i < SMAX; i++) {
+        const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+        if (live_sm<SMAX, FULL>(i, g)) m = min(m, d + c[i] * S);
+    }
+    if (n <= m) {
+        o.cur = (cur + n) % S;
+        upd.set_cursor(o.cur);
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+            const uint32_t x = d < n ? (n - d - 1u) / S + 1u : 0u;
+            upd(i, in.fa[i] - x * k.dA, in.fb[i] - x * k.dB);
+        }
+        o.I = in.I + (uint64_t)n * k.cA;
+        o.M = in.M + (uint64_t)n * k.cM;
+        o.K = in.K;
+    } else { /* m blocks close the round; full rounds of S*C; the rest from SM 0 of a fresh round */
+        rec.add(kid, m);
+        rec.close();
+        const uint32_t nfull = full_rounds(n - m - 1u, k);
+        rec.full(kid, nfull, k.SC);
+        o.K = in.K + round_key(in.I + (uint64_t)m * k.cA, in.M + (uint64_t)m * k.cM, g.num, g.den) +
+              (uint64_t)nfull * k.fullkey;
+        n -= m + nfull * k.SC;
+        const uint32_t q = n / S, r = n - q * S;
+        o.cur = r;
+        upd.set_cursor(r);
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            const uint32_t x = q + ((uint32_t)i < r ? 1u : 0u);
+            if (live_sm<SMAX, FULL>(i, g)) upd(i, g.freshA - x * k.dA, g.freshB - x * k.dB);
+            else upd(i, 0u, 0u);
+        }
+        o.I = (uint64_t)n * k.cA;
+        o.M = (uint64_t)n * k.cM;
+    }
+    rec.add(kid, n);
+    return o;
+}
+
 /* Dispatch all T_k blocks of kernel k on state `in`; the new
  * per-SM words are handed to upd(i, fa, fb) so callers either store them
  * (a new state) or consume them on the fly (the fused last level). */
@@ -357,50 +409,7 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
     }
     uint32_t n = k.T;
     Placed o;
-    if (g.flags & RK_FLAG_STRICT_RR) { /* L4 read literally: block b of the kernel goes to SM (cur + b) mod S */
-        const uint32_t S = nsm<SMAX, FULL>(g);
-        const uint32_t cur = (g.flags & RK_FLAG_CURSOR_PER_KERNEL) ? 0u : in.cur;
-        uint32_t m = 0xFFFFFFFFu; /* the first block that does not fit on its SM */
-#pragma unroll
-        for (int i = 0; i < SMAX; i++) {
-            const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
-            if (live_sm<SMAX, FULL>(i, g)) m = min(m, d + c[i] * S);
-        }
-        if (n <= m) {
-            o.cur = (cur + n) % S;
-            upd.set_cursor(o.cur);
-#pragma unroll
-            for (int i = 0; i < SMAX; i++) {
-                const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
-                const uint32_t x = d < n ? (n - d - 1u) / S + 1u : 0u;
-                upd(i, in.fa[i] - x * k.dA, in.fb[i] - x * k.dB);
-            }
-            o.I = in.I + (uint64_t)n * k.cA;
-            o.M = in.M + (uint64_t)n * k.cM;
-            o.K = in.K;
-        } else { /* m blocks close the round; full rounds of S*C; the rest from SM 0 of a fresh round */
-            rec.add(kid, m);
-            rec.close();
-            const uint32_t nfull = full_rounds(n - m - 1u, k);
-            rec.full(kid, nfull, k.SC);
-            o.K = in.K + round_key(in.I + (uint64_t)m * k.cA, in.M + (uint64_t)m * k.cM, g.num, g.den) +
-                  (uint64_t)nfull * k.fullkey;
-            n -= m + nfull * k.SC;
-            const uint32_t q = n / S, r = n - q * S;
-            o.cur = r;
-            upd.set_cursor(r);
-#pragma unroll
-            for (int i = 0; i < SMAX; i++) {
-                const uint32_t x = q + ((uint32_t)i < r ? 1u : 0u);
-                if (live_sm<SMAX, FULL>(i, g)) upd(i, g.freshA - x * k.dA, g.freshB - x * k.dB);
-                else upd(i, 0u, 0u);
-            }
-            o.I = (uint64_t)n * k.cA;
-            o.M = (uint64_t)n * k.cM;
-        }
-        rec.add(kid, n);
-        return o;
-    }
+    if (g.flags & RK_FLAG_STRICT_RR) return place_strict<SMAX, FULL>(in, c, k, kid, g, rec, upd);
     const bool ovf = n > F;
     /* n > F: every SM takes its c_s and the next block fits nowhere, so the round
      * closes; complete single-kernel rounds follow; the rest opens a
