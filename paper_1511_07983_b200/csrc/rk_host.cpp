@@ -94,6 +94,8 @@ struct rk_ctx {
     uint32_t* counter_dev = nullptr;  /* last-CTA counter (self-resetting) */
     rk_stats* stats_dev = nullptr;    /* one record for the synchronous calls */
     uint64_t* u64_dev = nullptr;      /* small scratch (indices / keys) */
+    void* batch_scratch = nullptr;    /* rk_eval_batch's memoised kernel: prefix states + rows per CTA */
+    size_t batch_scratch_bytes = 0;
     uint32_t max_ctas = 0;
     uint32_t sms = 0;                 /* SM count of `device` */
     uint32_t launches = 0;
@@ -1063,6 +1065,7 @@ void rk_destroy(rk_ctx* c) {
         cudaFree(c->counter_dev);
         cudaFree(c->stats_dev);
         cudaFree(c->u64_dev);
+        cudaFree(c->batch_scratch);
         for (cudaEvent_t ev : c->tev) cudaEventDestroy(ev);
         if (c->side) {
             cudaStreamDestroy(c->side);
@@ -1650,12 +1653,34 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     uint32_t smax_k = 0;
     for (uint32_t q = 0; q < n_sets; q++) smax_k = std::max(smax_k, vS(c, ptabs[q].g.S));
     if (!e) e = rk_launch_keys_of(tabs_dev, n, smax_k, idx_dev, n_sets, keys_dev, stream, &c->launches);
+    /* groups on S' <= 2 run the memoised batch kernel (RK_NO_MEMO=1: the direct one) */
+    auto memo_group = [&](uint32_t S) { return !c->no_memo && !(S & RK_S_POLICY) && rk_batch_memo_ok(n, S); };
+    size_t memo_bytes = 0;
+    for (uint32_t a = 0; a < n_sets;) {
+        uint32_t b = a;
+        while (b < n_sets && ptabs[b].g.S == ptabs[a].g.S) b++;
+        const uint32_t S = vS(c, ptabs[a].g.S);
+        if (memo_group(S))
+            memo_bytes = std::max(memo_bytes, rk_batch_memo_scratch(n, S, rk_batch_memo_grid(S, b - a)));
+        a = b;
+    }
+    if (!e && memo_bytes > c->batch_scratch_bytes) { /* grow-only, kept by the context */
+        cudaFree(c->batch_scratch);
+        c->batch_scratch = nullptr;
+        c->batch_scratch_bytes = 0;
+        e = cudaMalloc(&c->batch_scratch, memo_bytes);
+        if (!e) c->batch_scratch_bytes = memo_bytes;
+    }
     for (uint32_t a = 0; a < n_sets && !e;) {
         uint32_t b = a;
         while (b < n_sets && ptabs[b].g.S == ptabs[a].g.S) b++;
         const uint32_t S = vS(c, ptabs[a].g.S), chunks = (uint32_t)rk_batch_chunks_per_set(n, S);
-        e = rk_launch_batch(tabs_dev + a, n, S | 0x80000000u, b - a, keys_dev + a, out_dev + a, recs, chunks, stream,
-                            &c->launches);
+        if (memo_group(S))
+            e = rk_launch_batch_memo(tabs_dev + a, n, S, b - a, keys_dev + a, out_dev + a, c->batch_scratch,
+                                     (uint32_t)rk_batch_memo_grid(S, b - a), stream, &c->launches);
+        else
+            e = rk_launch_batch(tabs_dev + a, n, S | 0x80000000u, b - a, keys_dev + a, out_dev + a, recs, chunks,
+                                stream, &c->launches);
         a = b;
     }
     std::vector<uint64_t> keys(n_sets);

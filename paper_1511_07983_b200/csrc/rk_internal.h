@@ -97,6 +97,14 @@ int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n
 int rk_launch_heuristic(const rk_kernel* sets_dev, uint32_t n, uint32_t n_sets, const rk_gpu_params* p,
                         int32_t* orders_dev, uint64_t* index_dev, void* stream, uint32_t* launches);
 int rk_batch_chunks_per_set(uint32_t n, uint32_t S);
+/* memoised batch: 6 <= n <= 9 on S' <= 2 (one CTA per set, persistent grid;
+ * scratch = rk_batch_memo_scratch(S, grid) bytes of device memory) */
+bool rk_batch_memo_ok(uint32_t n, uint32_t S);
+int rk_batch_memo_grid(uint32_t S, uint32_t n_sets);
+size_t rk_batch_memo_scratch(uint32_t n, uint32_t S, uint32_t grid);
+int rk_launch_batch_memo(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n_sets,
+                         const uint64_t* cand_keys_dev, rk_stats* out_dev, void* scratch, uint32_t grid, void* stream,
+                         uint32_t* launches);
 int rk_eval_max_ctas(uint32_t S, int device);
 /* branch-and-bound exact optimum: gb_dev = 48-B BnbGlobal (best seeded, rest 0),
  * recs_dev = 2*rk_bnb_ctas() u64 */

@@ -341,58 +341,6 @@ __device__ __forceinline__ uint32_t water_fill(uint32_t n, const uint32_t (&c)[S
     return nc >= S ? nc - S : nc; /* cursor = SM of the last block + 1 */
 }
 
-/* Strict round robin (RK_FLAG_STRICT_RR, L4 read literally): block b of the
- * kernel goes to SM (cur + b) mod S; out of line, so the default path keeps
- * its register allocation. */
-template <int SMAX, bool FULL, class R, class U>
-__device__ __noinline__ Placed place_strict(const St<SMAX>& in, const uint32_t (&c)[SMAX], const RkKTab& k,
-                                            uint32_t kid, const RkGTab& g, R& rec, U& upd) {
-    uint32_t n = k.T;
-    Placed o;
-    const uint32_t S = nsm<SMAX, FULL>(g);
-    const uint32_t cur = (g.flags & RK_FLAG_CURSOR_PER_KERNEL) ? 0u : in.cur;
-    uint32_t m = 0xFFFFFFFFu; /* the first block that does not fit on its SM */
-#pragma unroll
-    for (int i = 0; i < SMAX; i++) {
-        const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
-        if (live_sm<SMAX, FULL>(i, g)) m = min(m, d + c[i] * S);
-    }
-    if (n <= m) {
-        o.cur = (cur + n) % S;
-        upd.set_cursor(o.cur);
-#pragma unroll
-        for (int i = 0; i < SMAX; i++) {
-            const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
-            const uint32_t x = d < n ? (n - d - 1u) / S + 1u : 0u;
-            upd(i, in.fa[i] - x * k.dA, in.fb[i] - x * k.dB);
-        }
-        o.I = in.I + (uint64_t)n * k.cA;
-        o.M = in.M + (uint64_t)n * k.cM;
-        o.K = in.K;
-    } else { /* m blocks close the round; full rounds of S*C; the rest from SM 0 of a fresh round */
-        rec.add(kid, m);
-        rec.close();
-        const uint32_t nfull = full_rounds(n - m - 1u, k);
-        rec.full(kid, nfull, k.SC);
-        o.K = in.K + round_key(in.I + (uint64_t)m * k.cA, in.M + (uint64_t)m * k.cM, g.num, g.den) +
-              (uint64_t)nfull * k.fullkey;
-        n -= m + nfull * k.SC;
-        const uint32_t q = n / S, r = n - q * S;
-        o.cur = r;
-        upd.set_cursor(r);
-#pragma unroll
-        for (int i = 0; i < SMAX; i++) {
-            const uint32_t x = q + ((uint32_t)i < r ? 1u : 0u);
-            if (live_sm<SMAX, FULL>(i, g)) upd(i, g.freshA - x * k.dA, g.freshB - x * k.dB);
-            else upd(i, 0u, 0u);
-        }
-        o.I = (uint64_t)n * k.cA;
-        o.M = (uint64_t)n * k.cM;
-    }
-    rec.add(kid, n);
-    return o;
-}
-
 /* Dispatch all T_k blocks of kernel k on state `in`; the new
  * per-SM words are handed to upd(i, fa, fb) so callers either store them
  * (a new state) or consume them on the fly (the fused last level). */
@@ -407,9 +355,29 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
         c[i] = cap1(in.fa[i], in.fb[i], ck);
         F += c[i];
     }
+    if (g.flags & RK_FLAG_STRICT_RR) {
+        /* L4 read literally: block b goes to SM (cur + b) mod S, so the round holds
+         * m = min_s ((s - cur) mod S + c_s S) of them (m <= F: SM s receives
+         * ceil((m - d_s) / S) <= c_s).  Up to m blocks that round robin never meets
+         * a full SM, so the water-fill below places them identically; beyond m the
+         * round closes and the rest is the same fresh-round fill — strict RR is the
+         * default dispatch with F := m. */
+        const uint32_t S = nsm<SMAX, FULL>(g);
+        const uint32_t cur = (g.flags & RK_FLAG_CURSOR_PER_KERNEL) ? 0u : in.cur;
+        uint32_t m = 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i < SMAX; i++) {
+            const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+            if (live_sm<SMAX, FULL>(i, g)) m = min(m, d + c[i] * S);
+        }
+        F = min(F, m);
+        /* the new cursor, for consumers that need it before the words (StrictCapUpd) */
+        const uint32_t n = k.T;
+        const uint32_t nr = n > F ? n - F - full_rounds(n - F - 1u, k) * k.SC : cur + n;
+        upd.set_cursor(nr % S);
+    }
     uint32_t n = k.T;
     Placed o;
-    if (g.flags & RK_FLAG_STRICT_RR) return place_strict<SMAX, FULL>(in, c, k, kid, g, rec, upd);
     const bool ovf = n > F;
     /* n > F: every SM takes its c_s and the next block fits nowhere, so the round
      * closes; complete single-kernel rounds follow; the rest opens a
@@ -693,7 +661,7 @@ __device__ __forceinline__ uint64_t place_finish(const St<SMAX>& in, const RkKTa
         rle_place(in, s1, kb, kbid, g, nr);
         return finish<0>(s1, kc, kcid, g, nr);
     } else {
-        if (g.flags & RK_FLAG_STRICT_RR) {
+        if (g.flags & RK_FLAG_STRICT_RR) { /* kc's fit depends on kb's new cursor (set before the words) */
             StrictCapUpd u{capk(kc), nsm<SMAX, FULL>(g), 0u, 0xFFFFFFFFu, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0};
             const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
             return finish_key(u.m, o.I, o.M, o.K, kc, kcid, g, nr);
@@ -1158,6 +1126,227 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     eval_space<SMAX, FULL>(t, lo, hi, threadIdx.x, blockDim.x, leaf);
     const rk_stats r = block_reduce(to_rec(ts));
     if (threadIdx.x == 0) recs[set * gridDim.x + blockIdx.x] = r;
+}
+
+/* C5 batch with suffix memoisation: one CTA per set, persistent over the sets.
+ * K only accumulates closed rounds (the order's key is
+ * the sum of its rounds' keys), so the key of an order is K_prefix + g(state
+ * after its (n-5)-prefix with K = 0, remaining kernels): runs whose prefix
+ * states agree on the per-SM words, cursor, open round (I, M) and remaining
+ * set share one 120-key suffix row.  (A) prefix state of every run; (B) exact
+ * dedup in a shared-memory hash table (fingerprint, then full compare against
+ * the representative); (C) the rows of the distinct states, each split five
+ * ways at its first suffix position; (D) each row's extremes; (E) per run:
+ * extremes from its row's, counts against the candidate from its row's range
+ * (whole-row scan only where the range straddles the candidate); smallest
+ * index on ties, as the direct kernels. */
+constexpr int kMemoD = 5;                /* rows of 5! = 120 keys */
+constexpr uint32_t kMemoRow = 120;
+constexpr uint32_t kMemoRunsMax = 4096;  /* n <= 9: 9!/120 = 3024 runs */
+constexpr uint32_t kMemoHT = 4096;       /* slots: fingerprint (44 b) | representative run (20 b) */
+constexpr size_t kMemoSmem = kMemoHT * 8 + kMemoRunsMax * 8 + 3 * kMemoRunsMax * 2;
+
+template <int SMAX>
+struct MemoRun {
+    St<SMAX> s;
+    uint32_t L; /* remaining kernels, ascending nibbles */
+};
+
+template <int SMAX>
+__device__ __forceinline__ uint64_t memo_fp(const St<SMAX>& s, uint32_t L) {
+    uint64_t h = ((uint64_t)L << 32 | s.cur) * 0x9E3779B97F4A7C15ull;
+    h = (h ^ (h >> 31) ^ s.I) * 0xBF58476D1CE4E5B9ull;
+    h = (h ^ (h >> 29) ^ s.M) * 0x94D049BB133111EBull;
+#pragma unroll
+    for (int i = 0; i < SMAX; i++) h = (h ^ (h >> 32) ^ ((uint64_t)s.fa[i] << 32 | s.fb[i])) * 0x9E3779B97F4A7C15ull;
+    return (h ^ (h >> 30)) >> 20;
+}
+
+template <int SMAX>
+__device__ __forceinline__ bool memo_eq(const MemoRun<SMAX>& a, const MemoRun<SMAX>& b) {
+    bool e = a.L == b.L && a.s.cur == b.s.cur && a.s.I == b.s.I && a.s.M == b.s.M;
+#pragma unroll
+    for (int i = 0; i < SMAX; i++) e = e && a.s.fa[i] == b.s.fa[i] && a.s.fb[i] == b.s.fb[i];
+    return e;
+}
+
+struct MemoRowStat {
+    uint64_t mn, mx;
+    uint32_t a; /* offset of the first minimum | offset of the first maximum << 8 */
+};
+
+struct RowLeaf {
+    uint64_t* row;
+    __device__ __forceinline__ void operator()(uint32_t off, uint64_t K) { row[off] = K; }
+    __device__ __forceinline__ void pair(uint32_t off, uint64_t K0, uint64_t K1) {
+        row[off] = K0;
+        row[off + 1u] = K1;
+    }
+};
+
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
+    rk_batch_memo_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ cand_keys, uint32_t n_sets,
+                         uint32_t stride, MemoRun<SMAX>* __restrict__ scratch_runs,
+                         uint64_t* __restrict__ scratch_rows, MemoRowStat* __restrict__ scratch_rst,
+                         rk_stats* __restrict__ out) {
+    __shared__ RkTables t;
+    __shared__ uint32_t nd;
+    extern __shared__ uint64_t memo_smem[];
+    uint64_t* ht = memo_smem;                                   /* [kMemoHT] */
+    uint64_t* Kp = ht + kMemoHT;                                /* [kMemoRunsMax] prefix K of each run */
+    uint16_t* rep = reinterpret_cast<uint16_t*>(Kp + kMemoRunsMax); /* run -> representative run -> row */
+    uint16_t* did = rep + kMemoRunsMax;                         /* representative run -> row */
+    uint16_t* repr = did + kMemoRunsMax;                        /* row -> representative run */
+    MemoRun<SMAX>* R = scratch_runs + (size_t)blockIdx.x * stride; /* stride = n!/120 runs per set */
+    uint64_t* rows = scratch_rows + (size_t)blockIdx.x * stride * kMemoRow;
+    MemoRowStat* rst = scratch_rst + (size_t)blockIdx.x * stride;
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    NoRec nr;
+    for (uint32_t set = blockIdx.x; set < n_sets; set += gridDim.x) {
+        __syncthreads(); /* the previous set is done with the shared arrays */
+        for (uint32_t i = tid; i < kMemoHT; i += nth) ht[i] = ~0ull;
+        if (tid == 0) nd = 0;
+        load_tables(t, tabs + set); /* (includes the barrier) */
+        const RkGTab& g = t.g;
+        const uint32_t n = g.n;
+        const uint32_t runs = (uint32_t)(g.fact[n] / kMemoRow);
+        /* (A) the (n-5)-prefix of run r = indices [120 r, 120 r + 120) */
+        for (uint32_t r = tid; r < runs; r += nth) {
+            St<SMAX> s;
+            st_fresh<SMAX, FULL>(s, g);
+            uint64_t L = identity_list(n);
+            uint32_t rem = r * kMemoRow;
+            for (uint32_t j = 0; j + kMemoD < n; j++) {
+                const uint32_t f = (uint32_t)g.fact[n - 1 - j];
+                const uint32_t d = rem / f;
+                rem -= d * f;
+                const uint32_t k = take_nibble(L, d);
+                place<SMAX, FULL>(s, s, t.k[k], k, g, nr);
+            }
+            Kp[r] = s.K;
+            R[r].s = s;
+            R[r].L = (uint32_t)L;
+        }
+        __syncthreads();
+        /* (B) exact dedup: the CAS winner of a fingerprint represents every run
+         * whose full state equals its own; a fingerprint collision probes on */
+        for (uint32_t r = tid; r < runs; r += nth) {
+            const MemoRun<SMAX> me = R[r];
+            const uint64_t fp = memo_fp<SMAX>(me.s, me.L);
+            uint32_t slot = (uint32_t)fp & (kMemoHT - 1u);
+            uint32_t q;
+            for (;;) {
+                uint64_t v = ht[slot];
+                if (v == ~0ull) {
+                    v = atomicCAS((unsigned long long*)&ht[slot], ~0ull, (fp << 20) | r);
+                    if (v == ~0ull) {
+                        q = r;
+                        break;
+                    }
+                }
+                if ((v >> 20) == fp) {
+                    q = (uint32_t)v & 0xFFFFFu;
+                    if (memo_eq<SMAX>(me, R[q])) break;
+                }
+                slot = (slot + 1u) & (kMemoHT - 1u);
+            }
+            rep[r] = (uint16_t)q;
+        }
+        __syncthreads();
+        for (uint32_t r = tid; r < runs; r += nth)
+            if (rep[r] == r) {
+                const uint32_t d = atomicAdd(&nd, 1u);
+                did[r] = (uint16_t)d;
+                repr[d] = (uint16_t)r;
+            }
+        __syncthreads();
+        for (uint32_t r = tid; r < runs; r += nth) rep[r] = did[rep[r]];
+        const uint32_t ndist = nd;
+        /* (C) row d, part a: the a-th remaining kernel first, then its 4! orders */
+        for (uint32_t it = tid; it < ndist * kMemoD; it += nth) {
+            const uint32_t d = it / kMemoD, a = it - d * kMemoD;
+            const MemoRun<SMAX>& m = R[repr[d]];
+            St<SMAX> s = m.s;
+            s.K = 0;
+            const uint32_t sh = 4u * a, ka = (m.L >> sh) & 15u;
+            const uint32_t rest = (m.L & ((1u << sh) - 1u)) | ((m.L >> (sh + 4u)) << sh);
+            St<SMAX> s1;
+            place<SMAX, FULL>(s, s1, t.k[ka], ka, g, nr);
+            RowLeaf lf{rows + (size_t)d * kMemoRow};
+            dfs<SMAX, FULL, kMemoD - 1>(t, s1, rest, a * cfact(kMemoD - 1), lf);
+        }
+        __syncthreads();
+        /* (D) row extremes (smallest offset on ties), one warp per row */
+        const uint32_t lane = tid & 31u, warp = tid >> 5, nw = nth >> 5;
+        for (uint32_t d = warp; d < ndist; d += nw) {
+            const uint64_t* row = rows + (size_t)d * kMemoRow;
+            uint64_t mn = ~0ull, mx = 0;
+            uint32_t an = 0xFFu, ax = 0xFFu;
+            for (uint32_t j = lane; j < kMemoRow; j += 32u) {
+                const uint64_t v = row[j];
+                if (v < mn) { mn = v; an = j; }
+                if (v > mx) { mx = v; ax = j; }
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                const uint64_t omn = __shfl_xor_sync(~0u, mn, off), omx = __shfl_xor_sync(~0u, mx, off);
+                const uint32_t oan = __shfl_xor_sync(~0u, an, off), oax = __shfl_xor_sync(~0u, ax, off);
+                if (omn < mn || (omn == mn && oan < an)) { mn = omn; an = oan; }
+                if (omx > mx || (omx == mx && oax < ax)) { mx = omx; ax = oax; }
+            }
+            if (lane == 0) rst[d] = MemoRowStat{mn, mx, an | ax << 8};
+        }
+        __syncthreads();
+        /* (E) orders 120 run + j, keys Kp[run] + row[rep[run]][j]: extremes from
+         * the row's, counts below / equal to the candidate from the row's range;
+         * a row that straddles the candidate is counted by the whole warp */
+        const uint64_t cand = cand_keys[set];
+        TStats ts;
+        ts.init();
+        for (uint32_t r0 = 0; r0 < runs; r0 += nth) {
+            const uint32_t r = r0 + tid;
+            const bool live = r < runs;
+            uint32_t d = 0;
+            uint64_t thr = 0;
+            bool straddle = false;
+            if (live) {
+                d = rep[r];
+                const uint64_t K0 = Kp[r];
+                const MemoRowStat rs = rst[d];
+                const uint64_t base = (uint64_t)r * kMemoRow;
+                if (K0 + rs.mn < ts.kmin) { ts.kmin = K0 + rs.mn; ts.amin = base + (rs.a & 0xFFu); }
+                if (K0 + rs.mx > ts.kmax) { ts.kmax = K0 + rs.mx; ts.amax = base + (rs.a >> 8); }
+                ts.cnt += kMemoRow;
+                if (cand >= K0) {
+                    thr = cand - K0; /* K < cand  <=>  row value < thr */
+                    if (thr > rs.mx) ts.nlt += kMemoRow;
+                    else straddle = thr >= rs.mn;
+                }
+            }
+            uint32_t mask = __ballot_sync(~0u, straddle);
+            while (mask) {
+                const uint32_t src = __ffs(mask) - 1u;
+                mask &= mask - 1u;
+                const uint64_t th = __shfl_sync(~0u, thr, src);
+                const uint64_t* row = rows + (size_t)__shfl_sync(~0u, d, src) * kMemoRow;
+                uint32_t lt = 0, eq = 0;
+#pragma unroll
+                for (uint32_t j0 = 0; j0 < 128u; j0 += 32u) {
+                    const uint32_t j = j0 + lane;
+                    const uint64_t v = j < kMemoRow ? row[j] : ~0ull;
+                    lt += __popc(__ballot_sync(~0u, j < kMemoRow && v < th));
+                    eq += __popc(__ballot_sync(~0u, j < kMemoRow && v == th));
+                }
+                if (lane == src) {
+                    ts.nlt += lt;
+                    ts.neq += eq;
+                }
+            }
+        }
+        const rk_stats rs = block_reduce(to_rec(ts));
+        if (tid == 0) out[set] = rs;
+    }
 }
 
 /* merge groups of `per` consecutive records: one warp per group */
@@ -3515,6 +3704,55 @@ int rk_launch_batch(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n
     if (e) return e;
     const unsigned blocks = (n_sets * 32 + 255) / 256;
     rk_merge_groups_kernel<<<blocks, 256, 0, st>>>(recs, n_sets, chunks, out_dev);
+    if (launches) (*launches)++;
+    return (int)cudaGetLastError();
+}
+
+/* memoised batch (rk_batch_memo_kernel): sets with 6 <= n <= 9 on one or two
+ * super-SMs (the compile-time FULL variants whose rows are 5! deep) */
+bool rk_batch_memo_ok(uint32_t n, uint32_t S) { return n >= 6 && n <= 9 && S >= 1 && S <= 2; }
+
+template <int SMAX>
+static int memo_grid(uint32_t n_sets) {
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(rk_batch_memo_kernel<SMAX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kMemoSmem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, rk_batch_memo_kernel<SMAX, true>, kThreads,
+                                                          kMemoSmem) != cudaSuccess || occ < 1)
+            occ = 1;
+    }
+    const uint64_t cap = (uint64_t)occ * num_sms();
+    return (int)(n_sets < cap ? n_sets : cap);
+}
+
+int rk_batch_memo_grid(uint32_t S, uint32_t n_sets) { return S == 1 ? memo_grid<1>(n_sets) : memo_grid<2>(n_sets); }
+
+static uint32_t memo_runs(uint32_t n) {
+    uint32_t f = 1;
+    for (uint32_t i = 6; i <= n; i++) f *= i;
+    return f; /* n! / 5! */
+}
+
+size_t rk_batch_memo_scratch(uint32_t n, uint32_t S, uint32_t grid) {
+    const size_t run = S == 1 ? sizeof(MemoRun<1>) : sizeof(MemoRun<2>);
+    return (size_t)grid * memo_runs(n) * (run + kMemoRow * sizeof(uint64_t) + sizeof(MemoRowStat));
+}
+
+int rk_launch_batch_memo(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n_sets,
+                         const uint64_t* cand_keys_dev, rk_stats* out_dev, void* scratch, uint32_t grid, void* stream,
+                         uint32_t* launches) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint32_t stride = memo_runs(n);
+    uint64_t* rows = reinterpret_cast<uint64_t*>(scratch);
+    MemoRowStat* rst = reinterpret_cast<MemoRowStat*>(rows + (size_t)grid * stride * kMemoRow);
+    char* runs = reinterpret_cast<char*>(rst + (size_t)grid * stride);
+    if (S == 1)
+        rk_batch_memo_kernel<1, true><<<grid, kThreads, kMemoSmem, st>>>(
+            tabs_dev, cand_keys_dev, n_sets, stride, reinterpret_cast<MemoRun<1>*>(runs), rows, rst, out_dev);
+    else
+        rk_batch_memo_kernel<2, true><<<grid, kThreads, kMemoSmem, st>>>(
+            tabs_dev, cand_keys_dev, n_sets, stride, reinterpret_cast<MemoRun<2>*>(runs), rows, rst, out_dev);
     if (launches) (*launches)++;
     return (int)cudaGetLastError();
 }

@@ -1305,3 +1305,36 @@ def test_strict_round_robin_on_the_memoised_and_bnb_paths(monkeypatch):
         assert memo_checked >= 8
     finally:
         ctx.close()
+
+
+def test_memoised_batch_vs_oracle_and_direct(ctx, monkeypatch):
+    """rk_eval_batch's memoised kernel (6 <= n <= 9 on S' <= 2: runs sharing an
+    equal prefix state share one 120-key suffix row) equals the oracle's per-set
+    sweep for n = 6..8 under every register-state reading, sets with repeated
+    kernels (many equal states) included, and the direct batch kernel
+    (RK_NO_MEMO=1) on 256 C5 sets; one launch per S' group (+ the candidate keys)."""
+    direct = _direct_ctx(monkeypatch)
+    try:
+        for n in (6, 7, 8):
+            sets = W.c5_sets(12, n=n)
+            sets += [[s[0]] * 2 + list(s[2:]) for s in sets[:4]]  # two identical kernels
+            sets += [[s[1]] * n for s in sets[:2]]                 # all identical
+            for flags in (0, 1, 2, 3):
+                g = list(W.GTX580) + [flags]
+                ctx.rk_set_gpu_params(g)
+                res = ctx.rk_eval_batch(sets)
+                assert ctx.launches <= 3  # candidate keys + one launch per S' group
+                want = O.sweep_sets(g, sets, threads=NCPU)
+                for (st, ck), (ost, oidx, ock) in zip(res, want):
+                    assert st.as_tuple() == ost.as_tuple() and ck == ock
+        sets = W.c5_sets(256)
+        for flags in (0, 2):
+            g = list(W.GTX580) + [flags]
+            ctx.rk_set_gpu_params(g)
+            direct.rk_set_gpu_params(g)
+            a = ctx.rk_eval_batch(sets)
+            b = direct.rk_eval_batch(sets)
+            assert direct.launches > ctx.launches
+            assert [(s.as_tuple(), k) for s, k in a] == [(s.as_tuple(), k) for s, k in b]
+    finally:
+        direct.close()
