@@ -14,6 +14,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rk.h"
@@ -1037,6 +1038,12 @@ rk_status rk_create(rk_ctx** out, int cuda_device) {
         int sms = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
         c->sms = sms > 0 ? (uint32_t)sms : 148u;
+        /* the batch calls' stream-ordered buffers stay in the device's default pool between calls */
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         /* per-CTA record slots: also for the memo extremes pass (8 CTAs per SM) */
         c->max_ctas = std::max<uint32_t>(c->max_ctas, (uint32_t)std::max(256, 8 * sms));
         bool ok = cudaMalloc(&c->tab_dev, sizeof(RkTables)) == cudaSuccess &&
@@ -1553,6 +1560,68 @@ rk_status rk_heuristic_order(rk_ctx* c, int32_t* order_out, int32_t* round_of_ou
     return RK_OK;
 }
 
+/* Validate and pack the tables of n_sets sets (rk_set_kernels' checks) on up to
+ * 16 host threads; the lowest failing set's error is reported. */
+static rk_status build_tables_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n_sets, RkTables* tabs) {
+    const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint32_t nt = std::max(1u, std::min({16u, hw, n_sets / 256u}));
+    std::vector<rk_status> st(nt, RK_OK);
+    std::vector<uint32_t> bad(nt, 0xFFFFFFFFu);
+    std::vector<std::string> msg(nt);
+    auto work = [&](uint32_t w) {
+        rk_ctx local; /* fail() writes the message here */
+        local.no_reduce = c->no_reduce;
+        RkTables tmp;
+        const uint32_t a = (uint32_t)((uint64_t)n_sets * w / nt), b = (uint32_t)((uint64_t)n_sets * (w + 1) / nt);
+        for (uint32_t q = a; q < b; q++) {
+            const rk_status s = build_tables(&local, c->gp, sets + (size_t)q * n, n, tabs ? tabs[q] : tmp);
+            if (s) {
+                st[w] = s;
+                bad[w] = q;
+                msg[w] = local.err;
+                return;
+            }
+        }
+    };
+    if (nt == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (uint32_t w = 0; w < nt; w++) th.emplace_back(work, w);
+        for (auto& t : th) t.join();
+    }
+    for (uint32_t w = 0; w < nt; w++)
+        if (st[w]) {
+            c->err = "set " + std::to_string(bad[w]) + ": " + msg[w];
+            return st[w];
+        }
+    return RK_OK;
+}
+
+/* Algorithm 1 on device for sets already validated */
+static rk_status heuristic_batch_dev(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n_sets,
+                                     int32_t* orders_out, uint64_t* index_out, void* stream) {
+    DeviceGuard dg(c->device);
+    c->launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    rk_kernel* sets_dev = nullptr;
+    int32_t* ord_dev = nullptr;
+    uint64_t* idx_dev = nullptr;
+    int e = cudaMallocAsync((void**)&sets_dev, sizeof(rk_kernel) * (size_t)n * n_sets, st);
+    if (!e) e = cudaMallocAsync((void**)&ord_dev, sizeof(int32_t) * (size_t)n * n_sets, st);
+    if (!e) e = cudaMallocAsync((void**)&idx_dev, sizeof(uint64_t) * n_sets, st);
+    if (!e) e = cudaMemcpyAsync(sets_dev, sets, sizeof(rk_kernel) * (size_t)n * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = rk_launch_heuristic(sets_dev, n, n_sets, &c->gp, ord_dev, idx_dev, stream, &c->launches);
+    if (!e) e = cudaMemcpyAsync(index_out, idx_dev, sizeof(uint64_t) * n_sets, cudaMemcpyDeviceToHost, st);
+    if (!e && orders_out)
+        e = cudaMemcpyAsync(orders_out, ord_dev, sizeof(int32_t) * (size_t)n * n_sets, cudaMemcpyDeviceToHost, st);
+    if (sets_dev) cudaFreeAsync(sets_dev, st);
+    if (ord_dev) cudaFreeAsync(ord_dev, st);
+    if (idx_dev) cudaFreeAsync(idx_dev, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    return e ? cuda_fail(c, e, "rk_heuristic_batch") : RK_OK;
+}
+
 rk_status rk_heuristic_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n_sets, int32_t* orders_out,
                              uint64_t* index_out, void* stream) {
     rk_status s = need_device(c);
@@ -1560,31 +1629,8 @@ rk_status rk_heuristic_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint3
     if (!c->has_params) return fail(c, RK_ESTATE, "rk_set_gpu_params first");
     if (!sets || !index_out || n_sets == 0) return fail(c, RK_EINVAL, "bad heuristic batch arguments");
     if (n == 0 || n > RK_MAX_N) return fail(c, n ? RK_ETOOMANY : RK_EINVAL, "n out of range");
-    RkTables tmp;
-    for (uint32_t q = 0; q < n_sets; q++) /* same validation as rk_set_kernels */
-        if ((s = build_tables(c, c->gp, sets + (size_t)q * n, n, tmp))) {
-            c->err = "set " + std::to_string(q) + ": " + c->err;
-            return s;
-        }
-    DeviceGuard dg(c->device);
-    c->launches = 0;
-    cudaStream_t st = (cudaStream_t)stream;
-    rk_kernel* sets_dev = nullptr;
-    int32_t* ord_dev = nullptr;
-    uint64_t* idx_dev = nullptr;
-    int e = cudaMalloc(&sets_dev, sizeof(rk_kernel) * (size_t)n * n_sets);
-    if (!e) e = cudaMalloc(&ord_dev, sizeof(int32_t) * (size_t)n * n_sets);
-    if (!e) e = cudaMalloc(&idx_dev, sizeof(uint64_t) * n_sets);
-    if (!e) e = cudaMemcpyAsync(sets_dev, sets, sizeof(rk_kernel) * (size_t)n * n_sets, cudaMemcpyHostToDevice, st);
-    if (!e) e = rk_launch_heuristic(sets_dev, n, n_sets, &c->gp, ord_dev, idx_dev, stream, &c->launches);
-    if (!e) e = cudaMemcpyAsync(index_out, idx_dev, sizeof(uint64_t) * n_sets, cudaMemcpyDeviceToHost, st);
-    if (!e && orders_out)
-        e = cudaMemcpyAsync(orders_out, ord_dev, sizeof(int32_t) * (size_t)n * n_sets, cudaMemcpyDeviceToHost, st);
-    if (!e) e = cudaStreamSynchronize(st);
-    cudaFree(sets_dev);
-    cudaFree(ord_dev);
-    cudaFree(idx_dev);
-    return e ? cuda_fail(c, e, "rk_heuristic_batch") : RK_OK;
+    if ((s = build_tables_batch(c, sets, n, n_sets, nullptr))) return s; /* same validation as rk_set_kernels */
+    return heuristic_batch_dev(c, sets, n, n_sets, orders_out, index_out, stream);
 }
 
 rk_status rk_percentile(rk_ctx* c, const int32_t* order, uint64_t first, uint64_t count, uint64_t* n_ge_out,
@@ -1611,19 +1657,16 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     if (s) return s;
     if (!c->has_params) return fail(c, RK_ESTATE, "rk_set_gpu_params first");
     if (!sets || !out_host || n_sets == 0) return fail(c, RK_EINVAL, "bad batch arguments");
+    if (n == 0 || n > RK_MAX_N) return fail(c, n ? RK_ETOOMANY : RK_EINVAL, "n out of range");
     std::vector<RkTables> tabs(n_sets);
     std::vector<uint64_t> idx(n_sets);
-    for (uint32_t q = 0; q < n_sets; q++) {
-        if ((s = build_tables(c, c->gp, sets + (size_t)q * n, n, tabs[q]))) {
-            c->err = "set " + std::to_string(q) + ": " + c->err;
-            return s;
-        }
-        if (cand_index) {
+    if ((s = build_tables_batch(c, sets, n, n_sets, tabs.data()))) return s;
+    if (cand_index)
+        for (uint32_t q = 0; q < n_sets; q++) {
             if (cand_index[q] >= fact64(n)) return fail(c, RK_EINVAL, "set %u: candidate index >= n!", q);
             idx[q] = cand_index[q];
         }
-    }
-    if (!cand_index && (s = rk_heuristic_batch(c, sets, n, n_sets, nullptr, idx.data(), stream))) return s;
+    if (!cand_index && (s = heuristic_batch_dev(c, sets, n, n_sets, nullptr, idx.data(), stream))) return s;
     /* group the sets by reduced SM count so every launch runs a compile-time variant */
     std::vector<uint32_t> perm(n_sets);
     for (uint32_t q = 0; q < n_sets; q++) perm[q] = q;
@@ -1643,11 +1686,11 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     RkTables* tabs_dev = nullptr;
     uint64_t *idx_dev = nullptr, *keys_dev = nullptr;
     rk_stats *recs = nullptr, *out_dev = nullptr;
-    int e = cudaMalloc(&tabs_dev, sizeof(RkTables) * n_sets);
-    if (!e) e = cudaMalloc(&idx_dev, sizeof(uint64_t) * n_sets);
-    if (!e) e = cudaMalloc(&keys_dev, sizeof(uint64_t) * n_sets);
-    if (!e) e = cudaMalloc(&recs, sizeof(rk_stats) * (size_t)n_sets * max_chunks);
-    if (!e) e = cudaMalloc(&out_dev, sizeof(rk_stats) * n_sets);
+    int e = cudaMallocAsync((void**)&tabs_dev, sizeof(RkTables) * n_sets, st);
+    if (!e) e = cudaMallocAsync((void**)&idx_dev, sizeof(uint64_t) * n_sets, st);
+    if (!e) e = cudaMallocAsync((void**)&keys_dev, sizeof(uint64_t) * n_sets, st);
+    if (!e) e = cudaMallocAsync((void**)&recs, sizeof(rk_stats) * (size_t)n_sets * max_chunks, st);
+    if (!e) e = cudaMallocAsync((void**)&out_dev, sizeof(rk_stats) * n_sets, st);
     if (!e) e = cudaMemcpyAsync(tabs_dev, ptabs.data(), sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
     if (!e) e = cudaMemcpyAsync(idx_dev, pidx.data(), sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
     uint32_t smax_k = 0;
@@ -1687,12 +1730,9 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     std::vector<rk_stats> pout(n_sets);
     if (!e) e = cudaMemcpyAsync(pout.data(), out_dev, sizeof(rk_stats) * n_sets, cudaMemcpyDeviceToHost, st);
     if (!e) e = cudaMemcpyAsync(keys.data(), keys_dev, sizeof(uint64_t) * n_sets, cudaMemcpyDeviceToHost, st);
+    for (void* p : {(void*)tabs_dev, (void*)idx_dev, (void*)keys_dev, (void*)recs, (void*)out_dev})
+        if (p) cudaFreeAsync(p, st);
     if (!e) e = cudaStreamSynchronize(st);
-    cudaFree(tabs_dev);
-    cudaFree(idx_dev);
-    cudaFree(keys_dev);
-    cudaFree(recs);
-    cudaFree(out_dev);
     if (e) return cuda_fail(c, e, "rk_eval_batch");
     for (uint32_t q = 0; q < n_sets; q++) {
         out_host[perm[q]] = pout[q];

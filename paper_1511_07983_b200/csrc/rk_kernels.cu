@@ -1175,12 +1175,19 @@ struct MemoRowStat {
     uint32_t a; /* offset of the first minimum | offset of the first maximum << 8 */
 };
 
+/* stores a part of a row and its extremes (leaves arrive in increasing offset) */
 struct RowLeaf {
     uint64_t* row;
-    __device__ __forceinline__ void operator()(uint32_t off, uint64_t K) { row[off] = K; }
+    uint64_t mn, mx;
+    uint32_t an, ax;
+    __device__ __forceinline__ void operator()(uint32_t off, uint64_t K) {
+        row[off] = K;
+        if (K < mn) { mn = K; an = off; }
+        if (K > mx) { mx = K; ax = off; }
+    }
     __device__ __forceinline__ void pair(uint32_t off, uint64_t K0, uint64_t K1) {
-        row[off] = K0;
-        row[off + 1u] = K1;
+        (*this)(off, K0);
+        (*this)(off + 1u, K1);
     }
 };
 
@@ -1200,7 +1207,8 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     uint16_t* repr = did + kMemoRunsMax;                        /* row -> representative run */
     MemoRun<SMAX>* R = scratch_runs + (size_t)blockIdx.x * stride; /* stride = n!/120 runs per set */
     uint64_t* rows = scratch_rows + (size_t)blockIdx.x * stride * kMemoRow;
-    MemoRowStat* rst = scratch_rst + (size_t)blockIdx.x * stride;
+    MemoRowStat* rst = scratch_rst + (size_t)blockIdx.x * stride * (kMemoD + 1); /* rows' extremes */
+    MemoRowStat* pst = rst + stride;                                            /* parts' extremes */
     const uint32_t tid = threadIdx.x, nth = blockDim.x;
     NoRec nr;
     for (uint32_t set = blockIdx.x; set < n_sets; set += gridDim.x) {
@@ -1273,31 +1281,24 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
             const uint32_t rest = (m.L & ((1u << sh) - 1u)) | ((m.L >> (sh + 4u)) << sh);
             St<SMAX> s1;
             place<SMAX, FULL>(s, s1, t.k[ka], ka, g, nr);
-            RowLeaf lf{rows + (size_t)d * kMemoRow};
+            RowLeaf lf{rows + (size_t)d * kMemoRow, ~0ull, 0ull, 0u, 0u};
             dfs<SMAX, FULL, kMemoD - 1>(t, s1, rest, a * cfact(kMemoD - 1), lf);
+            pst[it] = MemoRowStat{lf.mn, lf.mx, lf.an | lf.ax << 8};
         }
         __syncthreads();
-        /* (D) row extremes (smallest offset on ties), one warp per row */
-        const uint32_t lane = tid & 31u, warp = tid >> 5, nw = nth >> 5;
-        for (uint32_t d = warp; d < ndist; d += nw) {
-            const uint64_t* row = rows + (size_t)d * kMemoRow;
-            uint64_t mn = ~0ull, mx = 0;
-            uint32_t an = 0xFFu, ax = 0xFFu;
-            for (uint32_t j = lane; j < kMemoRow; j += 32u) {
-                const uint64_t v = row[j];
-                if (v < mn) { mn = v; an = j; }
-                if (v > mx) { mx = v; ax = j; }
-            }
+        /* (D) row extremes from its five parts (in offset order: smallest offset on ties) */
+        for (uint32_t d = tid; d < ndist; d += nth) {
+            MemoRowStat r = pst[d * kMemoD];
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) {
-                const uint64_t omn = __shfl_xor_sync(~0u, mn, off), omx = __shfl_xor_sync(~0u, mx, off);
-                const uint32_t oan = __shfl_xor_sync(~0u, an, off), oax = __shfl_xor_sync(~0u, ax, off);
-                if (omn < mn || (omn == mn && oan < an)) { mn = omn; an = oan; }
-                if (omx > mx || (omx == mx && oax < ax)) { mx = omx; ax = oax; }
+            for (uint32_t a = 1; a < (uint32_t)kMemoD; a++) {
+                const MemoRowStat p = pst[d * kMemoD + a];
+                if (p.mn < r.mn) r.a = (r.a & ~0xFFu) | (p.a & 0xFFu), r.mn = p.mn;
+                if (p.mx > r.mx) r.a = (r.a & 0xFFu) | (p.a & ~0xFFu), r.mx = p.mx;
             }
-            if (lane == 0) rst[d] = MemoRowStat{mn, mx, an | ax << 8};
+            rst[d] = r;
         }
         __syncthreads();
+        const uint32_t lane = tid & 31u;
         /* (E) orders 120 run + j, keys Kp[run] + row[rep[run]][j]: extremes from
          * the row's, counts below / equal to the candidate from the row's range;
          * a row that straddles the candidate is counted by the whole warp */
@@ -3736,7 +3737,7 @@ static uint32_t memo_runs(uint32_t n) {
 
 size_t rk_batch_memo_scratch(uint32_t n, uint32_t S, uint32_t grid) {
     const size_t run = S == 1 ? sizeof(MemoRun<1>) : sizeof(MemoRun<2>);
-    return (size_t)grid * memo_runs(n) * (run + kMemoRow * sizeof(uint64_t) + sizeof(MemoRowStat));
+    return (size_t)grid * memo_runs(n) * (run + kMemoRow * sizeof(uint64_t) + (kMemoD + 1) * sizeof(MemoRowStat));
 }
 
 int rk_launch_batch_memo(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint32_t n_sets,
@@ -3746,7 +3747,7 @@ int rk_launch_batch_memo(const RkTables* tabs_dev, uint32_t n, uint32_t S, uint3
     const uint32_t stride = memo_runs(n);
     uint64_t* rows = reinterpret_cast<uint64_t*>(scratch);
     MemoRowStat* rst = reinterpret_cast<MemoRowStat*>(rows + (size_t)grid * stride * kMemoRow);
-    char* runs = reinterpret_cast<char*>(rst + (size_t)grid * stride);
+    char* runs = reinterpret_cast<char*>(rst + (size_t)grid * stride * (kMemoD + 1));
     if (S == 1)
         rk_batch_memo_kernel<1, true><<<grid, kThreads, kMemoSmem, st>>>(
             tabs_dev, cand_keys_dev, n_sets, stride, reinterpret_cast<MemoRun<1>*>(runs), rows, rst, out_dev);

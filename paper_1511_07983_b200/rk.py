@@ -148,8 +148,11 @@ class _KArr:
 
         from itertools import chain
 
-        a = (np.fromiter(chain.from_iterable(kernels), dtype=np.uint64, count=6 * len(kernels)).reshape(-1, 6)
-             if len(kernels) else np.zeros((1, 6), np.uint64))
+        if isinstance(kernels, np.ndarray):  # (..., 6) integer array: no per-field Python iteration
+            a = kernels.reshape(-1, 6).astype(np.uint64) if kernels.size else np.zeros((1, 6), np.uint64)
+        else:
+            a = (np.fromiter(chain.from_iterable(kernels), dtype=np.uint64, count=6 * len(kernels)).reshape(-1, 6)
+                 if len(kernels) else np.zeros((1, 6), np.uint64))
         if a.size and (a.max() > 0xFFFFFFFF):
             raise RkError(RK_EINVAL, "kernel field exceeds u32")
         self.buf = np.ascontiguousarray(a.astype(np.uint32))
@@ -399,16 +402,18 @@ class Context:
         return nge.value, key.value
 
     def rk_eval_batch(self, sets, cand_index=None, stream=None):
-        """-> list of (Stats, cand_key) per set."""
+        """-> list of (Stats, cand_key) per set.  sets: a list of kernel lists, or an
+        integer array of shape (n_sets, n, 6)."""
         n = len(sets[0])
-        flat = [k for s in sets for k in s]
-        arr = kernels_array(flat)
+        arr = kernels_array(sets if hasattr(sets, "shape") else [k for s in sets for k in s])
         ns = len(sets)
         out = (rk_stats * ns)()
         keys = (ctypes.c_uint64 * ns)()
         ci = (ctypes.c_uint64 * ns)(*cand_index) if cand_index is not None else None
         self._chk(self._L.rk_eval_batch(self.h, arr, n, ns, ci, out, keys, _stream(stream)), "rk_eval_batch")
-        return [(Stats.from_c(out[i]), keys[i]) for i in range(ns)]
+        import numpy as np
+        rows = np.frombuffer(out, dtype=np.uint64).reshape(ns, 8).tolist()  # field order of rk_stats
+        return [(Stats(*r), k) for r, k in zip(rows, keys)]
 
     def rk_simulate_order(self, order, max_rounds: int = 4096):
         n = len(order)

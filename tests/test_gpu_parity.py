@@ -1336,5 +1336,7 @@ def test_memoised_batch_vs_oracle_and_direct(ctx, monkeypatch):
             b = direct.rk_eval_batch(sets)
             assert direct.launches > ctx.launches
             assert [(s.as_tuple(), k) for s, k in a] == [(s.as_tuple(), k) for s, k in b]
+            c = ctx.rk_eval_batch(np.array(sets, dtype=np.int64))  # (sets, n, 6) array input
+            assert [(s.as_tuple(), k) for s, k in c] == [(s.as_tuple(), k) for s, k in a]
     finally:
         direct.close()

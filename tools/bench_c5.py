@@ -6,7 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1511_07983_b200 import rk, workloads as W
 
-sets = W.c5_sets(int(os.environ.get("C5_SETS", "4096")))
+import numpy as np
+sets = np.array(W.c5_sets(int(os.environ.get("C5_SETS", "4096"))), dtype=np.int64)  # (sets, 9, 6), host-resident
 c = rk.Context(0)
 c.rk_set_gpu_params(W.GTX580)
 res = c.rk_eval_batch(sets)  # warm-up (also validates)

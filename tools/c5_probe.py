@@ -5,7 +5,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1511_07983_b200 import rk, workloads as W
 
-sets = W.c5_sets(4096)
+import numpy as np
+sets = np.array(W.c5_sets(4096), dtype=np.int64)  # (sets, 9, 6), host-resident
 os.environ["RK_NO_MEMO"] = "1"
 cd = rk.Context(0)
 del os.environ["RK_NO_MEMO"]
