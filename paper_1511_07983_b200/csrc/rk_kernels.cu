@@ -473,6 +473,19 @@ struct StrictCapUpd {
     }
 };
 
+struct CapBothUpd { /* CapSumUpd and StrictCapUpd in one pass */
+    CapK k;
+    uint32_t F, S, cur, m;
+    bool perk;
+    __device__ __forceinline__ void set_cursor(uint32_t c) { cur = perk ? 0u : c; }
+    __device__ __forceinline__ void operator()(int i, uint32_t a, uint32_t b) {
+        const uint32_t c = cap1(a, b, k);
+        F += c;
+        const uint32_t d = (uint32_t)i >= cur ? (uint32_t)i - cur : (uint32_t)i + S - cur;
+        if ((uint32_t)i < S) m = min(m, d + c * S);
+    }
+};
+
 /* ---- run-length state (SMAX == 0): the same dispatch rules (PAPER:69-81,
  * readings L4/L5) as place_core, on runs of identical SMs ---- */
 __device__ __forceinline__ uint32_t rle_end(const St<0>& s, uint32_t j, uint32_t S) {
@@ -661,14 +674,11 @@ __device__ __forceinline__ uint64_t place_finish(const St<SMAX>& in, const RkKTa
         rle_place(in, s1, kb, kbid, g, nr);
         return finish<0>(s1, kc, kcid, g, nr);
     } else {
-        if (g.flags & RK_FLAG_STRICT_RR) { /* kc's fit depends on kb's new cursor (set before the words) */
-            StrictCapUpd u{capk(kc), nsm<SMAX, FULL>(g), 0u, 0xFFFFFFFFu, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0};
-            const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
-            return finish_key(u.m, o.I, o.M, o.K, kc, kcid, g, nr);
-        }
-        CapSumUpd u{capk(kc), 0u};
+        /* one placement, both fits of kc: the capacity sum and, for strict round
+         * robin, the first block that fails from kb's new cursor (set before the words) */
+        CapBothUpd u{capk(kc), 0u, nsm<SMAX, FULL>(g), 0u, 0xFFFFFFFFu, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0};
         const Placed o = place_core<SMAX, FULL>(in, kb, kbid, g, nr, u);
-        return finish_key(u.F, o.I, o.M, o.K, kc, kcid, g, nr);
+        return finish_key((g.flags & RK_FLAG_STRICT_RR) ? u.m : u.F, o.I, o.M, o.K, kc, kcid, g, nr);
     }
 }
 
