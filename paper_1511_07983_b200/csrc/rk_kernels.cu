@@ -344,7 +344,9 @@ __device__ __forceinline__ uint32_t water_fill(uint32_t n, const uint32_t (&c)[S
 /* Dispatch all T_k blocks of kernel k on state `in`; the new
  * per-SM words are handed to upd(i, fa, fb) so callers either store them
  * (a new state) or consume them on the fly (the fused last level). */
-template <int SMAX, bool FULL, class R, class U>
+/* ST = false: a variant compiled without the strict round-robin reading (the
+ * direct kernels branch once per launch on the flag) */
+template <int SMAX, bool FULL, class R, class U, bool ST = true>
 __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k, uint32_t kid, const RkGTab& g,
                                              R& rec, U& upd) {
     const CapK ck = capk(k);
@@ -355,7 +357,7 @@ __device__ __forceinline__ Placed place_core(const St<SMAX>& in, const RkKTab& k
         c[i] = cap1(in.fa[i], in.fb[i], ck);
         F += c[i];
     }
-    if (g.flags & RK_FLAG_STRICT_RR) {
+    if (ST && (g.flags & RK_FLAG_STRICT_RR)) {
         /* L4 read literally: block b goes to SM (cur + b) mod S, so the round holds
          * m = min_s ((s - cur) mod S + c_s S) of them (m <= F: SM s receives
          * ceil((m - d_s) / S) <= c_s).  Up to m blocks that round robin never meets
@@ -604,7 +606,7 @@ __device__ void rle_place(const St<0>& in, St<0>& out, const RkKTab& k, uint32_t
     out = o;
 }
 
-template <int SMAX, bool FULL, class R>
+template <int SMAX, bool FULL, bool ST = true, class R>
 __device__ __forceinline__ void place(const St<SMAX>& in, St<SMAX>& out, const RkKTab& k, uint32_t kid,
                                       const RkGTab& g, R& rec) {
     if constexpr (SMAX == 0) {
@@ -612,7 +614,7 @@ __device__ __forceinline__ void place(const St<SMAX>& in, St<SMAX>& out, const R
         return;
     } else {
     StoreUpd<SMAX> u{out};
-    const Placed o = place_core<SMAX, FULL>(in, k, kid, g, rec, u);
+    const Placed o = place_core<SMAX, FULL, R, StoreUpd<SMAX>, ST>(in, k, kid, g, rec, u);
     out.cur = o.cur;
     out.I = o.I;
     out.M = o.M;
@@ -644,14 +646,14 @@ __device__ __forceinline__ uint64_t finish_key(uint32_t F, uint64_t I, uint64_t 
     return K + round_key((uint64_t)n * k.cA, (uint64_t)n * k.cM, g.num, g.den);
 }
 
-template <int SMAX, class R>
+template <int SMAX, bool ST = true, class R>
 __device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, uint32_t kid, const RkGTab& g,
                                            R& rec) {
     const CapK ck = capk(k);
     uint32_t F = 0;
     if constexpr (SMAX == 0) {
         F = rle_capsum(s, ck, g.S);
-    } else if (g.flags & RK_FLAG_STRICT_RR) { /* the first block that does not fit on its SM */
+    } else if (ST && (g.flags & RK_FLAG_STRICT_RR)) { /* the first block that does not fit on its SM */
         StrictCapUpd u{ck, g.S, 0u, 0xFFFFFFFFu, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0};
         u.set_cursor(s.cur);
 #pragma unroll
@@ -665,7 +667,7 @@ __device__ __forceinline__ uint64_t finish(const St<SMAX>& s, const RkKTab& k, u
 }
 
 /* place kb on `in`, then evaluate the last kernel kc — leaf of the suffix tree */
-template <int SMAX, bool FULL>
+template <int SMAX, bool FULL, bool ST = true>
 __device__ __forceinline__ uint64_t place_finish(const St<SMAX>& in, const RkKTab& kb, uint32_t kbid,
                                                  const RkKTab& kc, uint32_t kcid, const RkGTab& g) {
     NoRec nr;
@@ -674,6 +676,11 @@ __device__ __forceinline__ uint64_t place_finish(const St<SMAX>& in, const RkKTa
         rle_place(in, s1, kb, kbid, g, nr);
         return finish<0>(s1, kc, kcid, g, nr);
     } else {
+        if constexpr (!ST) {
+            CapSumUpd u{capk(kc), 0u};
+            const Placed o = place_core<SMAX, FULL, NoRec, CapSumUpd, false>(in, kb, kbid, g, nr, u);
+            return finish_key(u.F, o.I, o.M, o.K, kc, kcid, g, nr);
+        }
         /* one placement, both fits of kc: the capacity sum and, for strict round
          * robin, the first block that fails from kb's new cursor (set before the words) */
         CapBothUpd u{capk(kc), 0u, nsm<SMAX, FULL>(g), 0u, 0xFFFFFFFFu, (g.flags & RK_FLAG_CURSOR_PER_KERNEL) != 0};
@@ -964,12 +971,12 @@ struct Leaf {
 
 /* The D kernels left after a prefix are the low D nibbles of `rem` (ascending);
  * visit their D! orders in lexicographic order, leaf offsets off .. off+D!-1. */
-template <int SMAX, bool FULL, int D, class LF>
+template <int SMAX, bool FULL, int D, class LF, bool ST = true>
 __device__ __forceinline__ void dfs(const RkTables& t, const St<SMAX>& s, uint32_t rem, uint32_t off, LF& leaf) {
     if constexpr (D == 2) {
         const uint32_t x = rem & 15u, y = (rem >> 4) & 15u;
-        const uint64_t K0 = place_finish<SMAX, FULL>(s, t.k[x], x, t.k[y], y, t.g);
-        const uint64_t K1 = place_finish<SMAX, FULL>(s, t.k[y], y, t.k[x], x, t.g);
+        const uint64_t K0 = place_finish<SMAX, FULL, ST>(s, t.k[x], x, t.k[y], y, t.g);
+        const uint64_t K1 = place_finish<SMAX, FULL, ST>(s, t.k[y], y, t.k[x], x, t.g);
         leaf.pair(off, K0, K1);
     } else {
         NoRec nr;
@@ -979,14 +986,14 @@ __device__ __forceinline__ void dfs(const RkTables& t, const St<SMAX>& s, uint32
             const uint32_t ka = (rem >> sh) & 15u;
             const uint32_t rest = (rem & ((1u << sh) - 1u)) | ((rem >> (sh + 4u)) << sh);
             St<SMAX> s1;
-            place<SMAX, FULL>(s, s1, t.k[ka], ka, t.g, nr);
-            dfs<SMAX, FULL, D - 1>(t, s1, rest, off + a * cfact(D - 1), leaf);
+            place<SMAX, FULL, ST>(s, s1, t.k[ka], ka, t.g, nr);
+            dfs<SMAX, FULL, D - 1, LF, ST>(t, s1, rest, off + a * cfact(D - 1), leaf);
         }
     }
 }
 
 /* A run = the D! consecutive indices sharing an (n-D)-prefix. */
-template <int SMAX, bool FULL, int D, class LF>
+template <int SMAX, bool FULL, int D, class LF, bool ST = true>
 __device__ __forceinline__ void eval_run(const RkTables& t, uint64_t run, LF& leaf) {
     const RkGTab& g = t.g;
     const uint32_t n = g.n;
@@ -1007,31 +1014,31 @@ __device__ __forceinline__ void eval_run(const RkTables& t, uint64_t run, LF& le
         }
         rem -= (uint64_t)d * f;
         const uint32_t k = take_nibble(L, d);
-        place<SMAX, FULL>(s0, s0, t.k[k], k, g, nr);
+        place<SMAX, FULL, ST>(s0, s0, t.k[k], k, g, nr);
     }
-    dfs<SMAX, FULL, D>(t, s0, (uint32_t)L, 0u, leaf);
+    dfs<SMAX, FULL, D, LF, ST>(t, s0, (uint32_t)L, 0u, leaf);
     leaf.end_run();
 }
 
 /* All runs of [lo, hi) handled by this thread (stride over the grid). */
-template <int SMAX, bool FULL, int D, class LF>
+template <int SMAX, bool FULL, int D, class LF, bool ST = true>
 __device__ __forceinline__ void eval_runs(const RkTables& t, uint64_t lo, uint64_t hi, uint32_t tid, uint32_t nth,
                                           LF& leaf) {
     constexpr uint64_t R = cfact(D);
     const uint64_t rb = lo / R, re = (hi + R - 1u) / R;
-    for (uint64_t run = rb + tid; run < re; run += nth) eval_run<SMAX, FULL, D>(t, run, leaf);
+    for (uint64_t run = rb + tid; run < re; run += nth) eval_run<SMAX, FULL, D, LF, ST>(t, run, leaf);
 }
 
 /* n-dependent depth: D = min(n, Depth<SMAX>); n == 1 evaluates the single order. */
-template <int SMAX, bool FULL, class LF>
+template <int SMAX, bool FULL, class LF, bool ST = true>
 __device__ __forceinline__ void eval_space(const RkTables& t, uint64_t lo, uint64_t hi, uint32_t tid, uint32_t nth,
                                            LF& leaf) {
     constexpr int DM = Depth<SMAX>::value;
     const uint32_t n = t.g.n;
-    if (n >= (uint32_t)DM) eval_runs<SMAX, FULL, DM>(t, lo, hi, tid, nth, leaf);
+    if (n >= (uint32_t)DM) eval_runs<SMAX, FULL, DM, LF, ST>(t, lo, hi, tid, nth, leaf);
     else if (DM > 4 && n == 4) eval_runs<SMAX, FULL, (DM > 4 ? 4 : 2)>(t, lo, hi, tid, nth, leaf);
     else if (DM > 3 && n == 3) eval_runs<SMAX, FULL, (DM > 3 ? 3 : 2)>(t, lo, hi, tid, nth, leaf);
-    else if (n == 2) eval_runs<SMAX, FULL, 2>(t, lo, hi, tid, nth, leaf);
+    else if (n == 2) eval_runs<SMAX, FULL, 2, LF, ST>(t, lo, hi, tid, nth, leaf);
     else if (tid == 0 && lo < hi) {
         NoRec nr;
         leaf.begin_run(0ull, 1u);
@@ -1058,7 +1065,7 @@ struct MinBlocks {
 #endif
 };
 
-template <int SMAX, bool FULL, bool EXTRA>
+template <int SMAX, bool FULL, bool EXTRA, bool ST>
 __device__ __forceinline__ void eval_body(const RkTables* __restrict__ tab, uint64_t first, uint64_t count,
                                           const uint64_t* cand_dev, uint64_t cand_imm, rk_stats* out, uint64_t* keys,
                                           rk_stats* recs, uint32_t* counter, uint32_t* keys32, uint64_t key_base,
@@ -1078,7 +1085,7 @@ __device__ __forceinline__ void eval_body(const RkTables* __restrict__ tab, uint
     leaf.hcur = 0xFFFFFFFFu;
     leaf.hrun = 0;
     if (EXTRA && hist) leaf.bc.init(hist_range->key_min, hist_range->key_max, bins);
-    eval_space<SMAX, FULL>(t, lo, hi, gtid, nth, leaf);
+    eval_space<SMAX, FULL, Leaf<EXTRA>, ST>(t, lo, hi, gtid, nth, leaf);
     if constexpr (EXTRA) {
         leaf.flush();
         if (leaf.ovf) atomicOr(ovf_dev, 1u);
@@ -1099,8 +1106,12 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
                    uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter,
                    uint32_t* keys32, uint64_t key_base, uint32_t* ovf_dev, const rk_stats* hist_range,
                    uint32_t bins, uint64_t* hist) {
-    eval_body<SMAX, FULL, false>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, nullptr, 0, nullptr,
-                                 nullptr, 0, nullptr);
+    if (tab->g.flags & RK_FLAG_STRICT_RR) /* uniform: the strict-capable copy only when the reading is on */
+        eval_body<SMAX, FULL, false, true>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, nullptr, 0,
+                                           nullptr, nullptr, 0, nullptr);
+    else
+        eval_body<SMAX, FULL, false, false>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, nullptr, 0,
+                                            nullptr, nullptr, 0, nullptr);
 }
 
 /* + compact keys / fused histogram */
@@ -1110,15 +1121,19 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
                      uint64_t cand_imm, rk_stats* out, uint64_t* keys, rk_stats* recs, uint32_t* counter,
                      uint32_t* keys32, uint64_t key_base, uint32_t* ovf_dev, const rk_stats* hist_range,
                      uint32_t bins, uint64_t* hist) {
-    eval_body<SMAX, FULL, true>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, keys32, key_base,
-                                ovf_dev, hist_range, bins, hist);
+    if (tab->g.flags & RK_FLAG_STRICT_RR)
+        eval_body<SMAX, FULL, true, true>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, keys32,
+                                          key_base, ovf_dev, hist_range, bins, hist);
+    else
+        eval_body<SMAX, FULL, true, false>(tab, first, count, cand_dev, cand_imm, out, keys, recs, counter, keys32,
+                                           key_base, ovf_dev, hist_range, bins, hist);
 }
 
 /* C5 batch: blockIdx.y = set, blockIdx.x = chunk of that set's runs.  All sets
  * of one launch share the variant (max super-SM count over the batch). */
-template <int SMAX, bool FULL>
-__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
-    rk_batch_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ cand_keys, rk_stats* recs) {
+template <int SMAX, bool FULL, bool ST>
+__device__ __forceinline__ void batch_body(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ cand_keys,
+                                           rk_stats* recs) {
     __shared__ RkTables t;
     const uint32_t set = blockIdx.y;
     load_tables(t, tabs + set);
@@ -1133,9 +1148,16 @@ __global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
     const uint64_t per = (runs + gridDim.x - 1) / gridDim.x;
     const uint64_t lo = min(total, (uint64_t)blockIdx.x * per * R), hi = min(total, lo + per * R);
     Leaf<false> leaf{ts, nullptr, nullptr, 0ull, 0u, lo, hi, 0ull, cand, nullptr};
-    eval_space<SMAX, FULL>(t, lo, hi, threadIdx.x, blockDim.x, leaf);
+    eval_space<SMAX, FULL, Leaf<false>, ST>(t, lo, hi, threadIdx.x, blockDim.x, leaf);
     const rk_stats r = block_reduce(to_rec(ts));
     if (threadIdx.x == 0) recs[set * gridDim.x + blockIdx.x] = r;
+}
+
+template <int SMAX, bool FULL>
+__global__ void __launch_bounds__(kThreads, MinBlocks<SMAX>::value)
+    rk_batch_kernel(const RkTables* __restrict__ tabs, const uint64_t* __restrict__ cand_keys, rk_stats* recs) {
+    if (tabs[blockIdx.y].g.flags & RK_FLAG_STRICT_RR) batch_body<SMAX, FULL, true>(tabs, cand_keys, recs);
+    else batch_body<SMAX, FULL, false>(tabs, cand_keys, recs);
 }
 
 /* C5 batch with suffix memoisation: one CTA per set, persistent over the sets.
