@@ -248,9 +248,18 @@ rk_status rk_percentile(rk_ctx* ctx, const int32_t* order, uint64_t first, uint6
 /* Batch mode (config C5): n_sets independent kernel sets of equal size n,
  * sets[s*n + i]; per set the full n! space is evaluated against that set's
  * candidate.  cand_index (nullable host u64[n_sets]): candidate indices; if
- * NULL, Algorithm 1 is run for each set on the host.  out_host[n_sets] per-set
- * records; cand_key_out (nullable host u64[n_sets]).  Synchronous.
- * Uses the ctx's gpu params; does not change the ctx's kernel set. */
+ * NULL, Algorithm 1 runs for each set on the device (as rk_heuristic_batch,
+ * bit-identical to the host's).  out_host[n_sets] per-set records;
+ * cand_key_out (nullable host u64[n_sets]).  Synchronous.  Every set is
+ * validated as by rk_set_kernels (on up to 16 host threads); the lowest
+ * failing set is reported as "set q: ...".  Sets with 6 <= n <= 9 on at most
+ * two super-SMs run the memoised batch kernel (one CTA per set; runs whose
+ * (n-5)-prefix states are equal share one 120-key suffix row, PAPER:79-80 /
+ * SPEC:210), the others the direct one (RK_NO_MEMO=1: always direct); the
+ * memoised kernel keeps a grow-only device scratch in the ctx of about
+ * 1.1 KB x n!/120 per resident CTA (1.0 GB for n = 9 on a B200), freed by
+ * rk_destroy.  Uses the ctx's gpu params; does not change the ctx's kernel
+ * set. */
 rk_status rk_eval_batch(rk_ctx* ctx, const rk_kernel* sets, uint32_t n, uint32_t n_sets, const uint64_t* cand_index,
                         rk_stats* out_host, uint64_t* cand_key_out, void* stream);
 
