@@ -1340,3 +1340,21 @@ def test_memoised_batch_vs_oracle_and_direct(ctx, monkeypatch):
             assert [(s.as_tuple(), k) for s, k in c] == [(s.as_tuple(), k) for s, k in a]
     finally:
         direct.close()
+
+
+def test_memoised_batch_edge_cases(ctx):
+    """The memoised batch kernel on one set, on given candidate indices (first,
+    last and a middle order), and on n = 9 sets against the oracle directly."""
+    F9 = math.factorial(9)
+    ctx.rk_set_gpu_params(W.GTX580)
+    sets = W.c5_sets(3)
+    want = O.sweep_sets(list(W.GTX580), sets, threads=NCPU)
+    one = ctx.rk_eval_batch(sets[:1])
+    assert one[0][0].as_tuple() == want[0][0].as_tuple() and one[0][1] == want[0][2]
+    for idx in ([0, F9 - 1, 12345], [F9 - 1, 0, F9 // 2]):
+        res = ctx.rk_eval_batch(sets, cand_index=idx)
+        for q, (st, ck) in enumerate(res):
+            okey = O.simulate(list(W.GTX580), sets[q], O.unrank(idx[q], 9)).key
+            ost = O.sweep(list(W.GTX580), sets[q], cand_key=okey, threads=NCPU)
+            ost = ost[0] if isinstance(ost, tuple) else ost
+            assert ck == okey and st.as_tuple() == ost.as_tuple()
