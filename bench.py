@@ -150,10 +150,11 @@ def read_profile(kernel_sub: str = "rk_eval_kernel", name: str = "r01_ncu_full_e
 
 def int32_issue():
     """BASELINE.json's "% INT32 issue peak", from the committed ncu captures (profiles/): the
-    ALU-bound kernels of the memoised step (suffix rows, row24) and the direct per-order
-    kernel (rk_eval_kernel, the path for sets that do not memoise)."""
+    ALU-bound kernels of the memoised step (suffix rows, row24), the memoised C5 batch kernel
+    and the direct per-order kernel (rk_eval_kernel, the path for sets that do not memoise)."""
     out = {}
     for name, sub in (("r02_ncu_full_memo.json", "rk_dp_suffix_kernel"), ("r02_ncu_full_memo.json", "rk_dp_row24_kernel"),
+                      ("r02_ncu_full_memo_batch.json", "rk_batch_memo_kernel"),
                       ("r01_ncu_full_eval_hist.json", "rk_eval_kernel")):
         try:
             with open(os.path.join(ROOT, "profiles", name)) as f:
