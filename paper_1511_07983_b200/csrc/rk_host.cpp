@@ -7,11 +7,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -96,6 +98,8 @@ struct rk_ctx {
     rk_stats* stats_dev = nullptr;    /* one record for the synchronous calls */
     uint64_t* u64_dev = nullptr;      /* small scratch (indices / keys) */
     void* batch_scratch = nullptr;    /* rk_eval_batch's memoised kernel: prefix states + rows per CTA */
+    void* pin = nullptr;              /* rk_eval_batch's pinned upload staging (grow-only) */
+    size_t pin_bytes = 0;
     size_t batch_scratch_bytes = 0;
     uint32_t max_ctas = 0;
     uint32_t sms = 0;                 /* SM count of `device` */
@@ -1073,6 +1077,7 @@ void rk_destroy(rk_ctx* c) {
         cudaFree(c->stats_dev);
         cudaFree(c->u64_dev);
         cudaFree(c->batch_scratch);
+        if (c->pin) cudaFreeHost(c->pin);
         for (cudaEvent_t ev : c->tev) cudaEventDestroy(ev);
         if (c->side) {
             cudaStreamDestroy(c->side);
@@ -1658,25 +1663,51 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     if (!c->has_params) return fail(c, RK_ESTATE, "rk_set_gpu_params first");
     if (!sets || !out_host || n_sets == 0) return fail(c, RK_EINVAL, "bad batch arguments");
     if (n == 0 || n > RK_MAX_N) return fail(c, n ? RK_ETOOMANY : RK_EINVAL, "n out of range");
-    std::vector<RkTables> tabs(n_sets);
+    /* RK_BATCH_TRACE=1: host-side phase times of this call on stderr (profiling aid) */
+    static const bool trace = [] { const char* v = getenv("RK_BATCH_TRACE"); return v && v[0] == '1'; }();
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto t1 = now();
+        fprintf(stderr, "rk_eval_batch %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    };
+    std::unique_ptr<RkTables[]> tabs(new RkTables[n_sets]); /* every entry written by build_tables */
     std::vector<uint64_t> idx(n_sets);
-    if ((s = build_tables_batch(c, sets, n, n_sets, tabs.data()))) return s;
+    if ((s = build_tables_batch(c, sets, n, n_sets, tabs.get()))) return s;
+    mark("tables");
     if (cand_index)
         for (uint32_t q = 0; q < n_sets; q++) {
             if (cand_index[q] >= fact64(n)) return fail(c, RK_EINVAL, "set %u: candidate index >= n!", q);
             idx[q] = cand_index[q];
         }
     if (!cand_index && (s = heuristic_batch_dev(c, sets, n, n_sets, nullptr, idx.data(), stream))) return s;
+    mark("heuristic");
     /* group the sets by reduced SM count so every launch runs a compile-time variant */
-    std::vector<uint32_t> perm(n_sets);
-    for (uint32_t q = 0; q < n_sets; q++) perm[q] = q;
-    std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return tabs[a].g.S < tabs[b].g.S; });
-    std::vector<RkTables> ptabs(n_sets);
-    std::vector<uint64_t> pidx(n_sets);
+    std::vector<uint32_t> perm(n_sets), Sv(n_sets);
     for (uint32_t q = 0; q < n_sets; q++) {
-        ptabs[q] = tabs[perm[q]];
+        perm[q] = q;
+        Sv[q] = tabs[q].g.S;
+    }
+    std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return Sv[a] < Sv[b]; });
+    /* the sorted tables and candidate indices go up from a pinned staging buffer kept by the ctx
+     * (grow-only; every call ends with a stream synchronize, so no copy is in flight on reuse) */
+    const size_t pin_need = (sizeof(RkTables) + sizeof(uint64_t)) * (size_t)n_sets;
+    if (pin_need > c->pin_bytes) {
+        if (c->pin) cudaFreeHost(c->pin);
+        c->pin = nullptr;
+        c->pin_bytes = 0;
+        if (cudaMallocHost(&c->pin, pin_need) != cudaSuccess) return fail(c, RK_ECUDA, "pinned staging");
+        c->pin_bytes = pin_need;
+    }
+    RkTables* ptabs = reinterpret_cast<RkTables*>(c->pin);
+    uint64_t* pidx = reinterpret_cast<uint64_t*>(ptabs + n_sets);
+    for (uint32_t q = 0; q < n_sets; q++) {
+        std::memcpy(&ptabs[q], &tabs[perm[q]], sizeof(RkTables));
         pidx[q] = idx[perm[q]];
     }
+    mark("sort");
     DeviceGuard dg(c->device);
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1691,11 +1722,12 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     if (!e) e = cudaMallocAsync((void**)&keys_dev, sizeof(uint64_t) * n_sets, st);
     if (!e) e = cudaMallocAsync((void**)&recs, sizeof(rk_stats) * (size_t)n_sets * max_chunks, st);
     if (!e) e = cudaMallocAsync((void**)&out_dev, sizeof(rk_stats) * n_sets, st);
-    if (!e) e = cudaMemcpyAsync(tabs_dev, ptabs.data(), sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
-    if (!e) e = cudaMemcpyAsync(idx_dev, pidx.data(), sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemcpyAsync(tabs_dev, ptabs, sizeof(RkTables) * n_sets, cudaMemcpyHostToDevice, st);
+    if (!e) e = cudaMemcpyAsync(idx_dev, pidx, sizeof(uint64_t) * n_sets, cudaMemcpyHostToDevice, st);
     uint32_t smax_k = 0;
     for (uint32_t q = 0; q < n_sets; q++) smax_k = std::max(smax_k, vS(c, ptabs[q].g.S));
     if (!e) e = rk_launch_keys_of(tabs_dev, n, smax_k, idx_dev, n_sets, keys_dev, stream, &c->launches);
+    mark("upload");
     /* groups on S' <= 2 run the memoised batch kernel (RK_NO_MEMO=1: the direct one) */
     auto memo_group = [&](uint32_t S) { return !c->no_memo && !(S & RK_S_POLICY) && rk_batch_memo_ok(n, S); };
     size_t memo_bytes = 0;
@@ -1726,6 +1758,7 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
                                 stream, &c->launches);
         a = b;
     }
+    mark("launch");
     std::vector<uint64_t> keys(n_sets);
     std::vector<rk_stats> pout(n_sets);
     if (!e) e = cudaMemcpyAsync(pout.data(), out_dev, sizeof(rk_stats) * n_sets, cudaMemcpyDeviceToHost, st);
@@ -1733,6 +1766,7 @@ rk_status rk_eval_batch(rk_ctx* c, const rk_kernel* sets, uint32_t n, uint32_t n
     for (void* p : {(void*)tabs_dev, (void*)idx_dev, (void*)keys_dev, (void*)recs, (void*)out_dev})
         if (p) cudaFreeAsync(p, st);
     if (!e) e = cudaStreamSynchronize(st);
+    mark("device+d2h");
     if (e) return cuda_fail(c, e, "rk_eval_batch");
     for (uint32_t q = 0; q < n_sets; q++) {
         out_host[perm[q]] = pout[q];

@@ -383,10 +383,10 @@ class Context:
         return list(o), idx.value, key.value, nodes.value
 
     def rk_heuristic_batch(self, sets, stream=None):
-        """Algorithm 1 on the device for many sets -> (orders, indices)."""
+        """Algorithm 1 on the device for many sets -> (orders, indices).  sets: a list of
+        kernel lists, or an integer array of shape (n_sets, n, 6)."""
         n = len(sets[0])
-        flat = [k for s in sets for k in s]
-        arr = kernels_array(flat)
+        arr = kernels_array(sets if hasattr(sets, "shape") else [k for s in sets for k in s])
         ns = len(sets)
         orders = (ctypes.c_int32 * (ns * n))()
         idx = (ctypes.c_uint64 * ns)()
