@@ -58,7 +58,8 @@ typedef struct rk_ctx rk_ctx;
  * RK_OVERLAP=0 (the memoised step's side-stream work runs on the caller's
  * stream), RK_ROWS_CTAS=k (CTAs per SM of the side-stream counts/histogram),
  * RK_SIDE_PRIO=0|1 (both side streams at the default | high priority; by
- * default pass 1's is at the default and pass 2's at high priority). */
+ * default pass 1's is at the default and pass 2's at high priority).
+ * RK_BATCH_TRACE=1 prints rk_eval_batch's host phase times on stderr. */
 rk_status rk_create(rk_ctx** out, int cuda_device);
 void rk_destroy(rk_ctx* ctx);
 const char* rk_last_error(const rk_ctx* ctx);
